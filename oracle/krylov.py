@@ -1,0 +1,85 @@
+"""Krylov bases -- oracle side.
+
+partial_arnoldi: Arnoldi with k-partial orthogonalisation, Eq. (partorth)
+P:208-218 and Alg. 1 lines P:1296-1307:
+    b_1 = r/||r||, m_1 = A b_1;  for j = 2..d:
+    w_j = (I - b_{j-1}b_{j-1}^* - ... - b_{j-k}b_{j-k}^*) m_{j-1}   (b_{-i} = 0)
+    b_j = w_j/||w_j||,  m_j = A b_j.
+Reading O8: the sum form with all coefficients h_i = <b_i, m_{j-1}> taken from the
+same m_{j-1} (classical Gram-Schmidt, one pass), exactly as the display reads.
+Reading O10: breakdown when ||w_j|| <= 1e-14 ||m_{j-1}||; the basis stops at j-1.
+H records the recurrence: A B[:, :j] = B[:, :j+1] Hbar, i.e.
+  m_{j-1} = sum_i h_i b_i + ||w_j|| b_j  ->  Hbar[i, j-1] = h_i, Hbar[j, j-1] = ||w_j||
+(0-based column j-1 of Hbar belongs to m_{j-1}).
+
+full_arnoldi: the classic process of P:1081-1099 (q_{j+1} from (I - Q_j Q_j^*) A q_j),
+with two Gram-Schmidt passes ("Robust implementations usually incorporate double
+Gram-Schmidt").  Used only as a baseline in pins.
+"""
+import numpy as np
+
+
+def partial_arnoldi(matvec, r, d: int, k: int, breakdown_tol: float = 1e-14):
+    """Return dict(B (n x d_eff), M = AB (n x d_eff), H ((d_eff+1) x d_eff with the
+    last row filled only if the next column was formed), d_eff, breakdown, nu)."""
+    r = np.asarray(r, dtype=np.float64)
+    n = r.size
+    B = np.zeros((n, d))
+    M = np.zeros((n, d))
+    H = np.zeros((d + 1, d))
+    rho = np.linalg.norm(r)
+    B[:, 0] = r / rho
+    M[:, 0] = matvec(B[:, 0])
+    d_eff = d
+    breakdown = False
+    for j in range(1, d):                  # 0-based j is the paper's j+1
+        lo = max(0, j - k)
+        W = B[:, lo:j]
+        m = M[:, j - 1]
+        h = W.T @ m                        # all h from the same m_{j-1}
+        w = m - W @ h
+        nu = np.linalg.norm(w)
+        H[lo:j, j - 1] = h
+        H[j, j - 1] = nu
+        if nu <= breakdown_tol * np.linalg.norm(m):
+            d_eff = j
+            breakdown = True
+            break
+        B[:, j] = w / nu
+        M[:, j] = matvec(B[:, j])
+    return dict(B=B[:, :d_eff], M=M[:, :d_eff], H=H[:d_eff + 1, :d_eff],
+                d_eff=d_eff, breakdown=breakdown, rho=rho)
+
+
+def partial_arnoldi_next(matvec, B, M, k: int):
+    """One more column b_{d+1} (and its h, nu) after a partial_arnoldi basis: the
+    column of Hbar belonging to m_d.  Returns (b_next, h (len d), nu)."""
+    d = B.shape[1]
+    lo = max(0, d - k)
+    m = M[:, d - 1]
+    W = B[:, lo:d]
+    h_w = W.T @ m
+    w = m - W @ h_w
+    nu = np.linalg.norm(w)
+    h = np.zeros(d)
+    h[lo:d] = h_w
+    return w / nu, h, nu
+
+
+def full_arnoldi(matvec, r, p: int):
+    r = np.asarray(r, dtype=np.float64)
+    n = r.size
+    Q = np.zeros((n, p + 1))
+    H = np.zeros((p + 1, p))
+    Q[:, 0] = r / np.linalg.norm(r)
+    for j in range(p):
+        w = matvec(Q[:, j])
+        for _ in range(2):
+            c = Q[:, :j + 1].T @ w
+            w = w - Q[:, :j + 1] @ c
+            H[:j + 1, j] += c
+        H[j + 1, j] = np.linalg.norm(w)
+        if H[j + 1, j] == 0.0:
+            return Q[:, :j + 1], H[:j + 2, :j + 1]
+        Q[:, j + 1] = w / H[j + 1, j]
+    return Q, H

@@ -1,0 +1,65 @@
+"""Sketched Rayleigh-Ritz -- oracle side.  Alg. 2, Eq. Mhat-form
+(P:1598-1601), Eq. srr-resid-est.
+
+  b_1 = v0/||v0||; k-partial Arnoldi to d columns
+  C = S B,  D = S AB   (one shared S)                      (O11)
+  thin QR  C = U T
+  Mhat = T^{-1} (U^T D)                                    (Eq. Mhat-form; O22)
+  eig(Mhat) -> (theta_i, y_i)                              ("the QR algorithm" P:1603)
+  r_est,i = ||D y_i - theta_i C y_i|| / ||C y_i||          (Eq. srr-resid-est)
+  x_i = B y_i;  true residual ||A x_i - theta_i x_i|| / ||x_i||   (O24; no tau filter)
+Selection (O23): nev pairs of largest |theta|, ties broken by Im(theta)
+descending; if position nev splits a conjugate pair, the partner is included.
+"""
+import numpy as np
+from scipy.linalg import solve_triangular
+
+from .krylov import partial_arnoldi
+from .sgmres import thin_qr
+from .sketch import sketch_matrix
+
+
+def select_ritz(theta, nev):
+    """Indices of the nev largest-|theta| Ritz values, canonical order (O23)."""
+    theta = np.asarray(theta)
+    # lexsort: last key primary -> sort by -|theta| then by -Im
+    order = np.lexsort((-theta.imag, -np.abs(theta)))
+    sel = list(order[:nev])
+    if nev < len(order):
+        last = theta[order[nev - 1]]
+        nxt = theta[order[nev]]
+        if last.imag != 0.0 and np.isclose(nxt, np.conj(last), rtol=1e-12, atol=0.0):
+            sel.append(order[nev])
+    return np.array(sel, dtype=np.int64)
+
+
+def srr_from_basis(matvec, B, M, S, nev):
+    C = S @ B
+    D = S @ M
+    U, T = thin_qr(C)
+    Mhat = solve_triangular(T, U.T @ D, lower=False)
+    theta, Y = np.linalg.eig(Mhat)
+    sel = select_ritz(theta, nev)
+    th = theta[sel]
+    Ys = Y[:, sel]
+    res_est = np.array([np.linalg.norm(D @ y - t * (C @ y)) / np.linalg.norm(C @ y)
+                        for t, y in zip(th, Ys.T)])
+    X = B @ Ys
+    res_true = np.empty(len(sel))
+    for i in range(len(sel)):
+        x = X[:, i]
+        Ax = matvec(x.real) + 1j * matvec(x.imag)
+        res_true[i] = np.linalg.norm(Ax - th[i] * x) / np.linalg.norm(x)
+    return dict(theta=th, Y=Ys, X=X, res_est=res_est, res_true=res_true,
+                Mhat=Mhat, C=C, D=D, U=U, T=T, cond_SB=np.linalg.cond(C),
+                theta_all=theta)
+
+
+def srr_eigs(matvec, v0, d, k, s, zeta, seed, nev, cycle=0):
+    v0 = np.asarray(v0, dtype=np.float64)
+    n = v0.size
+    basis = partial_arnoldi(matvec, v0, d, k)
+    S = sketch_matrix(n, s, zeta, seed, cycle)
+    out = srr_from_basis(matvec, basis["B"], basis["M"], S, nev)
+    out["basis"] = basis
+    return out
