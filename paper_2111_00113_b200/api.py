@@ -1,0 +1,255 @@
+"""Python API over the C-ABI (same names as include/sks.h without the ``sks_`` prefix).
+
+Marshalling only: arrays may be torch tensors (CUDA or CPU) or numpy arrays; their
+pointers are passed straight to libsks, which detects host vs device memory.  Output
+arrays live where the main input lives (device in -> device out, host in -> host out).
+"""
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+
+try:
+    import torch
+except Exception:  # pragma: no cover - torch is part of the image
+    torch = None
+
+
+class SksError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{L.STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _is_torch(a):
+    return torch is not None and isinstance(a, torch.Tensor)
+
+
+def _prep(a, dtype=np.float64):
+    """-> (object kept alive, pointer) for a contiguous array of `dtype`."""
+    if a is None:
+        return None, None
+    if _is_torch(a):
+        tdt = {np.float64: torch.float64, np.int32: torch.int32, np.int8: torch.int8}[dtype]
+        t = a.detach()
+        if t.dtype != tdt:
+            t = t.to(tdt)
+        t = t.contiguous()
+        return t, t.data_ptr()
+    arr = np.ascontiguousarray(a, dtype=dtype)
+    return arr, arr.ctypes.data
+
+
+def _empty_like_place(ref, shape, dtype=np.float64):
+    if _is_torch(ref):
+        tdt = {np.float64: torch.float64, np.int32: torch.int32, np.int8: torch.int8}[dtype]
+        pin = ref.device.type == "cpu"
+        t = torch.empty(shape, dtype=tdt, device=ref.device, pin_memory=pin and torch.cuda.is_available())
+        return t, t.data_ptr()
+    arr = np.empty(shape, dtype=dtype)
+    return arr, arr.ctypes.data
+
+
+@dataclass
+class StencilOperator:
+    """-Lap(u) + beta (d/dx + d/dy [+ d/dz]) u on an m^dim Dirichlet grid (reading O18)."""
+    dim: int
+    m: int
+    beta: float
+    row_begin: int = 0
+    row_end: int = None
+
+    @property
+    def n_global(self):
+        return self.m ** self.dim
+
+    def struct(self):
+        rb = self.row_begin
+        re = self.n_global if self.row_end is None else self.row_end
+        kind = L.SKS_OP_STENCIL2D if self.dim == 2 else L.SKS_OP_STENCIL3D
+        return L.Operator(kind, 0, self.m, float(self.beta), self.n_global, rb, re, None, None, None, 0), ()
+
+
+@dataclass
+class CsrOperator:
+    """Rows [row_begin, row_end) of a general sparse A; col_idx are GLOBAL int32 indices."""
+    row_ptr: object
+    col_idx: object
+    val: object
+    n_global: int
+    row_begin: int = 0
+    row_end: int = None
+
+    def struct(self):
+        rp, prp = _prep(self.row_ptr, np.int32)
+        ci, pci = _prep(self.col_idx, np.int32)
+        va, pva = _prep(self.val, np.float64)
+        re = self.n_global if self.row_end is None else self.row_end
+        nnz = int(rp[-1])
+        return L.Operator(L.SKS_OP_CSR, 0, 0, 0.0, self.n_global, self.row_begin, re, prp, pci, pva, nnz), (rp, ci, va)
+
+
+def partition(kind: str, m: int, n_global: int, nranks: int, rank: int):
+    lib = L.load()
+    k = {"stencil2d": L.SKS_OP_STENCIL2D, "stencil3d": L.SKS_OP_STENCIL3D, "csr": L.SKS_OP_CSR}[kind]
+    lo, hi = C.c_int64(), C.c_int64()
+    st = lib.sks_partition(k, m, n_global, nranks, rank, C.byref(lo), C.byref(hi))
+    if st != 0:
+        raise SksError(st, "sks_partition")
+    return lo.value, hi.value
+
+
+def get_unique_id() -> bytes:
+    lib = L.load()
+    buf = (C.c_ubyte * 128)()
+    st = lib.sks_get_unique_id(buf)
+    if st != 0:
+        raise SksError(st, lib.sks_last_error(None).decode())
+    return bytes(buf)
+
+
+class Context:
+    def __init__(self, device: int = 0, rank: int = 0, nranks: int = 1, nccl_id: bytes = None):
+        self.lib = L.load()
+        self.h = C.c_void_p()
+        idp = None
+        if nccl_id is not None:
+            self._id = (C.c_ubyte * 128).from_buffer_copy(nccl_id)
+            idp = C.addressof(self._id)
+        st = self.lib.sks_create(C.byref(self.h), device, rank, nranks, idp)
+        if st != 0:
+            raise SksError(st, self.lib.sks_last_error(None).decode())
+        self.device, self.rank, self.nranks = device, rank, nranks
+
+    def close(self):
+        if self.h:
+            self.lib.sks_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _check(self, st, what, allow=()):
+        if st != 0 and st not in allow:
+            raise SksError(st, f"{what}: {self.lib.sks_last_error(self.h).decode()}")
+        return st
+
+    def set_stream(self, stream=None):
+        """Run the main work on `stream` (torch.cuda.Stream, raw handle, or None)."""
+        h = None
+        if stream is not None:
+            h = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        self._check(self.lib.sks_set_stream(self.h, h), "sks_set_stream")
+
+    # ---------------------------------------------------------------- sGMRES
+    def sgmres_solve(self, A, f, x0=None, *, d, k, s, zeta=8, seed=0, tol=1e-8, max_cycles=50,
+                     early_exit_factor=0.25, cond_tol=1e14, sketch_batch=0, hist_cap=None):
+        op, keep = A.struct()
+        fa, pf = _prep(f)
+        n = fa.shape[0]
+        if x0 is None:
+            if _is_torch(fa):
+                x = torch.zeros_like(fa)
+            else:
+                x = np.zeros(n)
+        else:
+            x = (x0.detach().clone().to(torch.float64).contiguous() if _is_torch(x0)
+                 else np.array(x0, dtype=np.float64, copy=True))
+        px = x.data_ptr() if _is_torch(x) else x.ctypes.data
+        cap = hist_cap or (d * max_cycles + 8)
+        hist = np.zeros(cap)
+        hist_true = np.zeros(max_cycles + 2)
+        opts = L.SgmresOpts(d, k, s, zeta, seed, tol, max_cycles, sketch_batch, early_exit_factor, cond_tol)
+        info = L.SgmresInfo()
+        st = self.lib.sks_sgmres_solve(self.h, C.byref(op), pf, px, C.byref(opts), C.byref(info),
+                                       hist.ctypes.data, cap, hist_true.ctypes.data, len(hist_true))
+        self._check(st, "sks_sgmres_solve", allow=(L.SKS_ENOTCONV,))
+        inf = {k_: getattr(info, k_) for k_, _ in info._fields_}
+        nh = min(cap, inf["columns"])
+        return SgmresResult(x=x, hist=hist[:nh], hist_true=hist_true[:inf["cycles"]], info=inf,
+                            converged=(st == 0))
+
+    # ---------------------------------------------------------------- sRR
+    def srr_eigs(self, A, v0, *, d, k, s, nev, zeta=8, seed=0, cond_tol=1e14, want_vectors=False):
+        op, keep = A.struct()
+        va, pv = _prep(v0)
+        n = va.shape[0]
+        cap = nev + 1
+        th_re, th_im, rt, re = (np.zeros(cap) for _ in range(4))
+        Xr = Xi = None
+        pxr = pxi = None
+        if want_vectors:
+            Xr, pxr = _empty_like_place(va, (cap, n))
+            Xi, pxi = _empty_like_place(va, (cap, n))
+        opts = L.SrrOpts(d, k, s, zeta, seed, cond_tol)
+        info = L.SrrInfo()
+        st = self.lib.sks_srr_eigs(self.h, C.byref(op), pv, C.byref(opts), nev, cap, th_re.ctypes.data,
+                                   th_im.ctypes.data, rt.ctypes.data, re.ctypes.data, pxr, pxi, C.byref(info))
+        self._check(st, "sks_srr_eigs")
+        inf = {k_: getattr(info, k_) for k_, _ in info._fields_}
+        m = inf["nev_out"]
+        out = dict(theta=th_re[:m] + 1j * th_im[:m], res_true=rt[:m], res_est=re[:m], info=inf)
+        if want_vectors:
+            out["X"] = (Xr[:m], Xi[:m])
+        return out
+
+    # ---------------------------------------------------------------- parity entry points
+    def sketch_apply(self, M, *, s, zeta, seed, cycle=0, n_global=None, row_begin=0):
+        Ma, pm = _prep(M)
+        if Ma.ndim == 1:
+            Ma = Ma.reshape(-1, 1) if not _is_torch(Ma) else Ma.reshape(-1, 1)
+        n, c = Ma.shape
+        # column-major n x c: pass the transpose-contiguous copy
+        Mt = Ma.t().contiguous() if _is_torch(Ma) else np.ascontiguousarray(Ma.T)
+        pm = Mt.data_ptr() if _is_torch(Mt) else Mt.ctypes.data
+        ng = row_begin + n if n_global is None else n_global
+        SM, psm = _empty_like_place(Ma, (c, s))
+        st = self.lib.sks_sketch_apply(self.h, ng, row_begin, row_begin + n, s, zeta, seed, cycle, pm, n, c, psm)
+        self._check(st, "sks_sketch_apply")
+        return SM.t() if _is_torch(SM) else SM.T
+
+    def sketch_table(self, row_begin, count, *, s, zeta, seed, cycle=0):
+        q = np.zeros(count * zeta, dtype=np.int32)
+        sg = np.zeros(count * zeta, dtype=np.int8)
+        st = self.lib.sks_sketch_table(self.h, row_begin, count, s, zeta, seed, cycle, q.ctypes.data,
+                                       sg.ctypes.data)
+        self._check(st, "sks_sketch_table")
+        return q.reshape(count, zeta), sg.reshape(count, zeta)
+
+    def apply_operator(self, A, x):
+        op, keep = A.struct()
+        xa, px = _prep(x)
+        y, py = _empty_like_place(xa, xa.shape)
+        self._check(self.lib.sks_apply_operator(self.h, C.byref(op), px, py), "sks_apply_operator")
+        return y
+
+    def basis(self, A, r0, *, k, ncols):
+        op, keep = A.struct()
+        ra, pr = _prep(r0)
+        n = ra.shape[0]
+        B, pb = _empty_like_place(ra, (ncols, n))      # column-major n x ncols
+        H = np.zeros((ncols - 1, ncols)) if ncols >= 2 else None
+        st = self.lib.sks_basis(self.h, C.byref(op), pr, k, ncols, pb, H.ctypes.data if H is not None else None)
+        self._check(st, "sks_basis")
+        Bm = B.t() if _is_torch(B) else B.T
+        return Bm, (H.T if H is not None else None)
+
+
+@dataclass
+class SgmresResult:
+    x: object
+    hist: np.ndarray
+    hist_true: np.ndarray
+    info: dict
+    converged: bool

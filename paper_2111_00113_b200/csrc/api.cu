@@ -1,0 +1,1150 @@
+// api.cu -- C-ABI (include/sks.h) and the host drivers of sGMRES / sRR.
+//
+// Driver structure:
+//   main stream : residual/start kernel, one fused step kernel per basis column (stencil)
+//                 or SpMV+orth (CSR), assembly; NCCL halo + partial-sum allreduce per column
+//                 when nranks > 1.
+//   side stream : every batch of up to 32 finished columns -> sketch batch (S W), then the
+//                 incremental sketched QR of the reduced matrix (BCGS2 + panel) with r_est,j
+//                 and the early-exit test.  Forks from / joins into the main stream.
+//   host        : enqueues ahead, polls the early-exit flag of batch b-1 before enqueuing
+//                 batch b+1 (bounded lag); one synchronisation per restart cycle.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sks.h"
+#include "common.cuh"
+#include "internal.h"
+#include "step.cuh"
+
+using namespace sks;
+
+// ------------------------------------------------------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  template <typename T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+struct sks_ctx {
+  int device = 0, rank = 0, nranks = 1, num_sms = 148;
+  cudaStream_t own_main = nullptr, side = nullptr, user_main = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr, ev_b0 = nullptr,
+              ev_b1 = nullptr;
+  std::vector<cudaEvent_t> ev_batch;
+  ncclComm_t comm = nullptr;
+  std::string err = "";
+  int64_t launches = 0;
+  // workspaces
+  DevBuf W, xb, fb, vb, mr, xg, part, part2, partsk, sigma, H, mnorm, SW, Xp, Zb, U, T, rvec, rho, rest, coef,
+      ctrl, small, Mh, Mh2, wr, wi, sel, th, yr, yi, ework, SAB, SB, Xr, Xi, AXr, AXi, rpb, cib, vab, cig, rbd,
+      tmp;
+  CtrlBlock* h_ctrl = nullptr;   // pinned mirror
+  double* h_small = nullptr;     // pinned scratch (4096 doubles)
+  int64_t w_zeroed_bytes = 0;
+  cudaStream_t main() const { return user_main ? user_main : own_main; }
+};
+
+static thread_local char g_err[512];
+
+#define SKS_CK(ctx, expr)                                                                 \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess) {                                                             \
+      (ctx)->err = std::string(#expr) + ": " + cudaGetErrorString(_e);                  \
+      return SKS_ECUDA;                                                                  \
+    }                                                                                    \
+  } while (0)
+
+#define SKS_NC(ctx, expr)                                                                 \
+  do {                                                                                   \
+    ncclResult_t _r = (expr);                                                            \
+    if (_r != ncclSuccess) {                                                             \
+      (ctx)->err = std::string(#expr) + ": " + ncclGetErrorString(_r);                  \
+      return SKS_ENCCL;                                                                  \
+    }                                                                                    \
+  } while (0)
+
+#define SKS_TRY(expr)          \
+  do {                         \
+    sks_status _s = (expr);    \
+    if (_s != SKS_OK) return _s; \
+  } while (0)
+
+static sks_status fail(sks_ctx* c, sks_status s, const std::string& m) {
+  if (c) c->err = m;
+  return s;
+}
+
+static sks_status ensure(sks_ctx* c, DevBuf& b, size_t bytes, bool zero = false) {
+  if (bytes == 0) bytes = 8;
+  if (b.bytes >= bytes) return SKS_OK;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+  cudaError_t e = cudaMalloc(&b.p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(c, SKS_ENOMEM, std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+  }
+  b.bytes = bytes;
+  if (zero) SKS_CK(c, cudaMemsetAsync(b.p, 0, bytes, c->main()));
+  return SKS_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// geometry of this rank's row block
+struct Geo {
+  int kind = 0, dim = 0;
+  int64_t m = 0, n_global = 0, row_begin = 0, row_end = 0, n = 0;
+  int64_t plane = 1, nz = 0, z0 = 0, G = 0, ld = 0, off = 0;
+  double cc = 0, cm = 0, cp = 0;
+};
+
+static sks_status make_geo(sks_ctx* c, const sks_operator* A, Geo* g) {
+  if (!A) return fail(c, SKS_EINVAL, "operator is NULL");
+  g->kind = A->kind;
+  g->n_global = A->n_global;
+  g->row_begin = A->row_begin;
+  g->row_end = A->row_end;
+  g->n = A->row_end - A->row_begin;
+  if (g->n <= 0 || A->row_begin < 0 || A->row_end > A->n_global)
+    return fail(c, SKS_EINVAL, "bad row block [row_begin,row_end)");
+  if (A->kind == SKS_OP_STENCIL2D || A->kind == SKS_OP_STENCIL3D) {
+    g->dim = A->kind == SKS_OP_STENCIL2D ? 2 : 3;
+    g->m = A->m;
+    if (g->m < 2) return fail(c, SKS_EINVAL, "stencil m must be >= 2");
+    g->plane = g->dim == 2 ? g->m : g->m * g->m;
+    const int64_t ng = g->dim == 2 ? g->m * g->m : g->m * g->m * g->m;
+    if (ng != A->n_global) return fail(c, SKS_EINVAL, "n_global != m^dim");
+    if (A->row_begin % g->plane || A->row_end % g->plane)
+      return fail(c, SKS_EINVAL, "stencil row block must consist of whole lines (2D) / planes (3D)");
+    g->nz = g->n / g->plane;
+    g->z0 = A->row_begin / g->plane;
+    g->G = 2;
+    if (c->nranks > 1 && g->nz < g->G) return fail(c, SKS_EINVAL, "each rank needs >= 2 planes/lines");
+    if (!std::isfinite(A->beta)) return fail(c, SKS_EINVAL, "beta not finite");
+    const double ih2 = (double)(g->m + 1) * (double)(g->m + 1);
+    const double ih = (double)(g->m + 1) / 2.0;
+    g->cc = 2.0 * g->dim * ih2;
+    g->cm = -ih2 - A->beta * ih;
+    g->cp = -ih2 + A->beta * ih;
+    g->off = g->G * g->plane;
+    g->ld = ((g->nz + 2 * g->G) * g->plane + 63) / 64 * 64;
+  } else if (A->kind == SKS_OP_CSR) {
+    g->dim = 0;
+    g->plane = 1;
+    g->nz = g->n;
+    g->z0 = A->row_begin;
+    g->G = 0;
+    g->off = 0;
+    g->ld = (g->n + 63) / 64 * 64;
+    if (!A->row_ptr || !A->col_idx || !A->val) return fail(c, SKS_EINVAL, "CSR arrays are NULL");
+  } else {
+    return fail(c, SKS_EINVAL, "unknown operator kind");
+  }
+  if (A->n_global > INT_MAX && A->kind == SKS_OP_CSR)
+    return fail(c, SKS_EUNSUPPORTED, "CSR with n_global >= 2^31 (int32 indices)");
+  return SKS_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// communication (nranks > 1): halo planes of a ghost-layout vector, allreduce of partials
+static sks_status halo_exchange(sks_ctx* c, const Geo& g, double* vec) {
+  if (c->nranks == 1 || g.G == 0) return SKS_OK;
+  const size_t cnt = (size_t)(g.G * g.plane);
+  const int lo = c->rank - 1, hi = c->rank + 1;
+  SKS_NC(c, ncclGroupStart());
+  if (lo >= 0) {
+    SKS_NC(c, ncclSend(vec + g.off, cnt, ncclDouble, lo, c->comm, c->main()));
+    SKS_NC(c, ncclRecv(vec + g.off - cnt, cnt, ncclDouble, lo, c->comm, c->main()));
+  }
+  if (hi < c->nranks) {
+    SKS_NC(c, ncclSend(vec + g.off + (g.nz - g.G) * g.plane, cnt, ncclDouble, hi, c->comm, c->main()));
+    SKS_NC(c, ncclRecv(vec + g.off + g.nz * g.plane, cnt, ncclDouble, hi, c->comm, c->main()));
+  }
+  SKS_NC(c, ncclGroupEnd());
+  return SKS_OK;
+}
+
+static sks_status allreduce_sum(sks_ctx* c, double* buf, size_t cnt, cudaStream_t st) {
+  if (c->nranks == 1) return SKS_OK;
+  SKS_NC(c, ncclAllReduce(buf, buf, cnt, ncclDouble, ncclSum, c->comm, st));
+  return SKS_OK;
+}
+
+// CSR: make w (n_local rows) available as the gathered vector for the SpMV
+static sks_status csr_gather(sks_ctx* c, const Geo& g, const double* w, const double** xg, int64_t maxn) {
+  if (c->nranks == 1) {
+    *xg = w;
+    return SKS_OK;
+  }
+  double* dst = c->xg.as<double>();
+  SKS_NC(c, ncclAllGather(w, dst, (size_t)maxn, ncclDouble, c->comm, c->main()));
+  *xg = dst;
+  return SKS_OK;
+}
+
+// ------------------------------------------------------------------------------------
+extern "C" {
+
+int sks_abi_version(void) { return SKS_ABI_VERSION; }
+
+const char* sks_last_error(const sks_ctx* ctx) {
+  if (!ctx) return g_err;
+  return ctx->err.c_str();
+}
+
+sks_status sks_get_unique_id(unsigned char id[128]) {
+  if (!id) return SKS_EINVAL;
+  ncclUniqueId u;
+  ncclResult_t r = ncclGetUniqueId(&u);
+  if (r != ncclSuccess) {
+    snprintf(g_err, sizeof(g_err), "ncclGetUniqueId: %s", ncclGetErrorString(r));
+    return SKS_ENCCL;
+  }
+  static_assert(sizeof(u.internal) == 128, "nccl id size");
+  memcpy(id, u.internal, 128);
+  return SKS_OK;
+}
+
+sks_status sks_partition(int kind, int64_t m, int64_t n_global, int nranks, int rank, int64_t* row_begin,
+                         int64_t* row_end) {
+  if (!row_begin || !row_end || nranks < 1 || rank < 0 || rank >= nranks) return SKS_EINVAL;
+  int64_t unit, count;
+  if (kind == SKS_OP_CSR) {
+    unit = 1;
+    count = n_global;
+  } else if (kind == SKS_OP_STENCIL2D) {
+    unit = m;
+    count = m;
+  } else if (kind == SKS_OP_STENCIL3D) {
+    unit = m * m;
+    count = m;
+  } else {
+    return SKS_EINVAL;
+  }
+  const int64_t base = count / nranks, rem = count % nranks;
+  const int64_t lo = rank * base + std::min<int64_t>(rank, rem);
+  const int64_t hi = lo + base + (rank < rem ? 1 : 0);
+  *row_begin = lo * unit;
+  *row_end = hi * unit;
+  return SKS_OK;
+}
+
+sks_status sks_create(sks_ctx** out, int device, int rank, int nranks, const unsigned char* id) {
+  if (!out) return SKS_EINVAL;
+  *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks) return SKS_EINVAL;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    snprintf(g_err, sizeof(g_err), "no CUDA device available (%s); libsks has no CPU fallback",
+             e != cudaSuccess ? cudaGetErrorString(e) : "0 devices");
+    return SKS_ECUDA;
+  }
+  if (device < 0 || device >= ndev) {
+    snprintf(g_err, sizeof(g_err), "device %d out of range (%d devices)", device, ndev);
+    return SKS_EINVAL;
+  }
+  sks_ctx* c = new sks_ctx();
+  c->device = device;
+  c->rank = rank;
+  c->nranks = nranks;
+  cudaSetDevice(device);
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  cudaStreamCreateWithFlags(&c->own_main, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
+  cudaEventCreate(&c->ev_t0);
+  cudaEventCreate(&c->ev_t1);
+  cudaEventCreate(&c->ev_b0);
+  cudaEventCreate(&c->ev_b1);
+  c->ev_batch.resize(256);
+  for (auto& ev : c->ev_batch) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  if (cudaMallocHost(&c->h_ctrl, sizeof(CtrlBlock)) != cudaSuccess ||
+      cudaMallocHost(&c->h_small, 4096 * sizeof(double)) != cudaSuccess) {
+    snprintf(g_err, sizeof(g_err), "cudaMallocHost failed");
+    delete c;
+    return SKS_ENOMEM;
+  }
+  if (nranks > 1) {
+    if (!id) {
+      snprintf(g_err, sizeof(g_err), "nranks > 1 needs the NCCL unique id");
+      delete c;
+      return SKS_EINVAL;
+    }
+    ncclUniqueId u;
+    memcpy(u.internal, id, 128);
+    ncclResult_t r = ncclCommInitRank(&c->comm, nranks, u, rank);
+    if (r != ncclSuccess) {
+      snprintf(g_err, sizeof(g_err), "ncclCommInitRank: %s", ncclGetErrorString(r));
+      delete c;
+      return SKS_ENCCL;
+    }
+  }
+  e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    snprintf(g_err, sizeof(g_err), "context setup: %s", cudaGetErrorString(e));
+    delete c;
+    return SKS_ECUDA;
+  }
+  *out = c;
+  return SKS_OK;
+}
+
+sks_status sks_destroy(sks_ctx* c) {
+  if (!c) return SKS_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  DevBuf* bufs[] = {&c->W,    &c->xb,   &c->fb,    &c->vb,   &c->mr,   &c->xg,   &c->part,  &c->part2, &c->partsk,
+                    &c->sigma, &c->H,   &c->mnorm, &c->SW,   &c->Xp,   &c->Zb,   &c->U,     &c->T,     &c->rvec,
+                    &c->rho,  &c->rest, &c->coef,  &c->ctrl, &c->small, &c->Mh,  &c->Mh2,   &c->wr,    &c->wi,
+                    &c->sel,  &c->th,   &c->yr,    &c->yi,   &c->ework, &c->SAB, &c->SB,    &c->Xr,    &c->Xi,
+                    &c->AXr,  &c->AXi,  &c->rpb,   &c->cib,  &c->vab,  &c->cig,  &c->rbd,   &c->tmp};
+  for (DevBuf* b : bufs)
+    if (b->p) cudaFree(b->p);
+  if (c->comm) ncclCommDestroy(c->comm);
+  for (auto& ev : c->ev_batch) cudaEventDestroy(ev);
+  cudaEvent_t evs[] = {c->ev_fork, c->ev_join, c->ev_t0, c->ev_t1, c->ev_b0, c->ev_b1};
+  for (auto e : evs)
+    if (e) cudaEventDestroy(e);
+  if (c->own_main) cudaStreamDestroy(c->own_main);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
+  if (c->h_small) cudaFreeHost(c->h_small);
+  delete c;
+  return SKS_OK;
+}
+
+sks_status sks_set_stream(sks_ctx* c, void* stream) {
+  if (!c) return SKS_EINVAL;
+  c->user_main = reinterpret_cast<cudaStream_t>(stream);
+  return SKS_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------------------
+// shared helpers of the drivers
+// ------------------------------------------------------------------------------------
+namespace {
+
+struct Basis {
+  sks_ctx* c;
+  Geo g;
+  int k;
+  int ncol;            // columns allocated
+  int ldH;
+  int step_grid = 0;   // stencil step grid, or CSR grid
+  int pslots = 0;      // partial slots (fixed across ranks)
+  StepArgs sa;
+  // CSR
+  const int32_t* rp = nullptr;
+  const int32_t* ci = nullptr;
+  const double* va = nullptr;
+  int64_t maxn = 0;    // max local rows over ranks (CSR gather)
+  int64_t nnz = 0;
+  double bytes = 0.0;  // algorithmic bytes of the basis loop
+  int64_t steps = 0;
+};
+
+static double* colp(sks_ctx* c, const Basis& b, int j) { return c->W.as<double>() + (int64_t)j * b.g.ld; }
+
+static sks_status setup_basis(sks_ctx* c, const sks_operator* A, int k, int ncol, Basis* b) {
+  b->c = c;
+  SKS_TRY(make_geo(c, A, &b->g));
+  b->k = k;
+  b->ncol = ncol;
+  b->ldH = ncol + 1;
+  const Geo& g = b->g;
+  const size_t wbytes = sizeof(double) * (size_t)g.ld * ncol;
+  const bool fresh_w = c->W.bytes < wbytes;
+  SKS_TRY(ensure(c, c->W, wbytes));
+  (void)fresh_w;
+  if (g.G > 0) {
+    // ghost planes must be zero at the physical boundary (Dirichlet) for THIS geometry:
+    // clear the G leading and G trailing planes (+ pitch padding) of every column.
+    const size_t head = sizeof(double) * (size_t)(g.G * g.plane);
+    const size_t tail_off = sizeof(double) * (size_t)(g.off + g.nz * g.plane);
+    const size_t tail = sizeof(double) * (size_t)g.ld - tail_off;
+    SKS_CK(c, cudaMemset2DAsync(c->W.p, sizeof(double) * g.ld, 0, head, ncol, c->main()));
+    SKS_CK(c, cudaMemset2DAsync(c->W.as<char>() + tail_off, sizeof(double) * g.ld, 0, tail, ncol, c->main()));
+  }
+  SKS_TRY(ensure(c, c->xb, sizeof(double) * g.ld));
+  SKS_TRY(ensure(c, c->fb, sizeof(double) * g.ld));
+  SKS_TRY(ensure(c, c->vb, sizeof(double) * g.ld));
+  SKS_TRY(ensure(c, c->sigma, sizeof(double) * (ncol + 2), true));
+  SKS_TRY(ensure(c, c->H, sizeof(double) * (size_t)(ncol + 1) * (ncol + 1)));
+  SKS_CK(c, cudaMemsetAsync(c->H.p, 0, sizeof(double) * (size_t)(ncol + 1) * (ncol + 1), c->main()));
+  SKS_TRY(ensure(c, c->mnorm, sizeof(double) * (ncol + 2), true));
+  SKS_TRY(ensure(c, c->ctrl, sizeof(CtrlBlock), true));
+  SKS_TRY(ensure(c, c->small, sizeof(double) * 4096, true));
+  b->pslots = c->num_sms * 4;
+  SKS_TRY(ensure(c, c->part, sizeof(double) * (size_t)2 * b->pslots * SKS_NP));
+  SKS_TRY(ensure(c, c->part2, sizeof(double) * (size_t)2 * b->pslots * SKS_NP));
+  SKS_CK(c, cudaMemsetAsync(c->part.p, 0, c->part.bytes, c->main()));
+  SKS_CK(c, cudaMemsetAsync(c->part2.p, 0, c->part2.bytes, c->main()));
+  if (g.kind != SKS_OP_CSR) {
+    StepArgs& a = b->sa;
+    memset(&a, 0, sizeof(a));
+    a.m = g.m;
+    a.nz = g.nz;
+    a.z0 = g.z0;
+    a.plane = g.plane;
+    a.ld = g.ld;
+    a.off = g.off;
+    a.G = (int)g.G;
+    a.dim = g.dim;
+    a.cc = g.cc;
+    a.cm = g.cm;
+    a.cp = g.cp;
+    a.k = k;
+    a.W = c->W.as<double>();
+    a.sigma = c->sigma.as<double>();
+    a.H = c->H.as<double>();
+    a.ldH = b->ldH;
+    a.mnorm = c->mnorm.as<double>();
+    a.ctrl = c->ctrl.as<CtrlBlock>();
+    stencil_tiling(g.dim, g.m, g.nz, c->num_sms, &a, &b->step_grid);
+    if (b->step_grid > b->pslots) b->step_grid = b->pslots;
+  } else {
+    b->step_grid = c->num_sms * 4;
+    b->nnz = A->nnz_local;
+    // device copies of the CSR arrays
+    SKS_TRY(ensure(c, c->rpb, sizeof(int32_t) * (g.n + 1)));
+    SKS_TRY(ensure(c, c->cib, sizeof(int32_t) * std::max<int64_t>(b->nnz, 1)));
+    SKS_TRY(ensure(c, c->vab, sizeof(double) * std::max<int64_t>(b->nnz, 1)));
+    SKS_CK(c, cudaMemcpyAsync(c->rpb.p, A->row_ptr, sizeof(int32_t) * (g.n + 1), cudaMemcpyDefault, c->main()));
+    SKS_CK(c, cudaMemcpyAsync(c->cib.p, A->col_idx, sizeof(int32_t) * b->nnz, cudaMemcpyDefault, c->main()));
+    SKS_CK(c, cudaMemcpyAsync(c->vab.p, A->val, sizeof(double) * b->nnz, cudaMemcpyDefault, c->main()));
+    SKS_TRY(ensure(c, c->mr, sizeof(double) * g.ld));
+    b->rp = c->rpb.as<int32_t>();
+    b->ci = c->cib.as<int32_t>();
+    b->va = c->vab.as<double>();
+    if (c->nranks > 1) {
+      // gathered-vector layout [rank][maxn]; remap global column indices once
+      std::vector<int64_t> rb(c->nranks + 1);
+      for (int r = 0; r < c->nranks; ++r) {
+        int64_t lo, hi;
+        sks_partition(SKS_OP_CSR, 0, g.n_global, c->nranks, r, &lo, &hi);
+        rb[r] = lo;
+        b->maxn = std::max(b->maxn, hi - lo);
+      }
+      rb[c->nranks] = g.n_global;
+      if (rb[c->rank] != g.row_begin) return fail(c, SKS_EINVAL, "CSR row block must follow sks_partition");
+      SKS_TRY(ensure(c, c->rbd, sizeof(int64_t) * (c->nranks + 1)));
+      SKS_CK(c, cudaMemcpyAsync(c->rbd.p, rb.data(), sizeof(int64_t) * (c->nranks + 1), cudaMemcpyHostToDevice,
+                                c->main()));
+      SKS_TRY(ensure(c, c->cig, sizeof(int32_t) * std::max<int64_t>(b->nnz, 1)));
+      SKS_CK(c, launch_remap_cols(b->nnz, b->ci, c->cig.as<int32_t>(), c->nranks, c->rbd.as<int64_t>(), b->maxn,
+                                  c->main()));
+      b->ci = c->cig.as<int32_t>();
+      SKS_TRY(ensure(c, c->xg, sizeof(double) * (size_t)b->maxn * c->nranks));
+      // every column must be readable up to maxn rows for the all-gather
+      if (b->maxn > g.ld) return fail(c, SKS_EINVAL, "internal: maxn > ld");
+    }
+    SKS_CK(c, cudaStreamSynchronize(c->main()));  // host CSR arrays may be freed after return
+  }
+  SKS_CK(c, cudaMemsetAsync(c->part.p, 0, c->part.bytes, c->main()));
+  return SKS_OK;
+}
+
+// partial-slot pointer (ping-pong)
+static double* pslot(sks_ctx* c, const Basis& b, DevBuf& buf, int j) {
+  return buf.as<double>() + (size_t)(j & 1) * b.pslots * SKS_NP;
+}
+
+// first column: mode 1 (w_0 = f - A x) or mode 2 (w_0 = v), into W[:,0]; partials in slot 0
+static sks_status first_column(sks_ctx* c, Basis& b, int mode, const double* xvec, const double* fvec) {
+  cudaStream_t st = c->main();
+  const Geo& g = b.g;
+  double* p0 = pslot(c, b, c->part, 0);
+  if (g.kind != SKS_OP_CSR) {
+    StepArgs a = b.sa;
+    a.mode = mode;
+    a.j = 0;
+    a.xin = xvec;
+    a.fin = fvec;
+    a.partials_out = p0;
+    a.partials_in = nullptr;
+    a.grid_prev = 0;
+    SKS_CK(c, launch_step_stencil(a, b.step_grid, st));
+    ++c->launches;
+    b.bytes += 8.0 * g.n * (mode == 1 ? 3 : 2);
+  } else {
+    if (mode == 1) {
+      const double* xg = nullptr;
+      SKS_TRY(csr_gather(c, g, xvec, &xg, b.maxn));
+      SKS_CK(c, launch_csr_spmv(g.n, b.rp, b.ci, b.va, xg, colp(c, b, 0), fvec, 1, nullptr, 0, 0, 0, b.k, p0,
+                                b.step_grid, st));
+    } else {
+      SKS_CK(c, launch_copy_norm(g.n, xvec, colp(c, b, 0), p0, b.step_grid, st));
+    }
+    ++c->launches;
+    b.bytes += (mode == 1) ? 12.0 * b.nnz + 4.0 * (g.n + 1) + 8.0 * 3 * g.n : 16.0 * g.n;
+  }
+  SKS_TRY(allreduce_sum(c, p0, (size_t)b.pslots * SKS_NP, st));
+  SKS_TRY(halo_exchange(c, g, colp(c, b, 0)));
+  ++b.steps;
+  return SKS_OK;
+}
+
+// produce column j >= 1
+static sks_status step_column(sks_ctx* c, Basis& b, int j) {
+  cudaStream_t st = c->main();
+  const Geo& g = b.g;
+  const int grid_prev = c->nranks > 1 ? b.pslots : b.step_grid;
+  const int nwin = std::min(b.k, j);
+  if (g.kind != SKS_OP_CSR) {
+    StepArgs a = b.sa;
+    a.mode = 0;
+    a.j = j;
+    a.partials_in = pslot(c, b, c->part, j - 1);
+    a.grid_prev = grid_prev;
+    a.partials_out = pslot(c, b, c->part, j);
+    SKS_CK(c, launch_step_stencil(a, b.step_grid, st));
+    ++c->launches;
+    SKS_TRY(allreduce_sum(c, a.partials_out, (size_t)b.pslots * SKS_NP, st));
+    SKS_TRY(halo_exchange(c, g, colp(c, b, j)));
+    b.bytes += 8.0 * g.n * (nwin + 1);
+  } else {
+    const int lo = std::max(0, j - b.k), nw = j - lo;
+    const double* xg = nullptr;
+    SKS_TRY(csr_gather(c, g, colp(c, b, j - 1), &xg, b.maxn));
+    double* pd = c->part2.as<double>();  // spmv partials (single slot)
+    SKS_CK(c, launch_csr_spmv(g.n, b.rp, b.ci, b.va, xg, c->mr.as<double>(), nullptr, 0, c->W.as<double>(), g.ld,
+                              lo, nw, b.k, pd, b.step_grid, st, c->ctrl.as<CtrlBlock>()));
+    SKS_TRY(allreduce_sum(c, pd, (size_t)b.pslots * SKS_NP, st));
+    SKS_CK(c, launch_csr_orth(g.n, j, b.k, c->W.as<double>(), g.ld, c->mr.as<double>(), pslot(c, b, c->part, j - 1),
+                              grid_prev, pd, grid_prev, pslot(c, b, c->part, j), c->sigma.as<double>(),
+                              c->H.as<double>(), b.ldH, c->mnorm.as<double>(), c->ctrl.as<CtrlBlock>(),
+                              b.step_grid, st));
+    SKS_TRY(allreduce_sum(c, pslot(c, b, c->part, j), (size_t)b.pslots * SKS_NP, st));
+    c->launches += 2;
+    b.bytes += 12.0 * b.nnz + 4.0 * (g.n + 1) + 8.0 * g.n * (nwin + 1);
+  }
+  ++b.steps;
+  return SKS_OK;
+}
+
+// ||v||_2 of this rank's interior, reduced over ranks, returned on the host (syncs)
+static sks_status global_norm(sks_ctx* c, Basis& b, const double* v_interior, double* out) {
+  cudaStream_t st = c->main();
+  double* p = c->tmp.as<double>();
+  SKS_CK(c, launch_copy_norm(b.g.n, v_interior, c->vb.as<double>() + b.g.off, p, b.step_grid, st));
+  ++c->launches;
+  // copy_norm writes [grid][SKS_NP] with slot 0
+  SKS_CK(c, launch_sum_partials(p, b.step_grid, SKS_NP, 1, c->small.as<double>(), st));
+  ++c->launches;
+  SKS_TRY(allreduce_sum(c, c->small.as<double>(), 1, st));
+  SKS_CK(c, cudaMemcpyAsync(c->h_small, c->small.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+  SKS_CK(c, cudaStreamSynchronize(st));
+  *out = std::sqrt(c->h_small[0]);
+  return SKS_OK;
+}
+
+// sketch columns [c0, c0+J) of W into SW (s x ncol, column-major), reduced over ranks
+static sks_status sketch_cols(sks_ctx* c, Basis& b, int c0, int J, int s, int zeta, uint64_t key,
+                              cudaStream_t st) {
+  const Geo& g = b.g;
+  const int grid = sketch_grid(c->num_sms, g.n);
+  double* out = c->SW.as<double>() + (int64_t)c0 * s;
+  SKS_CK(c, launch_sketch(colp(c, b, c0) + g.off, g.ld, g.n, g.row_begin, J, s, zeta, key, c->partsk.as<double>(),
+                          grid, out, s, 0, st, &c->launches));
+  SKS_TRY(allreduce_sum(c, out, (size_t)J * s, st));
+  return SKS_OK;
+}
+
+// append sketched columns [j0, j0+J) to the thin QR (mode 0: SAB via recurrence; 1: SB)
+static sks_status qr_append(sks_ctx* c, Basis& b, int mode, int j0, int J, int s, int track_res, int max_cols,
+                            cudaStream_t st) {
+  double* X = c->Xp.as<double>();
+  double* Z = c->Zb.as<double>();
+  double* U = c->U.as<double>();
+  double* T = c->T.as<double>();
+  const int ldT = b.ncol;
+  SKS_CK(c, launch_form_cols(mode, c->SW.as<double>(), s, j0, J, b.k, c->H.as<double>(), b.ldH,
+                             c->sigma.as<double>(), X, J, 1, st));
+  SKS_CK(c, launch_utx(U, s, s, j0, X, J, Z, T, ldT, j0, 0, st));
+  SKS_CK(c, launch_xmuz(U, s, s, j0, X, J, Z, st));
+  SKS_CK(c, launch_utx(U, s, s, j0, X, J, Z, T, ldT, j0, 1, st));
+  SKS_CK(c, launch_xmuz(U, s, s, j0, X, J, Z, st));
+  SKS_CK(c, launch_panel(X, s, J, j0, U, s, T, ldT, c->rvec.as<double>(), c->rho.as<double>(), c->rest.as<double>(),
+                         c->ctrl.as<CtrlBlock>(), track_res, max_cols, st));
+  c->launches += (j0 > 0) ? 6 : 2;
+  return SKS_OK;
+}
+
+static sks_status setup_small(sks_ctx* c, Basis& b, int s, int JB) {
+  const int ncol = b.ncol;
+  SKS_TRY(ensure(c, c->SW, sizeof(double) * (size_t)s * (ncol + 1)));
+  const int grid = sketch_grid(c->num_sms, b.g.n);
+  SKS_TRY(ensure(c, c->partsk, sizeof(double) * sketch_part_doubles(grid, SKS_JB, s)));
+  SKS_TRY(ensure(c, c->Xp, sizeof(double) * (size_t)s * JB));
+  SKS_TRY(ensure(c, c->Zb, sizeof(double) * (size_t)(ncol + 1) * JB));
+  SKS_TRY(ensure(c, c->U, sizeof(double) * (size_t)s * (ncol + 1)));
+  SKS_TRY(ensure(c, c->T, sizeof(double) * (size_t)(ncol + 1) * (ncol + 1)));
+  SKS_TRY(ensure(c, c->rvec, sizeof(double) * s));
+  SKS_TRY(ensure(c, c->rho, sizeof(double) * (ncol + 1)));
+  SKS_TRY(ensure(c, c->rest, sizeof(double) * (ncol + 1)));
+  SKS_TRY(ensure(c, c->coef, sizeof(double) * (ncol + 1)));
+  SKS_TRY(ensure(c, c->tmp, sizeof(double) * (size_t)std::max(b.pslots, 64) * SKS_NP * 2));
+  if (panel_smem(s, JB) > 227 * 1024) return fail(c, SKS_EUNSUPPORTED, "s too large for the panel kernel");
+  return SKS_OK;
+}
+
+static int panel_jb(int s, int want) {
+  int J = std::min(want, SKS_JB);
+  while (J > 1 && panel_smem(s, J) > 200 * 1024) --J;
+  return J;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------
+// sGMRES
+// ------------------------------------------------------------------------------------
+extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const double* f, double* x,
+                                       const sks_sgmres_opts* o, sks_sgmres_info* info, double* hist,
+                                       int64_t hist_cap, double* hist_true, int64_t hist_true_cap) {
+  if (!c) return SKS_EINVAL;
+  c->err.clear();
+  if (!A || !f || !x || !o) return fail(c, SKS_EINVAL, "NULL argument");
+  const int d = o->d, k = o->k, s = o->s, zeta = o->zeta;
+  if (d < 1 || k < 1 || k > SKS_KMAX || s < d + 1 || s > SKS_SMAX || zeta < 1 || zeta > std::min(s, SKS_ZETA_MAX))
+    return fail(c, SKS_EINVAL, "need d>=1, 1<=k<=8, d+1<=s<=2048, 1<=zeta<=min(s,16)");
+  if (!(o->tol >= 0.0) || o->max_cycles < 1) return fail(c, SKS_EINVAL, "bad tol / max_cycles");
+  cudaSetDevice(c->device);
+  const int64_t launches0 = c->launches;
+  cudaStream_t st = c->main();
+  Basis b;
+  SKS_TRY(setup_basis(c, A, k, d + 2, &b));
+  const Geo& g = b.g;
+  const int JB = panel_jb(s, o->sketch_batch > 0 ? o->sketch_batch : SKS_JB);
+  SKS_TRY(setup_small(c, b, s, JB));
+  const double cond_tol = o->cond_tol > 0 ? o->cond_tol : 1e14;
+
+  SKS_CK(c, cudaEventRecord(c->ev_t0, st));
+  // inputs into ghost-layout buffers
+  double* xb = c->xb.as<double>();
+  double* fb = c->fb.as<double>();
+  SKS_CK(c, cudaMemsetAsync(xb, 0, sizeof(double) * g.ld, st));
+  SKS_CK(c, cudaMemsetAsync(fb, 0, sizeof(double) * g.ld, st));
+  SKS_CK(c, cudaMemcpyAsync(xb + g.off, x, sizeof(double) * g.n, cudaMemcpyDefault, st));
+  SKS_CK(c, cudaMemcpyAsync(fb + g.off, f, sizeof(double) * g.n, cudaMemcpyDefault, st));
+  SKS_TRY(halo_exchange(c, g, xb));
+  SKS_TRY(halo_exchange(c, g, fb));
+  double fnorm = 0.0;
+  SKS_TRY(global_norm(c, b, fb + g.off, &fnorm));
+  if (!(fnorm >= 0.0) || !std::isfinite(fnorm)) return fail(c, SKS_EINVAL, "f is not finite");
+  const double thr = o->early_exit_factor > 0 ? o->early_exit_factor * o->tol * fnorm : -1.0;
+
+  int cycles = 0, columns = 0, generated = 0, flags = 0;
+  int64_t nh = 0, nht = 0;
+  double rel = 1.0, r_est_last = NAN, cond_last = 1.0;
+  float t_basis_ms = 0.f;
+  double bytes_basis_total = 0.0;
+  sks_status result = SKS_ENOTCONV;
+  CtrlBlock* dctrl = c->ctrl.as<CtrlBlock>();
+  CtrlBlock* hc = c->h_ctrl;
+
+  for (int cyc = 0; cyc <= o->max_cycles; ++cyc) {
+    // ---- residual r = f - A x  (w_0), true residual of the previous cycle
+    SKS_CK(c, launch_ctrl_reset(dctrl, thr, fnorm, st));
+    ++c->launches;
+    b.bytes = 0;  // per-cycle accounting of the basis loop below
+    SKS_TRY(first_column(c, b, 1, xb, fb));
+    SKS_CK(c, launch_sum_partials(pslot(c, b, c->part, 0), c->nranks > 1 ? b.pslots : b.step_grid, SKS_NP, 1,
+                                  c->small.as<double>(), st));
+    ++c->launches;
+    SKS_CK(c, cudaMemcpyAsync(c->h_small, c->small.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    SKS_CK(c, cudaStreamSynchronize(st));
+    const double rnorm = std::sqrt(c->h_small[0]);
+    rel = fnorm > 0 ? rnorm / fnorm : 0.0;
+    if (cyc > 0) {
+      if (hist_true && nht < hist_true_cap) hist_true[nht] = rel;
+      ++nht;
+    }
+    if (rel <= o->tol || rnorm == 0.0) {
+      result = SKS_OK;
+      break;
+    }
+    if (cyc == o->max_cycles) break;
+    ++cycles;
+    const uint64_t key = sks_key(o->seed, (uint32_t)cyc);
+    // ---- basis loop (main) with batched sketch + incremental QR (side)
+    const double bytes_first = b.bytes;
+    SKS_CK(c, cudaEventRecord(c->ev_b0, st));
+    int next_sk = 0;    // next column to sketch
+    int next_qr = 0;    // next SAB column to append
+    int nbatch = 0;
+    int last_col = d;   // columns 0..d are generated (d+1 columns)
+    SKS_CK(c, cudaMemsetAsync(c->rvec.p, 0, sizeof(double) * s, st));
+    auto enqueue_side = [&](int upto /* columns [0, upto) are complete */, bool final_) -> sks_status {
+      SKS_CK(c, cudaEventRecord(c->ev_fork, st));
+      SKS_CK(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+      while (next_sk < upto) {
+        const int J = std::min(JB, upto - next_sk);
+        SKS_TRY(sketch_cols(c, b, next_sk, J, s, zeta, key, c->side));
+        if (next_sk == 0) {  // g = S r = S w_0 starts the residual vector
+          SKS_CK(c, cudaMemcpyAsync(c->rvec.p, c->SW.p, sizeof(double) * s, cudaMemcpyDeviceToDevice, c->side));
+        }
+        next_sk += J;
+      }
+      // SAB column jj needs SW[:, jj+1]
+      const int qr_upto = std::min(next_sk - 1, d);
+      while (next_qr < qr_upto) {
+        const int J = std::min(JB, qr_upto - next_qr);
+        SKS_TRY(qr_append(c, b, 0, next_qr, J, s, 1, d, c->side));
+        next_qr += J;
+      }
+      SKS_CK(c, cudaMemcpyAsync(hc, dctrl, sizeof(CtrlBlock), cudaMemcpyDeviceToHost, c->side));
+      if (nbatch < (int)c->ev_batch.size()) SKS_CK(c, cudaEventRecord(c->ev_batch[nbatch], c->side));
+      ++nbatch;
+      (void)final_;
+      return SKS_OK;
+    };
+    int batch_size = std::min(8, JB);
+    int pending_upto = 0;
+    for (int j = 1; j <= d; ++j) {
+      SKS_TRY(step_column(c, b, j));
+      const bool batch_done = (j + 1 - pending_upto >= batch_size) || j == d;
+      if (batch_done) {
+        SKS_TRY(enqueue_side(j + 1, j == d));
+        pending_upto = j + 1;
+        batch_size = std::min(JB, batch_size * 2);
+        // poll the early-exit / breakdown flags of batch nbatch-2 (bounded lag)
+        if (nbatch >= 2 && nbatch - 2 < (int)c->ev_batch.size()) {
+          SKS_CK(c, cudaEventSynchronize(c->ev_batch[nbatch - 2]));
+          if (hc->exit_cols > 0 || hc->stop_col < INT_MAX || hc->rank_def) {
+            last_col = j;
+            break;
+          }
+        }
+      }
+    }
+    SKS_CK(c, cudaEventRecord(c->ev_b1, st));
+    // remaining side work for everything generated, then join
+    if (next_sk < last_col + 1) SKS_TRY(enqueue_side(last_col + 1, true));
+    SKS_CK(c, cudaEventRecord(c->ev_join, c->side));
+    SKS_CK(c, cudaStreamWaitEvent(st, c->ev_join, 0));
+    SKS_CK(c, cudaMemcpyAsync(hc, dctrl, sizeof(CtrlBlock), cudaMemcpyDeviceToHost, st));
+    SKS_CK(c, cudaStreamSynchronize(st));
+    {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, c->ev_b0, c->ev_b1);
+      t_basis_ms += ms;
+    }
+    bytes_basis_total += b.bytes - bytes_first;
+    generated += last_col + 1;
+    int jstar;
+    if (hc->exit_cols > 0) {
+      jstar = hc->exit_cols;
+    } else {
+      int dmax = d;
+      if (hc->stop_col < INT_MAX) dmax = std::min(dmax, hc->stop_col);
+      jstar = std::min(dmax, hc->qr_cols);
+    }
+    if (hc->breakdown) flags |= SKS_WARN_BREAKDOWN;
+    if (jstar <= 0) {  // nothing usable (r == 0 handled above); stop
+      break;
+    }
+    // ---- yhat = T^-1 (U^T g), coef = sigma .* yhat ; x += W coef
+    SKS_CK(c, launch_trsv(c->T.as<double>(), b.ncol, jstar, c->rho.as<double>(), c->sigma.as<double>(), nullptr,
+                          c->coef.as<double>(), st));
+    int* ncp = reinterpret_cast<int*>(c->small.as<double>() + 16);
+    c->h_small[32] = 0;
+    reinterpret_cast<int*>(c->h_small + 32)[0] = jstar;
+    SKS_CK(c, cudaMemcpyAsync(ncp, c->h_small + 32, sizeof(int), cudaMemcpyHostToDevice, st));
+    SKS_CK(c, launch_assemble(xb, c->W.as<double>(), g.ld, g.off, g.n, c->coef.as<double>(), ncp, jstar,
+                              c->num_sms, st));
+    SKS_CK(c, launch_cond(c->T.as<double>(), b.ncol, jstar, 12, nullptr, c->small.as<double>() + 8, st));
+    c->launches += 3;
+    SKS_TRY(halo_exchange(c, g, xb));
+    // history: r_est,j / ||f||
+    SKS_CK(c, cudaMemcpyAsync(c->h_small + 64, c->rest.p, sizeof(double) * std::min(jstar, 2048),
+                              cudaMemcpyDeviceToHost, st));
+    SKS_CK(c, cudaMemcpyAsync(c->h_small + 40, c->small.as<double>() + 8, sizeof(double), cudaMemcpyDeviceToHost,
+                              st));
+    SKS_CK(c, cudaStreamSynchronize(st));
+    for (int j = 0; j < jstar && j < 2048; ++j) {
+      if (hist && nh < hist_cap) hist[nh] = c->h_small[64 + j] / (fnorm > 0 ? fnorm : 1.0);
+      ++nh;
+    }
+    r_est_last = c->h_small[64 + jstar - 1] / (fnorm > 0 ? fnorm : 1.0);
+    cond_last = c->h_small[40];
+    if (cond_last > cond_tol) flags |= SKS_WARN_COND;
+    columns += jstar;
+  }
+  SKS_CK(c, cudaMemcpyAsync(x, xb + g.off, sizeof(double) * g.n, cudaMemcpyDefault, st));
+  SKS_CK(c, cudaEventRecord(c->ev_t1, st));
+  SKS_CK(c, cudaStreamSynchronize(st));
+  SKS_CK(c, cudaGetLastError());
+  if (info) {
+    memset(info, 0, sizeof(*info));
+    info->cycles = cycles;
+    info->columns = columns;
+    info->columns_generated = generated;
+    info->flags = flags;
+    info->rel_res_true = rel;
+    info->r_est = r_est_last;
+    info->cond_T = cond_last;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev_t0, c->ev_t1);
+    info->t_total_s = ms * 1e-3;
+    info->t_basis_s = t_basis_ms * 1e-3;
+    info->bytes_basis = bytes_basis_total;
+    info->kernel_launches = c->launches - launches0;
+    info->steps = b.steps;
+  }
+  return result;
+}
+
+// ------------------------------------------------------------------------------------
+// sRR (Alg. 2)
+// ------------------------------------------------------------------------------------
+namespace {
+
+// run the basis loop for columns 1..d with the sketch batches on the side stream (no QR)
+static sks_status basis_and_sketch(sks_ctx* c, Basis& b, int d, int s, int zeta, uint64_t key, int JB,
+                                   bool do_sketch, float* t_basis_ms) {
+  cudaStream_t st = c->main();
+  int next_sk = 0;
+  SKS_CK(c, cudaEventRecord(c->ev_b0, st));
+  auto side = [&](int upto) -> sks_status {
+    if (!do_sketch) return SKS_OK;
+    SKS_CK(c, cudaEventRecord(c->ev_fork, st));
+    SKS_CK(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    while (next_sk < upto) {
+      const int J = std::min(JB, upto - next_sk);
+      SKS_TRY(sketch_cols(c, b, next_sk, J, s, zeta, key, c->side));
+      next_sk += J;
+    }
+    return SKS_OK;
+  };
+  int pending = 0;
+  for (int j = 1; j <= d; ++j) {
+    SKS_TRY(step_column(c, b, j));
+    if (j + 1 - pending >= JB || j == d) {
+      SKS_TRY(side(j + 1));
+      pending = j + 1;
+    }
+  }
+  SKS_CK(c, cudaEventRecord(c->ev_b1, st));
+  if (do_sketch) {
+    SKS_CK(c, cudaEventRecord(c->ev_join, c->side));
+    SKS_CK(c, cudaStreamWaitEvent(st, c->ev_join, 0));
+  }
+  SKS_CK(c, cudaMemcpyAsync(c->h_ctrl, c->ctrl.p, sizeof(CtrlBlock), cudaMemcpyDeviceToHost, st));
+  SKS_CK(c, cudaStreamSynchronize(st));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, c->ev_b0, c->ev_b1);
+  if (t_basis_ms) *t_basis_ms += ms;
+  return SKS_OK;
+}
+
+}  // namespace
+
+extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const double* v0, const sks_srr_opts* o,
+                                   int32_t nev, int32_t nev_cap, double* theta_re, double* theta_im,
+                                   double* res_true, double* res_est, double* X_re, double* X_im,
+                                   sks_srr_info* info) {
+  if (!c) return SKS_EINVAL;
+  c->err.clear();
+  if (!A || !v0 || !o || !theta_re || !theta_im) return fail(c, SKS_EINVAL, "NULL argument");
+  const int d = o->d, k = o->k, s = o->s, zeta = o->zeta;
+  if (d < 2 || k < 1 || k > SKS_KMAX || s < d + 1 || s > SKS_SMAX || zeta < 1 || zeta > std::min(s, SKS_ZETA_MAX))
+    return fail(c, SKS_EINVAL, "need d>=2, 1<=k<=8, d+1<=s<=2048, 1<=zeta<=min(s,16)");
+  if (nev < 1 || nev > 11 || nev > d || nev_cap < nev + 1) return fail(c, SKS_EINVAL, "need 1<=nev<=min(11,d), nev_cap>=nev+1");
+  cudaSetDevice(c->device);
+  const int64_t launches0 = c->launches;
+  cudaStream_t st = c->main();
+  Basis b;
+  SKS_TRY(setup_basis(c, A, k, d + 2, &b));
+  const Geo& g = b.g;
+  const int JB = panel_jb(s, SKS_JB);
+  SKS_TRY(setup_small(c, b, s, JB));
+  const int nmax = nev + 1;
+  SKS_CK(c, cudaEventRecord(c->ev_t0, st));
+  double* vb = c->vb.as<double>();
+  SKS_CK(c, cudaMemsetAsync(vb, 0, sizeof(double) * g.ld, st));
+  SKS_CK(c, cudaMemcpyAsync(vb + g.off, v0, sizeof(double) * g.n, cudaMemcpyDefault, st));
+  SKS_TRY(halo_exchange(c, g, vb));
+  SKS_CK(c, launch_ctrl_reset(c->ctrl.as<CtrlBlock>(), -1.0, 0.0, st));
+  ++c->launches;
+  SKS_TRY(first_column(c, b, 2, g.kind == SKS_OP_CSR ? vb + g.off : vb, nullptr));
+  const uint64_t key = sks_key(o->seed, 0u);
+  float t_basis_ms = 0.f;
+  const double bytes0 = b.bytes;
+  SKS_TRY(basis_and_sketch(c, b, d, s, zeta, key, JB, true, &t_basis_ms));
+  const double bytes_basis = b.bytes - bytes0;
+  CtrlBlock* hc = c->h_ctrl;
+  int de = d;
+  int flags = 0;
+  if (hc->stop_col < INT_MAX) {
+    de = std::min(d, hc->stop_col);
+    flags |= SKS_WARN_BREAKDOWN;
+  }
+  if (de < 2) return fail(c, SKS_EINVAL, "basis broke down before 2 columns");
+  cudaEvent_t ev_s0 = c->ev_b0, ev_s1 = c->ev_b1;
+  SKS_CK(c, cudaEventRecord(ev_s0, st));
+  // ---- QR of SB[:, :de]
+  for (int j0 = 0; j0 < de; j0 += JB) {
+    const int J = std::min(JB, de - j0);
+    SKS_TRY(qr_append(c, b, 1, j0, J, s, 0, de, st));
+  }
+  // ---- t = T^-1 U^T S w_de ; Mhat = Hbar[:de,:de] + t e_{de}^T
+  SKS_CK(c, launch_form_cols(2, c->SW.as<double>(), s, de, 1, k, c->H.as<double>(), b.ldH, c->sigma.as<double>(),
+                             c->Xp.as<double>(), 1, 1, st));
+  SKS_CK(c, launch_utx(c->U.as<double>(), s, s, de, c->Xp.as<double>(), 1, c->Zb.as<double>(), nullptr, 0, 0, 0, st));
+  SKS_CK(c, launch_trsv(c->T.as<double>(), b.ncol, de, c->Zb.as<double>(), nullptr, nullptr, c->coef.as<double>(), st));
+  SKS_TRY(ensure(c, c->Mh, sizeof(double) * (size_t)de * de));
+  SKS_TRY(ensure(c, c->Mh2, sizeof(double) * (size_t)de * de));
+  SKS_CK(c, launch_build_mhat(c->H.as<double>(), b.ldH, de, c->coef.as<double>(), c->Mh.as<double>(), st));
+  SKS_CK(c, cudaMemcpyAsync(c->Mh2.p, c->Mh.p, sizeof(double) * (size_t)de * de, cudaMemcpyDeviceToDevice, st));
+  SKS_TRY(ensure(c, c->wr, sizeof(double) * de));
+  SKS_TRY(ensure(c, c->wi, sizeof(double) * de));
+  SKS_TRY(ensure(c, c->sel, sizeof(int) * 64, true));
+  SKS_TRY(ensure(c, c->th, sizeof(double) * 64));
+  int* d_info = c->sel.as<int>() + 32;
+  int* d_nsel = c->sel.as<int>() + 31;
+  SKS_CK(c, cudaMemsetAsync(d_info, 0, sizeof(int), st));
+  SKS_CK(c, launch_hqr(c->Mh2.as<double>(), de, de, c->wr.as<double>(), c->wi.as<double>(), d_info, st));
+  double* th_re = c->th.as<double>();
+  double* th_im = th_re + 32;
+  SKS_CK(c, launch_select(c->wr.as<double>(), c->wi.as<double>(), de, nev, c->sel.as<int>(), d_nsel, th_re, th_im,
+                          st));
+  SKS_TRY(ensure(c, c->ework, sizeof(double) * inverse_iteration_work_doubles(de, nmax)));
+  SKS_TRY(ensure(c, c->yr, sizeof(double) * (size_t)de * nmax, true));
+  SKS_TRY(ensure(c, c->yi, sizeof(double) * (size_t)de * nmax, true));
+  SKS_CK(c, cudaMemsetAsync(c->yr.p, 0, sizeof(double) * (size_t)de * nmax, st));
+  SKS_CK(c, cudaMemsetAsync(c->yi.p, 0, sizeof(double) * (size_t)de * nmax, st));
+  SKS_CK(c, launch_inverse_iteration(c->Mh.as<double>(), de, th_re, th_im, d_nsel, nmax, c->ework.as<double>(),
+                                     c->yr.as<double>(), c->yi.as<double>(), 3, 0.0, st));
+  // ---- sketched residual estimate with explicit C = SB, D = SAB
+  SKS_TRY(ensure(c, c->SAB, sizeof(double) * (size_t)s * de));
+  SKS_TRY(ensure(c, c->SB, sizeof(double) * (size_t)s * de));
+  SKS_CK(c, launch_form_cols(0, c->SW.as<double>(), s, 0, de, k, c->H.as<double>(), b.ldH, c->sigma.as<double>(),
+                             c->SAB.as<double>(), 1, s, st));
+  SKS_CK(c, launch_form_cols(1, c->SW.as<double>(), s, 0, de, k, c->H.as<double>(), b.ldH, c->sigma.as<double>(),
+                             c->SB.as<double>(), 1, s, st));
+  double* d_rest = c->small.as<double>() + 128;
+  SKS_CK(c, launch_srr_rest(c->SAB.as<double>(), c->SB.as<double>(), s, de, c->yr.as<double>(), c->yi.as<double>(),
+                            th_re, th_im, d_nsel, nmax, d_rest, st));
+  SKS_CK(c, launch_cond(c->T.as<double>(), b.ncol, de, 12, nullptr, c->small.as<double>() + 8, st));
+  SKS_CK(c, cudaEventRecord(ev_s1, st));
+  c->launches += 14;
+  // ---- Ritz vectors x_i = B y_i and true residuals ||A x - theta x|| / ||x||
+  SKS_TRY(ensure(c, c->Xr, sizeof(double) * (size_t)g.ld * nmax, true));
+  SKS_TRY(ensure(c, c->Xi, sizeof(double) * (size_t)g.ld * nmax, true));
+  SKS_CK(c, launch_ritz_vectors(c->W.as<double>(), g.ld, g.off, g.n, de, c->sigma.as<double>(), c->yr.as<double>(),
+                                c->yi.as<double>(), de, nmax, c->Xr.as<double>(), c->Xi.as<double>(), g.ld, g.off,
+                                c->num_sms, st));
+  ++c->launches;
+  const int rgrid = c->num_sms * 2;
+  double* rpart = c->tmp.as<double>();
+  SKS_TRY(ensure(c, c->tmp, sizeof(double) * (size_t)rgrid * nmax * 2 + 64));
+  rpart = c->tmp.as<double>();
+  if (g.kind != SKS_OP_CSR) {
+    for (int v = 0; v < nmax; ++v) {
+      SKS_TRY(halo_exchange(c, g, c->Xr.as<double>() + (int64_t)v * g.ld));
+      SKS_TRY(halo_exchange(c, g, c->Xi.as<double>() + (int64_t)v * g.ld));
+    }
+    SKS_CK(c, launch_ritz_residual_stencil(g.dim, g.m, g.nz, g.plane, g.off, g.ld, g.cc, g.cm, g.cp, nmax,
+                                           c->Xr.as<double>(), c->Xi.as<double>(), th_re, th_im, rpart, rgrid, st));
+    ++c->launches;
+  } else {
+    SKS_TRY(ensure(c, c->AXr, sizeof(double) * (size_t)g.ld * nmax));
+    SKS_TRY(ensure(c, c->AXi, sizeof(double) * (size_t)g.ld * nmax));
+    for (int v = 0; v < nmax; ++v) {
+      for (int part = 0; part < 2; ++part) {
+        const double* src = (part ? c->Xi : c->Xr).as<double>() + (int64_t)v * g.ld;
+        double* dst = (part ? c->AXi : c->AXr).as<double>() + (int64_t)v * g.ld;
+        const double* xg = nullptr;
+        SKS_TRY(csr_gather(c, g, src, &xg, b.maxn));
+        SKS_CK(c, launch_csr_spmv(g.n, b.rp, b.ci, b.va, xg, dst, nullptr, 0, nullptr, 0, 0, 0, k,
+                                  c->part2.as<double>(), b.step_grid, st));
+        ++c->launches;
+      }
+    }
+    SKS_CK(c, launch_complex_residual(g.n, c->AXr.as<double>(), c->AXi.as<double>(), c->Xr.as<double>(),
+                                      c->Xi.as<double>(), g.ld, g.ld, nmax, th_re, th_im, rpart, rgrid, st));
+    ++c->launches;
+  }
+  double* rsum = c->small.as<double>() + 256;
+  SKS_CK(c, launch_sum_partials(rpart, rgrid, nmax * 2, nmax * 2, rsum, st));
+  ++c->launches;
+  SKS_TRY(allreduce_sum(c, rsum, (size_t)nmax * 2, st));
+  SKS_CK(c, cudaEventRecord(c->ev_t1, st));
+  // ---- outputs
+  double* hs = c->h_small;
+  SKS_CK(c, cudaMemcpyAsync(hs, c->small.p, sizeof(double) * 512, cudaMemcpyDeviceToHost, st));
+  SKS_CK(c, cudaMemcpyAsync(hs + 512, c->th.p, sizeof(double) * 64, cudaMemcpyDeviceToHost, st));
+  SKS_CK(c, cudaMemcpyAsync(hs + 576, c->sel.p, sizeof(int) * 64, cudaMemcpyDeviceToHost, st));
+  SKS_CK(c, cudaStreamSynchronize(st));
+  SKS_CK(c, cudaGetLastError());
+  const int* hsel = reinterpret_cast<const int*>(hs + 576);
+  const int nsel = hsel[31];
+  const int hinfo = hsel[32];
+  if (hinfo != 0) return fail(c, SKS_ENOTCONV, "QR algorithm did not converge on Mhat");
+  for (int v = 0; v < nsel; ++v) {
+    theta_re[v] = hs[512 + v];
+    theta_im[v] = hs[512 + 32 + v];
+    if (res_est) res_est[v] = hs[128 + v];
+    if (res_true) res_true[v] = std::sqrt(hs[256 + 2 * v] / hs[256 + 2 * v + 1]);
+  }
+  if (X_re && X_im) {
+    for (int v = 0; v < nsel; ++v) {
+      SKS_CK(c, cudaMemcpyAsync(X_re + (int64_t)v * g.n, c->Xr.as<double>() + (int64_t)v * g.ld + g.off,
+                                sizeof(double) * g.n, cudaMemcpyDefault, st));
+      SKS_CK(c, cudaMemcpyAsync(X_im + (int64_t)v * g.n, c->Xi.as<double>() + (int64_t)v * g.ld + g.off,
+                                sizeof(double) * g.n, cudaMemcpyDefault, st));
+    }
+    SKS_CK(c, cudaStreamSynchronize(st));
+  }
+  if (info) {
+    memset(info, 0, sizeof(*info));
+    info->columns = de;
+    info->flags = flags | (hs[8] > (o->cond_tol > 0 ? o->cond_tol : 1e14) ? SKS_WARN_COND : 0);
+    info->nev_out = nsel;
+    info->cond_SB = hs[8];
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev_t0, c->ev_t1);
+    info->t_total_s = ms * 1e-3;
+    info->t_basis_s = t_basis_ms * 1e-3;
+    cudaEventElapsedTime(&ms, ev_s0, ev_s1);
+    info->t_small_s = ms * 1e-3;
+    info->bytes_basis = bytes_basis;
+    info->kernel_launches = c->launches - launches0;
+    info->steps = b.steps;
+  }
+  return SKS_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// test / parity entry points
+// ------------------------------------------------------------------------------------
+extern "C" sks_status sks_sketch_apply(sks_ctx* c, int64_t n_global, int64_t row_begin, int64_t row_end, int32_t s,
+                                       int32_t zeta, uint64_t seed, uint32_t cycle, const double* M, int64_t ldm,
+                                       int32_t cc, double* SM) {
+  if (!c) return SKS_EINVAL;
+  c->err.clear();
+  const int64_t n = row_end - row_begin;
+  if (!M || !SM || n <= 0 || row_begin < 0 || row_end > n_global || cc < 1 || ldm < n || s < 1 || s > SKS_SMAX ||
+      zeta < 1 || zeta > std::min<int>(s, SKS_ZETA_MAX))
+    return fail(c, SKS_EINVAL, "bad sketch_apply arguments");
+  cudaSetDevice(c->device);
+  cudaStream_t st = c->main();
+  const int64_t ldd = (n + 1) / 2 * 2;
+  SKS_TRY(ensure(c, c->tmp, sizeof(double) * (size_t)ldd * cc));
+  SKS_TRY(ensure(c, c->SAB, sizeof(double) * (size_t)s * cc));
+  const int grid = sketch_grid(c->num_sms, n);
+  SKS_TRY(ensure(c, c->partsk, sizeof(double) * sketch_part_doubles(grid, SKS_JB, s)));
+  SKS_CK(c, cudaMemcpy2DAsync(c->tmp.p, sizeof(double) * ldd, M, sizeof(double) * ldm, sizeof(double) * n, cc,
+                              cudaMemcpyDefault, st));
+  const uint64_t key = sks_key(seed, cycle);
+  for (int c0 = 0; c0 < cc; c0 += SKS_JB) {
+    const int J = std::min(SKS_JB, cc - c0);
+    SKS_CK(c, launch_sketch(c->tmp.as<double>() + (int64_t)c0 * ldd, ldd, n, row_begin, J, s, zeta, key,
+                            c->partsk.as<double>(), grid, c->SAB.as<double>() + (int64_t)c0 * s, s, 0, st,
+                            &c->launches));
+  }
+  SKS_TRY(allreduce_sum(c, c->SAB.as<double>(), (size_t)s * cc, st));
+  SKS_CK(c, cudaMemcpyAsync(SM, c->SAB.p, sizeof(double) * (size_t)s * cc, cudaMemcpyDefault, st));
+  SKS_CK(c, cudaStreamSynchronize(st));
+  return SKS_OK;
+}
+
+extern "C" sks_status sks_sketch_table(sks_ctx* c, int64_t row_begin, int64_t count, int32_t s, int32_t zeta,
+                                       uint64_t seed, uint32_t cycle, int32_t* q, int8_t* sign) {
+  if (!c) return SKS_EINVAL;
+  c->err.clear();
+  if (!q || !sign || count < 0 || s < 1 || zeta < 1 || zeta > std::min<int>(s, SKS_ZETA_MAX))
+    return fail(c, SKS_EINVAL, "bad sketch_table arguments");
+  if (count == 0) return SKS_OK;
+  cudaSetDevice(c->device);
+  cudaStream_t st = c->main();
+  SKS_TRY(ensure(c, c->cig, sizeof(int32_t) * (size_t)count * zeta));
+  SKS_TRY(ensure(c, c->tmp, sizeof(int8_t) * (size_t)count * zeta));
+  SKS_CK(c, launch_sketch_table(row_begin, count, s, zeta, sks_key(seed, cycle), c->cig.as<int32_t>(),
+                                c->tmp.as<int8_t>(), st));
+  SKS_CK(c, cudaMemcpyAsync(q, c->cig.p, sizeof(int32_t) * (size_t)count * zeta, cudaMemcpyDefault, st));
+  SKS_CK(c, cudaMemcpyAsync(sign, c->tmp.p, sizeof(int8_t) * (size_t)count * zeta, cudaMemcpyDefault, st));
+  SKS_CK(c, cudaStreamSynchronize(st));
+  return SKS_OK;
+}
+
+extern "C" sks_status sks_apply_operator(sks_ctx* c, const sks_operator* A, const double* x, double* y) {
+  if (!c) return SKS_EINVAL;
+  c->err.clear();
+  if (!A || !x || !y) return fail(c, SKS_EINVAL, "NULL argument");
+  cudaSetDevice(c->device);
+  cudaStream_t st = c->main();
+  Basis b;
+  SKS_TRY(setup_basis(c, A, 2, 2, &b));
+  const Geo& g = b.g;
+  double* xb = c->xb.as<double>();
+  double* yb = c->vb.as<double>();
+  SKS_CK(c, cudaMemsetAsync(xb, 0, sizeof(double) * g.ld, st));
+  SKS_CK(c, cudaMemcpyAsync(xb + g.off, x, sizeof(double) * g.n, cudaMemcpyDefault, st));
+  if (g.kind != SKS_OP_CSR) {
+    SKS_TRY(halo_exchange(c, g, xb));
+    SKS_CK(c, launch_apply_stencil(g.dim, g.m, g.nz, g.plane, g.off, g.cc, g.cm, g.cp, xb, yb, c->num_sms, st));
+  } else {
+    const double* xg = nullptr;
+    SKS_TRY(csr_gather(c, g, xb, &xg, b.maxn));
+    SKS_CK(c, launch_csr_spmv(g.n, b.rp, b.ci, b.va, xg, yb, nullptr, 0, nullptr, 0, 0, 0, 2, c->part2.as<double>(),
+                              b.step_grid, st));
+  }
+  ++c->launches;
+  SKS_CK(c, cudaMemcpyAsync(y, yb + g.off, sizeof(double) * g.n, cudaMemcpyDefault, st));
+  SKS_CK(c, cudaStreamSynchronize(st));
+  return SKS_OK;
+}
+
+extern "C" sks_status sks_basis(sks_ctx* c, const sks_operator* A, const double* r0, int32_t k, int32_t ncols,
+                                double* B_out, double* H_out) {
+  if (!c) return SKS_EINVAL;
+  c->err.clear();
+  if (!A || !r0 || !B_out || ncols < 1 || k < 1 || k > SKS_KMAX) return fail(c, SKS_EINVAL, "bad sks_basis arguments");
+  cudaSetDevice(c->device);
+  cudaStream_t st = c->main();
+  Basis b;
+  SKS_TRY(setup_basis(c, A, k, ncols + 2, &b));
+  const Geo& g = b.g;
+  SKS_TRY(ensure(c, c->tmp, sizeof(double) * (size_t)std::max<int64_t>(g.n * ncols, 4096)));
+  double* vb = c->vb.as<double>();
+  SKS_CK(c, cudaMemsetAsync(vb, 0, sizeof(double) * g.ld, st));
+  SKS_CK(c, cudaMemcpyAsync(vb + g.off, r0, sizeof(double) * g.n, cudaMemcpyDefault, st));
+  SKS_TRY(halo_exchange(c, g, vb));
+  SKS_CK(c, launch_ctrl_reset(c->ctrl.as<CtrlBlock>(), -1.0, 0.0, st));
+  ++c->launches;
+  SKS_TRY(first_column(c, b, 2, g.kind == SKS_OP_CSR ? vb + g.off : vb, nullptr));
+  SKS_TRY(basis_and_sketch(c, b, ncols, 0, 0, 0, SKS_JB, false, nullptr));
+  SKS_CK(c, launch_scale_cols(c->W.as<double>(), g.ld, g.off, g.n, ncols, c->sigma.as<double>(), c->tmp.as<double>(),
+                              g.n, st));
+  ++c->launches;
+  SKS_CK(c, cudaMemcpyAsync(B_out, c->tmp.p, sizeof(double) * (size_t)g.n * ncols, cudaMemcpyDefault, st));
+  if (H_out && ncols >= 2)
+    SKS_CK(c, cudaMemcpy2DAsync(H_out, sizeof(double) * ncols, c->H.p, sizeof(double) * b.ldH,
+                                sizeof(double) * ncols, ncols - 1, cudaMemcpyDefault, st));
+  SKS_CK(c, cudaStreamSynchronize(st));
+  if (c->h_ctrl->stop_col < ncols) {
+    c->err = "breakdown at column " + std::to_string(c->h_ctrl->stop_col);
+    return SKS_OK;  // columns past the breakdown are not meaningful (flagged via sks_last_error)
+  }
+  return SKS_OK;
+}

@@ -1,0 +1,498 @@
+// eig.cu -- the small nonsymmetric eigenproblem of sRR on the device (Alg. 2 P:1683:
+// "Solve eigenvalue problem T^-1 U^* D y_i = lambda_i y_i"; "the QR algorithm").
+//
+//  * build_mhat: Mhat = T^-1 U^T SAB.  With a Krylov basis the paper notes Mhat and the
+//    recurrence matrix "differ only in the final column":  since
+//    S m_j = sum_{i<=j+1} Hbar[i,j] S b_i, and T^-1 U^T S b_i = e_i for i < d,
+//        Mhat = Hbar[:d, :d] + e_{d-1}-column correction  nu_d T^-1 U^T S b_d,
+//    so Mhat is upper Hessenberg by construction (no Hessenberg reduction needed).
+//  * hqr: Francis double-shift QR iteration on the Hessenberg matrix, eigenvalues only
+//    (one CTA; the scalar bulge set-up on thread 0, row/column updates spread over the
+//    block).
+//  * inverse iteration per selected eigenvalue on (Mhat - theta I) in complex arithmetic
+//    (Hessenberg LU with partial pivoting), one CTA per eigenvalue, giving y_i.
+//  * sketched residual estimate  ||D y - theta C y|| / ||C y||  (Eq. srr-resid-est).
+#include "common.cuh"
+#include "internal.h"
+
+namespace sks {
+
+// Mhat (d x d column-major, ld = d): Hbar[:d,:d] (+ last column += t)
+__global__ void build_mhat_kernel(const double* __restrict__ H, int ldH, int d, const double* __restrict__ t,
+                                  double* __restrict__ Mh) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= d * d) return;
+  const int i = idx % d, j = idx / d;
+  double v = (i <= j + 1) ? H[i + (int64_t)j * ldH] : 0.0;
+  if (j == d - 1) v += t[i];
+  Mh[idx] = v;
+}
+
+#define HA(i, j) a[(i) + (int64_t)(j) * lda]
+
+__global__ void __launch_bounds__(256) hqr_kernel(double* __restrict__ a, int n, int lda, double* __restrict__ wr,
+                                                  double* __restrict__ wi, int* __restrict__ info) {
+  __shared__ double red[32];
+  __shared__ double sp, sq, sr, sx, sy, sz, sw, st;
+  __shared__ int sl, snn, sm, sflag, sits, sdone;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  // anorm
+  double loc = 0.0;
+  for (int64_t idx = tid; idx < (int64_t)n * n; idx += nt) {
+    const int i = (int)(idx % n), j = (int)(idx / n);
+    if (j >= i - 1) loc += fabs(HA(i, j));
+  }
+  const double anorm = block_sum(loc, red);
+  if (tid == 0) {
+    snn = n - 1;
+    st = 0.0;
+    sdone = 0;
+  }
+  __syncthreads();
+  while (true) {
+    if (snn < 0) break;
+    if (tid == 0) sits = 0;
+    __syncthreads();
+    while (true) {
+      // --- scalar part: find small subdiagonal, deflate or set up a double-shift sweep
+      if (tid == 0) {
+        int nn = snn, l;
+        for (l = nn; l >= 1; --l) {
+          double s = fabs(HA(l - 1, l - 1)) + fabs(HA(l, l));
+          if (s == 0.0) s = anorm;
+          if (fabs(HA(l, l - 1)) + s == s) {
+            HA(l, l - 1) = 0.0;
+            break;
+          }
+        }
+        if (l < 0) l = 0;
+        double x = HA(nn, nn);
+        sflag = 0;
+        if (l == nn) {
+          wr[nn] = x + st;
+          wi[nn] = 0.0;
+          snn = nn - 1;
+        } else {
+          double y = HA(nn - 1, nn - 1);
+          double w = HA(nn, nn - 1) * HA(nn - 1, nn);
+          if (l == nn - 1) {
+            double p = 0.5 * (y - x);
+            double q = p * p + w;
+            double z = sqrt(fabs(q));
+            x += st;
+            if (q >= 0.0) {
+              z = p + copysign(z, p);
+              wr[nn - 1] = wr[nn] = x + z;
+              if (z != 0.0) wr[nn] = x - w / z;
+              wi[nn - 1] = wi[nn] = 0.0;
+            } else {
+              wr[nn - 1] = wr[nn] = x + p;
+              wi[nn] = z;
+              wi[nn - 1] = -z;
+            }
+            snn = nn - 2;
+          } else {
+            if (sits >= 60) {
+              info[0] = 1;  // no convergence
+              sdone = 1;
+            } else {
+              if (sits > 0 && sits % 10 == 0) {  // exceptional shift
+                sflag = 2;
+                sx = x;
+              } else {
+                sflag = 1;
+              }
+              sx = x;
+              sy = y;
+              sw = w;
+            }
+          }
+        }
+        sl = l;
+      }
+      __syncthreads();
+      if (sdone) break;
+      if (sflag == 0) {  // deflated
+        const int nn = snn, l = sl;
+        __syncthreads();
+        if (!(l < nn - 1)) break;  // leave inner loop (reset iteration count)
+        continue;
+      }
+      if (sflag == 2) {
+        const double x = sx;
+        for (int i = tid; i <= snn; i += nt) HA(i, i) -= x;
+        __syncthreads();
+        if (tid == 0) {
+          const int nn = snn;
+          st += x;
+          double s = fabs(HA(nn, nn - 1)) + fabs(HA(nn - 1, nn - 2));
+          sx = sy = 0.75 * s;
+          sw = -0.4375 * s * s;
+        }
+        __syncthreads();
+      }
+      // choose m and the first Householder vector
+      if (tid == 0) {
+        sits = sits + 1;
+        const int nn = snn, l = sl;
+        const double x = sx, y = sy, w = sw;
+        int m;
+        double p = 0, q = 0, r = 0, z;
+        for (m = nn - 2; m >= l; --m) {
+          z = HA(m, m);
+          r = x - z;
+          double s = y - z;
+          p = (r * s - w) / HA(m + 1, m) + HA(m, m + 1);
+          q = HA(m + 1, m + 1) - z - r - s;
+          r = HA(m + 2, m + 1);
+          s = fabs(p) + fabs(q) + fabs(r);
+          p /= s;
+          q /= s;
+          r /= s;
+          if (m == l) break;
+          const double u = fabs(HA(m, m - 1)) * (fabs(q) + fabs(r));
+          const double v = fabs(p) * (fabs(HA(m - 1, m - 1)) + fabs(z) + fabs(HA(m + 1, m + 1)));
+          if (u + v == v) break;
+        }
+        sm = m;
+        sp = p;
+        sq = q;
+        sr = r;
+      }
+      __syncthreads();
+      {
+        const int nn = snn, m = sm;
+        for (int i = m + 2 + tid; i <= nn; i += nt) {
+          HA(i, i - 2) = 0.0;
+          if (i != m + 2) HA(i, i - 3) = 0.0;
+        }
+      }
+      __syncthreads();
+      const int nn = snn, l = sl, m = sm;
+      for (int k = m; k <= nn - 1; ++k) {
+        if (tid == 0) {
+          double p = sp, q = sq, r = sr, x = 0.0;
+          int doit = 0;
+          if (k != m) {
+            p = HA(k, k - 1);
+            q = HA(k + 1, k - 1);
+            r = 0.0;
+            if (k != nn - 1) r = HA(k + 2, k - 1);
+            x = fabs(p) + fabs(q) + fabs(r);
+            if (x != 0.0) {
+              p /= x;
+              q /= x;
+              r /= x;
+            }
+          }
+          const double s = copysign(sqrt(p * p + q * q + r * r), p);
+          if (s != 0.0) {
+            if (k == m) {
+              if (l != m) HA(k, k - 1) = -HA(k, k - 1);
+            } else {
+              HA(k, k - 1) = -s * x;
+            }
+            p += s;
+            sx = p / s;
+            sy = q / s;
+            sz = r / s;
+            sq = q / p;
+            sr = r / p;
+            doit = 1;
+          }
+          sflag = doit;
+        }
+        __syncthreads();
+        if (sflag) {
+          const double x = sx, y = sy, z = sz, q = sq, r = sr;
+          const bool three = (k != nn - 1);
+          for (int jj = k + tid; jj <= nn; jj += nt) {  // row transformation
+            double p = HA(k, jj) + q * HA(k + 1, jj);
+            if (three) {
+              p += r * HA(k + 2, jj);
+              HA(k + 2, jj) -= p * z;
+            }
+            HA(k + 1, jj) -= p * y;
+            HA(k, jj) -= p * x;
+          }
+          __syncthreads();
+          const int mmin = nn < k + 3 ? nn : k + 3;
+          for (int i = l + tid; i <= mmin; i += nt) {  // column transformation
+            double p = x * HA(i, k) + y * HA(i, k + 1);
+            if (three) {
+              p += z * HA(i, k + 2);
+              HA(i, k + 2) -= p * r;
+            }
+            HA(i, k + 1) -= p * q;
+            HA(i, k) -= p;
+          }
+        }
+        __syncthreads();
+      }
+      {
+        const int nn2 = snn, l2 = sl;
+        __syncthreads();
+        if (!(l2 < nn2 - 1)) break;
+      }
+    }
+    if (sdone) break;
+  }
+}
+
+// pick the nev largest |theta| (ties: Im descending, O23) and a split conjugate partner
+__global__ void select_kernel(const double* __restrict__ wr, const double* __restrict__ wi, int n, int nev,
+                              int* __restrict__ sel, int* __restrict__ nsel, double* __restrict__ th_re,
+                              double* __restrict__ th_im) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int cnt = 0;
+  const int want = min(nev, n);
+  for (int c = 0; c < want + 1 && c < n; ++c) {
+    int best = -1;
+    double bm = -1.0, bi = 0.0;
+    for (int i = 0; i < n; ++i) {
+      bool used = false;
+      for (int t = 0; t < cnt; ++t) used |= (sel[t] == i);
+      if (used) continue;
+      const double mg = hypot(wr[i], wi[i]);
+      if (best < 0 || mg > bm || (mg == bm && wi[i] > bi)) {
+        best = i;
+        bm = mg;
+        bi = wi[i];
+      }
+    }
+    if (c < want) {
+      sel[cnt++] = best;
+    } else {
+      // position nev splits a conjugate pair?
+      const int last = sel[cnt - 1];
+      if (wi[last] != 0.0 && best >= 0 && fabs(wr[best] - wr[last]) <= 1e-12 * fabs(wr[last]) &&
+          fabs(wi[best] + wi[last]) <= 1e-12 * fabs(wi[last]))
+        sel[cnt++] = best;
+    }
+  }
+  *nsel = cnt;
+  for (int t = 0; t < cnt; ++t) {
+    th_re[t] = wr[sel[t]];
+    th_im[t] = wi[sel[t]];
+  }
+}
+
+struct cplx {
+  double r, i;
+};
+__device__ __forceinline__ cplx cmul(cplx a, cplx b) { return {a.r * b.r - a.i * b.i, a.r * b.i + a.i * b.r}; }
+__device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
+  const double s = fabs(b.r) + fabs(b.i);
+  const double ar = a.r / s, ai = a.i / s, br = b.r / s, bi = b.i / s;
+  const double d = br * br + bi * bi;
+  return {(ar * br + ai * bi) / d, (ai * br - ar * bi) / d};
+}
+__device__ __forceinline__ double cabs1(cplx a) { return fabs(a.r) + fabs(a.i); }
+
+// One CTA per selected eigenvalue v: complex Hessenberg LU of (Mhat - theta I) with
+// partial pivoting, then `iters` inverse-iteration solves.  Output y (d complex, unit
+// 2-norm, largest-modulus entry real positive) in yr/yi[:, v] (ld = d).
+__global__ void __launch_bounds__(256) inverse_iteration_kernel(const double* __restrict__ Mh, int d,
+                                                                const double* __restrict__ th_re,
+                                                                const double* __restrict__ th_im,
+                                                                const int* __restrict__ nsel, double* __restrict__ work,
+                                                                double* __restrict__ yr, double* __restrict__ yi,
+                                                                int iters, double anorm) {
+  const int v = blockIdx.x;
+  if (v >= *nsel) return;
+  extern __shared__ double smv[];
+  cplx* b = reinterpret_cast<cplx*>(smv);  // d
+  __shared__ double red[32];
+  __shared__ cplx piv_l;
+  __shared__ int swp;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  // work layout: [A: nmax*d*d complex][L: nmax*d complex][perm: nmax*d int]
+  const int64_t nmax = gridDim.x;
+  cplx* A = reinterpret_cast<cplx*>(work) + (int64_t)v * d * d;  // column-major d x d
+  cplx* L = reinterpret_cast<cplx*>(work) + nmax * d * d + (int64_t)v * d;
+  int* perm = reinterpret_cast<int*>(reinterpret_cast<cplx*>(work) + nmax * d * d + nmax * d) + (int64_t)v * d;
+  const cplx th = {th_re[v], th_im[v]};
+  for (int64_t idx = tid; idx < (int64_t)d * d; idx += nt) {
+    const int i = (int)(idx % d), j = (int)(idx / d);
+    cplx e = {(i <= j + 1) ? Mh[idx] : 0.0, 0.0};
+    if (i == j) {
+      e.r -= th.r;
+      e.i -= th.i;
+    }
+    A[idx] = e;
+  }
+  __syncthreads();
+  double amax = 0.0;
+  for (int64_t idx = tid; idx < (int64_t)d * d; idx += nt) amax = fmax(amax, cabs1(A[idx]));
+  for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  if ((tid & 31) == 0) red[tid >> 5] = amax;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (nt + 31) / 32; ++w) t = fmax(t, red[w]);
+    red[0] = t;
+  }
+  __syncthreads();
+  const double tiny = 1e-15 * fmax(anorm, red[0]) + 1e-300;
+  __syncthreads();
+  // LU: for k, pivot rows k / k+1, eliminate row k+1
+  for (int k = 0; k < d - 1; ++k) {
+    if (tid == 0) {
+      cplx akk = A[k + (int64_t)k * d], ak1 = A[k + 1 + (int64_t)k * d];
+      int s = cabs1(ak1) > cabs1(akk) ? 1 : 0;
+      if (s) {
+        cplx t = akk;
+        akk = ak1;
+        ak1 = t;
+      }
+      if (cabs1(akk) == 0.0) akk = {tiny, 0.0};
+      swp = s;
+      piv_l = cdiv(ak1, akk);
+      perm[k] = s;
+      L[k] = piv_l;
+    }
+    __syncthreads();
+    const int s = swp;
+    const cplx lk = piv_l;
+    for (int j = k + tid; j < d; j += nt) {
+      cplx r0 = A[k + (int64_t)j * d], r1 = A[k + 1 + (int64_t)j * d];
+      if (s) {
+        cplx t = r0;
+        r0 = r1;
+        r1 = t;
+      }
+      if (j == k && cabs1(r0) == 0.0) r0 = {tiny, 0.0};
+      const cplx pr = cmul(lk, r0);
+      r1.r -= pr.r;
+      r1.i -= pr.i;
+      A[k + (int64_t)j * d] = r0;
+      A[k + 1 + (int64_t)j * d] = (j == k) ? cplx{0.0, 0.0} : r1;
+    }
+    __syncthreads();
+  }
+  if (tid == 0 && cabs1(A[(d - 1) + (int64_t)(d - 1) * d]) == 0.0) A[(d - 1) + (int64_t)(d - 1) * d] = {tiny, 0.0};
+  for (int i = tid; i < d; i += nt) b[i] = {1.0 / (1.0 + 0.37 * (i % 11)), 0.0};
+  __syncthreads();
+  for (int it = 0; it < iters; ++it) {
+    if (tid == 0) {
+      // forward: apply P and L
+      for (int k = 0; k < d - 1; ++k) {
+        if (perm[k]) {
+          cplx t = b[k];
+          b[k] = b[k + 1];
+          b[k + 1] = t;
+        }
+        const cplx pr = cmul(L[k], b[k]);
+        b[k + 1].r -= pr.r;
+        b[k + 1].i -= pr.i;
+      }
+    }
+    __syncthreads();
+    // backward: U y = b (column-oriented)
+    for (int i = d - 1; i >= 0; --i) {
+      if (tid == 0) b[i] = cdiv(b[i], A[i + (int64_t)i * d]);
+      __syncthreads();
+      const cplx yi_ = b[i];
+      for (int l = tid; l < i; l += nt) {
+        const cplx pr = cmul(A[l + (int64_t)i * d], yi_);
+        b[l].r -= pr.r;
+        b[l].i -= pr.i;
+      }
+      __syncthreads();
+    }
+    // normalise
+    double loc = 0.0;
+    for (int i = tid; i < d; i += nt) loc += b[i].r * b[i].r + b[i].i * b[i].i;
+    const double nr = sqrt(block_sum(loc, red));
+    for (int i = tid; i < d; i += nt) {
+      b[i].r /= nr;
+      b[i].i /= nr;
+    }
+    __syncthreads();
+  }
+  // canonical phase: largest-modulus entry real positive
+  if (tid == 0) {
+    int im = 0;
+    double bm = -1.0;
+    for (int i = 0; i < d; ++i) {
+      const double mg = b[i].r * b[i].r + b[i].i * b[i].i;
+      if (mg > bm) {
+        bm = mg;
+        im = i;
+      }
+    }
+    const double mg = sqrt(bm);
+    piv_l = {b[im].r / mg, -b[im].i / mg};  // conj phase
+  }
+  __syncthreads();
+  const cplx ph = piv_l;
+  for (int i = tid; i < d; i += nt) {
+    const cplx z = cmul(b[i], ph);
+    yr[i + (int64_t)v * d] = z.r;
+    yi[i + (int64_t)v * d] = (th.i == 0.0) ? 0.0 : z.i;
+  }
+}
+
+// r_est[v] = ||D y - theta C y|| / ||C y||, D = SAB (s x d, col-major), C = SB
+__global__ void srr_rest_kernel(const double* __restrict__ D, const double* __restrict__ C, int s, int d,
+                                const double* __restrict__ yr, const double* __restrict__ yi,
+                                const double* __restrict__ th_re, const double* __restrict__ th_im,
+                                const int* __restrict__ nsel, double* __restrict__ rest) {
+  const int v = blockIdx.x;
+  if (v >= *nsel) return;
+  __shared__ double red[64];
+  const double a = th_re[v], b = th_im[v];
+  double sr = 0.0, sc = 0.0;
+  for (int q = threadIdx.x; q < s; q += blockDim.x) {
+    double dr = 0, di = 0, cr = 0, ci = 0;
+    for (int j = 0; j < d; ++j) {
+      const double dd = D[q + (int64_t)j * s], cc = C[q + (int64_t)j * s];
+      const double y0 = yr[j + (int64_t)v * d], y1 = yi[j + (int64_t)v * d];
+      dr += dd * y0;
+      di += dd * y1;
+      cr += cc * y0;
+      ci += cc * y1;
+    }
+    // D y - theta C y
+    const double rr = dr - (a * cr - b * ci);
+    const double ri = di - (a * ci + b * cr);
+    sr += rr * rr + ri * ri;
+    sc += cr * cr + ci * ci;
+  }
+  double t[2] = {sr, sc}, o[2];
+  block_sum_n<2>(t, red, o);
+  if (threadIdx.x == 0) rest[v] = sqrt(o[0]) / sqrt(o[1]);
+}
+
+// ------------------------------------------------------------------------------
+cudaError_t launch_build_mhat(const double* H, int ldH, int d, const double* t, double* Mh, cudaStream_t st) {
+  build_mhat_kernel<<<(d * d + 255) / 256, 256, 0, st>>>(H, ldH, d, t, Mh);
+  return cudaGetLastError();
+}
+cudaError_t launch_hqr(double* a, int n, int lda, double* wr, double* wi, int* info, cudaStream_t st) {
+  hqr_kernel<<<1, 256, 0, st>>>(a, n, lda, wr, wi, info);
+  return cudaGetLastError();
+}
+cudaError_t launch_select(const double* wr, const double* wi, int n, int nev, int* sel, int* nsel, double* th_re,
+                          double* th_im, cudaStream_t st) {
+  select_kernel<<<1, 1, 0, st>>>(wr, wi, n, nev, sel, nsel, th_re, th_im);
+  return cudaGetLastError();
+}
+size_t inverse_iteration_work_doubles(int d, int nmax) {
+  return (size_t)nmax * d * d * 2 + (size_t)nmax * d * 2 + ((size_t)nmax * d + 1) / 2 + 16;
+}
+cudaError_t launch_inverse_iteration(const double* Mh, int d, const double* th_re, const double* th_im,
+                                     const int* nsel, int nmax, double* work, double* yr, double* yi, int iters,
+                                     double anorm, cudaStream_t st) {
+  inverse_iteration_kernel<<<nmax, 256, sizeof(double) * 2 * d, st>>>(Mh, d, th_re, th_im, nsel, work, yr, yi,
+                                                                       iters, anorm);
+  return cudaGetLastError();
+}
+cudaError_t launch_srr_rest(const double* D, const double* C, int s, int d, const double* yr, const double* yi,
+                            const double* th_re, const double* th_im, const int* nsel, int nmax, double* rest,
+                            cudaStream_t st) {
+  srr_rest_kernel<<<nmax, 256, 0, st>>>(D, C, s, d, yr, yi, th_re, th_im, nsel, rest);
+  return cudaGetLastError();
+}
+
+}  // namespace sks

@@ -1,0 +1,85 @@
+// internal.h -- host-side launchers shared between the kernel files and the driver.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <algorithm>
+
+struct StepArgs;
+struct CtrlBlock;
+
+namespace sks {
+
+// stencil.cu
+int step_km(int k);
+cudaError_t launch_step_stencil(const StepArgs& a, int grid, cudaStream_t st);
+void stencil_tiling(int dim, int64_t m, int64_t nz, int num_sms, StepArgs* a, int* grid);
+cudaError_t launch_apply_stencil(int dim, int64_t m, int64_t nz, int64_t plane, int64_t off, double cc, double cm,
+                                 double cp, const double* x, double* y, int num_sms, cudaStream_t st);
+cudaError_t launch_ritz_residual_stencil(int dim, int64_t m, int64_t nz, int64_t plane, int64_t off, int64_t ld,
+                                         double cc, double cm, double cp, int nvec, const double* Xr,
+                                         const double* Xi, const double* thr, const double* thi, double* partials,
+                                         int grid, cudaStream_t st);
+
+// sketch.cu
+int sketch_grid(int num_sms, int64_t nrows);
+size_t sketch_part_doubles(int grid, int J, int s);
+cudaError_t launch_sketch(const double* M, int64_t ldm, int64_t nrows, int64_t row_begin, int J, int s, int zeta,
+                          uint64_t key, double* part, int grid, double* out, int64_t ldo, int accumulate,
+                          cudaStream_t st, int64_t* launches);
+cudaError_t launch_sketch_table(int64_t row_begin, int64_t count, int s, int zeta, uint64_t key, int32_t* q,
+                                int8_t* sign, cudaStream_t st);
+
+// smallside.cu
+cudaError_t launch_form_cols(int mode, const double* SW, int s, int j0, int J, int k, const double* H, int ldH,
+                             const double* sigma, double* X, int64_t ldq, int64_t ldj, cudaStream_t st);
+cudaError_t launch_utx(const double* U, int ldu, int s, int j0, const double* X, int J, double* Z, double* T,
+                       int ldT, int tc0, int tacc, cudaStream_t st);
+cudaError_t launch_xmuz(const double* U, int ldu, int s, int j0, double* X, int J, const double* Z,
+                        cudaStream_t st);
+size_t panel_smem(int s, int J);
+cudaError_t launch_panel(double* X, int s, int J, int j0, double* U, int ldu, double* T, int ldT, double* rvec,
+                         double* rho, double* rest, CtrlBlock* ctrl, int track_res, int max_cols,
+                         cudaStream_t st);
+cudaError_t launch_trsv(const double* T, int ldT, int n, const double* b, const double* scale, double* yout,
+                        double* out, cudaStream_t st);
+cudaError_t launch_cond(const double* T, int ldT, int n, int iters, CtrlBlock* ctrl, double* out,
+                        cudaStream_t st);
+cudaError_t launch_assemble(double* x, const double* W, int64_t ld, int64_t off, int64_t n, const double* coef,
+                            const int* ncp, int nc_max, int num_sms, cudaStream_t st);
+cudaError_t launch_ritz_vectors(const double* W, int64_t ld, int64_t off, int64_t n, int nc, const double* sigma,
+                                const double* yr, const double* yi, int ldy, int nvec, double* Xr, double* Xi,
+                                int64_t ldx, int64_t xoff, int num_sms, cudaStream_t st);
+cudaError_t launch_scale_cols(const double* W, int64_t ld, int64_t off, int64_t n, int nc, const double* sigma,
+                              double* out, int64_t ldo, cudaStream_t st);
+cudaError_t launch_complex_residual(int64_t n, const double* Axr, const double* Axi, const double* xr,
+                                    const double* xi, int64_t ldx, int64_t ldax, int nvec, const double* thr,
+                                    const double* thi, double* partials, int grid, cudaStream_t st);
+cudaError_t launch_sum_partials(const double* part, int grid, int stride, int ncomp, double* out, cudaStream_t st);
+cudaError_t launch_ctrl_reset(CtrlBlock* c, double thr, double fnorm, cudaStream_t st);
+cudaError_t launch_remap_cols(int64_t nnz, const int32_t* ci_global, int32_t* ci_out, int nranks,
+                              const int64_t* rb_dev, int64_t maxn, cudaStream_t st);
+
+// eig.cu
+cudaError_t launch_build_mhat(const double* H, int ldH, int d, const double* t, double* Mh, cudaStream_t st);
+cudaError_t launch_hqr(double* a, int n, int lda, double* wr, double* wi, int* info, cudaStream_t st);
+cudaError_t launch_select(const double* wr, const double* wi, int n, int nev, int* sel, int* nsel, double* th_re,
+                          double* th_im, cudaStream_t st);
+size_t inverse_iteration_work_doubles(int d, int nmax);
+cudaError_t launch_inverse_iteration(const double* Mh, int d, const double* th_re, const double* th_im,
+                                     const int* nsel, int nmax, double* work, double* yr, double* yi, int iters,
+                                     double anorm, cudaStream_t st);
+cudaError_t launch_srr_rest(const double* D, const double* C, int s, int d, const double* yr, const double* yi,
+                            const double* th_re, const double* th_im, const int* nsel, int nmax, double* rest,
+                            cudaStream_t st);
+
+// csr.cu
+cudaError_t launch_csr_spmv(int64_t n, const int32_t* rp, const int32_t* ci, const double* va, const double* xg,
+                            double* out, const double* f, int mode, const double* W, int64_t ld, int lo, int nw,
+                            int k, double* partials, int grid, cudaStream_t st, const CtrlBlock* ctrl = nullptr);
+cudaError_t launch_csr_orth(int64_t n, int j, int k, double* W, int64_t ld, const double* mr, const double* pnorm,
+                            int grid_n, const double* pdot, int grid_s, double* partials, double* sigma, double* H,
+                            int ldH, double* mnorm, CtrlBlock* ctrl, int grid, cudaStream_t st);
+cudaError_t launch_copy_norm(int64_t n, const double* src, double* dst, double* partials, int grid,
+                             cudaStream_t st);
+
+}  // namespace sks

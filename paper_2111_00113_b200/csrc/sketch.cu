@@ -1,0 +1,281 @@
+// sketch.cu -- S M for a batch of up to 32 columns M (sparse sign map).
+//
+// Formulation: S is regenerated from the counter hash
+// (common.cuh) and never stored.  Each CTA owns a contiguous range of rows and walks it
+// in tiles of R rows.  Per tile:
+//   1. stage M[tile rows, 0..J) in shared memory as Mt[r][c] (row-major, 32 columns),
+//   2. hash the tile's rows -> zeta (q, sign) entries per row, counting-sort them by q
+//      (deterministic: buckets re-sorted by row),
+//   3. GATHER: warp w / lane c owns sketch rows q = w + 16 i and column c and keeps
+//      acc[i] = sum over its bucket entries of +-Mt[r][c] in REGISTERS.
+// The gather needs no atomics and reads shared memory conflict-free (a warp reads one
+// 256-byte row of Mt per entry).  Per-CTA partial sketches are summed in a fixed order
+// by a second kernel, so the result is bitwise reproducible.
+#include "common.cuh"
+#include "internal.h"
+
+namespace sks {
+
+constexpr int SK_R = 256;       // rows per tile
+constexpr int SK_THREADS = 512; // 16 warps
+constexpr int SK_WARPS = SK_THREADS / 32;
+
+struct SketchArgs {
+  const double* M;   // column c at M + c*ldm
+  int64_t ldm;
+  int64_t nrows;     // local rows
+  int64_t row_begin; // global index of local row 0
+  int J;             // columns in this batch (<= 32)
+  int s, zeta;
+  int q_base;        // first sketch row handled by this pass
+  uint64_t key;
+  double scale;      // 1/sqrt(zeta)
+  double* part;      // [grid][J][s] partial sketches (this pass writes q in [q_base, q_base+16*QPW))
+  int64_t tiles;     // ceil(nrows / SK_R)
+  int vec_ok;        // 16-byte vector loads allowed
+};
+
+template <int QPW, int ZETA>
+__global__ void __launch_bounds__(SK_THREADS, 1) sketch_batch_kernel(SketchArgs a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  double* Mt = reinterpret_cast<double*>(smraw);                    // [SK_R][32]
+  int* cnt = reinterpret_cast<int*>(Mt + SK_R * 32);                // [s+1]
+  int* cur = cnt + (a.s + 1);                                       // [s]
+  uint16_t* tab = reinterpret_cast<uint16_t*>(cur + a.s);            // [SK_R * zeta] raw entries (q | neg<<15)
+  uint16_t* ent = tab + SK_R * SKS_ZETA_MAX;                         // [SK_R * zeta] sorted (r | neg<<15)
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int s = a.s;
+  const int zeta = ZETA > 0 ? ZETA : a.zeta;
+  double acc[QPW];
+#pragma unroll
+  for (int i = 0; i < QPW; ++i) acc[i] = 0.0;
+
+  const int64_t t_lo = (a.tiles * blockIdx.x) / gridDim.x;
+  const int64_t t_hi = (a.tiles * (blockIdx.x + 1)) / gridDim.x;
+  for (int64_t tile = t_lo; tile < t_hi; ++tile) {
+    const int64_t r0 = tile * SK_R;
+    const int nr = (int)((a.nrows - r0) < (int64_t)SK_R ? (a.nrows - r0) : (int64_t)SK_R);
+    // ---- 1. stage Mt
+    if (a.vec_ok) {
+      for (int idx = tid; idx < (SK_R / 4) * 32; idx += SK_THREADS) {
+        const int rq = idx >> 5, c = idx & 31;
+        const int r = rq * 4;
+        double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+        if (c < a.J) {
+          const double* src = a.M + (int64_t)c * a.ldm + r0 + r;
+          if (r + 3 < nr) {
+            const double2 p = __ldg(reinterpret_cast<const double2*>(src));
+            const double2 q = __ldg(reinterpret_cast<const double2*>(src + 2));
+            v0 = p.x; v1 = p.y; v2 = q.x; v3 = q.y;
+          } else {
+            if (r + 0 < nr) v0 = src[0];
+            if (r + 1 < nr) v1 = src[1];
+            if (r + 2 < nr) v2 = src[2];
+          }
+        }
+        Mt[(r + 0) * 32 + c] = v0;
+        Mt[(r + 1) * 32 + c] = v1;
+        Mt[(r + 2) * 32 + c] = v2;
+        Mt[(r + 3) * 32 + c] = v3;
+      }
+    } else {
+      for (int idx = tid; idx < SK_R * 32; idx += SK_THREADS) {
+        const int r = idx >> 5, c = idx & 31;
+        double v = 0.0;
+        if (c < a.J && r < nr) v = a.M[(int64_t)c * a.ldm + r0 + r];
+        Mt[idx] = v;
+      }
+    }
+    // ---- 2. hash + counting sort by sketch row
+    for (int q = tid; q <= s; q += SK_THREADS) cnt[q] = 0;
+    __syncthreads();
+    if (tid < nr) {
+      int qq[ZETA > 0 ? ZETA : SKS_ZETA_MAX];
+      uint32_t neg;
+      if (ZETA > 0)
+        sks_column<(ZETA > 0 ? ZETA : 1)>(a.key, (uint64_t)(a.row_begin + r0 + tid), s, qq, &neg);
+      else
+        sks_column_rt(a.key, (uint64_t)(a.row_begin + r0 + tid), s, zeta, qq, &neg);
+      for (int t = 0; t < zeta; ++t) {
+        atomicAdd(&cnt[qq[t]], 1);
+        tab[tid * zeta + t] = (uint16_t)(qq[t] | (((neg >> t) & 1u) << 15));
+      }
+    }
+    __syncthreads();
+    if (wid == 0) {  // exclusive scan of cnt[0..s) by one warp (s <= 2048)
+      int carry = 0;
+      for (int base = 0; base < s; base += 32) {
+        const int q = base + lane;
+        int v = q < s ? cnt[q] : 0;
+        int incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          int t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        if (q < s) {
+          cnt[q] = carry + incl - v;
+          cur[q] = carry + incl - v;
+        }
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (lane == 0) cnt[s] = carry;
+    }
+    __syncthreads();
+    if (tid < nr) {
+      for (int t = 0; t < zeta; ++t) {
+        const uint16_t e = tab[tid * zeta + t];
+        const int q = e & 0x7fff;
+        const int pos = atomicAdd(&cur[q], 1);
+        ent[pos] = (uint16_t)(tid | (e & 0x8000));
+      }
+    }
+    __syncthreads();
+    for (int q = tid; q < s; q += SK_THREADS) {  // deterministic order inside a bucket
+      const int b = cnt[q], e = cnt[q + 1];
+      for (int i = b + 1; i < e; ++i) {
+        const uint16_t key = ent[i];
+        int j = i - 1;
+        while (j >= b && (ent[j] & 0x7fff) > (key & 0x7fff)) {
+          ent[j + 1] = ent[j];
+          --j;
+        }
+        ent[j + 1] = key;
+      }
+    }
+    __syncthreads();
+    // ---- 3. gather into register accumulators
+#pragma unroll
+    for (int i = 0; i < QPW; ++i) {
+      const int q = a.q_base + wid + SK_WARPS * i;
+      if (q < s) {
+        const int b = cnt[q], e = cnt[q + 1];
+        double t0 = 0.0, t1 = 0.0;
+        int p = b;
+        for (; p + 1 < e; p += 2) {
+          const uint16_t e0 = ent[p], e1 = ent[p + 1];
+          const double x0 = Mt[(e0 & 0x7fff) * 32 + lane];
+          const double x1 = Mt[(e1 & 0x7fff) * 32 + lane];
+          t0 += (e0 & 0x8000) ? -x0 : x0;
+          t1 += (e1 & 0x8000) ? -x1 : x1;
+        }
+        if (p < e) {
+          const uint16_t e0 = ent[p];
+          const double x0 = Mt[(e0 & 0x7fff) * 32 + lane];
+          t0 += (e0 & 0x8000) ? -x0 : x0;
+        }
+        acc[i] += t0 + t1;
+      }
+    }
+    __syncthreads();
+  }
+  // ---- partial sketch of this CTA
+  if (lane < a.J) {
+#pragma unroll
+    for (int i = 0; i < QPW; ++i) {
+      const int q = a.q_base + wid + SK_WARPS * i;
+      if (q < s) a.part[((int64_t)blockIdx.x * a.J + lane) * s + q] = acc[i] * a.scale;
+    }
+  }
+}
+
+// out[c*ldo + q] (+)= sum_b part[b][c][q]  (fixed order over b)
+__global__ void sketch_reduce_kernel(const double* __restrict__ part, int grid, int J, int s,
+                                     double* __restrict__ out, int64_t ldo, int accumulate) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)J * s) return;
+  const int c = (int)(idx / s), q = (int)(idx % s);
+  double t = 0.0;
+  for (int b = 0; b < grid; ++b) t += part[((int64_t)b * J + c) * s + q];
+  if (accumulate) out[(int64_t)c * ldo + q] += t;
+  else out[(int64_t)c * ldo + q] = t;
+}
+
+__global__ void sketch_table_kernel(int64_t row_begin, int64_t count, int s, int zeta, uint64_t key,
+                                    int32_t* __restrict__ q, int8_t* __restrict__ sign) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= count) return;
+  int qq[SKS_ZETA_MAX];
+  uint32_t neg;
+  sks_column_rt(key, (uint64_t)(row_begin + r), s, zeta, qq, &neg);
+  for (int t = 0; t < zeta; ++t) {
+    q[r * zeta + t] = qq[t];
+    sign[r * zeta + t] = ((neg >> t) & 1u) ? (int8_t)-1 : (int8_t)1;
+  }
+}
+
+// ------------------------------------------------------------------------------
+static size_t sketch_smem(int s) {
+  return sizeof(double) * SK_R * 32 + sizeof(int) * (2 * s + 1) + 2 * sizeof(uint16_t) * SK_R * SKS_ZETA_MAX + 16;
+}
+
+template <int QPW, int ZETA>
+static cudaError_t launch_sk(const SketchArgs& a, int grid, cudaStream_t st) {
+  const size_t smem = sketch_smem(a.s);
+  static size_t set = 0;
+  if (set < smem) {
+    cudaError_t e = cudaFuncSetAttribute(sketch_batch_kernel<QPW, ZETA>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    set = smem;
+  }
+  sketch_batch_kernel<QPW, ZETA><<<grid, SK_THREADS, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int ZETA>
+static cudaError_t launch_sk_z(const SketchArgs& a, int qspan, int grid, cudaStream_t st) {
+  if (qspan <= 8 * SK_WARPS) return launch_sk<8, ZETA>(a, grid, st);
+  if (qspan <= 16 * SK_WARPS) return launch_sk<16, ZETA>(a, grid, st);
+  if (qspan <= 24 * SK_WARPS) return launch_sk<24, ZETA>(a, grid, st);
+  if (qspan <= 32 * SK_WARPS) return launch_sk<32, ZETA>(a, grid, st);
+  return launch_sk<40, ZETA>(a, grid, st);
+}
+
+int sketch_grid(int num_sms, int64_t nrows) {
+  int64_t tiles = (nrows + SK_R - 1) / SK_R;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, num_sms));
+}
+
+size_t sketch_part_doubles(int grid, int J, int s) { return (size_t)grid * J * s; }
+
+// SM[:, 0..J) (column-major, ld = ldo) = S_key M[:, 0..J) for rows [row_begin, row_begin+nrows)
+cudaError_t launch_sketch(const double* M, int64_t ldm, int64_t nrows, int64_t row_begin, int J, int s,
+                          int zeta, uint64_t key, double* part, int grid, double* out, int64_t ldo,
+                          int accumulate, cudaStream_t st, int64_t* launches) {
+  if (J < 1 || J > SKS_JB) return cudaErrorInvalidValue;
+  SketchArgs a;
+  a.M = M;
+  a.ldm = ldm;
+  a.nrows = nrows;
+  a.row_begin = row_begin;
+  a.J = J;
+  a.s = s;
+  a.zeta = zeta;
+  a.key = key;
+  a.scale = 1.0 / sqrt((double)zeta);
+  a.part = part;
+  a.tiles = (nrows + SK_R - 1) / SK_R;
+  a.vec_ok = ((((uintptr_t)M) & 15) == 0) && (ldm % 2 == 0);
+  const int span_max = 40 * SK_WARPS;
+  for (int qb = 0; qb < s; qb += span_max) {
+    a.q_base = qb;
+    const int span = std::min(span_max, s - qb);
+    cudaError_t e = (zeta == 8) ? launch_sk_z<8>(a, span, grid, st) : launch_sk_z<0>(a, span, grid, st);
+    if (e != cudaSuccess) return e;
+    if (launches) ++*launches;
+  }
+  const int64_t tot = (int64_t)J * s;
+  sketch_reduce_kernel<<<(int)((tot + 255) / 256), 256, 0, st>>>(part, grid, J, s, out, ldo, accumulate);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sketch_table(int64_t row_begin, int64_t count, int s, int zeta, uint64_t key, int32_t* q,
+                                int8_t* sign, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  sketch_table_kernel<<<(int)((count + 255) / 256), 256, 0, st>>>(row_begin, count, s, zeta, key, q, sign);
+  return cudaGetLastError();
+}
+
+}  // namespace sks

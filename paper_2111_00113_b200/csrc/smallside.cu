@@ -1,0 +1,534 @@
+// smallside.cu -- the s x d side of sGMRES / sRR on the device.
+//
+//  * form_cols:  sketched reduced-matrix columns from the basis sketch via the Arnoldi
+//                recurrence  m_j = sum_i h_ij b_i + w_{j+1}, i.e.
+//                S m_j = S w_{j+1} + sum_i h_ij sigma_i S w_i,
+//                or plain  S b_j = sigma_j S w_j.
+//  * incremental thin QR of the sketched matrix (Eq. sgmres-iterative-qr),
+//    appended J columns at a time by block classical Gram-Schmidt with
+//    re-orthogonalisation (BCGS2) against the explicit orthonormal U, then CGS2
+//    inside the panel;  the residual s-vector  g - U_j U_j^T g  is updated column by
+//    column so r_est,j (Eq. sgmres-iterative-soln, reading O14) is a plain norm
+//    with no cancellation; early-exit test (reading O16).
+//  * triangular solves (yhat = T^-1 U^T g), kappa(T) estimate,
+//  * assembly x += B yhat (reading O13) and Ritz vectors X = B Y.
+#include "common.cuh"
+#include "internal.h"
+
+namespace sks {
+
+// X[q*ldq + jj*ldj], columns jj = 0..J-1 correspond to basis index j = j0+jj.
+// mode 0 (SAB):  X[:,jj] = SW[:, j+1] + sum_{i=max(0,j-k+1)}^{j} H[i,j] sigma_i SW[:, i]
+// mode 1 (SB):   X[:,jj] = sigma_j SW[:, j]
+// mode 2 (raw):  X[:,jj] = SW[:, j]
+__global__ void form_cols_kernel(int mode, const double* __restrict__ SW, int s, int j0, int J, int k,
+                                 const double* __restrict__ H, int ldH, const double* __restrict__ sigma,
+                                 double* __restrict__ X, int64_t ldq, int64_t ldj) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= s * J) return;
+  const int q = idx / J, jj = idx % J, j = j0 + jj;
+  double v;
+  if (mode == 1) {
+    v = sigma[j] * SW[(int64_t)j * s + q];
+  } else if (mode == 2) {
+    v = SW[(int64_t)j * s + q];
+  } else {
+    v = SW[(int64_t)(j + 1) * s + q];
+    const int lo = max(0, j - k + 1);
+    for (int i = lo; i <= j; ++i) v += H[i + (int64_t)j * ldH] * sigma[i] * SW[(int64_t)i * s + q];
+  }
+  X[(int64_t)q * ldq + (int64_t)jj * ldj] = v;
+}
+
+// Z[i*J + c] = sum_q U[q + i*ldu] X[q*J + c]  for i < j0;  T[i + (tc0+c)*ldT] (+)= Z
+__global__ void utx_kernel(const double* __restrict__ U, int ldu, int s, int j0, const double* __restrict__ X,
+                           int J, double* __restrict__ Z, double* __restrict__ T, int ldT, int tc0, int tacc) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int i = blockIdx.x * (blockDim.x >> 5) + w;
+  if (i >= j0) return;
+  const double* u = U + (int64_t)i * ldu;
+  double a0 = 0.0, a1 = 0.0;
+  int q = 0;
+  if (lane < J) {
+    for (; q + 1 < s; q += 2) {
+      a0 += u[q] * X[(int64_t)q * J + lane];
+      a1 += u[q + 1] * X[(int64_t)(q + 1) * J + lane];
+    }
+    if (q < s) a0 += u[q] * X[(int64_t)q * J + lane];
+    const double z = a0 + a1;
+    Z[(int64_t)i * J + lane] = z;
+    if (T) {
+      double* t = T + i + (int64_t)(tc0 + lane) * ldT;
+      *t = tacc ? (*t + z) : z;
+    }
+  }
+}
+
+// X[q*J + c] -= sum_{i<j0} U[q + i*ldu] Z[i*J + c]
+__global__ void xmuz_kernel(const double* __restrict__ U, int ldu, int s, int j0, double* __restrict__ X, int J,
+                            const double* __restrict__ Z) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int q = blockIdx.x * (blockDim.x >> 5) + w;
+  if (q >= s || lane >= J) return;
+  double a0 = 0.0, a1 = 0.0;
+  int i = 0;
+  for (; i + 1 < j0; i += 2) {
+    a0 += U[q + (int64_t)i * ldu] * Z[(int64_t)i * J + lane];
+    a1 += U[q + (int64_t)(i + 1) * ldu] * Z[(int64_t)(i + 1) * J + lane];
+  }
+  if (i < j0) a0 += U[q + (int64_t)i * ldu] * Z[(int64_t)i * J + lane];
+  X[(int64_t)q * J + lane] -= a0 + a1;
+}
+
+// One CTA: CGS2 QR of the panel X (s x J row-major, already projected against U),
+// writes U[:, j0..j0+J), T[j0.., j0..], updates the residual vector rvec (length s),
+// rho[j] = u_j^T rvec_{j-1}, rest[j] = ||rvec_j||, early exit (ctrl).
+__global__ void __launch_bounds__(1024) panel_kernel(double* __restrict__ X, int s, int J, int j0,
+                                                     double* __restrict__ U, int ldu, double* __restrict__ T,
+                                                     int ldT, double* __restrict__ rvec, double* __restrict__ rho,
+                                                     double* __restrict__ rest, CtrlBlock* ctrl, int track_res,
+                                                     int max_cols) {
+  extern __shared__ double sm[];
+  const int L = J + 1;            // odd smem row stride: conflict-free column walks
+  double* sX = sm;               // s x J, row stride L
+  double* sr = sX + (size_t)s * L;  // s
+  __shared__ double red[32];
+  __shared__ double zsh[SKS_JB];
+  __shared__ double bc;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  for (int i = tid; i < s * J; i += nt) sX[(i / J) * L + (i % J)] = X[i];
+  if (track_res)
+    for (int i = tid; i < s; i += nt) sr[i] = rvec[i];
+  __syncthreads();
+  int rankdef = 0;
+  for (int c = 0; c < J; ++c) {
+    if (j0 + c >= max_cols) break;
+    double tcol[SKS_JB];
+    for (int i = 0; i < SKS_JB; ++i) tcol[i] = 0.0;
+    for (int pass = 0; pass < 2; ++pass) {
+      // z_i = x_i . x_c for i < c  (warp i)
+      for (int i = wid; i < c; i += nw) {
+        double a = 0.0;
+        for (int q = lane; q < s; q += 32) a += sX[q * L + i] * sX[q * L + c];
+        a = warp_sum(a);
+        if (lane == 0) zsh[i] = a;
+      }
+      __syncthreads();
+      for (int q = tid; q < s; q += nt) {
+        double v = sX[q * L + c];
+        for (int i = 0; i < c; ++i) v -= sX[q * L + i] * zsh[i];
+        sX[q * L + c] = v;
+      }
+      for (int i = 0; i < c; ++i) tcol[i] += zsh[i];
+      __syncthreads();
+    }
+    double a = 0.0;
+    for (int q = tid; q < s; q += nt) a += sX[q * L + c] * sX[q * L + c];
+    a = warp_sum(a);
+    if (lane == 0) red[wid] = a;
+    __syncthreads();
+    if (wid == 0) {
+      double t = lane < nw ? red[lane] : 0.0;
+      t = warp_sum(t);
+      if (lane == 0) bc = sqrt(t);
+    }
+    __syncthreads();
+    const double nrm = bc;
+    const bool zero = !(nrm > 0.0) || !isfinite(nrm);
+    if (zero) rankdef = 1;
+    const double inv = zero ? 0.0 : 1.0 / nrm;
+    for (int q = tid; q < s; q += nt) {
+      const double v = sX[q * L + c] * inv;
+      sX[q * L + c] = v;
+      U[q + (int64_t)(j0 + c) * ldu] = v;
+    }
+    if (tid == 0) {
+      for (int i = 0; i < c; ++i) T[(j0 + i) + (int64_t)(j0 + c) * ldT] = tcol[i];
+      T[(j0 + c) + (int64_t)(j0 + c) * ldT] = nrm;
+      for (int i = j0 + c + 1; i < max_cols && i < j0 + J; ++i) T[i + (int64_t)(j0 + c) * ldT] = 0.0;
+    }
+    __syncthreads();
+    if (track_res) {
+      // rho = u_c . r ; r -= rho u_c ; rest = ||r||
+      double b = 0.0;
+      for (int q = tid; q < s; q += nt) b += sX[q * L + c] * sr[q];
+      b = warp_sum(b);
+      if (lane == 0) red[wid] = b;
+      __syncthreads();
+      if (wid == 0) {
+        double t = lane < nw ? red[lane] : 0.0;
+        t = warp_sum(t);
+        if (lane == 0) bc = t;
+      }
+      __syncthreads();
+      const double rh = bc;
+      double e = 0.0;
+      for (int q = tid; q < s; q += nt) {
+        const double v = sr[q] - rh * sX[q * L + c];
+        sr[q] = v;
+        e += v * v;
+      }
+      e = warp_sum(e);
+      __syncthreads();
+      if (lane == 0) red[wid] = e;
+      __syncthreads();
+      if (tid == 0) {
+        double t = 0.0;
+        for (int i = 0; i < nw; ++i) t += red[i];
+        const double re = sqrt(t);
+        rho[j0 + c] = rh;
+        rest[j0 + c] = re;
+        ctrl->r_est_last = re;
+        if (ctrl->exit_cols == 0 && !rankdef && re <= ctrl->thr) ctrl->exit_cols = j0 + c + 1;
+      }
+      __syncthreads();
+    }
+    if (tid == 0) ctrl->qr_cols = j0 + c + 1;
+    if (rankdef) break;
+  }
+  if (track_res)
+    for (int i = tid; i < s; i += nt) rvec[i] = sr[i];
+  if (tid == 0 && rankdef) ctrl->rank_def = 1;
+}
+
+// one warp: back substitution T[:n,:n] y = b (upper, column-major), then out[i] = y[i]*scale[i]
+// (scale may be NULL); also writes y to yout if non-NULL
+__global__ void trsv_upper_kernel(const double* __restrict__ T, int ldT, int n, const double* __restrict__ b,
+                                  const double* __restrict__ scale, double* __restrict__ yout,
+                                  double* __restrict__ out) {
+  extern __shared__ double y[];
+  const int lane = threadIdx.x;
+  for (int i = lane; i < n; i += 32) y[i] = b[i];
+  __syncwarp();
+  for (int i = n - 1; i >= 0; --i) {
+    if (lane == 0) y[i] = y[i] / T[i + (int64_t)i * ldT];
+    __syncwarp();
+    const double yi = y[i];
+    for (int l = lane; l < i; l += 32) y[l] -= T[l + (int64_t)i * ldT] * yi;
+    __syncwarp();
+  }
+  for (int i = lane; i < n; i += 32) {
+    if (yout) yout[i] = y[i];
+    if (out) out[i] = scale ? y[i] * scale[i] : y[i];
+  }
+}
+
+// kappa_2(T[:n,:n]) by power iteration on T^T T and on (T^T T)^-1 (one warp)
+__global__ void cond_kernel(const double* __restrict__ T, int ldT, int n, int iters, CtrlBlock* ctrl,
+                            double* __restrict__ out) {
+  extern __shared__ double sm[];
+  double* v = sm;
+  double* u = sm + n;
+  const int lane = threadIdx.x;
+  auto nrm = [&](double* a) {
+    double t = 0.0;
+    for (int i = lane; i < n; i += 32) t += a[i] * a[i];
+    return sqrt(warp_sum(t));
+  };
+  // largest singular value
+  for (int i = lane; i < n; i += 32) v[i] = 1.0 / sqrt((double)n) * (1.0 + 0.01 * (i % 7));
+  __syncwarp();
+  double smax = 0.0;
+  for (int it = 0; it < iters; ++it) {
+    double nv = nrm(v);
+    for (int i = lane; i < n; i += 32) v[i] /= nv;
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {  // u = T v
+      double t = 0.0;
+      for (int l = i; l < n; ++l) t += T[i + (int64_t)l * ldT] * v[l];
+      u[i] = t;
+    }
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {  // v = T^T u
+      double t = 0.0;
+      for (int l = 0; l <= i; ++l) t += T[l + (int64_t)i * ldT] * u[l];
+      v[i] = t;
+    }
+    __syncwarp();
+    smax = sqrt(nrm(v));
+  }
+  // smallest singular value: v <- T^-1 T^-T v
+  for (int i = lane; i < n; i += 32) v[i] = 1.0 / sqrt((double)n) * (1.0 + 0.01 * (i % 5));
+  __syncwarp();
+  double smin_inv = 0.0;
+  for (int it = 0; it < iters; ++it) {
+    double nv = nrm(v);
+    for (int i = lane; i < n; i += 32) v[i] /= nv;
+    __syncwarp();
+    // T^T z = v (forward)
+    for (int i = 0; i < n; ++i) {
+      if (lane == 0) v[i] = v[i] / T[i + (int64_t)i * ldT];
+      __syncwarp();
+      const double zi = v[i];
+      for (int l = i + 1 + lane; l < n; l += 32) v[l] -= T[i + (int64_t)l * ldT] * zi;
+      __syncwarp();
+    }
+    // T y = z (backward)
+    for (int i = n - 1; i >= 0; --i) {
+      if (lane == 0) v[i] = v[i] / T[i + (int64_t)i * ldT];
+      __syncwarp();
+      const double yi = v[i];
+      for (int l = lane; l < i; l += 32) v[l] -= T[l + (int64_t)i * ldT] * yi;
+      __syncwarp();
+    }
+    smin_inv = sqrt(nrm(v));
+  }
+  if (lane == 0) {
+    const double c = smax * smin_inv;
+    if (ctrl) ctrl->cond = c;
+    if (out) *out = c;
+  }
+}
+
+// x[off + p] += sum_{i<nc} coef[i] W[off + p + i*ld]   (p < n)
+__global__ void assemble_kernel(double* __restrict__ x, const double* __restrict__ W, int64_t ld, int64_t off,
+                                int64_t n, const double* __restrict__ coef, const int* __restrict__ ncp,
+                                int nc_max) {
+  extern __shared__ double cs[];
+  const int nc = min(*ncp, nc_max);
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) cs[i] = coef[i];
+  __syncthreads();
+  const int64_t n2 = n / 2;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n2; p += (int64_t)gridDim.x * blockDim.x) {
+    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+    const double* w = W + off + 2 * p;
+    int i = 0;
+    for (; i + 1 < nc; i += 2) {
+      const double2 u = *reinterpret_cast<const double2*>(w + (int64_t)i * ld);
+      const double2 v = *reinterpret_cast<const double2*>(w + (int64_t)(i + 1) * ld);
+      a0 += cs[i] * u.x;
+      a1 += cs[i] * u.y;
+      b0 += cs[i + 1] * v.x;
+      b1 += cs[i + 1] * v.y;
+    }
+    if (i < nc) {
+      const double2 u = *reinterpret_cast<const double2*>(w + (int64_t)i * ld);
+      a0 += cs[i] * u.x;
+      a1 += cs[i] * u.y;
+    }
+    x[off + 2 * p] += a0 + b0;
+    x[off + 2 * p + 1] += a1 + b1;
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    double a = 0.0;
+    for (int i = 0; i < nc; ++i) a += cs[i] * W[off + n - 1 + (int64_t)i * ld];
+    x[off + n - 1] += a;
+  }
+}
+
+// X_re/X_im[:, v] = sum_{i<nc} W[:, i] * sigma_i * Y(i, v)  (Y complex, yr/yi column-major ld = ldy)
+template <int NV>
+__global__ void ritz_vectors_kernel(const double* __restrict__ W, int64_t ld, int64_t off, int64_t n, int nc,
+                                    const double* __restrict__ sigma, const double* __restrict__ yr,
+                                    const double* __restrict__ yi, int ldy, int nvec, double* __restrict__ Xr,
+                                    double* __restrict__ Xi, int64_t ldx, int64_t xoff) {
+  extern __shared__ double cs[];  // [nc][2*NV]
+  for (int t = threadIdx.x; t < nc * NV; t += blockDim.x) {
+    const int i = t / NV, v = t % NV;
+    cs[i * 2 * NV + v] = v < nvec ? sigma[i] * yr[i + v * ldy] : 0.0;
+    cs[i * 2 * NV + NV + v] = v < nvec ? sigma[i] * yi[i + v * ldy] : 0.0;
+  }
+  __syncthreads();
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    double ar[NV], ai[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) ar[v] = ai[v] = 0.0;
+    for (int i = 0; i < nc; ++i) {
+      const double w = W[off + p + (int64_t)i * ld];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        ar[v] += cs[i * 2 * NV + v] * w;
+        ai[v] += cs[i * 2 * NV + NV + v] * w;
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+      if (v < nvec) {
+        Xr[xoff + p + v * ldx] = ar[v];
+        Xi[xoff + p + v * ldx] = ai[v];
+      }
+  }
+}
+
+
+// out[:, i] = sigma_i W[off:off+n, i]   (normalised basis columns, ld = ldo)
+__global__ void scale_cols_kernel(const double* __restrict__ W, int64_t ld, int64_t off, int64_t n, int nc,
+                                  const double* __restrict__ sigma, double* __restrict__ out, int64_t ldo) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n * nc;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = idx % n;
+    const int i = (int)(idx / n);
+    out[p + (int64_t)i * ldo] = sigma[i] * W[off + p + (int64_t)i * ld];
+  }
+}
+
+// partials[b][v][0..1] = sum ||(A - theta) x||^2, ||x||^2 for complex x = xr + i xi
+__global__ void complex_residual_kernel(int64_t n, const double* __restrict__ Axr, const double* __restrict__ Axi,
+                                        const double* __restrict__ xr, const double* __restrict__ xi, int64_t ldx,
+                                        int64_t ldax, int nvec, const double* __restrict__ thr,
+                                        const double* __restrict__ thi, double* __restrict__ partials) {
+  __shared__ double red[64];
+  for (int v = 0; v < nvec; ++v) {
+    const double a = thr[v], b = thi[v];
+    double s_res = 0.0, s_x = 0.0;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+      const double r0 = xr[p + v * ldx], i0 = xi[p + v * ldx];
+      const double rr = Axr[p + v * ldax] - a * r0 + b * i0;
+      const double ri = Axi[p + v * ldax] - a * i0 - b * r0;
+      s_res += rr * rr + ri * ri;
+      s_x += r0 * r0 + i0 * i0;
+    }
+    double t[2] = {s_res, s_x}, o[2];
+    block_sum_n<2>(t, red, o);
+    if (threadIdx.x == 0) {
+      partials[((int64_t)blockIdx.x * nvec + v) * 2 + 0] = o[0];
+      partials[((int64_t)blockIdx.x * nvec + v) * 2 + 1] = o[1];
+    }
+  }
+}
+
+// out[c] = sum_b part[b*stride + c], c < ncomp (fixed order)
+__global__ void sum_partials_kernel(const double* __restrict__ part, int grid, int stride, int ncomp,
+                                    double* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncomp) return;
+  double t = 0.0;
+  for (int b = 0; b < grid; ++b) t += part[(int64_t)b * stride + c];
+  out[c] = t;
+}
+
+__global__ void ctrl_reset_kernel(CtrlBlock* c, double thr, double fnorm) {
+  c->stop_col = 0x7fffffff;
+  c->breakdown = 0;
+  c->exit_cols = 0;
+  c->qr_cols = 0;
+  c->rank_def = 0;
+  c->rnorm = 0.0;
+  c->fnorm = fnorm;
+  c->thr = thr;
+  c->cond = 0.0;
+  c->r_est_last = 0.0;
+}
+
+// global column index -> index into the all-gathered vector [rank][maxn]
+__global__ void remap_cols_kernel(int64_t nnz, const int32_t* __restrict__ cg, int32_t* __restrict__ co,
+                                  int nranks, const int64_t* __restrict__ rb, int64_t maxn) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = cg[p];
+    int r = 0;
+    while (r + 1 < nranks && g >= rb[r + 1]) ++r;
+    co[p] = (int32_t)(r * maxn + (g - rb[r]));
+  }
+}
+
+// ------------------------------------------------------------------------------
+cudaError_t launch_form_cols(int mode, const double* SW, int s, int j0, int J, int k, const double* H, int ldH,
+                             const double* sigma, double* X, int64_t ldq, int64_t ldj, cudaStream_t st) {
+  const int tot = s * J;
+  form_cols_kernel<<<(tot + 255) / 256, 256, 0, st>>>(mode, SW, s, j0, J, k, H, ldH, sigma, X, ldq, ldj);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_utx(const double* U, int ldu, int s, int j0, const double* X, int J, double* Z, double* T,
+                       int ldT, int tc0, int tacc, cudaStream_t st) {
+  if (j0 <= 0) return cudaSuccess;
+  utx_kernel<<<(j0 + 7) / 8, 256, 0, st>>>(U, ldu, s, j0, X, J, Z, T, ldT, tc0, tacc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_xmuz(const double* U, int ldu, int s, int j0, double* X, int J, const double* Z,
+                        cudaStream_t st) {
+  if (j0 <= 0) return cudaSuccess;
+  xmuz_kernel<<<(s + 7) / 8, 256, 0, st>>>(U, ldu, s, j0, X, J, Z);
+  return cudaGetLastError();
+}
+
+size_t panel_smem(int s, int J) { return sizeof(double) * ((size_t)s * (J + 1) + s); }
+
+cudaError_t launch_panel(double* X, int s, int J, int j0, double* U, int ldu, double* T, int ldT, double* rvec,
+                         double* rho, double* rest, CtrlBlock* ctrl, int track_res, int max_cols,
+                         cudaStream_t st) {
+  const size_t smem = panel_smem(s, J);
+  static size_t set = 0;
+  if (set < smem) {
+    cudaError_t e = cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    set = smem;
+  }
+  panel_kernel<<<1, 1024, smem, st>>>(X, s, J, j0, U, ldu, T, ldT, rvec, rho, rest, ctrl, track_res, max_cols);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trsv(const double* T, int ldT, int n, const double* b, const double* scale, double* yout,
+                        double* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  trsv_upper_kernel<<<1, 32, sizeof(double) * n, st>>>(T, ldT, n, b, scale, yout, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cond(const double* T, int ldT, int n, int iters, CtrlBlock* ctrl, double* out,
+                        cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  cond_kernel<<<1, 32, sizeof(double) * 2 * n, st>>>(T, ldT, n, iters, ctrl, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_assemble(double* x, const double* W, int64_t ld, int64_t off, int64_t n, const double* coef,
+                            const int* ncp, int nc_max, int num_sms, cudaStream_t st) {
+  int grid = (int)std::min<int64_t>((n / 2 + 255) / 256 + 1, (int64_t)num_sms * 8);
+  assemble_kernel<<<grid, 256, sizeof(double) * std::max(nc_max, 1), st>>>(x, W, ld, off, n, coef, ncp, nc_max);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ritz_vectors(const double* W, int64_t ld, int64_t off, int64_t n, int nc, const double* sigma,
+                                const double* yr, const double* yi, int ldy, int nvec, double* Xr, double* Xi,
+                                int64_t ldx, int64_t xoff, int num_sms, cudaStream_t st) {
+  int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms * 4);
+  if (grid < 1) grid = 1;
+  if (nvec <= 4) {
+    ritz_vectors_kernel<4><<<grid, 256, sizeof(double) * nc * 8, st>>>(W, ld, off, n, nc, sigma, yr, yi, ldy, nvec,
+                                                                       Xr, Xi, ldx, xoff);
+  } else if (nvec <= 12) {
+    ritz_vectors_kernel<12><<<grid, 256, sizeof(double) * nc * 24, st>>>(W, ld, off, n, nc, sigma, yr, yi, ldy,
+                                                                         nvec, Xr, Xi, ldx, xoff);
+  } else {
+    return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scale_cols(const double* W, int64_t ld, int64_t off, int64_t n, int nc, const double* sigma,
+                              double* out, int64_t ldo, cudaStream_t st) {
+  int64_t tot = n * nc;
+  int grid = (int)std::min<int64_t>((tot + 255) / 256, 4096);
+  if (grid < 1) grid = 1;
+  scale_cols_kernel<<<grid, 256, 0, st>>>(W, ld, off, n, nc, sigma, out, ldo);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_complex_residual(int64_t n, const double* Axr, const double* Axi, const double* xr,
+                                    const double* xi, int64_t ldx, int64_t ldax, int nvec, const double* thr,
+                                    const double* thi, double* partials, int grid, cudaStream_t st) {
+  complex_residual_kernel<<<grid, 256, 0, st>>>(n, Axr, Axi, xr, xi, ldx, ldax, nvec, thr, thi, partials);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sum_partials(const double* part, int grid, int stride, int ncomp, double* out, cudaStream_t st) {
+  sum_partials_kernel<<<(ncomp + 127) / 128, 128, 0, st>>>(part, grid, stride, ncomp, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ctrl_reset(CtrlBlock* c, double thr, double fnorm, cudaStream_t st) {
+  ctrl_reset_kernel<<<1, 1, 0, st>>>(c, thr, fnorm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_remap_cols(int64_t nnz, const int32_t* ci_global, int32_t* ci_out, int nranks,
+                              const int64_t* rb_dev, int64_t maxn, cudaStream_t st) {
+  int grid = (int)std::min<int64_t>((nnz + 255) / 256, 8192);
+  if (grid < 1) grid = 1;
+  remap_cols_kernel<<<grid, 256, 0, st>>>(nnz, ci_global, ci_out, nranks, rb_dev, maxn);
+  return cudaGetLastError();
+}
+
+}  // namespace sks

@@ -1,0 +1,154 @@
+// step.cuh -- argument block and coefficient prologue of the fused Arnoldi step.
+//
+// One launch produces one new (unnormalised) basis column w_j of the k-truncated
+// Arnoldi recurrence (Eq. partorth; Alg. 1):
+//     w_j = m_{j-1} - sum_{i=j-k}^{j-1} h_i b_i,   h_i = <b_i, m_{j-1}>,  m_{j-1} = A b_{j-1}
+// with b_i = sigma_i w_i (sigma_i = 1/||w_i||, reading O9: columns stored unnormalised).
+// m_{j-1} is recomputed on the fly from w_{j-1} (matrix-free A), and in the SAME pass
+// the kernel forms A w_j and the partial sums the NEXT step needs:
+//     ||w_j||^2, <w_j, A w_j>, ||A w_j||^2, <w_i, A w_j> (i = j-k+1..j-1)
+// so h^{(j+1)} = { sigma_j sigma_i <w_i, A w_j>,  sigma_j^2 <w_j, A w_j> } are known at
+// the start of launch j+1 without another pass over memory.  Each CTA of launch j+1
+// re-reduces the per-CTA partials of launch j in a fixed order (deterministic).
+#pragma once
+#include "common.cuh"
+
+struct StepArgs {
+  // geometry (stencil): local slab of nz planes (2D: lines) starting at global plane z0
+  int64_t m;        // points per side
+  int64_t nz;       // local planes
+  int64_t z0;       // global index of the first local plane
+  int64_t plane;    // points per plane (m or m*m)
+  int64_t ld;       // column pitch (doubles)
+  int64_t off;      // offset of the first interior point (= G*plane)
+  int G;            // ghost planes per side
+  int dim;
+  double cc, cm, cp;  // stencil coefficients: centre, minus-neighbours, plus-neighbours
+  // recurrence
+  int mode;         // 0: step j >= 1;  1: w_0 = f - A x;  2: w_0 = v0
+  int j, k;
+  double* W;        // column i at W + i*ld
+  const double* xin;  // mode 1: x;   mode 2: v0
+  const double* fin;  // mode 1: f
+  const double* partials_in;  // [grid_prev][SKS_NP] of launch j-1
+  int grid_prev;
+  double* partials_out;       // [gridDim.x][SKS_NP]
+  double* sigma;    // sigma_i = 1/||w_i||
+  double* H;        // Hbar, column-major, ld = ldH: Hbar[i, j] = h coefficient of b_i in w_{j+1}
+  int ldH;
+  double* mnorm;    // ||m_i||
+  CtrlBlock* ctrl;
+  int64_t ntiles;   // work items
+  int tiles_x, tiles_y, zchunk;  // tiling
+};
+
+struct StepCoef {
+  const double* U;  // vector whose A-image is taken (w_{j-1}, x, or v0)
+  double alpha;     // coefficient of A U
+  double beta_u;    // coefficient of U itself
+  int nv;           // number of extra vectors
+  const double* V[SKS_KMAX];
+  double c[SKS_KMAX];
+  int vslot[SKS_KMAX];  // output partial slot of <V_l, A w>, -1 = none
+  int uslot;            // output partial slot of <U, A w>, -1 = none
+  int ok;
+};
+
+// Computes the coefficients of this launch into smem `cf` (block-uniform). Returns false
+// (for the whole block) if the basis has stopped (breakdown) -> nothing to do.
+__device__ __forceinline__ bool step_prologue(const StepArgs& a, StepCoef* cf, double* red) {
+  const int tid = threadIdx.x;
+  if (a.mode != 0) {
+    if (tid == 0) {
+      cf->ok = 1;
+      cf->U = a.xin;
+      cf->alpha = (a.mode == 1) ? -1.0 : 0.0;
+      cf->beta_u = (a.mode == 2) ? 1.0 : 0.0;
+      cf->nv = (a.mode == 1) ? 1 : 0;
+      cf->V[0] = a.fin;
+      cf->c[0] = 1.0;
+      cf->vslot[0] = -1;
+      cf->uslot = -1;
+    }
+    __syncthreads();
+    return true;
+  }
+  // fixed-order reduction of the previous launch's partials
+  double p[SKS_NP];
+#pragma unroll
+  for (int i = 0; i < SKS_NP; ++i) p[i] = 0.0;
+  for (int b = tid; b < a.grid_prev; b += blockDim.x) {
+#pragma unroll
+    for (int i = 0; i < SKS_NP; ++i) p[i] += a.partials_in[(int64_t)b * SKS_NP + i];
+  }
+  __shared__ double P[SKS_NP];
+  block_sum_n<SKS_NP>(p, red, P);
+  if (tid == 0) {
+    const int j = a.j, k = a.k;
+    const int jm = j - 1;
+    cf->ok = 1;
+    if (a.ctrl->stop_col <= jm || a.ctrl->exit_cols != 0) cf->ok = 0;
+    const double N = P[0];
+    const double nu = sqrt(N);
+    bool bd = !(N > 0.0) || !isfinite(N);
+    if (jm >= 1 && nu <= 1e-14 * a.mnorm[jm - 1]) bd = true;
+    if (cf->ok && bd) {
+      cf->ok = 0;
+      if (blockIdx.x == 0) {
+        a.ctrl->stop_col = jm;
+        a.ctrl->breakdown = 1;
+        if (jm >= 1) a.H[jm + (int64_t)(jm - 1) * a.ldH] = nu;
+        if (jm == 0) a.ctrl->rnorm = nu;
+      }
+    }
+    if (cf->ok) {
+      const double sg = 1.0 / nu;
+      const int lo = max(0, j - k);
+      const double hj = sg * sg * P[1];
+      cf->U = a.W + (int64_t)jm * a.ld;
+      cf->alpha = sg;
+      cf->beta_u = -hj * sg;
+      const int nv = jm - lo;
+      cf->nv = nv;
+      for (int l = 0; l < nv; ++l) {
+        const int i = lo + l;
+        const double si = a.sigma[i];
+        const double hi = sg * si * P[3 + i - (j - k)];
+        cf->V[l] = a.W + (int64_t)i * a.ld;
+        cf->c[l] = -hi * si;
+        const int sl = i - (j - k + 1);
+        cf->vslot[l] = (sl >= 0) ? 3 + sl : -1;
+        if (blockIdx.x == 0) a.H[i + (int64_t)jm * a.ldH] = hi;
+      }
+      cf->uslot = (k >= 2) ? k + 1 : -1;
+      if (blockIdx.x == 0) {
+        a.sigma[jm] = sg;
+        a.mnorm[jm] = sg * sqrt(P[2]);
+        a.H[jm + (int64_t)jm * a.ldH] = hj;
+        if (jm >= 1) a.H[jm + (int64_t)(jm - 1) * a.ldH] = nu;
+        if (jm == 0) a.ctrl->rnorm = nu;
+      }
+    }
+  }
+  __syncthreads();
+  return cf->ok != 0;
+}
+
+// write the block's partials into the output slots
+template <int KM>
+__device__ __forceinline__ void step_epilogue(const StepArgs& a, const StepCoef* cf,
+                                              double (&acc)[KM + 3], double* red) {
+  __shared__ double R[KM + 3];
+  block_sum_n<KM + 3>(acc, red, R);
+  if (threadIdx.x == 0) {
+    double out[SKS_NP];
+    for (int i = 0; i < SKS_NP; ++i) out[i] = 0.0;
+    out[0] = R[0];
+    out[1] = R[1];
+    out[2] = R[2];
+    for (int l = 0; l < KM - 1; ++l)
+      if (l < cf->nv && cf->vslot[l] >= 0) out[cf->vslot[l]] = R[3 + l];
+    if (cf->uslot >= 0) out[cf->uslot] = R[3 + KM - 1];
+    for (int i = 0; i < SKS_NP; ++i) a.partials_out[(int64_t)blockIdx.x * SKS_NP + i] = out[i];
+  }
+}

@@ -1,0 +1,224 @@
+"""GPU <-> oracle parity through the C-ABI (run on a B200 under gpurun: -m gpu).
+
+Tolerances (BASELINE.json north_star):
+  * S M for a given M: relative Frobenius error <= 1e-12;  S tables bit-exact (integer work);
+  * first 20 basis columns: <= 1e-10 relative;
+  * final relative residual ||Ax - f||/||f|| recomputed by the ORACLE's operator: <= 1e-8
+    (configs that restart to tol) and within 2x of the oracle's own final residual;
+  * Ritz values: <= 1e-8 relative (matched canonically, reading O23).
+Sizes span several tiles and ragged tails; the full-size configs are checked on
+properties that hold at any size (true residual via the oracle's SpMV).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from inputs import get_config, rhs_normal, start_vector, random_csr_c4
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import paper_2111_00113_b200 as P
+    from paper_2111_00113_b200 import build
+    build.build()
+    c = P.Context(0)
+    yield c
+    c.close()
+
+
+def _P():
+    import paper_2111_00113_b200 as P
+    return P
+
+
+# ---------------------------------------------------------------- sketch
+@pytest.mark.parametrize("s,zeta,seed,cycle,rb", [(600, 8, 2, 0, 0), (120, 8, 0, 3, 12345), (400, 8, 1, 13, 7),
+                                                  (40, 3, 9, 0, 0), (17, 16, 5, 1, 99), (2048, 8, 4, 2, 3)])
+def test_sketch_table_bit_exact(ctx, s, zeta, seed, cycle, rb):
+    count = 5000
+    q, sg = ctx.sketch_table(rb, count, s=s, zeta=zeta, seed=seed, cycle=cycle)
+    qo, so = O.sketch_table(np.arange(rb, rb + count), s, zeta, seed, cycle)
+    assert np.array_equal(q, qo)
+    assert np.array_equal(sg.astype(np.float64), so)
+
+
+@pytest.mark.parametrize("n,c,s,rb", [(1024, 1, 120, 0), (50_001, 40, 600, 0), (99_999, 32, 400, 4096 * 7),
+                                      (777, 5, 600, 3), (300_000, 7, 2048, 0)])
+def test_sketch_apply_parity(ctx, n, c, s, rb):
+    rng = np.random.default_rng(n + c)
+    M = rng.standard_normal((n, c))
+    SM = ctx.sketch_apply(M, s=s, zeta=8, seed=2, cycle=1, row_begin=rb, n_global=rb + n)
+    ref = O.sketch_apply(M, s, 8, 2, 1, row_begin=rb, n=rb + n)
+    err = np.linalg.norm(SM - ref) / np.linalg.norm(ref)
+    assert err <= 1e-12, err
+
+
+def test_sketch_apply_device_tensor_and_determinism(ctx):
+    import torch
+    rng = np.random.default_rng(0)
+    M = rng.standard_normal((70_000, 33))
+    Mt = torch.from_numpy(M).cuda()
+    a = ctx.sketch_apply(Mt, s=300, zeta=8, seed=3).cpu().numpy()
+    b = ctx.sketch_apply(Mt, s=300, zeta=8, seed=3).cpu().numpy()
+    assert np.array_equal(a, b)            # bitwise reproducible (fixed-order reductions)
+    ref = O.sketch_apply(M, 300, 8, 3)
+    assert np.linalg.norm(a - ref) / np.linalg.norm(ref) <= 1e-12
+
+
+# ---------------------------------------------------------------- operator
+@pytest.mark.parametrize("dim,m,beta", [(2, 32, 20.0), (2, 77, 50.0), (3, 20, 30.0), (3, 9, 3.0)])
+def test_apply_stencil(ctx, dim, m, beta):
+    P = _P()
+    x = np.random.default_rng(1).standard_normal(m ** dim)
+    y = ctx.apply_operator(P.StencilOperator(dim, m, beta), x)
+    ref = O.stencil_matrix(dim, m, beta) @ x
+    assert np.linalg.norm(y - ref) <= 1e-14 * np.linalg.norm(ref)
+
+
+def test_apply_csr(ctx):
+    P = _P()
+    n = 20_000
+    rp, ci, v, f = random_csr_c4(n, seed=3)
+    y = ctx.apply_operator(P.CsrOperator(rp, ci, v, n), f)
+    ref = O.csr_matrix(rp, ci, v, n) @ f
+    assert np.linalg.norm(y - ref) <= 1e-14 * np.linalg.norm(ref)
+
+
+# ---------------------------------------------------------------- basis (first 20 columns <= 1e-10)
+@pytest.mark.parametrize("case", ["C1", "C2s", "C3s", "C4s", "k1", "k8"])
+def test_basis_first_columns(ctx, case):
+    P = _P()
+    if case == "C1":
+        A, Ao, k, n = P.StencilOperator(2, 32, 20.0), O.stencil_matrix(2, 32, 20.0), 2, 1024
+    elif case == "C2s":
+        A, Ao, k, n = P.StencilOperator(2, 130, 50.0), O.stencil_matrix(2, 130, 50.0), 4, 130 ** 2
+    elif case == "C3s":
+        A, Ao, k, n = P.StencilOperator(3, 37, 30.0), O.stencil_matrix(3, 37, 30.0), 2, 37 ** 3
+    elif case == "C4s":
+        n = 30_000
+        rp, ci, v, _ = random_csr_c4(n, seed=3)
+        A, Ao, k = P.CsrOperator(rp, ci, v, n), O.csr_matrix(rp, ci, v, n), 2
+    elif case == "k1":
+        A, Ao, k, n = P.StencilOperator(2, 50, 10.0), O.stencil_matrix(2, 50, 10.0), 1, 2500
+    else:
+        A, Ao, k, n = P.StencilOperator(2, 40, 5.0), O.stencil_matrix(2, 40, 5.0), 8, 1600
+    r0 = rhs_normal(n, 7)
+    B, H = ctx.basis(A, r0, k=k, ncols=20)
+    ref = O.partial_arnoldi(lambda v: Ao @ v, r0, 20, k)
+    err = np.abs(B - ref["B"]).max() / np.abs(ref["B"]).max()
+    assert err <= 1e-10, err
+    Ho = ref["H"][:20, :19]
+    assert np.abs(H - Ho).max() <= 1e-10 * np.abs(Ho).max()
+
+
+# ---------------------------------------------------------------- sGMRES
+def test_sgmres_c1_parity(ctx):
+    P = _P()
+    c = get_config("C1")
+    f = rhs_normal(c.n, c.seed)
+    A = O.stencil_matrix(2, c.m, c.beta)
+    res = ctx.sgmres_solve(P.StencilOperator(2, c.m, c.beta), f, d=c.d, k=c.k, s=c.s, zeta=c.zeta, seed=c.seed,
+                           tol=c.tol, max_cycles=c.max_cycles)
+    orc = O.sgmres_solve(lambda v: A @ v, f, c.d, c.k, c.s, c.zeta, c.seed, tol=c.tol, max_cycles=c.max_cycles)
+    rel_gpu = np.linalg.norm(f - A @ res.x) / np.linalg.norm(f)      # recomputed by the oracle
+    assert rel_gpu <= 2 * orc["rel_res_true"] and orc["rel_res_true"] <= 2 * rel_gpu
+    assert abs(res.info["rel_res_true"] - rel_gpu) <= 1e-6 * rel_gpu
+    assert res.info["columns"] == orc["columns"]
+    np.testing.assert_allclose(res.hist, orc["hist_est"], rtol=1e-6)
+    np.testing.assert_allclose(res.x, orc["x"], rtol=0, atol=1e-6 * np.abs(orc["x"]).max())
+
+
+def test_sgmres_c1_restarted_to_tol(ctx):
+    P = _P()
+    c = get_config("C1")
+    f = rhs_normal(c.n, c.seed)
+    A = O.stencil_matrix(2, c.m, c.beta)
+    res = ctx.sgmres_solve(P.StencilOperator(2, c.m, c.beta), f, d=c.d, k=c.k, s=c.s, seed=c.seed, tol=1e-8,
+                           max_cycles=5)
+    orc = O.sgmres_solve(lambda v: A @ v, f, c.d, c.k, c.s, c.zeta, c.seed, tol=1e-8, max_cycles=5)
+    rel_gpu = np.linalg.norm(f - A @ res.x) / np.linalg.norm(f)
+    assert res.converged and rel_gpu <= 1e-8
+    assert rel_gpu <= 2 * orc["rel_res_true"] and orc["rel_res_true"] <= 2 * rel_gpu
+    assert res.info["cycles"] == orc["cycles"] and res.info["columns"] == orc["columns"]
+    np.testing.assert_allclose(res.hist_true, orc["hist_true"], rtol=1e-4)
+
+
+def test_sgmres_csr_small(ctx):
+    P = _P()
+    n = 40_000
+    rp, ci, v, f = random_csr_c4(n, seed=3)
+    Ao = O.csr_matrix(rp, ci, v, n)
+    res = ctx.sgmres_solve(P.CsrOperator(rp, ci, v, n), f, d=40, k=2, s=80, seed=3, tol=1e-8, max_cycles=3)
+    orc = O.sgmres_solve(lambda x: Ao @ x, f, 40, 2, 80, 8, 3, tol=1e-8, max_cycles=3)
+    rel_gpu = np.linalg.norm(f - Ao @ res.x) / np.linalg.norm(f)
+    assert rel_gpu <= 1e-8 and rel_gpu <= 2 * orc["rel_res_true"] and orc["rel_res_true"] <= 2 * rel_gpu
+    assert res.info["columns"] == orc["columns"]
+
+
+def test_sgmres_3d_small_restarts(ctx):
+    P = _P()
+    m = 24
+    f = rhs_normal(m ** 3, 2)
+    Ao = O.stencil_matrix(3, m, 30.0)
+    res = ctx.sgmres_solve(P.StencilOperator(3, m, 30.0), f, d=60, k=2, s=120, seed=2, tol=1e-8, max_cycles=10)
+    orc = O.sgmres_solve(lambda x: Ao @ x, f, 60, 2, 120, 8, 2, tol=1e-8, max_cycles=10)
+    rel_gpu = np.linalg.norm(f - Ao @ res.x) / np.linalg.norm(f)
+    assert res.converged and rel_gpu <= 1e-8
+    assert rel_gpu <= 2 * orc["rel_res_true"] and orc["rel_res_true"] <= 2 * rel_gpu
+    assert res.info["cycles"] == orc["cycles"]
+
+
+def test_sgmres_host_and_device_buffers_agree(ctx):
+    import torch
+    P = _P()
+    c = get_config("C1")
+    f = rhs_normal(c.n, c.seed)
+    A = P.StencilOperator(2, c.m, c.beta)
+    r1 = ctx.sgmres_solve(A, f, d=c.d, k=c.k, s=c.s, seed=c.seed, max_cycles=1)
+    r2 = ctx.sgmres_solve(A, torch.from_numpy(f).cuda(), d=c.d, k=c.k, s=c.s, seed=c.seed, max_cycles=1)
+    assert np.array_equal(r1.x, r2.x.cpu().numpy())   # deterministic, same kernels
+
+
+# ---------------------------------------------------------------- sRR
+def _match(th_gpu, th_orc):
+    err = 0.0
+    for t in th_gpu:
+        j = np.argmin(np.abs(th_orc - t))
+        err = max(err, abs(th_orc[j] - t) / abs(th_orc[j]))
+    return err
+
+
+@pytest.mark.parametrize("m,beta,d", [(32, 10.0, 40), (64, 10.0, 80)])
+def test_srr_parity_small(ctx, m, beta, d):
+    P = _P()
+    n = m * m
+    v0 = start_vector(n, 4)
+    Ao = O.stencil_matrix(2, m, beta)
+    out = ctx.srr_eigs(P.StencilOperator(2, m, beta), v0, d=d, k=2, s=2 * d, nev=10, seed=4)
+    orc = O.srr_eigs(lambda x: Ao @ x, v0, d, 2, 2 * d, 8, 4, 10)
+    assert _match(out["theta"], orc["theta_all"]) <= 1e-8
+    # same selection (canonical order, O23)
+    assert len(out["theta"]) == len(orc["theta"])
+    np.testing.assert_allclose(np.sort_complex(out["theta"]), np.sort_complex(orc["theta"]), rtol=1e-8)
+    np.testing.assert_allclose(np.sort(out["res_true"]), np.sort(orc["res_true"]), rtol=1e-4)
+    np.testing.assert_allclose(np.sort(out["res_est"]), np.sort(orc["res_est"]), rtol=1e-4)
+
+
+def test_srr_closed_form_full_dimension(ctx):
+    """d = n with k >= d-1 (full orthogonalisation) on a 2D grid.  The 2D spectrum
+    mu_p + mu_q (BASELINE north_star closed form) has repeated values, so the Krylov space
+    of one vector has dimension = number of DISTINCT eigenvalues: the basis breaks down
+    there (reading O10) and every Ritz value is one of the distinct eigenvalues."""
+    P = _P()
+    m, beta = 3, 3.0
+    n = m * m
+    v0 = start_vector(n, 4)
+    out = ctx.srr_eigs(P.StencilOperator(2, m, beta), v0, d=n, k=8, s=2 * n, nev=9, seed=4)
+    ev = O.closed_form_eigs(2, m, beta)
+    distinct = np.unique(np.round(ev / ev.max(), 12)) * ev.max()
+    assert out["info"]["flags"] & 2              # SKS_WARN_BREAKDOWN
+    assert out["info"]["columns"] == distinct.size
+    assert np.abs(out["theta"].imag).max() <= 1e-9 * ev.max()
+    np.testing.assert_allclose(np.sort(out["theta"].real), distinct, rtol=1e-9)
