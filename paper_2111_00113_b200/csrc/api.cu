@@ -13,6 +13,7 @@
 #include <nccl.h>
 
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -52,6 +53,9 @@ struct sks_ctx {
   CtrlBlock* h_ctrl = nullptr;   // pinned mirror
   double* h_small = nullptr;     // pinned scratch (4096 doubles)
   int64_t w_zeroed_bytes = 0;
+  void* tma_cache = nullptr;   // encoded tensor maps of the stencil step
+  int use_tma = 1;             // SKS_NO_TMA=1 forces the generic stencil kernels
+  int tma_mask = 7;
   cudaStream_t main() const { return user_main ? user_main : own_main; }
 };
 
@@ -260,6 +264,12 @@ sks_status sks_create(sks_ctx** out, int device, int rank, int nranks, const uns
   }
   sks_ctx* c = new sks_ctx();
   c->device = device;
+  {
+    const char* e = getenv("SKS_NO_TMA");
+    c->use_tma = !(e && e[0] == '1');
+    const char* mk = getenv("SKS_TMA_MASK");  // debug: bit i = use TMA for step mode i
+    c->tma_mask = mk ? atoi(mk) : 7;
+  }
   c->rank = rank;
   c->nranks = nranks;
   cudaSetDevice(device);
@@ -317,6 +327,7 @@ sks_status sks_destroy(sks_ctx* c) {
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->comm) ncclCommDestroy(c->comm);
+  if (c->tma_cache) stencil_tma_free(c->tma_cache);
   for (auto& ev : c->ev_batch) cudaEventDestroy(ev);
   cudaEvent_t evs[] = {c->ev_fork, c->ev_join, c->ev_t0, c->ev_t1, c->ev_b0, c->ev_b1};
   for (auto e : evs)
@@ -349,6 +360,10 @@ struct Basis {
   int ncol;            // columns allocated
   int ldH;
   int step_grid = 0;   // stencil step grid, or CSR grid
+  bool tma = false;    // TMA-fed stencil kernels
+  int last_grid = 0;   // grid of the previous step launch (its partial count)
+  StepArgs sat;        // step arguments with the TMA tiling
+  int tma_grid = 0;
   int pslots = 0;      // partial slots (fixed across ranks)
   StepArgs sa;
   // CSR
@@ -418,8 +433,14 @@ static sks_status setup_basis(sks_ctx* c, const sks_operator* A, int k, int ncol
     a.ldH = b->ldH;
     a.mnorm = c->mnorm.as<double>();
     a.ctrl = c->ctrl.as<CtrlBlock>();
+    b->tma = c->use_tma && stencil_tma_supported(g.dim, g.m, k);
+    b->sat = a;
     stencil_tiling(g.dim, g.m, g.nz, c->num_sms, &a, &b->step_grid);
     if (b->step_grid > b->pslots) b->step_grid = b->pslots;
+    if (b->tma) {
+      stencil_tma_tiling(g.dim, g.m, g.nz, c->num_sms, &b->sat, &b->tma_grid);
+      if (b->tma_grid > b->pslots) b->tma_grid = b->pslots;
+    }
   } else {
     b->step_grid = c->num_sms * 4;
     b->nnz = A->nnz_local;
@@ -473,7 +494,8 @@ static sks_status first_column(sks_ctx* c, Basis& b, int mode, const double* xve
   const Geo& g = b.g;
   double* p0 = pslot(c, b, c->part, 0);
   if (g.kind != SKS_OP_CSR) {
-    StepArgs a = b.sa;
+    const bool use_t = b.tma && (c->tma_mask >> mode & 1);
+    StepArgs a = use_t ? b.sat : b.sa;
     a.mode = mode;
     a.j = 0;
     a.xin = xvec;
@@ -481,10 +503,16 @@ static sks_status first_column(sks_ctx* c, Basis& b, int mode, const double* xve
     a.partials_out = p0;
     a.partials_in = nullptr;
     a.grid_prev = 0;
-    SKS_CK(c, launch_step_stencil(a, b.step_grid, st));
+    b.last_grid = use_t ? b.tma_grid : b.step_grid;
+    if (use_t)
+      SKS_CK(c, launch_step_stencil_tma(a, c->W.as<double>(), b.ncol, c->xb.as<double>(), c->fb.as<double>(),
+                                        c->vb.as<double>(), b.tma_grid, st, &c->tma_cache));
+    else
+      SKS_CK(c, launch_step_stencil(a, b.step_grid, st));
     ++c->launches;
     b.bytes += 8.0 * g.n * (mode == 1 ? 3 : 2);
   } else {
+    b.last_grid = b.step_grid;
     if (mode == 1) {
       const double* xg = nullptr;
       SKS_TRY(csr_gather(c, g, xvec, &xg, b.maxn));
@@ -509,13 +537,19 @@ static sks_status step_column(sks_ctx* c, Basis& b, int j) {
   const int grid_prev = c->nranks > 1 ? b.pslots : b.step_grid;
   const int nwin = std::min(b.k, j);
   if (g.kind != SKS_OP_CSR) {
-    StepArgs a = b.sa;
+    const bool use_t = b.tma && (c->tma_mask & 1);
+    StepArgs a = use_t ? b.sat : b.sa;
     a.mode = 0;
     a.j = j;
     a.partials_in = pslot(c, b, c->part, j - 1);
-    a.grid_prev = grid_prev;
+    a.grid_prev = c->nranks > 1 ? b.pslots : b.last_grid;
     a.partials_out = pslot(c, b, c->part, j);
-    SKS_CK(c, launch_step_stencil(a, b.step_grid, st));
+    b.last_grid = use_t ? b.tma_grid : b.step_grid;
+    if (use_t)
+      SKS_CK(c, launch_step_stencil_tma(a, c->W.as<double>(), b.ncol, c->xb.as<double>(), c->fb.as<double>(),
+                                        c->vb.as<double>(), b.tma_grid, st, &c->tma_cache));
+    else
+      SKS_CK(c, launch_step_stencil(a, b.step_grid, st));
     ++c->launches;
     SKS_TRY(allreduce_sum(c, a.partials_out, (size_t)b.pslots * SKS_NP, st));
     SKS_TRY(halo_exchange(c, g, colp(c, b, j)));
@@ -667,7 +701,7 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
     ++c->launches;
     b.bytes = 0;  // per-cycle accounting of the basis loop below
     SKS_TRY(first_column(c, b, 1, xb, fb));
-    SKS_CK(c, launch_sum_partials(pslot(c, b, c->part, 0), c->nranks > 1 ? b.pslots : b.step_grid, SKS_NP, 1,
+    SKS_CK(c, launch_sum_partials(pslot(c, b, c->part, 0), c->nranks > 1 ? b.pslots : b.last_grid, SKS_NP, 1,
                                   c->small.as<double>(), st));
     ++c->launches;
     SKS_CK(c, cudaMemcpyAsync(c->h_small, c->small.p, sizeof(double), cudaMemcpyDeviceToHost, st));

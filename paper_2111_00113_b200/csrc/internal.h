@@ -20,6 +20,13 @@ cudaError_t launch_ritz_residual_stencil(int dim, int64_t m, int64_t nz, int64_t
                                          const double* Xi, const double* thr, const double* thi, double* partials,
                                          int grid, cudaStream_t st);
 
+// stencil_tma.cu (even m: TMA-fed persistent kernels)
+bool stencil_tma_supported(int dim, int64_t m, int k);
+void stencil_tma_tiling(int dim, int64_t m, int64_t nz, int num_sms, StepArgs* a, int* grid);
+cudaError_t launch_step_stencil_tma(const StepArgs& a, const double* W, int64_t ncol, const double* xb,
+                                    const double* fb, const double* vb, int grid, cudaStream_t st, void** cache);
+void stencil_tma_free(void* cache);
+
 // sketch.cu
 int sketch_grid(int num_sms, int64_t nrows);
 size_t sketch_part_doubles(int grid, int J, int s);

@@ -57,26 +57,37 @@ __global__ void __launch_bounds__(SK_THREADS, 1) sketch_batch_kernel(SketchArgs 
     const int nr = (int)((a.nrows - r0) < (int64_t)SK_R ? (a.nrows - r0) : (int64_t)SK_R);
     // ---- 1. stage Mt
     if (a.vec_ok) {
-      for (int idx = tid; idx < (SK_R / 4) * 32; idx += SK_THREADS) {
+      // all loads first (one DRAM latency per tile), then the shared stores
+      constexpr int NIT = (SK_R / 4) * 32 / SK_THREADS;
+      double2 va[NIT], vb[NIT];
+#pragma unroll
+      for (int u = 0; u < NIT; ++u) {
+        const int idx = tid + u * SK_THREADS;
         const int rq = idx >> 5, c = idx & 31;
         const int r = rq * 4;
-        double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+        va[u] = make_double2(0.0, 0.0);
+        vb[u] = make_double2(0.0, 0.0);
         if (c < a.J) {
           const double* src = a.M + (int64_t)c * a.ldm + r0 + r;
           if (r + 3 < nr) {
-            const double2 p = __ldg(reinterpret_cast<const double2*>(src));
-            const double2 q = __ldg(reinterpret_cast<const double2*>(src + 2));
-            v0 = p.x; v1 = p.y; v2 = q.x; v3 = q.y;
+            va[u] = __ldg(reinterpret_cast<const double2*>(src));
+            vb[u] = __ldg(reinterpret_cast<const double2*>(src + 2));
           } else {
-            if (r + 0 < nr) v0 = src[0];
-            if (r + 1 < nr) v1 = src[1];
-            if (r + 2 < nr) v2 = src[2];
+            if (r + 0 < nr) va[u].x = src[0];
+            if (r + 1 < nr) va[u].y = src[1];
+            if (r + 2 < nr) vb[u].x = src[2];
           }
         }
-        Mt[(r + 0) * 32 + c] = v0;
-        Mt[(r + 1) * 32 + c] = v1;
-        Mt[(r + 2) * 32 + c] = v2;
-        Mt[(r + 3) * 32 + c] = v3;
+      }
+#pragma unroll
+      for (int u = 0; u < NIT; ++u) {
+        const int idx = tid + u * SK_THREADS;
+        const int rq = idx >> 5, c = idx & 31;
+        const int r = rq * 4;
+        Mt[(r + 0) * 32 + c] = va[u].x;
+        Mt[(r + 1) * 32 + c] = va[u].y;
+        Mt[(r + 2) * 32 + c] = vb[u].x;
+        Mt[(r + 3) * 32 + c] = vb[u].y;
       }
     } else {
       for (int idx = tid; idx < SK_R * 32; idx += SK_THREADS) {
