@@ -803,29 +803,39 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
     c->h_small[32] = 0;
     reinterpret_cast<int*>(c->h_small + 32)[0] = jstar;
     SKS_CK(c, cudaMemcpyAsync(ncp, c->h_small + 32, sizeof(int), cudaMemcpyHostToDevice, st));
+    // kappa(T) estimate on the side stream, overlapping the assembly and the next cycle (slot per cycle)
+    SKS_CK(c, cudaEventRecord(c->ev_fork, st));
+    SKS_CK(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    SKS_CK(c, launch_cond(c->T.as<double>(), b.ncol, jstar, 6, nullptr,
+                          c->small.as<double>() + 1024 + std::min(cycles - 1, 1023), c->side));
     SKS_CK(c, launch_assemble(xb, c->W.as<double>(), g.ld, g.off, g.n, c->coef.as<double>(), ncp, jstar,
                               c->num_sms, st));
-    SKS_CK(c, launch_cond(c->T.as<double>(), b.ncol, jstar, 12, nullptr, c->small.as<double>() + 8, st));
     c->launches += 3;
     SKS_TRY(halo_exchange(c, g, xb));
     // history: r_est,j / ||f||
     SKS_CK(c, cudaMemcpyAsync(c->h_small + 64, c->rest.p, sizeof(double) * std::min(jstar, 2048),
                               cudaMemcpyDeviceToHost, st));
-    SKS_CK(c, cudaMemcpyAsync(c->h_small + 40, c->small.as<double>() + 8, sizeof(double), cudaMemcpyDeviceToHost,
-                              st));
     SKS_CK(c, cudaStreamSynchronize(st));
     for (int j = 0; j < jstar && j < 2048; ++j) {
       if (hist && nh < hist_cap) hist[nh] = c->h_small[64 + j] / (fnorm > 0 ? fnorm : 1.0);
       ++nh;
     }
     r_est_last = c->h_small[64 + jstar - 1] / (fnorm > 0 ? fnorm : 1.0);
-    cond_last = c->h_small[40];
-    if (cond_last > cond_tol) flags |= SKS_WARN_COND;
     columns += jstar;
   }
+  // join the side stream (kappa estimates) and collect them
+  SKS_CK(c, cudaEventRecord(c->ev_join, c->side));
+  SKS_CK(c, cudaStreamWaitEvent(st, c->ev_join, 0));
   SKS_CK(c, cudaMemcpyAsync(x, xb + g.off, sizeof(double) * g.n, cudaMemcpyDefault, st));
   SKS_CK(c, cudaEventRecord(c->ev_t1, st));
+  if (cycles > 0)
+    SKS_CK(c, cudaMemcpyAsync(c->h_small + 1024, c->small.as<double>() + 1024,
+                              sizeof(double) * std::min(cycles, 1024), cudaMemcpyDeviceToHost, st));
   SKS_CK(c, cudaStreamSynchronize(st));
+  for (int i = 0; i < std::min(cycles, 1024); ++i) {
+    cond_last = c->h_small[1024 + i];
+    if (cond_last > cond_tol) flags |= SKS_WARN_COND;
+  }
   SKS_CK(c, cudaGetLastError());
   if (info) {
     memset(info, 0, sizeof(*info));
