@@ -65,6 +65,7 @@ static thread_local char g_err[512];
   do {                                                                                   \
     cudaError_t _e = (expr);                                                             \
     if (_e != cudaSuccess) {                                                             \
+      cudaGetLastError(); /* do not leak a non-sticky error into the next call */        \
       (ctx)->err = std::string(#expr) + ": " + cudaGetErrorString(_e);                  \
       return SKS_ECUDA;                                                                  \
     }                                                                                    \

@@ -215,15 +215,16 @@ template <int QPW, int ZETA>
 __global__ void __launch_bounds__(SK_THREADS, 1) sketch_v3_kernel(SketchArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   double* Mt = reinterpret_cast<double*>(smraw);                      // [SK_R][32]
-  uint32_t* ent = reinterpret_cast<uint32_t*>(Mt + SK_R * 32);         // [SK_R * zeta] row byte offsets
-  int* kst = reinterpret_cast<int*>(ent + SK_R * SKS_ZETA_MAX);        // [NK + 1] key starts
-  uint16_t* wc = reinterpret_cast<uint16_t*>(kst + S3_NKMAX + 8);      // [16][NKP] per-warp key counts/offsets
   __shared__ int wsum[SK_WARPS];
   __shared__ double sstage[SK_WARPS * 8 * 32];                        // per-warp bucket sums (8 q x 32 cols)
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int s = a.s, NK = 2 * s, NKP = (NK + 7) & ~7;
   constexpr int Z = ZETA > 0 ? ZETA : SKS_ZETA_MAX;
   const int zeta = ZETA > 0 ? ZETA : a.zeta;
+  // dynamic layout sized by (s, zeta): see sketch_v3_smem()
+  uint32_t* ent = reinterpret_cast<uint32_t*>(Mt + SK_R * 32);         // [SK_R * zeta] row byte offsets
+  int* kst = reinterpret_cast<int*>(ent + SK_R * zeta);                // [NKP + 8] key starts
+  uint16_t* wc = reinterpret_cast<uint16_t*>(kst + NKP + 8);           // [16][NKP] per-warp key counts/offsets
   const unsigned char* mtl = reinterpret_cast<const unsigned char*>(Mt) + lane * 8;
   const int qlo = a.q_base + wid * QPW;
   const uint32_t ltmask = (1u << lane) - 1u;
@@ -451,27 +452,49 @@ static cudaError_t launch_sk(const SketchArgs& a, int grid, cudaStream_t st) {
   if (set < smem) {
     cudaError_t e = cudaFuncSetAttribute(sketch_batch_kernel<QPW, ZETA>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return e;
+    }
     set = smem;
   }
   sketch_batch_kernel<QPW, ZETA><<<grid, SK_THREADS, smem, st>>>(a);
   return cudaGetLastError();
 }
 
-static size_t sketch_v3_smem() {
-  return sizeof(double) * SK_R * 32 + sizeof(uint32_t) * SK_R * SKS_ZETA_MAX + sizeof(int) * (S3_NKMAX + 8) +
-         sizeof(uint16_t) * SK_WARPS * S3_NKMAX + 64;
+// dynamic shared memory of sketch_v3_kernel for (s, zeta); its static part is sstage+wsum
+static size_t sketch_v3_smem(int s, int zeta) {
+  const size_t nkp = (size_t)((2 * s + 7) & ~7);
+  return sizeof(double) * SK_R * 32 + sizeof(uint32_t) * SK_R * zeta + sizeof(int) * (nkp + 8) +
+         sizeof(uint16_t) * SK_WARPS * nkp + 64;
+}
+constexpr size_t SK3_STATIC = sizeof(double) * SK_WARPS * 8 * 32 + sizeof(int) * SK_WARPS + 256;
+
+static bool sketch_v3_fits(int s, int zeta) {
+  static int optin = 0;
+  if (!optin) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) {
+      cudaGetLastError();
+      optin = 232448;
+    }
+  }
+  return 2 * s <= S3_NKMAX && sketch_v3_smem(s, zeta) + SK3_STATIC <= (size_t)optin;
 }
 
 template <int QPW, int ZETA>
 static cudaError_t launch_v3(const SketchArgs& a, int grid, cudaStream_t st) {
-  const size_t smem = sketch_v3_smem();
-  static bool set = false;
-  if (!set) {
+  const size_t smem = sketch_v3_smem(a.s, a.zeta);
+  static size_t set = 0;
+  if (set < smem) {
     cudaError_t e =
         cudaFuncSetAttribute(sketch_v3_kernel<QPW, ZETA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    set = true;
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return e;
+    }
+    set = smem;
   }
   sketch_v3_kernel<QPW, ZETA><<<grid, SK_THREADS, smem, st>>>(a);
   return cudaGetLastError();
@@ -522,7 +545,7 @@ cudaError_t launch_sketch(const double* M, int64_t ldm, int64_t nrows, int64_t r
   a.part = part;
   a.tiles = (nrows + SK_R - 1) / SK_R;
   a.vec_ok = ((((uintptr_t)M) & 15) == 0) && (ldm % 2 == 0);
-  if (2 * s <= S3_NKMAX) {
+  if (sketch_v3_fits(s, zeta)) {
     a.q_base = 0;
     cudaError_t e = (zeta == 8) ? launch_v3_z<8>(a, grid, st) : launch_v3_z<0>(a, grid, st);
     if (e != cudaSuccess) return e;
