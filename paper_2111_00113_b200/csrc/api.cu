@@ -49,7 +49,7 @@ struct sks_ctx {
   // workspaces
   DevBuf W, xb, fb, vb, mr, xg, part, part2, partsk, sigma, H, mnorm, SW, Xp, Zb, U, T, rvec, rho, rest, coef,
       ctrl, small, Mh, Mh2, wr, wi, sel, th, yr, yi, ework, SAB, SB, Xr, Xi, AXr, AXi, rpb, cib, vab, cig, rbd,
-      tmp;
+      tmp, bgsw, bgsc;
   CtrlBlock* h_ctrl = nullptr;   // pinned mirror
   double* h_small = nullptr;     // pinned scratch (4096 doubles)
   int64_t w_zeroed_bytes = 0;
@@ -324,7 +324,8 @@ sks_status sks_destroy(sks_ctx* c) {
                     &c->sigma, &c->H,   &c->mnorm, &c->SW,   &c->Xp,   &c->Zb,   &c->U,     &c->T,     &c->rvec,
                     &c->rho,  &c->rest, &c->coef,  &c->ctrl, &c->small, &c->Mh,  &c->Mh2,   &c->wr,    &c->wi,
                     &c->sel,  &c->th,   &c->yr,    &c->yi,   &c->ework, &c->SAB, &c->SB,    &c->Xr,    &c->Xi,
-                    &c->AXr,  &c->AXi,  &c->rpb,   &c->cib,  &c->vab,  &c->cig,  &c->rbd,   &c->tmp};
+                    &c->AXr,  &c->AXi,  &c->rpb,   &c->cib,  &c->vab,  &c->cig,  &c->rbd,   &c->tmp,
+                    &c->bgsw, &c->bgsc};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->comm) ncclCommDestroy(c->comm);
@@ -613,10 +614,12 @@ static sks_status qr_append(sks_ctx* c, Basis& b, int mode, int j0, int J, int s
   const int ldT = b.ncol;
   SKS_CK(c, launch_form_cols(mode, c->SW.as<double>(), s, j0, J, b.k, c->H.as<double>(), b.ldH,
                              c->sigma.as<double>(), X, J, 1, st));
-  SKS_CK(c, launch_utx(U, s, s, j0, X, J, Z, T, ldT, j0, 0, st));
-  SKS_CK(c, launch_xmuz(U, s, s, j0, X, J, Z, st));
-  SKS_CK(c, launch_utx(U, s, s, j0, X, J, Z, T, ldT, j0, 1, st));
-  SKS_CK(c, launch_xmuz(U, s, s, j0, X, J, Z, st));
+  double* ws = c->bgsw.as<double>();
+  int* cnt = c->bgsc.as<int>();
+  SKS_CK(c, launch_utx(U, s, s, j0, X, J, Z, T, ldT, j0, 0, ws, cnt, st));
+  SKS_CK(c, launch_xmuz(U, s, s, j0, X, J, Z, ws, cnt, st));
+  SKS_CK(c, launch_utx(U, s, s, j0, X, J, Z, T, ldT, j0, 1, ws, cnt, st));
+  SKS_CK(c, launch_xmuz(U, s, s, j0, X, J, Z, ws, cnt, st));
   SKS_CK(c, launch_panel(X, s, J, j0, U, s, T, ldT, c->rvec.as<double>(), c->rho.as<double>(), c->rest.as<double>(),
                          c->ctrl.as<CtrlBlock>(), track_res, max_cols, st));
   c->launches += (j0 > 0) ? 6 : 2;
@@ -637,6 +640,11 @@ static sks_status setup_small(sks_ctx* c, Basis& b, int s, int JB) {
   SKS_TRY(ensure(c, c->rest, sizeof(double) * (ncol + 1)));
   SKS_TRY(ensure(c, c->coef, sizeof(double) * (ncol + 1)));
   SKS_TRY(ensure(c, c->tmp, sizeof(double) * (size_t)std::max(b.pslots, 64) * SKS_NP * 2));
+  SKS_TRY(ensure(c, c->bgsw, sizeof(double) * bgs_workspace_doubles(s, ncol + 1)));
+  if (c->bgsc.bytes < sizeof(int) * 128) {
+    SKS_TRY(ensure(c, c->bgsc, sizeof(int) * 128));
+    SKS_CK(c, cudaMemsetAsync(c->bgsc.p, 0, sizeof(int) * 128, c->main()));
+  }
   if (panel_smem(s, JB) > 227 * 1024) return fail(c, SKS_EUNSUPPORTED, "s too large for the panel kernel");
   return SKS_OK;
 }
@@ -954,7 +962,8 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
   // ---- t = T^-1 U^T S w_de ; Mhat = Hbar[:de,:de] + t e_{de}^T
   SKS_CK(c, launch_form_cols(2, c->SW.as<double>(), s, de, 1, k, c->H.as<double>(), b.ldH, c->sigma.as<double>(),
                              c->Xp.as<double>(), 1, 1, st));
-  SKS_CK(c, launch_utx(c->U.as<double>(), s, s, de, c->Xp.as<double>(), 1, c->Zb.as<double>(), nullptr, 0, 0, 0, st));
+  SKS_CK(c, launch_utx(c->U.as<double>(), s, s, de, c->Xp.as<double>(), 1, c->Zb.as<double>(), nullptr, 0, 0, 0,
+                       c->bgsw.as<double>(), c->bgsc.as<int>(), st));
   SKS_CK(c, launch_trsv(c->T.as<double>(), b.ncol, de, c->Zb.as<double>(), nullptr, nullptr, c->coef.as<double>(), st));
   SKS_TRY(ensure(c, c->Mh, sizeof(double) * (size_t)de * de));
   SKS_TRY(ensure(c, c->Mh2, sizeof(double) * (size_t)de * de));

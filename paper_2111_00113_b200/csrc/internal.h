@@ -40,9 +40,10 @@ cudaError_t launch_sketch_table(int64_t row_begin, int64_t count, int s, int zet
 cudaError_t launch_form_cols(int mode, const double* SW, int s, int j0, int J, int k, const double* H, int ldH,
                              const double* sigma, double* X, int64_t ldq, int64_t ldj, cudaStream_t st);
 cudaError_t launch_utx(const double* U, int ldu, int s, int j0, const double* X, int J, double* Z, double* T,
-                       int ldT, int tc0, int tacc, cudaStream_t st);
-cudaError_t launch_xmuz(const double* U, int ldu, int s, int j0, double* X, int J, const double* Z,
-                        cudaStream_t st);
+                       int ldT, int tc0, int tacc, double* ws, int* cnt, cudaStream_t st);
+cudaError_t launch_xmuz(const double* U, int ldu, int s, int j0, double* X, int J, const double* Z, double* ws,
+                        int* cnt, cudaStream_t st);
+size_t bgs_workspace_doubles(int s, int ncol);
 size_t panel_smem(int s, int J);
 cudaError_t launch_panel(double* X, int s, int J, int j0, double* U, int ldu, double* T, int ldT, double* rvec,
                          double* rho, double* rest, CtrlBlock* ctrl, int track_res, int max_cols,

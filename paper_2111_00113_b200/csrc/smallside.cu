@@ -12,6 +12,8 @@
 //    with no cancellation; early-exit test (reading O16).
 //  * triangular solves (yhat = T^-1 U^T g), kappa(T) estimate,
 //  * assembly x += B yhat (reading O13) and Ritz vectors X = B Y.
+#include <cstring>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -40,45 +42,103 @@ __global__ void form_cols_kernel(int mode, const double* __restrict__ SW, int s,
   X[(int64_t)q * ldq + (int64_t)jj * ldj] = v;
 }
 
-// Z[i*J + c] = sum_q U[q + i*ldu] X[q*J + c]  for i < j0;  T[i + (tc0+c)*ldT] (+)= Z
-__global__ void utx_kernel(const double* __restrict__ U, int ldu, int s, int j0, const double* __restrict__ X,
-                           int J, double* __restrict__ Z, double* __restrict__ T, int ldT, int tc0, int tacc) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int i = blockIdx.x * (blockDim.x >> 5) + w;
-  if (i >= j0) return;
-  const double* u = U + (int64_t)i * ldu;
-  double a0 = 0.0, a1 = 0.0;
-  int q = 0;
-  if (lane < J) {
-    for (; q + 1 < s; q += 2) {
-      a0 += u[q] * X[(int64_t)q * J + lane];
-      a1 += u[q + 1] * X[(int64_t)(q + 1) * J + lane];
+// ------------------------------------------------------------------------------------
+// Split-K fp64 GEMM for the two block Gram-Schmidt products of the sketched QR
+// (BCGS2 projection of a panel X against the explicit U):
+//   utx :  Z (j0 x J) = U[:, :j0]^T X          (A(m=i, k=q) = U[q + i*ldu]),  T[i, tc0+c] (+)= Z
+//   xmuz:  X (s x J) -= U[:, :j0] Z            (A(m=q, k=i) = U[q + i*ldu])
+// 32 x 32 output tiles, 32-deep k steps through shared memory, k split over gridDim.y CTAs;
+// the last CTA of a tile (atomic ticket) adds the k-partials in ascending split order, so
+// the result is bitwise reproducible.
+// ------------------------------------------------------------------------------------
+struct GemmArgs {
+  const double* A;
+  int64_t sAm, sAk;
+  const double* B;  // K x J row-major (ld = J)
+  int M, J, K, KC, KS;
+  double* P;        // partials [KS][Mpad][32]
+  int Mpad;
+  int* cnt;         // one ticket per m tile (zero between calls)
+  int mode;         // 0: utx, 1: xmuz
+  double* Z;
+  double* T;
+  int ldT, tc0, tacc;
+  double* X;
+};
+
+template <bool AK>
+__global__ void __launch_bounds__(256) bgs_gemm_kernel(GemmArgs g) {
+  __shared__ double As[32][33];
+  __shared__ double Bs[32][33];
+  __shared__ int last;
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  const int m0 = blockIdx.x * 32, z = blockIdx.y;
+  const int kb0 = z * g.KC, ke = min(g.K, kb0 + g.KC);
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int kb = kb0; kb < ke; kb += 32) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int e = tid + 256 * r;
+      const int mm = AK ? (e >> 5) : (e & 31), kk = AK ? (e & 31) : (e >> 5);
+      const int m = m0 + mm, k = kb + kk;
+      As[kk][mm] = (m < g.M && k < ke) ? g.A[(int64_t)m * g.sAm + (int64_t)k * g.sAk] : 0.0;
+      const int kk2 = e >> 5, nn = e & 31, k2 = kb + kk2;
+      Bs[kk2][nn] = (k2 < ke && nn < g.J) ? g.B[(int64_t)k2 * g.J + nn] : 0.0;
     }
-    if (q < s) a0 += u[q] * X[(int64_t)q * J + lane];
-    const double z = a0 + a1;
-    Z[(int64_t)i * J + lane] = z;
-    if (T) {
-      double* t = T + i + (int64_t)(tc0 + lane) * ldT;
-      *t = tacc ? (*t + z) : z;
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < 32; ++kk) {
+      const double b = Bs[kk][tx];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[r] += As[kk][ty * 4 + r] * b;
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) g.P[((int64_t)z * g.Mpad + m0 + ty * 4 + r) * 32 + tx] = acc[r];
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = (atomicAdd(&g.cnt[blockIdx.x], 1) == g.KS - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int m = m0 + ty * 4 + r;
+    if (m >= g.M || tx >= g.J) continue;
+    double v = 0.0;
+    for (int zz = 0; zz < g.KS; ++zz) v += __ldcg(&g.P[((int64_t)zz * g.Mpad + m) * 32 + tx]);
+    if (g.mode == 0) {
+      g.Z[(int64_t)m * g.J + tx] = v;
+      if (g.T) {
+        double* t = g.T + m + (int64_t)(g.tc0 + tx) * g.ldT;
+        *t = g.tacc ? (*t + v) : v;
+      }
+    } else {
+      g.X[(int64_t)m * g.J + tx] -= v;
     }
   }
+  if (tid == 0) g.cnt[blockIdx.x] = 0;
 }
 
-// X[q*J + c] -= sum_{i<j0} U[q + i*ldu] Z[i*J + c]
-__global__ void xmuz_kernel(const double* __restrict__ U, int ldu, int s, int j0, double* __restrict__ X, int J,
-                            const double* __restrict__ Z) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int q = blockIdx.x * (blockDim.x >> 5) + w;
-  if (q >= s || lane >= J) return;
-  double a0 = 0.0, a1 = 0.0;
-  int i = 0;
-  for (; i + 1 < j0; i += 2) {
-    a0 += U[q + (int64_t)i * ldu] * Z[(int64_t)i * J + lane];
-    a1 += U[q + (int64_t)(i + 1) * ldu] * Z[(int64_t)(i + 1) * J + lane];
-  }
-  if (i < j0) a0 += U[q + (int64_t)i * ldu] * Z[(int64_t)i * J + lane];
-  X[(int64_t)q * J + lane] -= a0 + a1;
+static cudaError_t launch_bgs_gemm(GemmArgs g, bool ak, double* ws, int* cnt, cudaStream_t st) {
+  const int mt = (g.M + 31) / 32;
+  int ks = (120 + mt - 1) / mt;
+  ks = std::max(1, std::min(ks, 8));
+  int kc = ((g.K + ks - 1) / ks + 31) / 32 * 32;
+  ks = (g.K + kc - 1) / kc;
+  g.KC = kc;
+  g.KS = ks;
+  g.Mpad = mt * 32;
+  g.P = ws;
+  g.cnt = cnt;
+  dim3 grid(mt, ks);
+  if (ak) bgs_gemm_kernel<true><<<grid, 256, 0, st>>>(g);
+  else bgs_gemm_kernel<false><<<grid, 256, 0, st>>>(g);
+  return cudaGetLastError();
 }
+
+size_t bgs_workspace_doubles(int s, int ncol) { return (size_t)8 * ((std::max(s, ncol) + 31) / 32 * 32) * 32; }
 
 // One CTA: CGS2 QR of the panel X (s x J row-major, already projected against U),
 // writes U[:, j0..j0+J), T[j0.., j0..], updates the residual vector rvec (length s),
@@ -213,67 +273,113 @@ __global__ void trsv_upper_kernel(const double* __restrict__ T, int ldT, int n, 
   }
 }
 
-// kappa_2(T[:n,:n]) by power iteration on T^T T and on (T^T T)^-1 (one warp)
-__global__ void cond_kernel(const double* __restrict__ T, int ldT, int n, int iters, CtrlBlock* ctrl,
-                            double* __restrict__ out) {
+// kappa_2(T[:n,:n]) = sigma_max / sigma_min of the upper-triangular factor, estimated by
+// power iteration on T^T T and inverse iteration (T^T T)^-1 (reading O25).  One CTA of 1024
+// threads: products are row- / column-parallel with coalesced column reads, the triangular
+// solves are blocked (32 x 32 diagonal blocks solved by one warp from shared memory, the
+// off-diagonal updates by the whole CTA).
+constexpr int CN_T = 1024;
+
+__device__ __forceinline__ double cta_norm(const double* v, int n, double* red) {
+  double t = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) t += v[i] * v[i];
+  return sqrt(block_sum(t, red));
+}
+
+// y := T^-1 y (upper, backward) or T^-T y (forward), in place on shared y
+__device__ void cta_trsv(const double* __restrict__ T, int ldT, int n, double* y, bool trans, double* blk) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  const int nb = (n + 31) / 32;
+  for (int bb = 0; bb < nb; ++bb) {
+    const int b = trans ? bb : nb - 1 - bb;
+    const int i0 = b * 32, bs = min(32, n - i0);
+    // diagonal block into shared memory (blk[r*33 + c] = T[i0+r, i0+c])
+    for (int e = tid; e < 32 * 32; e += blockDim.x) {
+      const int r = e & 31, c = e >> 5;
+      blk[r * 33 + c] = (r < bs && c < bs && r <= c) ? T[(i0 + r) + (int64_t)(i0 + c) * ldT] : 0.0;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      double yl = lane < bs ? y[i0 + lane] : 0.0;
+      if (!trans) {
+        for (int c = bs - 1; c >= 0; --c) {
+          const double yc = __shfl_sync(0xffffffffu, yl, c) / blk[c * 33 + c];
+          if (lane == c) yl = yc;
+          if (lane < c) yl -= blk[lane * 33 + c] * yc;
+        }
+      } else {
+        for (int c = 0; c < bs; ++c) {
+          const double yc = __shfl_sync(0xffffffffu, yl, c) / blk[c * 33 + c];
+          if (lane == c) yl = yc;
+          if (lane > c && lane < bs) yl -= blk[c * 33 + lane] * yc;
+        }
+      }
+      if (lane < bs) y[i0 + lane] = yl;
+    }
+    __syncthreads();
+    if (!trans) {
+      // y[0:i0) -= T[0:i0, i0:i0+bs) y_b
+      for (int i = tid; i < i0; i += blockDim.x) {
+        double t = 0.0;
+        for (int c = 0; c < bs; ++c) t += T[i + (int64_t)(i0 + c) * ldT] * y[i0 + c];
+        y[i] -= t;
+      }
+    } else {
+      // y[l] -= T[i0:i0+bs, l]^T y_b for l >= i0+bs: warp per column
+      for (int l = i0 + bs + wid; l < n; l += nw) {
+        double t = lane < bs ? T[(i0 + lane) + (int64_t)l * ldT] * y[i0 + lane] : 0.0;
+        t = warp_sum(t);
+        if (lane == 0) y[l] -= t;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(CN_T) cond_kernel(const double* __restrict__ T, int ldT, int n, int iters,
+                                                    CtrlBlock* ctrl, double* __restrict__ out) {
   extern __shared__ double sm[];
   double* v = sm;
   double* u = sm + n;
-  const int lane = threadIdx.x;
-  auto nrm = [&](double* a) {
-    double t = 0.0;
-    for (int i = lane; i < n; i += 32) t += a[i] * a[i];
-    return sqrt(warp_sum(t));
-  };
-  // largest singular value
-  for (int i = lane; i < n; i += 32) v[i] = 1.0 / sqrt((double)n) * (1.0 + 0.01 * (i % 7));
-  __syncwarp();
+  __shared__ double blk[32 * 33];
+  __shared__ double red[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  // largest singular value: v <- T^T T v
+  for (int i = tid; i < n; i += blockDim.x) v[i] = 1.0 / sqrt((double)n) * (1.0 + 0.01 * (i % 7));
+  __syncthreads();
   double smax = 0.0;
   for (int it = 0; it < iters; ++it) {
-    double nv = nrm(v);
-    for (int i = lane; i < n; i += 32) v[i] /= nv;
-    __syncwarp();
-    for (int i = lane; i < n; i += 32) {  // u = T v
+    const double nv = cta_norm(v, n, red);
+    for (int i = tid; i < n; i += blockDim.x) v[i] /= nv;
+    __syncthreads();
+    for (int i = tid; i < n; i += blockDim.x) {  // u = T v (row-parallel, coalesced columns)
       double t = 0.0;
       for (int l = i; l < n; ++l) t += T[i + (int64_t)l * ldT] * v[l];
       u[i] = t;
     }
-    __syncwarp();
-    for (int i = lane; i < n; i += 32) {  // v = T^T u
+    __syncthreads();
+    for (int l = wid; l < n; l += nw) {  // v = T^T u (warp per column)
       double t = 0.0;
-      for (int l = 0; l <= i; ++l) t += T[l + (int64_t)i * ldT] * u[l];
-      v[i] = t;
+      for (int i = lane; i <= l; i += 32) t += T[i + (int64_t)l * ldT] * u[i];
+      t = warp_sum(t);
+      if (lane == 0) v[l] = t;
     }
-    __syncwarp();
-    smax = sqrt(nrm(v));
+    __syncthreads();
+    smax = sqrt(cta_norm(v, n, red));
   }
   // smallest singular value: v <- T^-1 T^-T v
-  for (int i = lane; i < n; i += 32) v[i] = 1.0 / sqrt((double)n) * (1.0 + 0.01 * (i % 5));
-  __syncwarp();
+  for (int i = tid; i < n; i += blockDim.x) v[i] = 1.0 / sqrt((double)n) * (1.0 + 0.01 * (i % 5));
+  __syncthreads();
   double smin_inv = 0.0;
   for (int it = 0; it < iters; ++it) {
-    double nv = nrm(v);
-    for (int i = lane; i < n; i += 32) v[i] /= nv;
-    __syncwarp();
-    // T^T z = v (forward)
-    for (int i = 0; i < n; ++i) {
-      if (lane == 0) v[i] = v[i] / T[i + (int64_t)i * ldT];
-      __syncwarp();
-      const double zi = v[i];
-      for (int l = i + 1 + lane; l < n; l += 32) v[l] -= T[i + (int64_t)l * ldT] * zi;
-      __syncwarp();
-    }
-    // T y = z (backward)
-    for (int i = n - 1; i >= 0; --i) {
-      if (lane == 0) v[i] = v[i] / T[i + (int64_t)i * ldT];
-      __syncwarp();
-      const double yi = v[i];
-      for (int l = lane; l < i; l += 32) v[l] -= T[l + (int64_t)i * ldT] * yi;
-      __syncwarp();
-    }
-    smin_inv = sqrt(nrm(v));
+    const double nv = cta_norm(v, n, red);
+    for (int i = tid; i < n; i += blockDim.x) v[i] /= nv;
+    __syncthreads();
+    cta_trsv(T, ldT, n, v, true, blk);
+    cta_trsv(T, ldT, n, v, false, blk);
+    smin_inv = sqrt(cta_norm(v, n, red));
   }
-  if (lane == 0) {
+  if (tid == 0) {
     const double c = smax * smin_inv;
     if (ctrl) ctrl->cond = c;
     if (out) *out = c;
@@ -430,17 +536,41 @@ cudaError_t launch_form_cols(int mode, const double* SW, int s, int j0, int J, i
 }
 
 cudaError_t launch_utx(const double* U, int ldu, int s, int j0, const double* X, int J, double* Z, double* T,
-                       int ldT, int tc0, int tacc, cudaStream_t st) {
+                       int ldT, int tc0, int tacc, double* ws, int* cnt, cudaStream_t st) {
   if (j0 <= 0) return cudaSuccess;
-  utx_kernel<<<(j0 + 7) / 8, 256, 0, st>>>(U, ldu, s, j0, X, J, Z, T, ldT, tc0, tacc);
-  return cudaGetLastError();
+  GemmArgs g;
+  memset(&g, 0, sizeof(g));
+  g.A = U;
+  g.sAm = ldu;
+  g.sAk = 1;
+  g.B = X;
+  g.M = j0;
+  g.J = J;
+  g.K = s;
+  g.mode = 0;
+  g.Z = Z;
+  g.T = T;
+  g.ldT = ldT;
+  g.tc0 = tc0;
+  g.tacc = tacc;
+  return launch_bgs_gemm(g, true, ws, cnt, st);
 }
 
-cudaError_t launch_xmuz(const double* U, int ldu, int s, int j0, double* X, int J, const double* Z,
-                        cudaStream_t st) {
+cudaError_t launch_xmuz(const double* U, int ldu, int s, int j0, double* X, int J, const double* Z, double* ws,
+                        int* cnt, cudaStream_t st) {
   if (j0 <= 0) return cudaSuccess;
-  xmuz_kernel<<<(s + 7) / 8, 256, 0, st>>>(U, ldu, s, j0, X, J, Z);
-  return cudaGetLastError();
+  GemmArgs g;
+  memset(&g, 0, sizeof(g));
+  g.A = U;
+  g.sAm = 1;
+  g.sAk = ldu;
+  g.B = Z;
+  g.M = s;
+  g.J = J;
+  g.K = j0;
+  g.mode = 1;
+  g.X = X;
+  return launch_bgs_gemm(g, false, ws, cnt, st);
 }
 
 size_t panel_smem(int s, int J) { return sizeof(double) * ((size_t)s * (J + 1) + s); }
@@ -469,7 +599,7 @@ cudaError_t launch_trsv(const double* T, int ldT, int n, const double* b, const 
 cudaError_t launch_cond(const double* T, int ldT, int n, int iters, CtrlBlock* ctrl, double* out,
                         cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  cond_kernel<<<1, 32, sizeof(double) * 2 * n, st>>>(T, ldT, n, iters, ctrl, out);
+  cond_kernel<<<1, CN_T, sizeof(double) * 2 * n, st>>>(T, ldT, n, iters, ctrl, out);
   return cudaGetLastError();
 }
 
