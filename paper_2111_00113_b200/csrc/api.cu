@@ -49,7 +49,7 @@ struct sks_ctx {
   // workspaces
   DevBuf W, xb, fb, vb, mr, xg, part, part2, partsk, sigma, H, mnorm, SW, Xp, Zb, U, T, rvec, rho, rest, coef,
       ctrl, small, Mh, Mh2, wr, wi, sel, th, yr, yi, ework, SAB, SB, Xr, Xi, AXr, AXi, rpb, cib, vab, cig, rbd,
-      tmp, bgsw, bgsc;
+      tmp, bgsw, bgsc, plan;
   CtrlBlock* h_ctrl = nullptr;   // pinned mirror
   double* h_small = nullptr;     // pinned scratch (4096 doubles)
   int64_t w_zeroed_bytes = 0;
@@ -325,7 +325,7 @@ sks_status sks_destroy(sks_ctx* c) {
                     &c->rho,  &c->rest, &c->coef,  &c->ctrl, &c->small, &c->Mh,  &c->Mh2,   &c->wr,    &c->wi,
                     &c->sel,  &c->th,   &c->yr,    &c->yi,   &c->ework, &c->SAB, &c->SB,    &c->Xr,    &c->Xi,
                     &c->AXr,  &c->AXi,  &c->rpb,   &c->cib,  &c->vab,  &c->cig,  &c->rbd,   &c->tmp,
-                    &c->bgsw, &c->bgsc};
+                    &c->bgsw, &c->bgsc, &c->plan};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->comm) ncclCommDestroy(c->comm);
@@ -593,13 +593,26 @@ static sks_status global_norm(sks_ctx* c, Basis& b, const double* v_interior, do
 }
 
 // sketch columns [c0, c0+J) of W into SW (s x ncol, column-major), reduced over ranks
+// per-cycle sketch plan of this rank's rows (S is fixed within a cycle, reading O7); NULL if the
+// (s, zeta) combination has no plan kernel (the generic sketch kernel hashes per batch)
+static sks_status sketch_plan(sks_ctx* c, const Geo& g, int s, int zeta, uint64_t key, cudaStream_t st,
+                              const void** plan) {
+  *plan = nullptr;
+  if (!sketch_plan_supported(s, zeta)) return SKS_OK;
+  SKS_TRY(ensure(c, c->plan, sketch_plan_bytes(g.n, s, zeta)));
+  SKS_CK(c, launch_sketch_plan(g.n, g.row_begin, s, zeta, key, c->plan.p, c->num_sms, st));
+  ++c->launches;
+  *plan = c->plan.p;
+  return SKS_OK;
+}
+
 static sks_status sketch_cols(sks_ctx* c, Basis& b, int c0, int J, int s, int zeta, uint64_t key,
-                              cudaStream_t st) {
+                              cudaStream_t st, const void* plan) {
   const Geo& g = b.g;
   const int grid = sketch_grid(c->num_sms, g.n);
   double* out = c->SW.as<double>() + (int64_t)c0 * s;
   SKS_CK(c, launch_sketch(colp(c, b, c0) + g.off, g.ld, g.n, g.row_begin, J, s, zeta, key, c->partsk.as<double>(),
-                          grid, out, s, 0, st, &c->launches));
+                          grid, out, s, 0, st, &c->launches, plan));
   SKS_TRY(allreduce_sum(c, out, (size_t)J * s, st));
   return SKS_OK;
 }
@@ -733,6 +746,7 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
     SKS_CK(c, cudaEventRecord(c->ev_b0, st));
     int next_sk = 0;    // next column to sketch
     int next_qr = 0;    // next SAB column to append
+    const void* plan = nullptr;
     int nbatch = 0;
     int last_col = d;   // columns 0..d are generated (d+1 columns)
     SKS_CK(c, cudaMemsetAsync(c->rvec.p, 0, sizeof(double) * s, st));
@@ -741,7 +755,8 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
       SKS_CK(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
       while (next_sk < upto) {
         const int J = std::min(JB, upto - next_sk);
-        SKS_TRY(sketch_cols(c, b, next_sk, J, s, zeta, key, c->side));
+        if (next_sk == 0) SKS_TRY(sketch_plan(c, g, s, zeta, key, c->side, &plan));
+        SKS_TRY(sketch_cols(c, b, next_sk, J, s, zeta, key, c->side, plan));
         if (next_sk == 0) {  // g = S r = S w_0 starts the residual vector
           SKS_CK(c, cudaMemcpyAsync(c->rvec.p, c->SW.p, sizeof(double) * s, cudaMemcpyDeviceToDevice, c->side));
         }
@@ -876,6 +891,7 @@ static sks_status basis_and_sketch(sks_ctx* c, Basis& b, int d, int s, int zeta,
                                    bool do_sketch, float* t_basis_ms) {
   cudaStream_t st = c->main();
   int next_sk = 0;
+  const void* plan = nullptr;
   SKS_CK(c, cudaEventRecord(c->ev_b0, st));
   auto side = [&](int upto) -> sks_status {
     if (!do_sketch) return SKS_OK;
@@ -883,7 +899,8 @@ static sks_status basis_and_sketch(sks_ctx* c, Basis& b, int d, int s, int zeta,
     SKS_CK(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
     while (next_sk < upto) {
       const int J = std::min(JB, upto - next_sk);
-      SKS_TRY(sketch_cols(c, b, next_sk, J, s, zeta, key, c->side));
+      if (next_sk == 0) SKS_TRY(sketch_plan(c, b.g, s, zeta, key, c->side, &plan));
+      SKS_TRY(sketch_cols(c, b, next_sk, J, s, zeta, key, c->side, plan));
       next_sk += J;
     }
     return SKS_OK;
@@ -1110,11 +1127,16 @@ extern "C" sks_status sks_sketch_apply(sks_ctx* c, int64_t n_global, int64_t row
   SKS_CK(c, cudaMemcpy2DAsync(c->tmp.p, sizeof(double) * ldd, M, sizeof(double) * ldm, sizeof(double) * n, cc,
                               cudaMemcpyDefault, st));
   const uint64_t key = sks_key(seed, cycle);
+  Geo gq;
+  gq.n = n;
+  gq.row_begin = row_begin;
+  const void* plan = nullptr;
+  SKS_TRY(sketch_plan(c, gq, s, zeta, key, st, &plan));
   for (int c0 = 0; c0 < cc; c0 += SKS_JB) {
     const int J = std::min(SKS_JB, cc - c0);
     SKS_CK(c, launch_sketch(c->tmp.as<double>() + (int64_t)c0 * ldd, ldd, n, row_begin, J, s, zeta, key,
                             c->partsk.as<double>(), grid, c->SAB.as<double>() + (int64_t)c0 * s, s, 0, st,
-                            &c->launches));
+                            &c->launches, plan));
   }
   SKS_TRY(allreduce_sum(c, c->SAB.as<double>(), (size_t)s * cc, st));
   SKS_CK(c, cudaMemcpyAsync(SM, c->SAB.p, sizeof(double) * (size_t)s * cc, cudaMemcpyDefault, st));

@@ -30,9 +30,14 @@ void stencil_tma_free(void* cache);
 // sketch.cu
 int sketch_grid(int num_sms, int64_t nrows);
 size_t sketch_part_doubles(int grid, int J, int s);
+// plan: per-cycle sketch plan of these rows (launch_sketch_plan), or NULL for the generic kernel
 cudaError_t launch_sketch(const double* M, int64_t ldm, int64_t nrows, int64_t row_begin, int J, int s, int zeta,
                           uint64_t key, double* part, int grid, double* out, int64_t ldo, int accumulate,
-                          cudaStream_t st, int64_t* launches);
+                          cudaStream_t st, int64_t* launches, const void* plan);
+bool sketch_plan_supported(int s, int zeta);
+size_t sketch_plan_bytes(int64_t nrows, int s, int zeta);
+cudaError_t launch_sketch_plan(int64_t nrows, int64_t row_begin, int s, int zeta, uint64_t key, void* plan,
+                               int num_sms, cudaStream_t st);
 cudaError_t launch_sketch_table(int64_t row_begin, int64_t count, int s, int zeta, uint64_t key, int32_t* q,
                                 int8_t* sign, cudaStream_t st);
 

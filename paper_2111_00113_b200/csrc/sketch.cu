@@ -199,134 +199,132 @@ __global__ void __launch_bounds__(SK_THREADS, 1) sketch_batch_kernel(SketchArgs 
 }
 
 // ------------------------------------------------------------------------------
-// v4 (s <= 768): swizzled row-major staging by cp.async, deterministic counting sort by
-// sketch row q without atomics, and a register gather at 32 warps per SM.
+// v5 (s <= 768): the sketch PLAN is built once per restart cycle (S is fixed within a cycle,
+// reading O7), the per-batch kernel only stages the batch and gathers.
 //
-//  * Mt[r][c] (R = 512 rows + one zero row, 32 columns) lives at byte offset
-//    r*256 + 8*(c ^ g(r&3)), g = {0, 8, 1, 9}: a 32-byte global sector (4 rows of one column)
-//    lands in 4 distinct bank pairs, a staging warp (4 rows x 8 columns) and a gather warp
-//    (one row, lane = column) are both conflict free, and the gather address is
-//    (E ^ 8*lane) & 0x7fffffff with E = r*256 + 8*g(r&3) | sign<<31 stored per entry.
-//  * Entries of one tile are bucketed by q (both signs in one bucket; the sign is an XOR
-//    on the value's high word).  Placement order inside a bucket is (warp, t, lane):
-//    per-warp ranks come from __match_any_sync, per-bucket warp offsets from a prefix
-//    over the 16 hashing warps -- no atomics, so the result is bitwise reproducible.
-//  * Every bucket is padded to an even length with an entry pointing at the zero row, so
-//    the gather walks each bucket two entries at a time with no tail code.
-//  * 32 warps: warp w owns sketch rows [w*QPW, (w+1)*QPW) (sums in registers, statically
-//    unrolled over its buckets), lane c owns column c; 32 resident warps hide the
-//    shared-memory latency of the dependent entry -> value loads.
-//  * The staging of a tile is issued before its hash/sort, so the global loads overlap it.
+// Plan of one tile of R = 512 rows: the tile's R*zeta entries bucketed by sketch row q
+// (both signs in one bucket), each bucket padded to an even length with an entry pointing at
+// a zero row; placement order inside a bucket is (warp, t, lane) from __match_any_sync ranks
+// and a prefix over warps -- no atomics, so the plan (and every sum) is bitwise reproducible.
+// An entry is E = r*256 + 8*g(r) | sign<<31, the byte offset of row r in the staged tile.
+//
+// Gather (per batch of J <= 32 columns): Mt[r][c] (R rows + one zero row, 32 columns) lives
+// at byte r*256 + 8*(c ^ g(r)), g(r) = r & 31: the staging warp (32 consecutive rows of one
+// column, 256 contiguous global bytes) and the gather warp (one row, lane = column) are both
+// bank-conflict free and the gather address is one LOP3 ((E ^ 8*lane) & 0x7fffffff).
+// 32 warps; warp w owns sketch rows [w*QPW, (w+1)*QPW) with its sums in registers.
 // ------------------------------------------------------------------------------
 constexpr int S4_R = 512;
 constexpr int S4_QMAX = 768;
 constexpr int S4_THREADS = 1024;
 constexpr int S4_WARPS = S4_THREADS / 32;
-constexpr int S4_HWARPS = S4_R / 32;  // warps that hash (one row per thread)
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ double ld_shared_f64(uint32_t addr) {
-  double v;
-  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
-  return v;
-}
 __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 __host__ __device__ __forceinline__ uint32_t s4_g(uint32_t r) { return r & 31u; }
-
-// dynamic shared memory: Mt[(R+1)*32] doubles | ent[R*zeta + s + 4] u32 | kst[s + 2] int | cw[16][NQP] u16
 __host__ __device__ __forceinline__ int s4_nqp(int s) { return (s + 7) & ~7; }
-__host__ __device__ __forceinline__ size_t s4_ent_words(int s, int zeta) { return (size_t)S4_R * zeta + s + 4; }
+// plan strides: entries (u32) and bucket starts (u16) per tile, both 16-byte multiples
+__host__ __device__ __forceinline__ int s5_ent_stride(int s, int zeta) { return (S4_R * zeta + s + 4 + 3) & ~3; }
+__host__ __device__ __forceinline__ int s5_kst_stride(int s) { return (s + 1 + 7) & ~7; }
 
-template <int QPW, int ZETA>
-__global__ void __launch_bounds__(S4_THREADS, 1) sketch_v4_kernel(SketchArgs a) {
+// ---- plan kernel: one CTA per tile (grid-stride), 1024 threads
+template <int ZETA>
+__global__ void __launch_bounds__(S4_THREADS, 1) sketch_plan_kernel(int64_t nrows, int64_t row_begin, int s,
+                                                                     int zeta_rt, uint64_t key, int64_t tiles,
+                                                                     uint32_t* __restrict__ pent,
+                                                                     uint16_t* __restrict__ pkst) {
   extern __shared__ __align__(16) unsigned char smraw[];
   constexpr int Z = ZETA > 0 ? ZETA : SKS_ZETA_MAX;
-  const int zeta = ZETA > 0 ? ZETA : a.zeta;
-  const int s = a.s, NQP = s4_nqp(s);
-  // Mt base aligned to 256 B, so an entry can carry the absolute shared address of its row
-  double* Mt = reinterpret_cast<double*>(smraw + ((256u - (smem_addr(smraw) & 255u)) & 255u));
-  uint32_t* ent = reinterpret_cast<uint32_t*>(Mt + (S4_R + 1) * 32);
-  int* kst = reinterpret_cast<int*>(ent + s4_ent_words(s, zeta));
-  uint16_t* cw = reinterpret_cast<uint16_t*>(kst + s + 2);
+  constexpr int ZH = (Z + 1) / 2;  // draws per thread (a row's draws are split over two threads)
+  const int zeta = ZETA > 0 ? ZETA : zeta_rt;
+  const int zh = (zeta + 1) / 2;
+  const int NQP = s4_nqp(s), ES = s5_ent_stride(s, zeta), KS = s5_kst_stride(s);
+  uint32_t* ent = reinterpret_cast<uint32_t*>(smraw);       // [ES]
+  int* kst = reinterpret_cast<int*>(ent + ES);               // [s + 1]
+  uint16_t* cw = reinterpret_cast<uint16_t*>(kst + s + 4);   // [32 warps][NQP]
+  uint16_t* qa = cw + S4_WARPS * NQP;                        // [R][ZH]
   __shared__ int wsum4[S4_WARPS];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  uint32_t lane8, amask;  // opaque to the optimiser (keeps the gather address a single LOP3)
-  asm("mov.b32 %0, %1;" : "=r"(lane8) : "r"((uint32_t)lane * 8u));
-  asm("mov.b32 %0, %1;" : "=r"(amask) : "r"(0x7fffffffu));
-  const uint32_t mt_s = smem_addr(Mt);
   const uint32_t ltmask = (1u << lane) - 1u;
-  const uint32_t PAD = mt_s + (uint32_t)S4_R * 256u;  // row R (zero); g(R) == 0
-  const int qlo = wid * QPW;
-  const bool hwarp = wid < S4_HWARPS;
-  const uint32_t st_base = mt_s + (uint32_t)lane * 256u + 8u * ((uint32_t)(wid ^ lane) & 31u);
+  const uint32_t PAD = (uint32_t)S4_R * 256u;  // the zero row
   uint16_t* cwm = cw + wid * NQP;
-  if (tid < 32) Mt[S4_R * 32 + tid] = 0.0;
-
-  double acc[QPW];
-#pragma unroll
-  for (int i = 0; i < QPW; ++i) acc[i] = 0.0;
-
-  const int64_t t_lo = (a.tiles * blockIdx.x) / gridDim.x;
-  const int64_t t_hi = (a.tiles * (blockIdx.x + 1)) / gridDim.x;
-  for (int64_t tile = t_lo; tile < t_hi; ++tile) {
+  const int row = tid & (S4_R - 1), half = tid >> 9;  // this thread hashes draws [t0, t1) of `row`
+  const int t0 = half ? zh : 0, t1 = half ? zeta : zh;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const int64_t r0 = tile * S4_R;
-    const int nr = (int)((a.nrows - r0) < (int64_t)S4_R ? (a.nrows - r0) : (int64_t)S4_R);
-    // ---- 1. issue the staging of Mt (async; overlaps steps 2-5).  Warp w moves column w:
-    //         each instruction 32 consecutive rows (256 contiguous global bytes); the swizzle
-    //         puts row r = 32 i + lane at r*256 + 8*(w ^ lane), all bank pairs distinct.
-    if (wid < a.J) {
-      const double* src = a.M + (int64_t)wid * a.ldm + r0 + lane;
-      const uint32_t dst = st_base;
-      if (nr == S4_R) {
-#pragma unroll
-        for (int i = 0; i < S4_R / 32; ++i) cp_async8(dst + i * 8192u, src + i * 32);
-      } else {
-        for (int i = 0; i < S4_R / 32; ++i)
-          if (i * 32 + lane < nr) cp_async8(dst + i * 8192u, src + i * 32);
-      }
-    }
-    // ---- 2. hash this thread's row; per-warp ranks per bucket q (hashing warps only)
-    const bool valid = tid < nr;
-    int kp[Z];  // bucket q (bits 0..15) | rank inside the warp's part of the bucket (bits 16..31)
+    const int nr = (int)((nrows - r0) < (int64_t)S4_R ? (nrows - r0) : (int64_t)S4_R);
+    // ---- hash (reading O5)
+    for (int i = lane; i < NQP / 2; i += 32) reinterpret_cast<uint32_t*>(cwm)[i] = 0u;
+    const bool valid = row < nr;
+    const uint64_t hbase = key + SKS_GAMMA * (16ull * (uint64_t)(row_begin + r0 + row));
+    int kq[ZH];
     uint32_t neg = 0;
-    if (hwarp) {
-      for (int i = lane; i < NQP / 2; i += 32) reinterpret_cast<uint32_t*>(cwm)[i] = 0u;
-      __syncwarp();
-      {
-        int qq[Z];
-        if (valid) {
-          if (ZETA > 0)
-            sks_column<(ZETA > 0 ? ZETA : 1)>(a.key, (uint64_t)(a.row_begin + r0 + tid), s, qq, &neg);
-          else
-            sks_column_rt(a.key, (uint64_t)(a.row_begin + r0 + tid), s, zeta, qq, &neg);
+#pragma unroll
+    for (int u = 0; u < ZH; ++u) kq[u] = 0;
+    if (valid) {
+#pragma unroll
+      for (int u = 0; u < ZH; ++u) {
+        const int t = t0 + u;
+        if (t < t1) {
+          const uint64_t w = sks_fmix64(hbase + SKS_GAMMA * (uint64_t)(t >> 1));
+          const uint32_t uu = (t & 1) ? (uint32_t)(w >> 32) : (uint32_t)(w & 0xffffffffu);
+          const uint32_t J = (uint32_t)(s - zeta + t);
+          kq[u] = (int)(((uint64_t)uu * (uint64_t)(J + 1u)) >> 32);  // raw draw v_t
         }
-#pragma unroll
-        for (int t = 0; t < Z; ++t) kp[t] = (valid && t < zeta) ? qq[t] : -1 - lane;
       }
+      neg = (uint32_t)(sks_fmix64(hbase + SKS_GAMMA * 8ull) & ((1ull << zeta) - 1ull));
+      if (half == 0) {  // Floyd among the first-half draws
 #pragma unroll
-      for (int t = 0; t < Z; ++t) {
-        if (t < zeta) {
-          const int key = kp[t];
-          const uint32_t mm = __match_any_sync(0xffffffffu, key);
-          const int base = (key >= 0) ? (int)cwm[key] : 0;
-          kp[t] = (key & 0xffff) | ((base + __popc(mm & ltmask)) << 16);
-          __syncwarp();
-          if (key >= 0 && (mm & ltmask) == 0u) cwm[key] = (uint16_t)(base + __popc(mm));
-          __syncwarp();
+        for (int u = 0; u < ZH; ++u) {
+          bool taken = false;
+#pragma unroll
+          for (int i = 0; i < u; ++i) taken |= (kq[i] == kq[u]);
+          if (taken) kq[u] = s - zeta + u;
+          if (u < t1) qa[row * ZH + u] = (uint16_t)kq[u];
         }
       }
     }
     __syncthreads();
-    // ---- 3. per-bucket prefix over the hashing warps (cw := warp offset in the bucket)
+    if (valid && half == 1) {  // Floyd for the second half against all earlier draws
+      int q0[ZH];
+#pragma unroll
+      for (int i = 0; i < ZH; ++i) q0[i] = (i < zh) ? (int)qa[row * ZH + i] : -1;
+#pragma unroll
+      for (int u = 0; u < ZH; ++u) {
+        bool taken = false;
+#pragma unroll
+        for (int i = 0; i < ZH; ++i) taken |= (q0[i] == kq[u]);
+#pragma unroll
+        for (int i = 0; i < u; ++i) taken |= (kq[i] == kq[u]);
+        if (taken) kq[u] = s - zeta + t0 + u;
+      }
+    }
+    // ---- per-warp ranks per bucket q (warp slot = wid)
+#pragma unroll
+    for (int u = 0; u < ZH; ++u) {
+      const int t = t0 + u;
+      const int k = (valid && t < t1) ? kq[u] : -1 - lane;
+      const uint32_t mm = __match_any_sync(0xffffffffu, k);
+      const int base = (k >= 0) ? (int)cwm[k] : 0;
+      kq[u] = (k & 0xffff) | ((base + __popc(mm & ltmask)) << 16);
+      __syncwarp();
+      if (k >= 0 && (mm & ltmask) == 0u) cwm[k] = (uint16_t)(base + __popc(mm));
+      __syncwarp();
+    }
+    __syncthreads();
+    // ---- per-bucket prefix over the 32 warp slots (cw := warp offset in the bucket)
     for (int q = tid; q < s; q += S4_THREADS) {
       int run = 0;
-#pragma unroll
-      for (int w = 0; w < S4_HWARPS; ++w) {
+#pragma unroll 8
+      for (int w = 0; w < S4_WARPS; ++w) {
         const int c = cw[w * NQP + q];
         cw[w * NQP + q] = (uint16_t)run;
         run += c;
@@ -334,7 +332,7 @@ __global__ void __launch_bounds__(S4_THREADS, 1) sketch_v4_kernel(SketchArgs a) 
       kst[q] = run;
     }
     __syncthreads();
-    // ---- 4. exclusive scan of the even-padded bucket sizes (one bucket per thread); pads
+    // ---- exclusive scan of the even-padded bucket sizes (one bucket per thread); pads
     {
       const int raw = (tid < s) ? kst[tid] : 0;
       const int v = raw + (raw & 1);
@@ -357,39 +355,99 @@ __global__ void __launch_bounds__(S4_THREADS, 1) sketch_v4_kernel(SketchArgs a) 
       if (tid == S4_THREADS - 1) kst[s] = ex + v;
     }
     __syncthreads();
-    // ---- 5. place this thread's entries
+    // ---- place this thread's entries
     if (valid) {
-      const uint32_t eoff = mt_s + (uint32_t)tid * 256u + 8u * s4_g((uint32_t)tid);
+      const uint32_t eoff = (uint32_t)row * 256u + 8u * s4_g((uint32_t)row);
 #pragma unroll
-      for (int t = 0; t < Z; ++t)
-        if (t < zeta) {
-          const int q = kp[t] & 0xffff;
-          ent[kst[q] + cw[wid * NQP + q] + (kp[t] >> 16)] = eoff | (((neg >> t) & 1u) << 31);
+      for (int u = 0; u < ZH; ++u) {
+        const int t = t0 + u;
+        if (t < t1) {
+          const int q = kq[u] & 0xffff;
+          ent[kst[q] + cwm[q] + (kq[u] >> 16)] = eoff | (((neg >> t) & 1u) << 31);
         }
+      }
+    }
+    __syncthreads();
+    // ---- write the plan of this tile
+    const int ne = kst[s];
+    uint32_t* ge = pent + tile * (int64_t)ES;
+    for (int i = tid; i < ne; i += S4_THREADS) ge[i] = ent[i];
+    uint16_t* gk = pkst + tile * (int64_t)KS;
+    for (int i = tid; i < KS; i += S4_THREADS) gk[i] = (uint16_t)(i <= s ? kst[i] : ne);
+    __syncthreads();
+  }
+}
+
+// ---- gather kernel: stage the batch + load the tile plan (cp.async), gather
+template <int QPW>
+__global__ void __launch_bounds__(S4_THREADS, 1) sketch_v5_kernel(SketchArgs a, const uint32_t* __restrict__ pent,
+                                                                  const uint16_t* __restrict__ pkst, int ES, int KS) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int s = a.s;
+  double* Mt = reinterpret_cast<double*>(smraw);                   // [(R+1)*32]
+  uint32_t* ent = reinterpret_cast<uint32_t*>(Mt + (S4_R + 1) * 32);  // [ES]
+  uint16_t* kst = reinterpret_cast<uint16_t*>(ent + ES);             // [KS]
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  uint32_t lane8, amask;  // opaque to the optimiser (keeps the gather address a single LOP3)
+  asm("mov.b32 %0, %1;" : "=r"(lane8) : "r"((uint32_t)lane * 8u));
+  asm("mov.b32 %0, %1;" : "=r"(amask) : "r"(0x7fffffffu));
+  const uint32_t mt_s = smem_addr(Mt), ent_s = smem_addr(ent), kst_s = smem_addr(kst);
+  const int qlo = wid * QPW;
+  const uint32_t st_base = mt_s + (uint32_t)lane * 256u + 8u * ((uint32_t)(wid ^ lane) & 31u);
+  if (tid < 32) Mt[S4_R * 32 + tid] = 0.0;
+
+  double acc[QPW];
+#pragma unroll
+  for (int i = 0; i < QPW; ++i) acc[i] = 0.0;
+
+  const int64_t t_lo = (a.tiles * blockIdx.x) / gridDim.x;
+  const int64_t t_hi = (a.tiles * (blockIdx.x + 1)) / gridDim.x;
+  for (int64_t tile = t_lo; tile < t_hi; ++tile) {
+    const int64_t r0 = tile * S4_R;
+    const int nr = (int)((a.nrows - r0) < (int64_t)S4_R ? (a.nrows - r0) : (int64_t)S4_R);
+    // ---- stage: warp w moves column w (32 consecutive rows per instruction)
+    if (wid < a.J) {
+      const double* src = a.M + (int64_t)wid * a.ldm + r0 + lane;
+      if (nr == S4_R) {
+#pragma unroll
+        for (int i = 0; i < S4_R / 32; ++i) cp_async8(st_base + i * 8192u, src + i * 32);
+      } else {
+        for (int i = 0; i < S4_R / 32; ++i)
+          if (i * 32 + lane < nr) cp_async8(st_base + i * 8192u, src + i * 32);
+      }
+    }
+    // ---- the tile's plan (16-byte chunks)
+    {
+      const uint32_t* ge = pent + tile * (int64_t)ES;
+      for (int i = tid; i < ES / 4; i += S4_THREADS) cp_async16(ent_s + 16u * i, ge + 4 * i);
+      const uint16_t* gk = pkst + tile * (int64_t)KS;
+      for (int i = tid; i < KS / 8; i += S4_THREADS) cp_async16(kst_s + 16u * i, gk + 8 * i);
     }
     cp_async_wait_all();
     __syncthreads();
-    // ---- 6. gather: warp-owned buckets, lane = column, two entries per iteration
+    // ---- gather: warp-owned buckets, lane = column, two entries per iteration; the bucket
+    //      boundaries of the warp come from one load + shuffles
     {
-      int p = (qlo < s) ? kst[qlo] : 0;
+      const int kb = (lane <= QPW) ? (int)kst[min(qlo + lane, s)] : 0;
+      int p = __shfl_sync(0xffffffffu, kb, 0);
 #pragma unroll
       for (int i = 0; i < QPW; ++i) {
-        const int q = qlo + i;
-        if (q < s) {
-          const int e = kst[q + 1];
-          double t0 = 0.0, t1 = 0.0;
+        const int e = __shfl_sync(0xffffffffu, kb, i + 1);
+        double t0a = 0.0, t1a = 0.0;
 #pragma unroll 1
-          for (; p < e; p += 2) {
-            const uint2 ee = *reinterpret_cast<const uint2*>(ent + p);
-            double x0, x1;  // both loads in flight before either is used
-            asm volatile("ld.shared.f64 %0, [%2];\n\tld.shared.f64 %1, [%3];"
-                         : "=d"(x0), "=d"(x1)
-                         : "r"((ee.x ^ lane8) & amask), "r"((ee.y ^ lane8) & amask));
-            t0 += __hiloint2double(__double2hiint(x0) ^ (int)(ee.x & 0x80000000u), __double2loint(x0));
-            t1 += __hiloint2double(__double2hiint(x1) ^ (int)(ee.y & 0x80000000u), __double2loint(x1));
-          }
-          acc[i] += t0 + t1;
+        for (; p < e; p += 2) {
+          const uint2 ee = *reinterpret_cast<const uint2*>(ent + p);
+          double x0, x1;  // both loads in flight before either is used
+          uint32_t o0, o1;  // (E ^ 8 lane) & 0x7fffffff as one LOP3 each
+          asm("lop3.b32 %0, %1, %2, %3, 0x28;" : "=r"(o0) : "r"(ee.x), "r"(lane8), "r"(amask));
+          asm("lop3.b32 %0, %1, %2, %3, 0x28;" : "=r"(o1) : "r"(ee.y), "r"(lane8), "r"(amask));
+          asm volatile("ld.shared.f64 %0, [%2];\n\tld.shared.f64 %1, [%3];"
+                       : "=d"(x0), "=d"(x1)
+                       : "r"(mt_s + o0), "r"(mt_s + o1));
+          t0a += __hiloint2double(__double2hiint(x0) ^ (int)(ee.x & 0x80000000u), __double2loint(x0));
+          t1a += __hiloint2double(__double2hiint(x1) ^ (int)(ee.y & 0x80000000u), __double2loint(x1));
         }
+        acc[i] += t0a + t1a;
       }
     }
     __syncthreads();
@@ -465,13 +523,7 @@ static cudaError_t launch_sk(const SketchArgs& a, int grid, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-// dynamic shared memory of sketch_v4_kernel for (s, zeta); static part: wsum4
-static size_t sketch_v4_smem(int s, int zeta) {
-  return 256 + sizeof(double) * (S4_R + 1) * 32 + sizeof(uint32_t) * s4_ent_words(s, zeta) + sizeof(int) * (s + 2) +
-         sizeof(uint16_t) * S4_HWARPS * s4_nqp(s) + 16;
-}
-
-static bool sketch_v4_fits(int s, int zeta) {
+static int sm_optin() {
   static int optin = 0;
   if (!optin) {
     int dev = 0;
@@ -481,34 +533,81 @@ static bool sketch_v4_fits(int s, int zeta) {
       optin = 232448;
     }
   }
-  return s <= S4_QMAX && sketch_v4_smem(s, zeta) + 1024 <= (size_t)optin;
+  return optin;
 }
 
-template <int QPW, int ZETA>
-static cudaError_t launch_v4(const SketchArgs& a, int grid, cudaStream_t st) {
-  const size_t smem = sketch_v4_smem(a.s, a.zeta);
-  static size_t set = 0;
-  if (set < smem) {
-    cudaError_t e =
-        cudaFuncSetAttribute(sketch_v4_kernel<QPW, ZETA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      return e;
-    }
-    set = smem;
+static size_t sketch_plan_smem(int s, int zeta) {
+  return sizeof(uint32_t) * s5_ent_stride(s, zeta) + sizeof(int) * (s + 4) + sizeof(uint16_t) * S4_WARPS * s4_nqp(s) +
+         sizeof(uint16_t) * S4_R * 8 + 16;
+}
+static size_t sketch_v5_smem(int s, int zeta) {
+  return sizeof(double) * (S4_R + 1) * 32 + sizeof(uint32_t) * s5_ent_stride(s, zeta) +
+         sizeof(uint16_t) * s5_kst_stride(s) + 16;
+}
+
+bool sketch_plan_supported(int s, int zeta) {
+  return s <= S4_QMAX && zeta <= SKS_ZETA_MAX && sketch_v5_smem(s, zeta) + 1024 <= (size_t)sm_optin() &&
+         sketch_plan_smem(s, zeta) + 1024 <= (size_t)sm_optin();
+}
+
+size_t sketch_plan_bytes(int64_t nrows, int s, int zeta) {
+  const int64_t tiles = (nrows + S4_R - 1) / S4_R;
+  return (size_t)tiles * (sizeof(uint32_t) * s5_ent_stride(s, zeta) + sizeof(uint16_t) * s5_kst_stride(s));
+}
+
+template <typename K>
+static cudaError_t set_smem(K kern, size_t smem, size_t* set) {
+  if (*set >= smem) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return e;
   }
-  sketch_v4_kernel<QPW, ZETA><<<grid, S4_THREADS, smem, st>>>(a);
+  *set = smem;
+  return cudaSuccess;
+}
+
+cudaError_t launch_sketch_plan(int64_t nrows, int64_t row_begin, int s, int zeta, uint64_t key, void* plan,
+                               int num_sms, cudaStream_t st) {
+  if (!sketch_plan_supported(s, zeta)) return cudaErrorInvalidValue;
+  const int64_t tiles = (nrows + S4_R - 1) / S4_R;
+  uint32_t* pent = reinterpret_cast<uint32_t*>(plan);
+  uint16_t* pkst = reinterpret_cast<uint16_t*>(pent + tiles * (int64_t)s5_ent_stride(s, zeta));
+  const size_t smem = sketch_plan_smem(s, zeta);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)num_sms * 2));
+  cudaError_t e;
+  if (zeta == 8) {
+    static size_t set8 = 0;
+    if ((e = set_smem(sketch_plan_kernel<8>, smem, &set8)) != cudaSuccess) return e;
+    sketch_plan_kernel<8><<<grid, S4_THREADS, smem, st>>>(nrows, row_begin, s, zeta, key, tiles, pent, pkst);
+  } else {
+    static size_t set0 = 0;
+    if ((e = set_smem(sketch_plan_kernel<0>, smem, &set0)) != cudaSuccess) return e;
+    sketch_plan_kernel<0><<<grid, S4_THREADS, smem, st>>>(nrows, row_begin, s, zeta, key, tiles, pent, pkst);
+  }
   return cudaGetLastError();
 }
 
-template <int ZETA>
-static cudaError_t launch_v4_z(const SketchArgs& a, int grid, cudaStream_t st) {
+template <int QPW>
+static cudaError_t launch_v5(const SketchArgs& a, const void* plan, int grid, cudaStream_t st) {
+  const size_t smem = sketch_v5_smem(a.s, a.zeta);
+  static size_t set = 0;
+  cudaError_t e = set_smem(sketch_v5_kernel<QPW>, smem, &set);
+  if (e != cudaSuccess) return e;
+  const int ES = s5_ent_stride(a.s, a.zeta), KS = s5_kst_stride(a.s);
+  const uint32_t* pent = reinterpret_cast<const uint32_t*>(plan);
+  const uint16_t* pkst = reinterpret_cast<const uint16_t*>(pent + a.tiles * (int64_t)ES);
+  sketch_v5_kernel<QPW><<<grid, S4_THREADS, smem, st>>>(a, pent, pkst, ES, KS);
+  return cudaGetLastError();
+}
+
+static cudaError_t launch_v5_q(const SketchArgs& a, const void* plan, int grid, cudaStream_t st) {
   const int span = a.s;
-  if (span <= 8 * S4_WARPS) return launch_v4<8, ZETA>(a, grid, st);
-  if (span <= 12 * S4_WARPS) return launch_v4<12, ZETA>(a, grid, st);
-  if (span <= 16 * S4_WARPS) return launch_v4<16, ZETA>(a, grid, st);
-  if (span <= 20 * S4_WARPS) return launch_v4<20, ZETA>(a, grid, st);
-  return launch_v4<24, ZETA>(a, grid, st);
+  if (span <= 8 * S4_WARPS) return launch_v5<8>(a, plan, grid, st);
+  if (span <= 12 * S4_WARPS) return launch_v5<12>(a, plan, grid, st);
+  if (span <= 16 * S4_WARPS) return launch_v5<16>(a, plan, grid, st);
+  if (span <= 20 * S4_WARPS) return launch_v5<20>(a, plan, grid, st);
+  return launch_v5<24>(a, plan, grid, st);
 }
 
 template <int ZETA>
@@ -530,7 +629,7 @@ size_t sketch_part_doubles(int grid, int J, int s) { return (size_t)grid * J * s
 // SM[:, 0..J) (column-major, ld = ldo) = S_key M[:, 0..J) for rows [row_begin, row_begin+nrows)
 cudaError_t launch_sketch(const double* M, int64_t ldm, int64_t nrows, int64_t row_begin, int J, int s,
                           int zeta, uint64_t key, double* part, int grid, double* out, int64_t ldo,
-                          int accumulate, cudaStream_t st, int64_t* launches) {
+                          int accumulate, cudaStream_t st, int64_t* launches, const void* plan) {
   if (J < 1 || J > SKS_JB) return cudaErrorInvalidValue;
   SketchArgs a;
   a.M = M;
@@ -545,10 +644,11 @@ cudaError_t launch_sketch(const double* M, int64_t ldm, int64_t nrows, int64_t r
   a.part = part;
   a.tiles = (nrows + SK_R - 1) / SK_R;
   a.vec_ok = ((((uintptr_t)M) & 15) == 0) && (ldm % 2 == 0);
-  if (sketch_v4_fits(s, zeta)) {
+  if (plan != nullptr) {
+    if (!sketch_plan_supported(s, zeta)) return cudaErrorInvalidValue;
     a.q_base = 0;
     a.tiles = (nrows + S4_R - 1) / S4_R;
-    cudaError_t e = (zeta == 8) ? launch_v4_z<8>(a, grid, st) : launch_v4_z<0>(a, grid, st);
+    cudaError_t e = launch_v5_q(a, plan, grid, st);
     if (e != cudaSuccess) return e;
     if (launches) ++*launches;
     const int64_t tot = (int64_t)J * s;

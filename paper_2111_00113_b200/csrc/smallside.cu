@@ -140,136 +140,155 @@ static cudaError_t launch_bgs_gemm(GemmArgs g, bool ak, double* ws, int* cnt, cu
 
 size_t bgs_workspace_doubles(int s, int ncol) { return (size_t)8 * ((std::max(s, ncol) + 31) / 32 * 32) * 32; }
 
-// One CTA: CGS2 QR of the panel X (s x J row-major, already projected against U),
-// writes U[:, j0..j0+J), T[j0.., j0..], updates the residual vector rvec (length s),
-// rho[j] = u_j^T rvec_{j-1}, rest[j] = ||rvec_j||, early exit (ctrl).
+// One CTA: thin QR of the panel X (s x J row-major, already projected twice against U) by
+// shifted Cholesky QR, three passes (sCholQR3: pass 1 factors X^T X + sigma I with
+// sigma = 11 (sJ + J(J+1)) u ||X||_F^2, passes 2-3 are plain CholQR; orthogonality O(u) for
+// kappa(X) up to O(1/u)).  Writes U[:, j0..j0+J), T[j0.., j0..] = R3 R2 R1, updates the
+// residual vector rvec (length s): rho[j] = u_j^T r_{j-1}, rest[j] = ||r_j|| with the
+// explicit vectors r_j = r - sum_{i<=j} rho_i u_i (one warp per j: no cancellation), and the
+// early-exit test (reading O16).  A pivot that is not positive marks the panel rank deficient
+// at that column (columns from there on are not used).
+constexpr int PJ = SKS_JB;  // max panel width
+constexpr int PL = PJ + 1;  // smem row stride of the 32 x 32 factors
+
 __global__ void __launch_bounds__(1024) panel_kernel(double* __restrict__ X, int s, int J, int j0,
                                                      double* __restrict__ U, int ldu, double* __restrict__ T,
                                                      int ldT, double* __restrict__ rvec, double* __restrict__ rho,
                                                      double* __restrict__ rest, CtrlBlock* ctrl, int track_res,
                                                      int max_cols) {
   extern __shared__ double sm[];
-  const int L = J + 1;            // odd smem row stride: conflict-free column walks
-  double* sX = sm;               // s x J, row stride L
-  double* sr = sX + (size_t)s * L;  // s
-  __shared__ double red[32];
-  __shared__ double zsh[SKS_JB];
-  __shared__ double bc;
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  const int L = J + 1;               // odd smem row stride
+  double* sX = sm;                   // s x J, row stride L
+  double* sr = sX + (size_t)s * L;   // s
+  __shared__ double G[PJ * PL];      // Gram / Cholesky factor of the current pass
+  __shared__ double Rt[PJ * PL];     // accumulated R (upper)
+  __shared__ double Rn[PJ * PL];     // scratch for the product
+  __shared__ double rh[PJ];
+  __shared__ int nbad;               // first rank-deficient column (J if none)
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
+  const int Jv = max(0, min(J, max_cols - j0));
   for (int i = tid; i < s * J; i += nt) sX[(i / J) * L + (i % J)] = X[i];
   if (track_res)
     for (int i = tid; i < s; i += nt) sr[i] = rvec[i];
+  {
+    const int i = tid >> 5, j = tid & 31;
+    Rt[i * PL + j] = (i == j) ? 1.0 : 0.0;
+  }
+  if (tid == 0) nbad = Jv;
   __syncthreads();
-  int rankdef = 0;
-  for (int c = 0; c < J; ++c) {
-    if (j0 + c >= max_cols) break;
-    double tcol[SKS_JB];
-    for (int i = 0; i < SKS_JB; ++i) tcol[i] = 0.0;
-    for (int pass = 0; pass < 2; ++pass) {
-      // z_i = x_i . x_c for i < c  (warp i)
-      for (int i = wid; i < c; i += nw) {
-        double a = 0.0;
-        for (int q = lane; q < s; q += 32) a += sX[q * L + i] * sX[q * L + c];
-        a = warp_sum(a);
-        if (lane == 0) zsh[i] = a;
-      }
-      __syncthreads();
-      for (int q = tid; q < s; q += nt) {
-        double v = sX[q * L + c];
-        for (int i = 0; i < c; ++i) v -= sX[q * L + i] * zsh[i];
-        sX[q * L + c] = v;
-      }
-      for (int i = 0; i < c; ++i) tcol[i] += zsh[i];
-      __syncthreads();
+  for (int pass = 0; pass < 3; ++pass) {
+    const int Jc = nbad;  // columns still factored
+    // ---- Gram G = X^T X (thread (i, j), i = warp, j = lane)
+    {
+      const int i = tid >> 5, j = tid & 31;
+      double g = 0.0;
+      if (i < Jc && j < Jc && i <= j)
+        for (int q = 0; q < s; ++q) g += sX[q * L + i] * sX[q * L + j];
+      G[i * PL + j] = g;
     }
-    double a = 0.0;
-    for (int q = tid; q < s; q += nt) a += sX[q * L + c] * sX[q * L + c];
-    a = warp_sum(a);
-    if (lane == 0) red[wid] = a;
     __syncthreads();
+    // ---- Cholesky G = R^T R (upper R in place), one warp; lane j owns column j
     if (wid == 0) {
-      double t = lane < nw ? red[lane] : 0.0;
-      t = warp_sum(t);
-      if (lane == 0) bc = sqrt(t);
-    }
-    __syncthreads();
-    const double nrm = bc;
-    const bool zero = !(nrm > 0.0) || !isfinite(nrm);
-    if (zero) rankdef = 1;
-    const double inv = zero ? 0.0 : 1.0 / nrm;
-    for (int q = tid; q < s; q += nt) {
-      const double v = sX[q * L + c] * inv;
-      sX[q * L + c] = v;
-      U[q + (int64_t)(j0 + c) * ldu] = v;
-    }
-    if (tid == 0) {
-      for (int i = 0; i < c; ++i) T[(j0 + i) + (int64_t)(j0 + c) * ldT] = tcol[i];
-      T[(j0 + c) + (int64_t)(j0 + c) * ldT] = nrm;
-      for (int i = j0 + c + 1; i < max_cols && i < j0 + J; ++i) T[i + (int64_t)(j0 + c) * ldT] = 0.0;
-    }
-    __syncthreads();
-    if (track_res) {
-      // rho = u_c . r ; r -= rho u_c ; rest = ||r||
-      double b = 0.0;
-      for (int q = tid; q < s; q += nt) b += sX[q * L + c] * sr[q];
-      b = warp_sum(b);
-      if (lane == 0) red[wid] = b;
-      __syncthreads();
-      if (wid == 0) {
-        double t = lane < nw ? red[lane] : 0.0;
-        t = warp_sum(t);
-        if (lane == 0) bc = t;
+      double shift = 0.0;
+      if (pass == 0) {
+        double tr = lane < Jc ? G[lane * PL + lane] : 0.0;
+        tr = warp_sum(tr);
+        shift = 11.0 * ((double)s * Jc + (double)Jc * (Jc + 1)) * 1.1102230246251565e-16 * tr;
+        if (lane < Jc) G[lane * PL + lane] += shift;
       }
-      __syncthreads();
-      const double rh = bc;
+      __syncwarp();
+      int bad = Jc;
+      for (int k = 0; k < Jc; ++k) {
+        const double d = G[k * PL + k];
+        if (!(d > 0.0) || !isfinite(d)) {
+          bad = k;
+          break;
+        }
+        const double rk = sqrt(d);
+        __syncwarp();
+        if (lane == k) G[k * PL + k] = rk;
+        if (lane > k && lane < Jc) G[k * PL + lane] /= rk;
+        __syncwarp();
+        if (lane > k && lane < Jc) {
+          const double gkj = G[k * PL + lane];
+          for (int i = k + 1; i <= lane; ++i) G[i * PL + lane] -= G[k * PL + i] * gkj;
+        }
+        __syncwarp();
+      }
+      if (lane == 0) nbad = bad;
+    }
+    __syncthreads();
+    const int Jn = nbad;
+    // ---- X <- X R^-1 (thread per row, forward substitution over the columns)
+    for (int q = tid; q < s; q += nt) {
+      double* xr = sX + q * L;
+      for (int j = 0; j < Jn; ++j) {
+        double v = xr[j];
+        for (int i = 0; i < j; ++i) v -= xr[i] * G[i * PL + j];
+        xr[j] = v / G[j * PL + j];
+      }
+    }
+    // ---- Rt <- R Rt (upper triangular product)
+    {
+      const int i = tid >> 5, j = tid & 31;
+      double v = 0.0;
+      if (i <= j && j < Jn)
+        for (int l = i; l <= j; ++l) v += G[i * PL + l] * Rt[l * PL + j];
+      Rn[i * PL + j] = v;
+    }
+    __syncthreads();
+    {
+      const int i = tid >> 5, j = tid & 31;
+      if (j < Jn) Rt[i * PL + j] = Rn[i * PL + j];
+    }
+    __syncthreads();
+  }
+  const int Jg = nbad;  // good columns
+  // ---- outputs: U columns, T block
+  for (int i = tid; i < s * Jg; i += nt) {
+    const int q = i % s, c = i / s;
+    U[q + (int64_t)(j0 + c) * ldu] = sX[q * L + c];
+  }
+  {
+    const int i = tid >> 5, j = tid & 31;
+    if (j < Jg && i < Jv) T[(j0 + i) + (int64_t)(j0 + j) * ldT] = (i <= j) ? Rt[i * PL + j] : 0.0;
+  }
+  if (track_res && Jg > 0) {
+    // rho_c = u_c . r  (warp c)
+    if (wid < Jg) {
+      double t = 0.0;
+      for (int q = lane; q < s; q += 32) t += sX[q * L + wid] * sr[q];
+      t = warp_sum(t);
+      if (lane == 0) rh[wid] = t;
+    }
+    __syncthreads();
+    // rest_c = || r - sum_{i<=c} rho_i u_i ||  (warp c, explicit residual vector)
+    if (wid < Jg) {
       double e = 0.0;
-      for (int q = tid; q < s; q += nt) {
-        const double v = sr[q] - rh * sX[q * L + c];
-        sr[q] = v;
+      for (int q = lane; q < s; q += 32) {
+        double v = sr[q];
+        for (int i = 0; i <= wid; ++i) v -= rh[i] * sX[q * L + i];
         e += v * v;
+        if (wid == Jg - 1) rvec[q] = v;
       }
       e = warp_sum(e);
-      __syncthreads();
-      if (lane == 0) red[wid] = e;
-      __syncthreads();
-      if (tid == 0) {
-        double t = 0.0;
-        for (int i = 0; i < nw; ++i) t += red[i];
-        const double re = sqrt(t);
-        rho[j0 + c] = rh;
-        rest[j0 + c] = re;
-        ctrl->r_est_last = re;
-        if (ctrl->exit_cols == 0 && !rankdef && re <= ctrl->thr) ctrl->exit_cols = j0 + c + 1;
+      if (lane == 0) {
+        rho[j0 + wid] = rh[wid];
+        rest[j0 + wid] = sqrt(e);
+        Rn[wid] = sqrt(e);
       }
-      __syncthreads();
     }
-    if (tid == 0) ctrl->qr_cols = j0 + c + 1;
-    if (rankdef) break;
+    __syncthreads();
+    if (tid == 0) {
+      for (int c = 0; c < Jg; ++c) {
+        ctrl->r_est_last = Rn[c];
+        if (ctrl->exit_cols == 0 && Rn[c] <= ctrl->thr) ctrl->exit_cols = j0 + c + 1;
+      }
+    }
   }
-  if (track_res)
-    for (int i = tid; i < s; i += nt) rvec[i] = sr[i];
-  if (tid == 0 && rankdef) ctrl->rank_def = 1;
-}
-
-// one warp: back substitution T[:n,:n] y = b (upper, column-major), then out[i] = y[i]*scale[i]
-// (scale may be NULL); also writes y to yout if non-NULL
-__global__ void trsv_upper_kernel(const double* __restrict__ T, int ldT, int n, const double* __restrict__ b,
-                                  const double* __restrict__ scale, double* __restrict__ yout,
-                                  double* __restrict__ out) {
-  extern __shared__ double y[];
-  const int lane = threadIdx.x;
-  for (int i = lane; i < n; i += 32) y[i] = b[i];
-  __syncwarp();
-  for (int i = n - 1; i >= 0; --i) {
-    if (lane == 0) y[i] = y[i] / T[i + (int64_t)i * ldT];
-    __syncwarp();
-    const double yi = y[i];
-    for (int l = lane; l < i; l += 32) y[l] -= T[l + (int64_t)i * ldT] * yi;
-    __syncwarp();
-  }
-  for (int i = lane; i < n; i += 32) {
-    if (yout) yout[i] = y[i];
-    if (out) out[i] = scale ? y[i] * scale[i] : y[i];
+  if (tid == 0) {
+    if (Jg > 0) ctrl->qr_cols = j0 + Jg;
+    if (Jg < Jv) ctrl->rank_def = 1;
   }
 }
 
@@ -333,6 +352,23 @@ __device__ void cta_trsv(const double* __restrict__ T, int ldT, int n, double* y
       }
     }
     __syncthreads();
+  }
+}
+
+// back substitution T[:n,:n] y = b (upper, column-major), then out[i] = y[i]*scale[i] (scale may be
+// NULL); also writes y to yout if non-NULL.  Blocked, one CTA (yhat = T^-1 U^T g).
+__global__ void __launch_bounds__(CN_T) trsv_upper_kernel(const double* __restrict__ T, int ldT, int n,
+                                                          const double* __restrict__ b,
+                                                          const double* __restrict__ scale,
+                                                          double* __restrict__ yout, double* __restrict__ out) {
+  extern __shared__ double y[];
+  __shared__ double blk[32 * 33];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) y[i] = b[i];
+  __syncthreads();
+  cta_trsv(T, ldT, n, y, false, blk);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    if (yout) yout[i] = y[i];
+    if (out) out[i] = scale ? y[i] * scale[i] : y[i];
   }
 }
 
@@ -592,7 +628,7 @@ cudaError_t launch_panel(double* X, int s, int J, int j0, double* U, int ldu, do
 cudaError_t launch_trsv(const double* T, int ldT, int n, const double* b, const double* scale, double* yout,
                         double* out, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  trsv_upper_kernel<<<1, 32, sizeof(double) * n, st>>>(T, ldT, n, b, scale, yout, out);
+  trsv_upper_kernel<<<1, CN_T, sizeof(double) * n, st>>>(T, ldT, n, b, scale, yout, out);
   return cudaGetLastError();
 }
 
