@@ -27,6 +27,13 @@ cudaError_t launch_step_stencil_tma(const StepArgs& a, const double* W, int64_t 
                                     const double* fb, const double* vb, int grid, cudaStream_t st, void** cache);
 void stencil_tma_free(void* cache);
 
+// stencil_zm.cu (3D, even m: TMA-fed z-march kernel)
+bool stencil_zm_supported(int dim, int64_t m, int k);
+void stencil_zm_tiling(int64_t m, int64_t nz, int num_sms, StepArgs* a, int* grid);
+cudaError_t launch_step_stencil_zm(const StepArgs& a, const double* W, int64_t ncol, const double* xb,
+                                   const double* fb, const double* vb, int grid, cudaStream_t st, void** cache);
+void stencil_zm_free(void* cache);
+
 // sketch.cu
 int sketch_grid(int num_sms, int64_t nrows);
 size_t sketch_part_doubles(int grid, int J, int s);

@@ -11,6 +11,7 @@
 //     of U and of w_j in registers (5 shared loads per 7-point stencil instead of 7).
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -328,8 +329,15 @@ static size_t tma_smem(int dim, int KM, int NST) {
   return 128 + sizeof(double) * ((size_t)NST * (QU2 + (KM - 1) * QB2P) + QV2P);
 }
 
+static int tma_env(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
 static int tma_nst(int dim, int KM) {
+  const int want = tma_env("SKS_TMA_NST", 2);
   const size_t lim = 200 * 1024;
+  if (want == 1 && tma_smem(dim, KM, 1) <= lim) return 1;
   if (tma_smem(dim, KM, 2) <= lim) return 2;
   if (tma_smem(dim, KM, 1) <= lim) return 1;
   return 0;
@@ -388,7 +396,7 @@ void stencil_tma_tiling(int dim, int64_t m, int64_t nz, int num_sms, StepArgs* a
     a->ntiles = (int64_t)a->tiles_x * a->tiles_y;
   }
   a->zchunk = 0;
-  *grid = (int)std::max<int64_t>(1, std::min<int64_t>(a->ntiles, num_sms));
+  *grid = (int)std::max<int64_t>(1, std::min<int64_t>(a->ntiles, (int64_t)num_sms * tma_env("SKS_TMA_CPS", 1)));
 }
 
 // mode 0: U = column j-1, V_l = columns lo+l of W; mode 1: U = x, V0 = f; mode 2: U = v0.

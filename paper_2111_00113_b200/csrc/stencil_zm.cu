@@ -1,0 +1,337 @@
+// stencil_zm.cu -- fused truncated-Arnoldi step for the 3D 7-point operator, z-march design.
+//
+// Same arithmetic as step.cuh / stencil.cu (one launch produces w_j and the next step's
+// partial sums, Eq. partorth, Alg. 1), organised to minimise on-chip
+// traffic:
+//
+//   * a CTA owns an xy tile of TX x TY = 32 x 16 output columns and marches through a range
+//     of z planes, ZS planes per step; all CTAs together get equal shares of the
+//     (tile, plane) units, so the persistent grid (one CTA per SM) is balanced for any m
+//     and slab depth;
+//   * per step the TMA brings ZS+2 U planes (36 x 20, 2-point xy halo) and ZS planes of each
+//     window vector V_l (36 x 18) into one of two stages (mbarrier completion; the next
+//     step's stage is in flight during this step); out-of-bounds boxes are zero-filled, so
+//     the Dirichlet x/y boundary costs nothing;
+//   * each of the 34 x 18 W-box threads owns one xy column: it forms w_j for ZS planes from
+//     the staged U/V (z neighbours in registers), stores them into a ring of 2 ZS + 2 w_j
+//     planes, and -- after ONE __syncthreads per step -- interior threads form A w_j for
+//     the ZS planes one behind, store w_j and accumulate ||w||^2, <w,Aw>, ||Aw||^2 and the
+//     window dots in registers.
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+#include <cstring>
+
+#include "common.cuh"
+#include "internal.h"
+#include "step.cuh"
+#include "tma.cuh"
+
+namespace sks {
+
+constexpr int ZX = 32, ZY = 16;                  // output tile
+constexpr int ZWX = ZX + 2, ZWY = ZY + 2;        // W box 34 x 18 (one thread per column)
+constexpr int ZUX = ZX + 4, ZUY = ZY + 4;        // U plane box 36 x 20
+constexpr int ZVX = ZX + 4, ZVY = ZY + 2;        // V plane box 36 x 18 (origin x0-2: 16-byte aligned)
+constexpr int ZUP = ZUX * ZUY;                   // 720 doubles per U plane
+constexpr int ZVP = ZVX * ZVY;                   // 648 doubles per V plane
+constexpr int ZW = ZWX * ZWY;                    // 612
+constexpr int ZT = 640;                          // threads (20 warps; 28 idle in the compute)
+
+struct ZmArgs {
+  int ucol;
+  int vcol[SKS_KMAX];
+  int ncolxy;      // xy tiles
+  int tiles_x;
+  int64_t units;   // ncolxy * nz
+};
+
+__host__ __device__ constexpr int zm_al16(int d) { return (d + 15) & ~15; }  // 128-byte multiple (doubles)
+template <int KM, int ZS>
+__host__ __device__ constexpr int zm_ublk() { return zm_al16(ZUP * (ZS + 2)); }
+template <int KM, int ZS>
+__host__ __device__ constexpr int zm_vblk() { return zm_al16(ZVP * ZS); }
+template <int KM, int ZS>
+__host__ __device__ constexpr int zm_stage() { return zm_ublk<KM, ZS>() + (KM - 1) * zm_vblk<KM, ZS>(); }
+template <int KM, int ZS>
+__host__ __device__ constexpr size_t zm_smem_bytes() {
+  return 128 + sizeof(double) * ((size_t)2 * zm_stage<KM, ZS>() + (size_t)(2 * ZS + 2) * ZW);
+}
+
+template <int KM, int ZS>
+__global__ void __launch_bounds__(ZT, 1)
+    step3d_zm_kernel(StepArgs a, ZmArgs z, const __grid_constant__ CUtensorMap tmU,
+                     const __grid_constant__ CUtensorMap tmV) {
+  extern __shared__ __align__(128) unsigned char smraw_z[];
+  double* sm = reinterpret_cast<double*>(smraw_z + ((128u - (smem_u32(smraw_z) & 127u)) & 127u));
+  constexpr int STG = zm_stage<KM, ZS>();
+  constexpr int UB = zm_ublk<KM, ZS>(), VB = zm_vblk<KM, ZS>();
+  constexpr int R = 2 * ZS + 2;  // w_j plane ring
+  double* ring = sm + 2 * STG;
+  __shared__ StepCoef cf;
+  __shared__ double red[SKS_NP * 32];
+  __shared__ __align__(8) uint64_t bar[2];
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    tma_prefetch_desc(&tmU);
+    tma_prefetch_desc(&tmV);
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  if (!step_prologue(a, &cf, red)) return;  // contains __syncthreads
+  const int nv = cf.nv;
+  const uint32_t sbytes = (uint32_t)(ZUP * (ZS + 2) * 8 + nv * ZVP * ZS * 8);
+  const int m = (int)a.m, nz = (int)a.nz, z0g = (int)a.z0, G = a.G;
+  const int64_t pl = a.plane;
+  const double cc = a.cc, cm = a.cm, cp = a.cp, alpha = cf.alpha, beta_u = cf.beta_u;
+  double cl[KM - 1];
+#pragma unroll
+  for (int l = 0; l < KM - 1; ++l) cl[l] = (l < nv) ? cf.c[l] : 0.0;
+  const bool uslot = cf.uslot >= 0;
+  double* Wout = a.W + (a.mode == 0 ? (int64_t)a.j * a.ld : 0) + a.off;
+
+  // this thread's W-box column
+  const bool wt = tid < ZW;
+  const int bx = tid % ZWX, by = tid / ZWX;
+  const int cu = (by + 1) * ZUX + (bx + 1);  // U-plane offset of the column
+  const int cvv = by * ZVX + (bx + 1);       // V-plane offset
+  const int cwb = by * ZWX + bx;             // W-plane offset
+  const bool inner = wt && bx >= 1 && bx <= ZX && by >= 1 && by <= ZY;
+
+  double acc[KM + 3];
+#pragma unroll
+  for (int i = 0; i < KM + 3; ++i) acc[i] = 0.0;
+
+  uint32_t phase = 0;  // parity bits of the two stage barriers
+  uint32_t sidx = 0;   // global stage counter (slot = sidx & 1)
+  const int64_t u_lo = (z.units * blockIdx.x) / gridDim.x, u_hi = (z.units * (blockIdx.x + 1)) / gridDim.x;
+  for (int64_t u = u_lo; u < u_hi;) {
+    const int col = (int)(u / nz);
+    const int za = (int)(u % nz);
+    const int64_t zr = za + (u_hi - u);
+    const int zb = (int)(zr < nz ? zr : nz);
+    u += zb - za;
+    const int tx = col % z.tiles_x, ty = col / z.tiles_x;
+    const int x0 = tx * ZX, y0 = ty * ZY;
+    const int wa = za - 1;                         // first w_j plane of the piece
+    const int nsteps = (zb - wa + 1 + ZS - 1) / ZS;  // w_j planes wa .. zb
+    const uint32_t s0 = sidx;
+    auto issue = [&](int t) {  // stage t: U planes [wa+t ZS-1, wa+t ZS+ZS], V planes [wa+t ZS, +ZS)
+      const uint32_t slot = (s0 + (uint32_t)t) & 1u;
+      double* dst = sm + slot * STG;
+      const int p0 = wa + t * ZS;
+      mbar_arrive_expect_tx(&bar[slot], sbytes);
+      tma_load_4d(dst, &tmU, &bar[slot], x0 - 2, y0 - 2, p0 - 1 + G, z.ucol);
+      for (int l = 0; l < nv; ++l) tma_load_4d(dst + UB + l * VB, &tmV, &bar[slot], x0 - 2, y0 - 1, p0 + G, z.vcol[l]);
+    };
+    if (tid == 0) {
+      issue(0);
+      if (nsteps > 1) issue(1);
+    }
+    double wp1 = 0.0, wp2 = 0.0;  // w_j at planes p0-1, p0-2 (carried)
+    double vlast[KM - 1];         // V_l at plane p0-1 (carried)
+#pragma unroll
+    for (int l = 0; l < KM - 1; ++l) vlast[l] = 0.0;
+    const int gxw = x0 - 1 + bx, gyw = y0 - 1 + by;  // global xy of this W column
+    const bool xyin = wt && (unsigned)gxw < (unsigned)m && (unsigned)gyw < (unsigned)m;
+    const bool aw = inner && gxw < m && gyw < m;    // this thread forms A w_j (interior output)
+    double* wcol = Wout + (int64_t)(wa - 1) * pl + (int64_t)gyw * m + gxw;  // plane wa-1 of the column
+    int rs = (wa + R) % R;  // ring slot of plane p0
+    for (int t = 0; t < nsteps; ++t) {
+      const uint32_t slot = (s0 + (uint32_t)t) & 1u;
+      mbar_wait(&bar[slot], (phase >> slot) & 1u);
+      phase ^= 1u << slot;
+      const double* sU = sm + slot * STG;
+      const double* sV = sU + UB;
+      const int p0 = wa + t * ZS;
+      double w[ZS], c[ZS + 2], v[KM - 1][ZS];
+      // ---- w_j on planes p0 .. p0+ZS-1 (this thread's column)
+#pragma unroll
+      for (int k = 0; k < ZS + 2; ++k) c[k] = wt ? sU[k * ZUP + cu] : 0.0;
+#pragma unroll
+      for (int i = 0; i < ZS; ++i) {
+        const int p = p0 + i;
+#pragma unroll
+        for (int l = 0; l < KM - 1; ++l) v[l][i] = (wt && l < nv) ? sV[l * VB + i * ZVP + cvv] : 0.0;
+        const double* q = sU + (i + 1) * ZUP + cu;
+        double wv = 0.0;
+        if (xyin && (unsigned)(z0g + p) < (unsigned)m && p <= zb) {
+          const double Au = cc * c[i + 1] + cm * (q[-1] + q[-ZUX] + c[i]) + cp * (q[1] + q[ZUX] + c[i + 2]);
+          wv = alpha * Au + beta_u * c[i + 1];
+#pragma unroll
+          for (int l = 0; l < KM - 1; ++l)
+            if (l < nv) wv += cl[l] * v[l][i];
+        }
+        w[i] = wv;
+        const int si = (rs + i < R) ? rs + i : rs + i - R;
+        if (wt) ring[si * ZW + cwb] = wv;
+      }
+      __syncthreads();
+      if (tid == 0 && t + 2 < nsteps) issue(t + 2);  // the stage just consumed is free
+      // ---- A w_j on planes p0-1 .. p0+ZS-2
+      if (aw) {
+#pragma unroll
+        for (int i = 0; i < ZS; ++i) {
+          const int qp = p0 - 1 + i;
+          if (qp >= za && qp < zb) {
+            const double wq = (i == 0) ? wp1 : w[i - 1];
+            const double wqm = (i == 0) ? wp2 : (i == 1 ? wp1 : w[i - 2]);
+            const int si = (rs + i - 1 < 0) ? rs + i - 1 + R : (rs + i - 1 < R ? rs + i - 1 : rs + i - 1 - R);
+            const double* r = ring + si * ZW + cwb;
+            const double Aw = cc * wq + cm * (r[-1] + r[-ZWX] + wqm) + cp * (r[1] + r[ZWX] + w[i]);
+            wcol[(int64_t)i * pl] = wq;
+            acc[0] += wq * wq;
+            acc[1] += wq * Aw;
+            acc[2] += Aw * Aw;
+            if (uslot) acc[KM + 2] += c[i] * Aw;
+#pragma unroll
+            for (int l = 0; l < KM - 1; ++l)
+              if (l < nv) acc[3 + l] += ((i == 0) ? vlast[l] : v[l][i - 1]) * Aw;
+          }
+        }
+      }
+      if (ZS >= 2) {
+        wp2 = w[ZS >= 2 ? ZS - 2 : 0];
+        wp1 = w[ZS - 1];
+      } else {
+        wp2 = wp1;
+        wp1 = w[0];
+      }
+#pragma unroll
+      for (int l = 0; l < KM - 1; ++l) vlast[l] = v[l][ZS - 1];
+      wcol += (int64_t)ZS * pl;
+      rs = (rs + ZS < R) ? rs + ZS : rs + ZS - R;
+    }
+    sidx = s0 + (uint32_t)nsteps;
+    __syncthreads();  // ring and stages are reused by the next piece
+  }
+  step_epilogue<KM>(a, &cf, acc, red);
+}
+
+// ---------------------------------------------------------------- host side
+static PFN_cuTensorMapEncodeTiled_v12000 g_enc_zm = nullptr;
+
+static bool zm_encode_fn() {
+  if (g_enc_zm) return true;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !fn) {
+    cudaGetLastError();
+    return false;
+  }
+  g_enc_zm = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return true;
+}
+
+// 4D map {x: m, y: m, z_storage: nz+2G, column: ncol} over columns of pitch ld; one plane per box
+static bool zm_encode(CUtensorMap* out, const double* base, int64_t m, int64_t nz, int G, int64_t ld, int64_t ncol,
+                      bool ubox, int bdepth) {
+  if (!zm_encode_fn()) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)m, (cuuint64_t)m, (cuuint64_t)(nz + 2 * G), (cuuint64_t)ncol};
+  cuuint64_t strides[3] = {(cuuint64_t)(m * 8), (cuuint64_t)(m * m * 8), (cuuint64_t)(ld * 8)};
+  cuuint32_t box[4] = {(cuuint32_t)(ubox ? ZUX : ZVX), (cuuint32_t)(ubox ? ZUY : ZVY), (cuuint32_t)bdepth, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = g_enc_zm(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+struct ZmMaps {
+  CUtensorMap WU, WV, XU, FV, VU;
+  const void* key[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+};
+
+template <int KM>
+constexpr int zm_zs() {
+  return zm_smem_bytes<KM, 4>() <= 200 * 1024 ? 4 : (zm_smem_bytes<KM, 2>() <= 200 * 1024 ? 2 : 1);
+}
+
+bool stencil_zm_supported(int dim, int64_t m, int k) {
+  if (dim != 3 || m % 2) return false;  // TMA global strides must be multiples of 16 bytes
+  const char* e = getenv("SKS_NO_ZM");
+  if (e && e[0] == '1') return false;
+  return zm_encode_fn();
+}
+
+void stencil_zm_tiling(int64_t m, int64_t nz, int num_sms, StepArgs* a, int* grid) {
+  a->tiles_x = (int)((m + ZX - 1) / ZX);
+  a->tiles_y = (int)((m + ZY - 1) / ZY);
+  a->zchunk = 0;
+  a->ntiles = (int64_t)a->tiles_x * a->tiles_y * nz;  // (tile, plane) units
+  *grid = (int)std::max<int64_t>(1, std::min<int64_t>(a->ntiles, num_sms));
+}
+
+template <int KM>
+static cudaError_t zm_launch(const StepArgs& a, const ZmArgs& z, const CUtensorMap& mu, const CUtensorMap& mv,
+                             int grid, cudaStream_t st) {
+  constexpr int ZS = zm_zs<KM>();
+  const size_t smem = zm_smem_bytes<KM, ZS>();
+  static bool set = false;
+  if (!set) {
+    cudaError_t e = cudaFuncSetAttribute(step3d_zm_kernel<KM, ZS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return e;
+    }
+    set = true;
+  }
+  step3d_zm_kernel<KM, ZS><<<grid, ZT, smem, st>>>(a, z, mu, mv);
+  return cudaGetLastError();
+}
+
+// mode 0: U = column j-1, V_l = columns lo+l of W; mode 1: U = x, V0 = f; mode 2: U = v0.
+cudaError_t launch_step_stencil_zm(const StepArgs& a, const double* W, int64_t ncol, const double* xb,
+                                   const double* fb, const double* vb, int grid, cudaStream_t st, void** cache) {
+  ZmMaps* mp = reinterpret_cast<ZmMaps*>(*cache);
+  if (!mp) {
+    mp = new ZmMaps();
+    *cache = mp;
+  }
+  const int km = step_km(a.k);
+  const int zs = km == 2 ? zm_zs<2>() : (km == 4 ? zm_zs<4>() : zm_zs<8>());
+  auto upd = [&](CUtensorMap* mpp, int slot, const double* base, int64_t nc, bool ub) -> bool {
+    const void* key = reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(base) ^
+                                                    (uintptr_t)(a.ld * 1315423911ull + a.nz * 2654435761ull +
+                                                                a.m * 97ull + nc * 7ull + zs * 31ull));
+    if (mp->key[slot] == key) return true;
+    if (!zm_encode(mpp, base, a.m, a.nz, a.G, a.ld, nc, ub, ub ? zs + 2 : zs)) return false;
+    mp->key[slot] = key;
+    return true;
+  };
+  ZmArgs z;
+  memset(&z, 0, sizeof(z));
+  z.tiles_x = a.tiles_x;
+  z.ncolxy = a.tiles_x * a.tiles_y;
+  z.units = a.ntiles;
+  const CUtensorMap* mu;
+  const CUtensorMap* mv;
+  if (a.mode == 0) {
+    if (!upd(&mp->WU, 0, W, ncol, true) || !upd(&mp->WV, 1, W, ncol, false)) return cudaErrorInvalidValue;
+    mu = &mp->WU;
+    mv = &mp->WV;
+    const int lo = std::max(0, a.j - a.k);
+    z.ucol = a.j - 1;
+    for (int l = 0; l < a.j - 1 - lo; ++l) z.vcol[l] = lo + l;
+  } else if (a.mode == 1) {
+    if (!upd(&mp->XU, 2, xb, 1, true) || !upd(&mp->FV, 3, fb, 1, false)) return cudaErrorInvalidValue;
+    mu = &mp->XU;
+    mv = &mp->FV;
+  } else {
+    if (!upd(&mp->VU, 4, vb, 1, true) || !upd(&mp->WV, 1, W, ncol, false)) return cudaErrorInvalidValue;
+    mu = &mp->VU;
+    mv = &mp->WV;  // unused (nv = 0)
+  }
+  switch (km) {
+    case 2: return zm_launch<2>(a, z, *mu, *mv, grid, st);
+    case 4: return zm_launch<4>(a, z, *mu, *mv, grid, st);
+    default: return zm_launch<8>(a, z, *mu, *mv, grid, st);
+  }
+}
+
+void stencil_zm_free(void* cache) { delete reinterpret_cast<ZmMaps*>(cache); }
+
+}  // namespace sks

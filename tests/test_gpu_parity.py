@@ -87,10 +87,20 @@ def test_apply_csr(ctx):
 
 
 # ---------------------------------------------------------------- basis (first 20 columns <= 1e-10)
-@pytest.mark.parametrize("case", ["C1", "C2s", "C3s", "C4s", "k1", "k8"])
+@pytest.mark.parametrize("case", ["C1", "C2s", "C3s", "C4s", "k1", "k8", "3d_even", "3d_k4", "3d_k8", "3d_tiny"])
 def test_basis_first_columns(ctx, case):
+    """Odd m runs the generic stencil kernels; even m the TMA kernels (3D: z-march, ragged
+    32 x 16 tiles in x/y and plane ranges split across CTAs; k = 4, 8 use 2 and 1 planes/step)."""
     P = _P()
-    if case == "C1":
+    if case == "3d_even":
+        A, Ao, k, n = P.StencilOperator(3, 50, 30.0), O.stencil_matrix(3, 50, 30.0), 2, 50 ** 3
+    elif case == "3d_k4":
+        A, Ao, k, n = P.StencilOperator(3, 36, 20.0), O.stencil_matrix(3, 36, 20.0), 4, 36 ** 3
+    elif case == "3d_k8":
+        A, Ao, k, n = P.StencilOperator(3, 28, 10.0), O.stencil_matrix(3, 28, 10.0), 8, 28 ** 3
+    elif case == "3d_tiny":
+        A, Ao, k, n = P.StencilOperator(3, 6, 3.0), O.stencil_matrix(3, 6, 3.0), 2, 6 ** 3
+    elif case == "C1":
         A, Ao, k, n = P.StencilOperator(2, 32, 20.0), O.stencil_matrix(2, 32, 20.0), 2, 1024
     elif case == "C2s":
         A, Ao, k, n = P.StencilOperator(2, 130, 50.0), O.stencil_matrix(2, 130, 50.0), 4, 130 ** 2
