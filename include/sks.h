@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SKS_ABI_VERSION 1
+#define SKS_ABI_VERSION 2
 
 typedef enum {
   SKS_OK = 0,
@@ -122,8 +122,14 @@ typedef struct {
   int32_t sketch_batch;      /* columns per sketch batch, 0 = default (32), <= 32 */
   double early_exit_factor;  /* in-cycle exit when r_est,j <= factor*tol*||f|| (O16); 0 = never */
   double cond_tol;           /* kappa(T) warning threshold, default 1e14 */
-  int32_t reserved[4];
+  int32_t flags;             /* SKS_OPT_* bits */
+  int32_t reserved[3];
 } sks_sgmres_opts;
+
+enum {
+  SKS_OPT_TIME_STEPS = 1  /* bracket every basis-step launch with CUDA events on the main stream and
+                             report the summed kernel time in info->t_step_s (measurement only) */
+};
 
 typedef struct {
   int32_t cycles;       /* cycles run */
@@ -138,6 +144,9 @@ typedef struct {
   double bytes_basis;   /* algorithmic HBM bytes of the basis loops */
   int64_t kernel_launches; /* CUDA kernels this call launched */
   int64_t steps;        /* step-kernel launches (one per basis column) */
+  double t_step_s;      /* SKS_OPT_TIME_STEPS: summed duration of the step launches (events), else 0 */
+  int64_t steps_timed;  /* step launches included in t_step_s */
+  double bytes_step;    /* algorithmic HBM bytes of those launches */
 } sks_sgmres_info;
 
 /* Solve A x = f.  f, x: this rank's rows (n_local = row_end - row_begin); x is in/out

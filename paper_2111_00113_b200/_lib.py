@@ -30,14 +30,18 @@ class SgmresOpts(C.Structure):
     _fields_ = [("d", C.c_int32), ("k", C.c_int32), ("s", C.c_int32), ("zeta", C.c_int32),
                 ("seed", C.c_uint64), ("tol", C.c_double), ("max_cycles", C.c_int32),
                 ("sketch_batch", C.c_int32), ("early_exit_factor", C.c_double), ("cond_tol", C.c_double),
-                ("reserved", C.c_int32 * 4)]
+                ("flags", C.c_int32), ("reserved", C.c_int32 * 3)]
 
 
 class SgmresInfo(C.Structure):
     _fields_ = [("cycles", C.c_int32), ("columns", C.c_int32), ("columns_generated", C.c_int32),
                 ("flags", C.c_int32), ("rel_res_true", C.c_double), ("r_est", C.c_double),
                 ("cond_T", C.c_double), ("t_total_s", C.c_double), ("t_basis_s", C.c_double),
-                ("bytes_basis", C.c_double), ("kernel_launches", C.c_int64), ("steps", C.c_int64)]
+                ("bytes_basis", C.c_double), ("kernel_launches", C.c_int64), ("steps", C.c_int64),
+                ("t_step_s", C.c_double), ("steps_timed", C.c_int64), ("bytes_step", C.c_double)]
+
+
+SKS_OPT_TIME_STEPS = 1
 
 
 class SrrOpts(C.Structure):

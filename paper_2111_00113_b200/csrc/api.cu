@@ -43,6 +43,7 @@ struct sks_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr, ev_b0 = nullptr,
               ev_b1 = nullptr;
   std::vector<cudaEvent_t> ev_batch;
+  std::vector<cudaEvent_t> ev_step;  // SKS_OPT_TIME_STEPS: [2 i] before / [2 i + 1] after step launch i
   ncclComm_t comm = nullptr;
   std::string err = "";
   int64_t launches = 0;
@@ -333,6 +334,7 @@ sks_status sks_destroy(sks_ctx* c) {
   if (c->tma_cache) stencil_tma_free(c->tma_cache);
   if (c->zm_cache) stencil_zm_free(c->zm_cache);
   for (auto& ev : c->ev_batch) cudaEventDestroy(ev);
+  for (auto& ev : c->ev_step) cudaEventDestroy(ev);
   cudaEvent_t evs[] = {c->ev_fork, c->ev_join, c->ev_t0, c->ev_t1, c->ev_b0, c->ev_b1};
   for (auto e : evs)
     if (e) cudaEventDestroy(e);
@@ -379,6 +381,9 @@ struct Basis {
   int64_t nnz = 0;
   double bytes = 0.0;  // algorithmic bytes of the basis loop
   int64_t steps = 0;
+  bool time_steps = false;  // bracket step launches with events (SKS_OPT_TIME_STEPS)
+  int ntimed = 0;           // event pairs recorded in this cycle
+  double bytes_timed = 0.0; // algorithmic bytes of the timed launches (this cycle)
 };
 
 static double* colp(sks_ctx* c, const Basis& b, int j) { return c->W.as<double>() + (int64_t)j * b.g.ld; }
@@ -554,6 +559,7 @@ static sks_status step_column(sks_ctx* c, Basis& b, int j) {
     StepArgs a = use_t ? b.sat : b.sa;
     a.mode = 0;
     a.j = j;
+    if (b.time_steps && 2 * b.ntimed + 1 < (int)c->ev_step.size()) SKS_CK(c, cudaEventRecord(c->ev_step[2 * b.ntimed], st));
     a.partials_in = pslot(c, b, c->part, j - 1);
     a.grid_prev = c->nranks > 1 ? b.pslots : b.last_grid;
     a.partials_out = pslot(c, b, c->part, j);
@@ -567,12 +573,19 @@ static sks_status step_column(sks_ctx* c, Basis& b, int j) {
     else
       SKS_CK(c, launch_step_stencil(a, b.step_grid, st));
     ++c->launches;
+    if (b.time_steps && 2 * b.ntimed + 1 < (int)c->ev_step.size()) {
+      SKS_CK(c, cudaEventRecord(c->ev_step[2 * b.ntimed + 1], st));
+      ++b.ntimed;
+      b.bytes_timed += 8.0 * g.n * (nwin + 1);
+    }
     SKS_TRY(allreduce_sum(c, a.partials_out, (size_t)b.pslots * SKS_NP, st));
     SKS_TRY(halo_exchange(c, g, colp(c, b, j)));
     b.bytes += 8.0 * g.n * (nwin + 1);
   } else {
     const int lo = std::max(0, j - b.k), nw = j - lo;
     const double* xg = nullptr;
+    const bool tm = b.time_steps && 2 * b.ntimed + 1 < (int)c->ev_step.size();
+    if (tm) SKS_CK(c, cudaEventRecord(c->ev_step[2 * b.ntimed], st));
     SKS_TRY(csr_gather(c, g, colp(c, b, j - 1), &xg, b.maxn));
     double* pd = c->part2.as<double>();  // spmv partials (single slot)
     SKS_CK(c, launch_csr_spmv(g.n, b.rp, b.ci, b.va, xg, c->mr.as<double>(), nullptr, 0, c->W.as<double>(), g.ld,
@@ -584,6 +597,11 @@ static sks_status step_column(sks_ctx* c, Basis& b, int j) {
                               b.step_grid, st));
     SKS_TRY(allreduce_sum(c, pslot(c, b, c->part, j), (size_t)b.pslots * SKS_NP, st));
     c->launches += 2;
+    if (tm) {
+      SKS_CK(c, cudaEventRecord(c->ev_step[2 * b.ntimed + 1], st));
+      ++b.ntimed;
+      b.bytes_timed += 12.0 * b.nnz + 4.0 * (g.n + 1) + 8.0 * g.n * (nwin + 1);
+    }
     b.bytes += 12.0 * b.nnz + 4.0 * (g.n + 1) + 8.0 * g.n * (nwin + 1);
   }
   ++b.steps;
@@ -704,6 +722,14 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
   SKS_TRY(setup_basis(c, A, k, d + 2, &b));
   const Geo& g = b.g;
   const int JB = panel_jb(s, o->sketch_batch > 0 ? o->sketch_batch : SKS_JB);
+  b.time_steps = (o->flags & SKS_OPT_TIME_STEPS) != 0;
+  if (b.time_steps && (int)c->ev_step.size() < 2 * (d + 2)) {
+    const size_t old_n = c->ev_step.size();
+    c->ev_step.resize(2 * (d + 2));
+    for (size_t i = old_n; i < c->ev_step.size(); ++i) SKS_CK(c, cudaEventCreate(&c->ev_step[i]));
+  }
+  double t_step_total = 0.0, bytes_step_total = 0.0;
+  int64_t steps_timed = 0;
   SKS_TRY(setup_small(c, b, s, JB));
   const double cond_tol = o->cond_tol > 0 ? o->cond_tol : 1e14;
 
@@ -819,6 +845,15 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
       float ms = 0.f;
       cudaEventElapsedTime(&ms, c->ev_b0, c->ev_b1);
       t_basis_ms += ms;
+      for (int i = 0; i < b.ntimed; ++i) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, c->ev_step[2 * i], c->ev_step[2 * i + 1]);
+        t_step_total += t * 1e-3;
+      }
+      steps_timed += b.ntimed;
+      bytes_step_total += b.bytes_timed;
+      b.ntimed = 0;
+      b.bytes_timed = 0.0;
     }
     bytes_basis_total += b.bytes - bytes_first;
     generated += last_col + 1;
@@ -891,6 +926,9 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
     info->bytes_basis = bytes_basis_total;
     info->kernel_launches = c->launches - launches0;
     info->steps = b.steps;
+    info->t_step_s = t_step_total;
+    info->steps_timed = steps_timed;
+    info->bytes_step = bytes_step_total;
   }
   return result;
 }

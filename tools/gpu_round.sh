@@ -24,9 +24,9 @@ if [[ $ST == *l* ]]; then
   python tools/launches.py "$OUT/launches.csv" > "$OUT/launches_summary.txt" 2>&1
 fi
 if [[ $ST == *f* ]]; then
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:step3d --launch-skip 60 --launch-count 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:step3d_zm --launch-skip 60 --launch-count 1 \
     -o "$OUT/step3d" -f python tools/run_c3_once.py C3 1 > "$OUT/ncu_step.log" 2>&1; echo "ncu-step rc=$?" >> "$OUT/rc.txt"
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:sketch --launch-skip 4 --launch-count 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:sketch_v5 --launch-skip 4 --launch-count 1 \
     -o "$OUT/sketch" -f python tools/run_c3_once.py C3 1 > "$OUT/ncu_sketch.log" 2>&1; echo "ncu-sketch rc=$?" >> "$OUT/rc.txt"
 fi
 cat "$OUT/rc.txt"
