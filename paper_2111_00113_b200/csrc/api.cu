@@ -39,6 +39,7 @@ struct DevBuf {
 
 struct sks_ctx {
   int device = 0, rank = 0, nranks = 1, num_sms = 148;
+  int main_sms = 146;  // SMs the persistent basis/sketch kernels use; the rest run the side stream's QR
   cudaStream_t own_main = nullptr, side = nullptr, user_main = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr, ev_b0 = nullptr,
               ev_b1 = nullptr;
@@ -277,6 +278,11 @@ sks_status sks_create(sks_ctx** out, int device, int rank, int nranks, const uns
   c->nranks = nranks;
   cudaSetDevice(device);
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  {
+    const char* e = getenv("SKS_RESERVE_SMS");  // SMs kept free for the side stream (default 2)
+    const int r = e ? atoi(e) : 2;
+    c->main_sms = std::max(1, c->num_sms - std::max(0, r));
+  }
   cudaStreamCreateWithFlags(&c->own_main, cudaStreamNonBlocking);
   cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
   cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
@@ -445,15 +451,15 @@ static sks_status setup_basis(sks_ctx* c, const sks_operator* A, int k, int ncol
     a.ctrl = c->ctrl.as<CtrlBlock>();
     b->tma = c->use_tma && stencil_tma_supported(g.dim, g.m, k);
     b->sat = a;
-    stencil_tiling(g.dim, g.m, g.nz, c->num_sms, &a, &b->step_grid);
+    stencil_tiling(g.dim, g.m, g.nz, c->main_sms, &a, &b->step_grid);
     if (b->step_grid > b->pslots) b->step_grid = b->pslots;
     b->zm = c->use_tma && stencil_zm_supported(g.dim, g.m, k);
     if (b->zm) {
       b->tma = true;
-      stencil_zm_tiling(g.m, g.nz, c->num_sms, &b->sat, &b->tma_grid);
+      stencil_zm_tiling(g.m, g.nz, c->main_sms, &b->sat, &b->tma_grid);
       if (b->tma_grid > b->pslots) b->tma_grid = b->pslots;
     } else if (b->tma) {
-      stencil_tma_tiling(g.dim, g.m, g.nz, c->num_sms, &b->sat, &b->tma_grid);
+      stencil_tma_tiling(g.dim, g.m, g.nz, c->main_sms, &b->sat, &b->tma_grid);
       if (b->tma_grid > b->pslots) b->tma_grid = b->pslots;
     }
   } else {
@@ -632,7 +638,7 @@ static sks_status sketch_plan(sks_ctx* c, const Geo& g, int s, int zeta, uint64_
   *plan = nullptr;
   if (!sketch_plan_supported(s, zeta)) return SKS_OK;
   SKS_TRY(ensure(c, c->plan, sketch_plan_bytes(g.n, s, zeta)));
-  SKS_CK(c, launch_sketch_plan(g.n, g.row_begin, s, zeta, key, c->plan.p, c->num_sms, st));
+  SKS_CK(c, launch_sketch_plan(g.n, g.row_begin, s, zeta, key, c->plan.p, c->main_sms, st));
   ++c->launches;
   *plan = c->plan.p;
   return SKS_OK;
@@ -641,7 +647,7 @@ static sks_status sketch_plan(sks_ctx* c, const Geo& g, int s, int zeta, uint64_
 static sks_status sketch_cols(sks_ctx* c, Basis& b, int c0, int J, int s, int zeta, uint64_t key,
                               cudaStream_t st, const void* plan) {
   const Geo& g = b.g;
-  const int grid = sketch_grid(c->num_sms, g.n);
+  const int grid = sketch_grid(c->main_sms, g.n);
   double* out = c->SW.as<double>() + (int64_t)c0 * s;
   SKS_CK(c, launch_sketch(colp(c, b, c0) + g.off, g.ld, g.n, g.row_begin, J, s, zeta, key, c->partsk.as<double>(),
                           grid, out, s, 0, st, &c->launches, plan));
@@ -674,7 +680,7 @@ static sks_status qr_append(sks_ctx* c, Basis& b, int mode, int j0, int J, int s
 static sks_status setup_small(sks_ctx* c, Basis& b, int s, int JB) {
   const int ncol = b.ncol;
   SKS_TRY(ensure(c, c->SW, sizeof(double) * (size_t)s * (ncol + 1)));
-  const int grid = sketch_grid(c->num_sms, b.g.n);
+  const int grid = sketch_grid(c->main_sms, b.g.n);
   SKS_TRY(ensure(c, c->partsk, sizeof(double) * sketch_part_doubles(grid, SKS_JB, s)));
   SKS_TRY(ensure(c, c->Xp, sizeof(double) * (size_t)s * JB));
   SKS_TRY(ensure(c, c->Zb, sizeof(double) * (size_t)(ncol + 1) * JB));
@@ -790,18 +796,20 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
     int nbatch = 0;
     int last_col = d;   // columns 0..d are generated (d+1 columns)
     SKS_CK(c, cudaMemsetAsync(c->rvec.p, 0, sizeof(double) * s, st));
+    // the sketch batches run on the main stream (bandwidth kernels, all SMs but the reserved
+    // ones); the sketched QR (latency kernels) on the side stream, on the reserved SMs
     auto enqueue_side = [&](int upto /* columns [0, upto) are complete */, bool final_) -> sks_status {
-      SKS_CK(c, cudaEventRecord(c->ev_fork, st));
-      SKS_CK(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
       while (next_sk < upto) {
         const int J = std::min(JB, upto - next_sk);
-        if (next_sk == 0) SKS_TRY(sketch_plan(c, g, s, zeta, key, c->side, &plan));
-        SKS_TRY(sketch_cols(c, b, next_sk, J, s, zeta, key, c->side, plan));
+        if (next_sk == 0) SKS_TRY(sketch_plan(c, g, s, zeta, key, st, &plan));
+        SKS_TRY(sketch_cols(c, b, next_sk, J, s, zeta, key, st, plan));
         if (next_sk == 0) {  // g = S r = S w_0 starts the residual vector
-          SKS_CK(c, cudaMemcpyAsync(c->rvec.p, c->SW.p, sizeof(double) * s, cudaMemcpyDeviceToDevice, c->side));
+          SKS_CK(c, cudaMemcpyAsync(c->rvec.p, c->SW.p, sizeof(double) * s, cudaMemcpyDeviceToDevice, st));
         }
         next_sk += J;
       }
+      SKS_CK(c, cudaEventRecord(c->ev_fork, st));
+      SKS_CK(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
       // SAB column jj needs SW[:, jj+1]
       const int qr_upto = std::min(next_sk - 1, d);
       while (next_qr < qr_upto) {
@@ -938,7 +946,7 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
 // ------------------------------------------------------------------------------------
 namespace {
 
-// run the basis loop for columns 1..d with the sketch batches on the side stream (no QR)
+// run the basis loop for columns 1..d with the sketch batches interleaved (no QR)
 static sks_status basis_and_sketch(sks_ctx* c, Basis& b, int d, int s, int zeta, uint64_t key, int JB,
                                    bool do_sketch, float* t_basis_ms) {
   cudaStream_t st = c->main();
@@ -947,12 +955,10 @@ static sks_status basis_and_sketch(sks_ctx* c, Basis& b, int d, int s, int zeta,
   SKS_CK(c, cudaEventRecord(c->ev_b0, st));
   auto side = [&](int upto) -> sks_status {
     if (!do_sketch) return SKS_OK;
-    SKS_CK(c, cudaEventRecord(c->ev_fork, st));
-    SKS_CK(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-    while (next_sk < upto) {
+    while (next_sk < upto) {  // sketch batches on the main stream (see sks_sgmres_solve)
       const int J = std::min(JB, upto - next_sk);
-      if (next_sk == 0) SKS_TRY(sketch_plan(c, b.g, s, zeta, key, c->side, &plan));
-      SKS_TRY(sketch_cols(c, b, next_sk, J, s, zeta, key, c->side, plan));
+      if (next_sk == 0) SKS_TRY(sketch_plan(c, b.g, s, zeta, key, st, &plan));
+      SKS_TRY(sketch_cols(c, b, next_sk, J, s, zeta, key, st, plan));
       next_sk += J;
     }
     return SKS_OK;
@@ -966,10 +972,6 @@ static sks_status basis_and_sketch(sks_ctx* c, Basis& b, int d, int s, int zeta,
     }
   }
   SKS_CK(c, cudaEventRecord(c->ev_b1, st));
-  if (do_sketch) {
-    SKS_CK(c, cudaEventRecord(c->ev_join, c->side));
-    SKS_CK(c, cudaStreamWaitEvent(st, c->ev_join, 0));
-  }
   SKS_CK(c, cudaMemcpyAsync(c->h_ctrl, c->ctrl.p, sizeof(CtrlBlock), cudaMemcpyDeviceToHost, st));
   SKS_CK(c, cudaStreamSynchronize(st));
   float ms = 0.f;

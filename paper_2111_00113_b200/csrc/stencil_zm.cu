@@ -92,8 +92,9 @@ __global__ void __launch_bounds__(ZT, 1)
   double* Wout = a.W + (a.mode == 0 ? (int64_t)a.j * a.ld : 0) + a.off;
 
   // this thread's W-box column
-  const bool wt = tid < ZW;
-  const int bx = tid % ZWX, by = tid / ZWX;
+  const bool wt = tid < ZW;  // threads past the W box shadow its last column (no stores)
+  const int tcol = wt ? tid : ZW - 1;
+  const int bx = tcol % ZWX, by = tcol / ZWX;
   const int cu = (by + 1) * ZUX + (bx + 1);  // U-plane offset of the column
   const int cvv = by * ZVX + (bx + 1);       // V-plane offset
   const int cwb = by * ZWX + bx;             // W-plane offset
@@ -148,21 +149,19 @@ __global__ void __launch_bounds__(ZT, 1)
       double w[ZS], c[ZS + 2], v[KM - 1][ZS];
       // ---- w_j on planes p0 .. p0+ZS-1 (this thread's column)
 #pragma unroll
-      for (int k = 0; k < ZS + 2; ++k) c[k] = wt ? sU[k * ZUP + cu] : 0.0;
+      for (int k = 0; k < ZS + 2; ++k) c[k] = sU[k * ZUP + cu];
 #pragma unroll
       for (int i = 0; i < ZS; ++i) {
         const int p = p0 + i;
 #pragma unroll
-        for (int l = 0; l < KM - 1; ++l) v[l][i] = (wt && l < nv) ? sV[l * VB + i * ZVP + cvv] : 0.0;
+        for (int l = 0; l < KM - 1; ++l) v[l][i] = (l < nv) ? sV[l * VB + i * ZVP + cvv] : 0.0;
         const double* q = sU + (i + 1) * ZUP + cu;
-        double wv = 0.0;
-        if (xyin && (unsigned)(z0g + p) < (unsigned)m && p <= zb) {
-          const double Au = cc * c[i + 1] + cm * (q[-1] + q[-ZUX] + c[i]) + cp * (q[1] + q[ZUX] + c[i + 2]);
-          wv = alpha * Au + beta_u * c[i + 1];
+        const double Au = cc * c[i + 1] + cm * (q[-1] + q[-ZUX] + c[i]) + cp * (q[1] + q[ZUX] + c[i + 2]);
+        double wv = alpha * Au + beta_u * c[i + 1];
 #pragma unroll
-          for (int l = 0; l < KM - 1; ++l)
-            if (l < nv) wv += cl[l] * v[l][i];
-        }
+        for (int l = 0; l < KM - 1; ++l)
+          if (l < nv) wv += cl[l] * v[l][i];
+        wv = (xyin && (unsigned)(z0g + p) < (unsigned)m && p <= zb) ? wv : 0.0;
         w[i] = wv;
         const int si = (rs + i < R) ? rs + i : rs + i - R;
         if (wt) ring[si * ZW + cwb] = wv;
