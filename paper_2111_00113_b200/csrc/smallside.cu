@@ -652,11 +652,17 @@ cudaError_t launch_ritz_vectors(const double* W, int64_t ld, int64_t off, int64_
   int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms * 4);
   if (grid < 1) grid = 1;
   if (nvec <= 4) {
-    ritz_vectors_kernel<4><<<grid, 256, sizeof(double) * nc * 8, st>>>(W, ld, off, n, nc, sigma, yr, yi, ldy, nvec,
-                                                                       Xr, Xi, ldx, xoff);
+    const size_t smem = sizeof(double) * nc * 8;
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(ritz_vectors_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return cudaGetLastError();
+    ritz_vectors_kernel<4><<<grid, 256, smem, st>>>(W, ld, off, n, nc, sigma, yr, yi, ldy, nvec, Xr, Xi, ldx, xoff);
   } else if (nvec <= 12) {
-    ritz_vectors_kernel<12><<<grid, 256, sizeof(double) * nc * 24, st>>>(W, ld, off, n, nc, sigma, yr, yi, ldy,
-                                                                         nvec, Xr, Xi, ldx, xoff);
+    const size_t smem = sizeof(double) * nc * 24;
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(ritz_vectors_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return cudaGetLastError();
+    ritz_vectors_kernel<12><<<grid, 256, smem, st>>>(W, ld, off, n, nc, sigma, yr, yi, ldy, nvec, Xr, Xi, ldx, xoff);
   } else {
     return cudaErrorInvalidValue;
   }
