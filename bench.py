@@ -176,7 +176,7 @@ def main():
     f_host = torch.from_numpy(f_full[rb:re_].copy()).pin_memory()
     f_dev = f_host.cuda()
     kw = dict(d=cfg.d, k=cfg.k, s=cfg.s, zeta=cfg.zeta, seed=cfg.seed, tol=cfg.tol, max_cycles=cfg.max_cycles,
-              early_exit_factor=cfg.early_exit_factor, time_steps=True)
+              early_exit_factor=cfg.early_exit_factor, time_steps=True, time_stride=16)
 
     def barrier():
         torch.cuda.synchronize()

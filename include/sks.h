@@ -123,7 +123,8 @@ typedef struct {
   double early_exit_factor;  /* in-cycle exit when r_est,j <= factor*tol*||f|| (O16); 0 = never */
   double cond_tol;           /* kappa(T) warning threshold, default 1e14 */
   int32_t flags;             /* SKS_OPT_* bits */
-  int32_t reserved[3];
+  int32_t time_stride;       /* SKS_OPT_TIME_STEPS: time every time_stride-th step launch (0/1 = all) */
+  int32_t reserved[2];
 } sks_sgmres_opts;
 
 enum {

@@ -30,7 +30,7 @@ class SgmresOpts(C.Structure):
     _fields_ = [("d", C.c_int32), ("k", C.c_int32), ("s", C.c_int32), ("zeta", C.c_int32),
                 ("seed", C.c_uint64), ("tol", C.c_double), ("max_cycles", C.c_int32),
                 ("sketch_batch", C.c_int32), ("early_exit_factor", C.c_double), ("cond_tol", C.c_double),
-                ("flags", C.c_int32), ("reserved", C.c_int32 * 3)]
+                ("flags", C.c_int32), ("time_stride", C.c_int32), ("reserved", C.c_int32 * 2)]
 
 
 class SgmresInfo(C.Structure):

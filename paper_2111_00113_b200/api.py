@@ -154,7 +154,7 @@ class Context:
 
     # ---------------------------------------------------------------- sGMRES
     def sgmres_solve(self, A, f, x0=None, *, d, k, s, zeta=8, seed=0, tol=1e-8, max_cycles=50,
-                     early_exit_factor=0.25, cond_tol=1e14, sketch_batch=0, hist_cap=None, time_steps=False):
+                     early_exit_factor=0.25, cond_tol=1e14, sketch_batch=0, hist_cap=None, time_steps=False, time_stride=1):
         op, keep = A.struct()
         fa, pf = _prep(f)
         n = fa.shape[0]
@@ -171,7 +171,7 @@ class Context:
         hist = np.zeros(cap)
         hist_true = np.zeros(max_cycles + 2)
         opts = L.SgmresOpts(d, k, s, zeta, seed, tol, max_cycles, sketch_batch, early_exit_factor, cond_tol,
-                            L.SKS_OPT_TIME_STEPS if time_steps else 0)
+                            L.SKS_OPT_TIME_STEPS if time_steps else 0, time_stride)
         info = L.SgmresInfo()
         st = self.lib.sks_sgmres_solve(self.h, C.byref(op), pf, px, C.byref(opts), C.byref(info),
                                        hist.ctypes.data, cap, hist_true.ctypes.data, len(hist_true))

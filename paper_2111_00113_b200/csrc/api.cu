@@ -388,6 +388,7 @@ struct Basis {
   double bytes = 0.0;  // algorithmic bytes of the basis loop
   int64_t steps = 0;
   bool time_steps = false;  // bracket step launches with events (SKS_OPT_TIME_STEPS)
+  int time_stride = 1;      // ... every time_stride-th launch
   int ntimed = 0;           // event pairs recorded in this cycle
   double bytes_timed = 0.0; // algorithmic bytes of the timed launches (this cycle)
 };
@@ -565,7 +566,8 @@ static sks_status step_column(sks_ctx* c, Basis& b, int j) {
     StepArgs a = use_t ? b.sat : b.sa;
     a.mode = 0;
     a.j = j;
-    if (b.time_steps && 2 * b.ntimed + 1 < (int)c->ev_step.size()) SKS_CK(c, cudaEventRecord(c->ev_step[2 * b.ntimed], st));
+    const bool tm = b.time_steps && j % b.time_stride == 0 && 2 * b.ntimed + 1 < (int)c->ev_step.size();
+    if (tm) SKS_CK(c, cudaEventRecord(c->ev_step[2 * b.ntimed], st));
     a.partials_in = pslot(c, b, c->part, j - 1);
     a.grid_prev = c->nranks > 1 ? b.pslots : b.last_grid;
     a.partials_out = pslot(c, b, c->part, j);
@@ -579,7 +581,7 @@ static sks_status step_column(sks_ctx* c, Basis& b, int j) {
     else
       SKS_CK(c, launch_step_stencil(a, b.step_grid, st));
     ++c->launches;
-    if (b.time_steps && 2 * b.ntimed + 1 < (int)c->ev_step.size()) {
+    if (tm) {
       SKS_CK(c, cudaEventRecord(c->ev_step[2 * b.ntimed + 1], st));
       ++b.ntimed;
       b.bytes_timed += 8.0 * g.n * (nwin + 1);
@@ -590,7 +592,7 @@ static sks_status step_column(sks_ctx* c, Basis& b, int j) {
   } else {
     const int lo = std::max(0, j - b.k), nw = j - lo;
     const double* xg = nullptr;
-    const bool tm = b.time_steps && 2 * b.ntimed + 1 < (int)c->ev_step.size();
+    const bool tm = b.time_steps && j % b.time_stride == 0 && 2 * b.ntimed + 1 < (int)c->ev_step.size();
     if (tm) SKS_CK(c, cudaEventRecord(c->ev_step[2 * b.ntimed], st));
     SKS_TRY(csr_gather(c, g, colp(c, b, j - 1), &xg, b.maxn));
     double* pd = c->part2.as<double>();  // spmv partials (single slot)
@@ -729,6 +731,7 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
   const Geo& g = b.g;
   const int JB = panel_jb(s, o->sketch_batch > 0 ? o->sketch_batch : SKS_JB);
   b.time_steps = (o->flags & SKS_OPT_TIME_STEPS) != 0;
+  b.time_stride = o->time_stride > 1 ? o->time_stride : 1;
   if (b.time_steps && (int)c->ev_step.size() < 2 * (d + 2)) {
     const size_t old_n = c->ev_step.size();
     c->ev_step.resize(2 * (d + 2));
