@@ -12,6 +12,8 @@
 //  * inverse iteration per selected eigenvalue on (Mhat - theta I) in complex arithmetic
 //    (Hessenberg LU with partial pivoting), one CTA per eigenvalue, giving y_i.
 //  * sketched residual estimate  ||D y - theta C y|| / ||C y||  (Eq. srr-resid-est).
+#include <climits>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -30,9 +32,22 @@ __global__ void build_mhat_kernel(const double* __restrict__ H, int ldH, int d, 
 
 #define HA(i, j) a[(i) + (int64_t)(j) * lda]
 
+// block-wide max of an int (all threads get the result)
+__device__ __forceinline__ int block_max_int(int v, int* smem) {
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if (lane == 0) smem[wid] = v;
+  __syncthreads();
+  int r = lane < nw ? smem[lane] : INT_MIN;
+  for (int o = 16; o > 0; o >>= 1) r = max(r, __shfl_xor_sync(0xffffffffu, r, o));
+  return r;
+}
+
 __global__ void __launch_bounds__(256) hqr_kernel(double* __restrict__ a, int n, int lda, double* __restrict__ wr,
                                                   double* __restrict__ wi, int* __restrict__ info) {
   __shared__ double red[32];
+  __shared__ int ired[32];
   __shared__ double sp, sq, sr, sx, sy, sz, sw, st;
   __shared__ int sl, snn, sm, sflag, sits, sdone;
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -54,18 +69,24 @@ __global__ void __launch_bounds__(256) hqr_kernel(double* __restrict__ a, int n,
     if (tid == 0) sits = 0;
     __syncthreads();
     while (true) {
-      // --- scalar part: find small subdiagonal, deflate or set up a double-shift sweep
-      if (tid == 0) {
-        int nn = snn, l;
-        for (l = nn; l >= 1; --l) {
+      // --- find the largest l in [1, nn] with a negligible subdiagonal (all threads, one pass
+      //     over the subdiagonal instead of a serial scan with one L2 round trip per element)
+      {
+        const int nn = snn;
+        int best = 0;
+        for (int l = 1 + tid; l <= nn; l += nt) {
           double s = fabs(HA(l - 1, l - 1)) + fabs(HA(l, l));
           if (s == 0.0) s = anorm;
-          if (fabs(HA(l, l - 1)) + s == s) {
-            HA(l, l - 1) = 0.0;
-            break;
-          }
+          if (fabs(HA(l, l - 1)) + s == s) best = max(best, l);
         }
-        if (l < 0) l = 0;
+        best = block_max_int(best, ired);
+        if (tid == 0) sl = best;
+      }
+      __syncthreads();
+      // --- scalar part: deflate or set up a double-shift sweep
+      if (tid == 0) {
+        int nn = snn, l = sl;
+        if (l >= 1) HA(l, l - 1) = 0.0;
         double x = HA(nn, nn);
         sflag = 0;
         if (l == nn) {
@@ -131,14 +152,12 @@ __global__ void __launch_bounds__(256) hqr_kernel(double* __restrict__ a, int n,
         }
         __syncthreads();
       }
-      // choose m and the first Householder vector
-      if (tid == 0) {
-        sits = sits + 1;
+      // choose m (largest m in [l, nn-2] with m == l or two small consecutive subdiagonals,
+      // evaluated for all m in parallel) and the first Householder vector
+      {
         const int nn = snn, l = sl;
         const double x = sx, y = sy, w = sw;
-        int m;
-        double p = 0, q = 0, r = 0, z;
-        for (m = nn - 2; m >= l; --m) {
+        auto pqr = [&](int m, double& p, double& q, double& r, double& z) {
           z = HA(m, m);
           r = x - z;
           double s = y - z;
@@ -149,15 +168,25 @@ __global__ void __launch_bounds__(256) hqr_kernel(double* __restrict__ a, int n,
           p /= s;
           q /= s;
           r /= s;
-          if (m == l) break;
+        };
+        int best = l;
+        for (int m = l + 1 + tid; m <= nn - 2; m += nt) {
+          double p, q, r, z;
+          pqr(m, p, q, r, z);
           const double u = fabs(HA(m, m - 1)) * (fabs(q) + fabs(r));
           const double v = fabs(p) * (fabs(HA(m - 1, m - 1)) + fabs(z) + fabs(HA(m + 1, m + 1)));
-          if (u + v == v) break;
+          if (u + v == v) best = max(best, m);
         }
-        sm = m;
-        sp = p;
-        sq = q;
-        sr = r;
+        best = block_max_int(best, ired);
+        if (tid == 0) {
+          sits = sits + 1;
+          double p, q, r, z;
+          pqr(best, p, q, r, z);
+          sm = best;
+          sp = p;
+          sq = q;
+          sr = r;
+        }
       }
       __syncthreads();
       {
