@@ -44,6 +44,7 @@ struct ZmArgs {
   int ncolxy;      // xy tiles
   int tiles_x;
   int64_t units;   // ncolxy * nz
+  int nv;          // window vectors of this launch (= StepCoef::nv, known on the host)
 };
 
 __host__ __device__ constexpr int zm_al16(int d) { return (d + 15) & ~15; }  // 128-byte multiple (doubles)
@@ -55,10 +56,10 @@ template <int KM, int ZS>
 __host__ __device__ constexpr int zm_stage() { return zm_ublk<KM, ZS>() + (KM - 1) * zm_vblk<KM, ZS>(); }
 template <int KM, int ZS>
 __host__ __device__ constexpr size_t zm_smem_bytes() {
-  return 128 + sizeof(double) * ((size_t)2 * zm_stage<KM, ZS>() + (size_t)(2 * ZS + 2) * ZW);
+  return 128 + sizeof(double) * ((size_t)2 * zm_stage<KM, ZS>() + (size_t)(3 * ZS) * ZW);
 }
 
-template <int KM, int ZS>
+template <int KM, int ZS, bool FULL, bool USL>
 __global__ void __launch_bounds__(ZT, 1)
     step3d_zm_kernel(StepArgs a, ZmArgs z, const __grid_constant__ CUtensorMap tmU,
                      const __grid_constant__ CUtensorMap tmV) {
@@ -66,7 +67,7 @@ __global__ void __launch_bounds__(ZT, 1)
   double* sm = reinterpret_cast<double*>(smraw_z + ((128u - (smem_u32(smraw_z) & 127u)) & 127u));
   constexpr int STG = zm_stage<KM, ZS>();
   constexpr int UB = zm_ublk<KM, ZS>(), VB = zm_vblk<KM, ZS>();
-  constexpr int R = 2 * ZS + 2;  // w_j plane ring
+  constexpr int R = 3 * ZS;  // w_j plane ring: plane p in slot (p - wa + ZS) mod 3 ZS
   double* ring = sm + 2 * STG;
   __shared__ StepCoef cf;
   __shared__ double red[SKS_NP * 32];
@@ -80,7 +81,7 @@ __global__ void __launch_bounds__(ZT, 1)
     fence_mbar_init();
   }
   if (!step_prologue(a, &cf, red)) return;  // contains __syncthreads
-  const int nv = cf.nv;
+  const int nv = FULL ? KM - 1 : cf.nv;
   const uint32_t sbytes = (uint32_t)(ZUP * (ZS + 2) * 8 + nv * ZVP * ZS * 8);
   const int m = (int)a.m, nz = (int)a.nz, z0g = (int)a.z0, G = a.G;
   const int64_t pl = a.plane;
@@ -88,7 +89,7 @@ __global__ void __launch_bounds__(ZT, 1)
   double cl[KM - 1];
 #pragma unroll
   for (int l = 0; l < KM - 1; ++l) cl[l] = (l < nv) ? cf.c[l] : 0.0;
-  const bool uslot = cf.uslot >= 0;
+  constexpr bool uslot = USL;
   double* Wout = a.W + (a.mode == 0 ? (int64_t)a.j * a.ld : 0) + a.off;
 
   // this thread's W-box column
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(ZT, 1)
     const bool xyin = wt && (unsigned)gxw < (unsigned)m && (unsigned)gyw < (unsigned)m;
     const bool aw = inner && gxw < m && gyw < m;    // this thread forms A w_j (interior output)
     double* wcol = Wout + (int64_t)(wa - 1) * pl + (int64_t)gyw * m + gxw;  // plane wa-1 of the column
-    int rs = (wa + R) % R;  // ring slot of plane p0
+    int sbw = ZS;  // ring slot of plane p0 (= ((t+1) mod 3) ZS), uniform; plane p0-1 is at sbw-1 (mod R)
     for (int t = 0; t < nsteps; ++t) {
       const uint32_t slot = (s0 + (uint32_t)t) & 1u;
       mbar_wait(&bar[slot], (phase >> slot) & 1u);
@@ -147,6 +148,8 @@ __global__ void __launch_bounds__(ZT, 1)
       const double* sV = sU + UB;
       const int p0 = wa + t * ZS;
       double w[ZS], c[ZS + 2], v[KM - 1][ZS];
+      double* rw = ring + sbw * ZW + cwb;                       // plane p0 (+ i ZW for p0 + i)
+      const double* rp = ring + (sbw == 0 ? R - 1 : sbw - 1) * ZW + cwb;  // plane p0-1
       // ---- w_j on planes p0 .. p0+ZS-1 (this thread's column)
 #pragma unroll
       for (int k = 0; k < ZS + 2; ++k) c[k] = sU[k * ZUP + cu];
@@ -154,40 +157,40 @@ __global__ void __launch_bounds__(ZT, 1)
       for (int i = 0; i < ZS; ++i) {
         const int p = p0 + i;
 #pragma unroll
-        for (int l = 0; l < KM - 1; ++l) v[l][i] = (l < nv) ? sV[l * VB + i * ZVP + cvv] : 0.0;
+        for (int l = 0; l < KM - 1; ++l) v[l][i] = (FULL || l < nv) ? sV[l * VB + i * ZVP + cvv] : 0.0;
         const double* q = sU + (i + 1) * ZUP + cu;
         const double Au = cc * c[i + 1] + cm * (q[-1] + q[-ZUX] + c[i]) + cp * (q[1] + q[ZUX] + c[i + 2]);
         double wv = alpha * Au + beta_u * c[i + 1];
 #pragma unroll
         for (int l = 0; l < KM - 1; ++l)
-          if (l < nv) wv += cl[l] * v[l][i];
+          if (FULL || l < nv) wv += cl[l] * v[l][i];
         wv = (xyin && (unsigned)(z0g + p) < (unsigned)m && p <= zb) ? wv : 0.0;
         w[i] = wv;
-        const int si = (rs + i < R) ? rs + i : rs + i - R;
-        if (wt) ring[si * ZW + cwb] = wv;
+        if (wt) rw[i * ZW] = wv;
       }
       __syncthreads();
       if (tid == 0 && t + 2 < nsteps) issue(t + 2);  // the stage just consumed is free
       // ---- A w_j on planes p0-1 .. p0+ZS-2
       if (aw) {
+        double* wo = wcol;
 #pragma unroll
         for (int i = 0; i < ZS; ++i) {
           const int qp = p0 - 1 + i;
           if (qp >= za && qp < zb) {
             const double wq = (i == 0) ? wp1 : w[i - 1];
             const double wqm = (i == 0) ? wp2 : (i == 1 ? wp1 : w[i - 2]);
-            const int si = (rs + i - 1 < 0) ? rs + i - 1 + R : (rs + i - 1 < R ? rs + i - 1 : rs + i - 1 - R);
-            const double* r = ring + si * ZW + cwb;
+            const double* r = (i == 0) ? rp : rw + (i - 1) * ZW;
             const double Aw = cc * wq + cm * (r[-1] + r[-ZWX] + wqm) + cp * (r[1] + r[ZWX] + w[i]);
-            wcol[(int64_t)i * pl] = wq;
+            *wo = wq;
             acc[0] += wq * wq;
             acc[1] += wq * Aw;
             acc[2] += Aw * Aw;
             if (uslot) acc[KM + 2] += c[i] * Aw;
 #pragma unroll
             for (int l = 0; l < KM - 1; ++l)
-              if (l < nv) acc[3 + l] += ((i == 0) ? vlast[l] : v[l][i - 1]) * Aw;
+              if (FULL || l < nv) acc[3 + l] += ((i == 0) ? vlast[l] : v[l][i - 1]) * Aw;
           }
+          wo += pl;
         }
       }
       if (ZS >= 2) {
@@ -200,7 +203,7 @@ __global__ void __launch_bounds__(ZT, 1)
 #pragma unroll
       for (int l = 0; l < KM - 1; ++l) vlast[l] = v[l][ZS - 1];
       wcol += (int64_t)ZS * pl;
-      rs = (rs + ZS < R) ? rs + ZS : rs + ZS - R;
+      sbw = (sbw + ZS == R) ? 0 : sbw + ZS;
     }
     sidx = s0 + (uint32_t)nsteps;
     __syncthreads();  // ring and stages are reused by the next piece
@@ -263,23 +266,34 @@ void stencil_zm_tiling(int64_t m, int64_t nz, int num_sms, StepArgs* a, int* gri
   *grid = (int)std::max<int64_t>(1, std::min<int64_t>(a->ntiles, num_sms));
 }
 
-template <int KM>
-static cudaError_t zm_launch(const StepArgs& a, const ZmArgs& z, const CUtensorMap& mu, const CUtensorMap& mv,
-                             int grid, cudaStream_t st) {
+template <int KM, bool FULL, bool USL>
+static cudaError_t zm_launch_v(const StepArgs& a, const ZmArgs& z, const CUtensorMap& mu, const CUtensorMap& mv,
+                               int grid, cudaStream_t st) {
   constexpr int ZS = zm_zs<KM>();
   const size_t smem = zm_smem_bytes<KM, ZS>();
   static bool set = false;
   if (!set) {
-    cudaError_t e = cudaFuncSetAttribute(step3d_zm_kernel<KM, ZS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(step3d_zm_kernel<KM, ZS, FULL, USL>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
       cudaGetLastError();
       return e;
     }
     set = true;
   }
-  step3d_zm_kernel<KM, ZS><<<grid, ZT, smem, st>>>(a, z, mu, mv);
+  step3d_zm_kernel<KM, ZS, FULL, USL><<<grid, ZT, smem, st>>>(a, z, mu, mv);
   return cudaGetLastError();
+}
+
+template <int KM>
+static cudaError_t zm_launch(const StepArgs& a, const ZmArgs& z, const CUtensorMap& mu, const CUtensorMap& mv,
+                             int grid, cudaStream_t st) {
+  const bool full = z.nv == KM - 1;
+  const bool usl = a.mode == 0 && a.k >= 2;  // step_prologue: uslot = k+1 for k >= 2 (mode 0)
+  if (full && usl) return zm_launch_v<KM, true, true>(a, z, mu, mv, grid, st);
+  if (full) return zm_launch_v<KM, true, false>(a, z, mu, mv, grid, st);
+  if (usl) return zm_launch_v<KM, false, true>(a, z, mu, mv, grid, st);
+  return zm_launch_v<KM, false, false>(a, z, mu, mv, grid, st);
 }
 
 // mode 0: U = column j-1, V_l = columns lo+l of W; mode 1: U = x, V0 = f; mode 2: U = v0.
@@ -306,6 +320,7 @@ cudaError_t launch_step_stencil_zm(const StepArgs& a, const double* W, int64_t n
   z.tiles_x = a.tiles_x;
   z.ncolxy = a.tiles_x * a.tiles_y;
   z.units = a.ntiles;
+  z.nv = (a.mode == 0) ? std::min(a.j, a.k) - 1 : (a.mode == 1 ? 1 : 0);
   const CUtensorMap* mu;
   const CUtensorMap* mv;
   if (a.mode == 0) {
