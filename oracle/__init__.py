@@ -19,12 +19,12 @@ none ("parity unpinned" would be stated here and in DESIGN.md).
 """
 from .operators import (  # noqa: F401
     stencil_coeffs, stencil_matrix, csr_matrix, closed_form_eigs_1d,
-    closed_form_eigs, toeplitz_1d,
+    closed_form_eigs, toeplitz_1d, spectral_box,
 )
 from .sketch import (  # noqa: F401
     sketch_key, sketch_table, sketch_matrix, sketch_apply, fmix64,
 )
-from .krylov import partial_arnoldi, full_arnoldi  # noqa: F401
+from .krylov import partial_arnoldi, full_arnoldi, chebyshev_basis  # noqa: F401
 from .sgmres import (  # noqa: F401
     thin_qr, sgmres_cycle, sgmres_solve, gmres_exact_ls, sketched_lsq,
 )

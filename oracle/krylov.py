@@ -83,3 +83,43 @@ def full_arnoldi(matvec, r, p: int):
             return Q[:, :j + 1], H[:j + 2, :j + 1]
         Q[:, j + 1] = w / H[j + 1, j]
     return Q, H
+
+
+def chebyshev_basis(matvec, r, d: int, c: float, dx: float, dy: float = 0.0):
+    """Shifted-and-scaled Chebyshev basis, Eq. (Chebrecurse) P:1192-1199:
+        b_1 = r/||r||,  b_2 = (2 rho)^-1 (A - c I) b_1,
+        b_j = rho^-1 [ (A - c I) b_{j-1} - (dx^2 - dy^2)/(4 rho) b_{j-2} ],  j = 3..d,
+    rho = max(dx, dy), for a spectrum inside the rectangle [c +- dx, +- i dy].  "In practice, we
+    also rescale each basis vector b_j to have unit norm after it has played its role in the
+    recurrence": the recurrence runs on the raw vectors, the returned basis holds
+    them normalised.  No inner products.
+    Returns dict(B (n x d, unit columns), M = A B, raw (n x d raw recurrence vectors),
+    H ((d+1) x d): A B[:, :d-1] = B H[:d, :d-1] (recurrence identity), d_eff, rho, rnorm)."""
+    r = np.asarray(r, dtype=np.float64)
+    n = r.size
+    rho = max(dx, dy)
+    e = (dx * dx - dy * dy) / (4.0 * rho)
+    raw = np.zeros((n, d))
+    rnorm = np.linalg.norm(r)
+    raw[:, 0] = r / rnorm
+    Ab = [matvec(raw[:, 0])]
+    if d >= 2:
+        raw[:, 1] = (Ab[0] - c * raw[:, 0]) / (2.0 * rho)
+    for j in range(2, d):
+        Ab.append(matvec(raw[:, j - 1]))
+        raw[:, j] = (Ab[j - 1] - c * raw[:, j - 1] - e * raw[:, j - 2]) / rho
+    if d >= 2:
+        Ab.append(matvec(raw[:, d - 1]))
+    nu = np.linalg.norm(raw, axis=0)
+    B = raw / nu[None, :]
+    M = np.stack([a / nu[j] for j, a in enumerate(Ab[:d])], axis=1)
+    # recurrence identity on the normalised basis: A raw_0 = 2 rho raw_1 + c raw_0,
+    # A raw_j = rho raw_{j+1} + c raw_j + e raw_{j-1}  (j >= 1)
+    H = np.zeros((d + 1, d))
+    for j in range(d - 1):
+        lead = 2.0 * rho if j == 0 else rho
+        H[j + 1, j] = lead * nu[j + 1] / nu[j]
+        H[j, j] = c
+        if j >= 1:
+            H[j - 1, j] = e * nu[j - 1] / nu[j]
+    return dict(B=B, M=M, raw=raw, H=H, d_eff=d, rho=rho, rnorm=rnorm, breakdown=False, nu=nu)

@@ -75,3 +75,16 @@ def closed_form_eigs(dim: int, m: int, beta: float):
     if dim == 2:
         return np.sort((mu[:, None] + mu[None, :]).ravel())
     return np.sort((mu[:, None, None] + mu[None, :, None] + mu[None, None, :]).ravel())
+
+
+def spectral_box(dim: int, m: int, beta: float):
+    """(c, dx, dy) of an axis-aligned box containing the spectrum of the dim-D operator
+    (closed form: Kronecker sum of the 1D tridiagonal Toeplitz factor, eigenvalues
+    a + 2 sqrt(bc) cos(p pi/(m+1)); real when bc > 0, on a vertical segment when bc < 0).
+    Used for the Chebyshev basis ("the spectrum of A is contained in the
+    rectangle [c +- dx, +- dy]")."""
+    a, b, c = stencil_coeffs(m, beta)
+    cosm = np.cos(np.pi / (m + 1))
+    if b * c >= 0.0:
+        return dim * a, dim * 2.0 * np.sqrt(b * c) * cosm, 0.0
+    return dim * a, 0.0, dim * 2.0 * np.sqrt(-b * c) * cosm

@@ -17,7 +17,7 @@ Cycles repeat with a fresh S_{c+1} while ||f - A x||/||f|| > tol, up to max_cycl
 import numpy as np
 from scipy.linalg import solve_triangular
 
-from .krylov import partial_arnoldi
+from .krylov import partial_arnoldi, chebyshev_basis
 from .sketch import sketch_matrix
 
 WARN_COND = 1
@@ -48,7 +48,9 @@ def gmres_exact_ls(M, r0):
 
 
 def sgmres_cycle(matvec, f, x, d, k, s, zeta, seed, cycle, tol=1e-8,
-                 early_exit_factor=0.25, cond_tol=1e14, fnorm=None, S=None):
+                 early_exit_factor=0.25, cond_tol=1e14, fnorm=None, S=None, cheb=None):
+    """One cycle; cheb = (c, dx, dy) selects the Chebyshev basis of Eq. Chebrecurse
+     instead of k-truncated Arnoldi."""
     f = np.asarray(f, dtype=np.float64)
     n = f.size
     if fnorm is None:
@@ -60,7 +62,7 @@ def sgmres_cycle(matvec, f, x, d, k, s, zeta, seed, cycle, tol=1e-8,
         return dict(x=x.copy(), j=0, r_est=np.zeros(0), yhat=np.zeros(0),
                     cond_T=1.0, flags=0, basis=None, C=None, g=None)
     g = S @ r
-    basis = partial_arnoldi(matvec, r, d, k)
+    basis = partial_arnoldi(matvec, r, d, k) if cheb is None else chebyshev_basis(matvec, r, d, *cheb)
     B, M, de = basis["B"], basis["M"], basis["d_eff"]
     C = S @ M
     U, T = thin_qr(C)
@@ -80,7 +82,7 @@ def sgmres_cycle(matvec, f, x, d, k, s, zeta, seed, cycle, tol=1e-8,
 
 
 def sgmres_solve(matvec, f, d, k, s, zeta, seed, tol=1e-8, max_cycles=50,
-                 early_exit_factor=0.25, cond_tol=1e14, x0=None, keep_last=False):
+                 early_exit_factor=0.25, cond_tol=1e14, x0=None, keep_last=False, cheb=None):
     """Restarted sGMRES.  Returns dict(x, cycles, columns, rel_res_true, r_est,
     hist_est (r_est_j/||f|| per column, concatenated), hist_true (per cycle),
     cond_T, flags)."""
@@ -93,7 +95,7 @@ def sgmres_solve(matvec, f, d, k, s, zeta, seed, tol=1e-8, max_cycles=50,
     cycles = 0
     for c in range(max_cycles):
         out = sgmres_cycle(matvec, f, x, d, k, s, zeta, seed, c, tol,
-                           early_exit_factor, cond_tol, fnorm)
+                           early_exit_factor, cond_tol, fnorm, cheb=cheb)
         cycles += 1
         x = out["x"]
         columns += out["j"]
