@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SKS_ABI_VERSION 2
+#define SKS_ABI_VERSION 3
 
 typedef enum {
   SKS_OK = 0,
@@ -124,8 +124,18 @@ typedef struct {
   double cond_tol;           /* kappa(T) warning threshold, default 1e14 */
   int32_t flags;             /* SKS_OPT_* bits */
   int32_t time_stride;       /* SKS_OPT_TIME_STEPS: time every time_stride-th step launch (0/1 = all) */
-  int32_t reserved[2];
+  int32_t basis;             /* SKS_BASIS_ARNOLDI (k-truncated, Eq. partorth) or SKS_BASIS_CHEBYSHEV */
+  int32_t reserved1;
+  double cheb_c, cheb_dx, cheb_dy;  /* Chebyshev: spectrum inside [c +- dx] x [+- i dy];
+                                       all 0 = closed-form box of the stencil operator */
 } sks_sgmres_opts;
+
+enum {
+  SKS_BASIS_ARNOLDI = 0,   /* k-partial Arnoldi, Eq. (partorth) */
+  SKS_BASIS_CHEBYSHEV = 1  /* shifted-scaled Chebyshev recurrence, Eq. (Chebrecurse) P:1192-1199,
+                              vectors rescaled to unit norm after use; no inner
+                              products in the recurrence (stencil operators only) */
+};
 
 enum {
   SKS_OPT_TIME_STEPS = 1  /* bracket every basis-step launch with CUDA events on the main stream and
@@ -166,7 +176,9 @@ typedef struct {
   int32_t d, k, s, zeta;
   uint64_t seed;
   double cond_tol;
-  int32_t reserved[4];
+  int32_t basis;        /* SKS_BASIS_* */
+  int32_t reserved[3];
+  double cheb_c, cheb_dx, cheb_dy;  /* as in sks_sgmres_opts */
 } sks_srr_opts;
 
 typedef struct {

@@ -30,7 +30,8 @@ class SgmresOpts(C.Structure):
     _fields_ = [("d", C.c_int32), ("k", C.c_int32), ("s", C.c_int32), ("zeta", C.c_int32),
                 ("seed", C.c_uint64), ("tol", C.c_double), ("max_cycles", C.c_int32),
                 ("sketch_batch", C.c_int32), ("early_exit_factor", C.c_double), ("cond_tol", C.c_double),
-                ("flags", C.c_int32), ("time_stride", C.c_int32), ("reserved", C.c_int32 * 2)]
+                ("flags", C.c_int32), ("time_stride", C.c_int32), ("basis", C.c_int32), ("reserved1", C.c_int32),
+                ("cheb_c", C.c_double), ("cheb_dx", C.c_double), ("cheb_dy", C.c_double)]
 
 
 class SgmresInfo(C.Structure):
@@ -42,11 +43,14 @@ class SgmresInfo(C.Structure):
 
 
 SKS_OPT_TIME_STEPS = 1
+SKS_BASIS_ARNOLDI, SKS_BASIS_CHEBYSHEV = 0, 1
+BASES = {"arnoldi": SKS_BASIS_ARNOLDI, "chebyshev": SKS_BASIS_CHEBYSHEV}
 
 
 class SrrOpts(C.Structure):
     _fields_ = [("d", C.c_int32), ("k", C.c_int32), ("s", C.c_int32), ("zeta", C.c_int32),
-                ("seed", C.c_uint64), ("cond_tol", C.c_double), ("reserved", C.c_int32 * 4)]
+                ("seed", C.c_uint64), ("cond_tol", C.c_double), ("basis", C.c_int32), ("reserved", C.c_int32 * 3),
+                ("cheb_c", C.c_double), ("cheb_dx", C.c_double), ("cheb_dy", C.c_double)]
 
 
 class SrrInfo(C.Structure):

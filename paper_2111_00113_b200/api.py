@@ -154,7 +154,8 @@ class Context:
 
     # ---------------------------------------------------------------- sGMRES
     def sgmres_solve(self, A, f, x0=None, *, d, k, s, zeta=8, seed=0, tol=1e-8, max_cycles=50,
-                     early_exit_factor=0.25, cond_tol=1e14, sketch_batch=0, hist_cap=None, time_steps=False, time_stride=1):
+                     early_exit_factor=0.25, cond_tol=1e14, sketch_batch=0, hist_cap=None, time_steps=False, time_stride=1,
+                     basis="arnoldi", cheb=None):
         op, keep = A.struct()
         fa, pf = _prep(f)
         n = fa.shape[0]
@@ -170,8 +171,10 @@ class Context:
         cap = hist_cap or (d * max_cycles + 8)
         hist = np.zeros(cap)
         hist_true = np.zeros(max_cycles + 2)
+        cc, cdx, cdy = cheb if cheb is not None else (0.0, 0.0, 0.0)
         opts = L.SgmresOpts(d, k, s, zeta, seed, tol, max_cycles, sketch_batch, early_exit_factor, cond_tol,
-                            L.SKS_OPT_TIME_STEPS if time_steps else 0, time_stride)
+                            L.SKS_OPT_TIME_STEPS if time_steps else 0, time_stride, L.BASES[basis], 0,
+                            cc, cdx, cdy)
         info = L.SgmresInfo()
         st = self.lib.sks_sgmres_solve(self.h, C.byref(op), pf, px, C.byref(opts), C.byref(info),
                                        hist.ctypes.data, cap, hist_true.ctypes.data, len(hist_true))
@@ -182,7 +185,8 @@ class Context:
                             converged=(st == 0))
 
     # ---------------------------------------------------------------- sRR
-    def srr_eigs(self, A, v0, *, d, k, s, nev, zeta=8, seed=0, cond_tol=1e14, want_vectors=False):
+    def srr_eigs(self, A, v0, *, d, k, s, nev, zeta=8, seed=0, cond_tol=1e14, want_vectors=False,
+                 basis="arnoldi", cheb=None):
         op, keep = A.struct()
         va, pv = _prep(v0)
         n = va.shape[0]
@@ -193,7 +197,8 @@ class Context:
         if want_vectors:
             Xr, pxr = _empty_like_place(va, (cap, n))
             Xi, pxi = _empty_like_place(va, (cap, n))
-        opts = L.SrrOpts(d, k, s, zeta, seed, cond_tol)
+        cc, cdx, cdy = cheb if cheb is not None else (0.0, 0.0, 0.0)
+        opts = L.SrrOpts(d, k, s, zeta, seed, cond_tol, L.BASES[basis], (C.c_int32 * 3)(), cc, cdx, cdy)
         info = L.SrrInfo()
         st = self.lib.sks_srr_eigs(self.h, C.byref(op), pv, C.byref(opts), nev, cap, th_re.ctypes.data,
                                    th_im.ctypes.data, rt.ctypes.data, re.ctypes.data, pxr, pxi, C.byref(info))

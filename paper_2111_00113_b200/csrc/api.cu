@@ -51,7 +51,7 @@ struct sks_ctx {
   // workspaces
   DevBuf W, xb, fb, vb, mr, xg, part, part2, partsk, sigma, H, mnorm, SW, Xp, Zb, U, T, rvec, rho, rest, coef,
       ctrl, small, Mh, Mh2, wr, wi, sel, th, yr, yi, ework, SAB, SB, Xr, Xi, AXr, AXi, rpb, cib, vab, cig, rbd,
-      tmp, bgsw, bgsc, plan;
+      tmp, bgsw, bgsc, plan, gam;
   CtrlBlock* h_ctrl = nullptr;   // pinned mirror
   double* h_small = nullptr;     // pinned scratch (4096 doubles)
   int64_t w_zeroed_bytes = 0;
@@ -333,7 +333,7 @@ sks_status sks_destroy(sks_ctx* c) {
                     &c->rho,  &c->rest, &c->coef,  &c->ctrl, &c->small, &c->Mh,  &c->Mh2,   &c->wr,    &c->wi,
                     &c->sel,  &c->th,   &c->yr,    &c->yi,   &c->ework, &c->SAB, &c->SB,    &c->Xr,    &c->Xi,
                     &c->AXr,  &c->AXi,  &c->rpb,   &c->cib,  &c->vab,  &c->cig,  &c->rbd,   &c->tmp,
-                    &c->bgsw, &c->bgsc, &c->plan};
+                    &c->bgsw, &c->bgsc, &c->plan, &c->gam};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->comm) ncclCommDestroy(c->comm);
@@ -422,6 +422,11 @@ static sks_status setup_basis(sks_ctx* c, const sks_operator* A, int k, int ncol
   SKS_TRY(ensure(c, c->H, sizeof(double) * (size_t)(ncol + 1) * (ncol + 1)));
   SKS_CK(c, cudaMemsetAsync(c->H.p, 0, sizeof(double) * (size_t)(ncol + 1) * (ncol + 1), c->main()));
   SKS_TRY(ensure(c, c->mnorm, sizeof(double) * (ncol + 2), true));
+  SKS_TRY(ensure(c, c->gam, sizeof(double) * (ncol + 2)));
+  {
+    std::vector<double> ones(ncol + 2, 1.0);  // gam_i = 1 unless a Chebyshev step sets it
+    SKS_CK(c, cudaMemcpy(c->gam.p, ones.data(), sizeof(double) * (ncol + 2), cudaMemcpyHostToDevice));
+  }
   SKS_TRY(ensure(c, c->ctrl, sizeof(CtrlBlock), true));
   SKS_TRY(ensure(c, c->small, sizeof(double) * 4096, true));
   b->pslots = c->num_sms * 4;
@@ -449,6 +454,8 @@ static sks_status setup_basis(sks_ctx* c, const sks_operator* A, int k, int ncol
     a.H = c->H.as<double>();
     a.ldH = b->ldH;
     a.mnorm = c->mnorm.as<double>();
+    a.gam = c->gam.as<double>();
+    a.basis = 0;
     a.ctrl = c->ctrl.as<CtrlBlock>();
     b->tma = c->use_tma && stencil_tma_supported(g.dim, g.m, k);
     b->sat = a;
@@ -502,6 +509,42 @@ static sks_status setup_basis(sks_ctx* c, const sks_operator* A, int k, int ncol
     SKS_CK(c, cudaStreamSynchronize(c->main()));  // host CSR arrays may be freed after return
   }
   SKS_CK(c, cudaMemsetAsync(c->part.p, 0, c->part.bytes, c->main()));
+  return SKS_OK;
+}
+
+// Chebyshev basis (Eq. Chebrecurse): k = 2 internally (the recurrence reads w_{j-1}
+// and w_{j-2}); the spectral box defaults to the closed form of the stencil operator:
+// eigenvalues of the 1D factor a + 2 sqrt(bc) cos(p pi/(m+1)) (real if bc >= 0), summed over
+// the dim axes (Kronecker sum).
+static sks_status set_basis(sks_ctx* c, const sks_operator* A, Basis& b, int basis, double bc_, double bdx,
+                            double bdy) {
+  if (basis == SKS_BASIS_ARNOLDI) return SKS_OK;
+  if (basis != SKS_BASIS_CHEBYSHEV) return fail(c, SKS_EINVAL, "unknown basis kind");
+  if (b.g.kind == SKS_OP_CSR) return fail(c, SKS_EUNSUPPORTED, "Chebyshev basis needs a stencil operator");
+  if (bdx == 0.0 && bdy == 0.0) {
+    const double m1 = (double)(b.g.m + 1);
+    const double ih2 = m1 * m1, ih = m1 / 2.0;
+    const double a1 = 2.0 * ih2, b1 = -ih2 - A->beta * ih, c1 = -ih2 + A->beta * ih;
+    const double cosm = std::cos(M_PI / m1);
+    bc_ = b.g.dim * a1;
+    if (b1 * c1 >= 0.0) {
+      bdx = b.g.dim * 2.0 * std::sqrt(b1 * c1) * cosm;
+      bdy = 0.0;
+    } else {
+      bdx = 0.0;
+      bdy = b.g.dim * 2.0 * std::sqrt(-b1 * c1) * cosm;
+    }
+  }
+  const double rho = std::max(bdx, bdy);
+  if (!(rho > 0.0) || !std::isfinite(rho) || !std::isfinite(bc_)) return fail(c, SKS_EINVAL, "bad Chebyshev box");
+  for (StepArgs* a : {&b.sa, &b.sat}) {
+    a->basis = 1;
+    a->k = 2;
+    a->cheb_c = bc_;
+    a->cheb_rho = rho;
+    a->cheb_e = (bdx * bdx - bdy * bdy) / (4.0 * rho);
+  }
+  b.k = 2;
   return SKS_OK;
 }
 
@@ -666,7 +709,7 @@ static sks_status qr_append(sks_ctx* c, Basis& b, int mode, int j0, int J, int s
   double* T = c->T.as<double>();
   const int ldT = b.ncol;
   SKS_CK(c, launch_form_cols(mode, c->SW.as<double>(), s, j0, J, b.k, c->H.as<double>(), b.ldH,
-                             c->sigma.as<double>(), X, J, 1, st));
+                             c->sigma.as<double>(), c->gam.as<double>(), X, J, 1, st));
   double* ws = c->bgsw.as<double>();
   int* cnt = c->bgsc.as<int>();
   SKS_CK(c, launch_utx(U, s, s, j0, X, J, Z, T, ldT, j0, 0, ws, cnt, st));
@@ -728,6 +771,7 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
   cudaStream_t st = c->main();
   Basis b;
   SKS_TRY(setup_basis(c, A, k, d + 2, &b));
+  SKS_TRY(set_basis(c, A, b, o->basis, o->cheb_c, o->cheb_dx, o->cheb_dy));
   const Geo& g = b.g;
   const int JB = panel_jb(s, o->sketch_batch > 0 ? o->sketch_batch : SKS_JB);
   b.time_steps = (o->flags & SKS_OPT_TIME_STEPS) != 0;
@@ -1001,6 +1045,7 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
   cudaStream_t st = c->main();
   Basis b;
   SKS_TRY(setup_basis(c, A, k, d + 2, &b));
+  SKS_TRY(set_basis(c, A, b, o->basis, o->cheb_c, o->cheb_dx, o->cheb_dy));
   const Geo& g = b.g;
   const int JB = panel_jb(s, SKS_JB);
   SKS_TRY(setup_small(c, b, s, JB));
@@ -1034,14 +1079,15 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
     SKS_TRY(qr_append(c, b, 1, j0, J, s, 0, de, st));
   }
   // ---- t = T^-1 U^T S w_de ; Mhat = Hbar[:de,:de] + t e_{de}^T
-  SKS_CK(c, launch_form_cols(2, c->SW.as<double>(), s, de, 1, k, c->H.as<double>(), b.ldH, c->sigma.as<double>(),
-                             c->Xp.as<double>(), 1, 1, st));
+  SKS_CK(c, launch_form_cols(2, c->SW.as<double>(), s, de, 1, b.k, c->H.as<double>(), b.ldH, c->sigma.as<double>(),
+                             c->gam.as<double>(), c->Xp.as<double>(), 1, 1, st));
   SKS_CK(c, launch_utx(c->U.as<double>(), s, s, de, c->Xp.as<double>(), 1, c->Zb.as<double>(), nullptr, 0, 0, 0,
                        c->bgsw.as<double>(), c->bgsc.as<int>(), st));
   SKS_CK(c, launch_trsv(c->T.as<double>(), b.ncol, de, c->Zb.as<double>(), nullptr, nullptr, c->coef.as<double>(), st));
   SKS_TRY(ensure(c, c->Mh, sizeof(double) * (size_t)de * de));
   SKS_TRY(ensure(c, c->Mh2, sizeof(double) * (size_t)de * de));
-  SKS_CK(c, launch_build_mhat(c->H.as<double>(), b.ldH, de, c->coef.as<double>(), c->Mh.as<double>(), st));
+  SKS_CK(c, launch_build_mhat(c->H.as<double>(), b.ldH, de, c->coef.as<double>(), c->gam.as<double>(),
+                              c->Mh.as<double>(), st));
   SKS_CK(c, cudaMemcpyAsync(c->Mh2.p, c->Mh.p, sizeof(double) * (size_t)de * de, cudaMemcpyDeviceToDevice, st));
   SKS_TRY(ensure(c, c->wr, sizeof(double) * de));
   SKS_TRY(ensure(c, c->wi, sizeof(double) * de));
@@ -1065,9 +1111,11 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
   // ---- sketched residual estimate with explicit C = SB, D = SAB
   SKS_TRY(ensure(c, c->SAB, sizeof(double) * (size_t)s * de));
   SKS_TRY(ensure(c, c->SB, sizeof(double) * (size_t)s * de));
-  SKS_CK(c, launch_form_cols(0, c->SW.as<double>(), s, 0, de, k, c->H.as<double>(), b.ldH, c->sigma.as<double>(),
+  SKS_CK(c, launch_form_cols(0, c->SW.as<double>(), s, 0, de, b.k, c->H.as<double>(), b.ldH, c->sigma.as<double>(),
+                             c->gam.as<double>(),
                              c->SAB.as<double>(), 1, s, st));
-  SKS_CK(c, launch_form_cols(1, c->SW.as<double>(), s, 0, de, k, c->H.as<double>(), b.ldH, c->sigma.as<double>(),
+  SKS_CK(c, launch_form_cols(1, c->SW.as<double>(), s, 0, de, b.k, c->H.as<double>(), b.ldH, c->sigma.as<double>(),
+                             c->gam.as<double>(),
                              c->SB.as<double>(), 1, s, st));
   double* d_rest = c->small.as<double>() + 128;
   SKS_CK(c, launch_srr_rest(c->SAB.as<double>(), c->SB.as<double>(), s, de, c->yr.as<double>(), c->yi.as<double>(),
@@ -1076,8 +1124,12 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
   SKS_CK(c, cudaEventRecord(ev_s1, st));
   c->launches += 14;
   // ---- Ritz vectors x_i = B y_i and true residuals ||A x - theta x|| / ||x||
-  SKS_TRY(ensure(c, c->Xr, sizeof(double) * (size_t)g.ld * nmax, true));
-  SKS_TRY(ensure(c, c->Xi, sizeof(double) * (size_t)g.ld * nmax, true));
+  SKS_TRY(ensure(c, c->Xr, sizeof(double) * (size_t)g.ld * nmax));
+  SKS_TRY(ensure(c, c->Xi, sizeof(double) * (size_t)g.ld * nmax));
+  // ghost planes must be zero (Dirichlet) for the residual stencil: clear the whole ghost layout
+  // (the buffers may hold another geometry's data from an earlier call)
+  SKS_CK(c, cudaMemsetAsync(c->Xr.p, 0, sizeof(double) * (size_t)g.ld * nmax, st));
+  SKS_CK(c, cudaMemsetAsync(c->Xi.p, 0, sizeof(double) * (size_t)g.ld * nmax, st));
   SKS_CK(c, launch_ritz_vectors(c->W.as<double>(), g.ld, g.off, g.n, de, c->sigma.as<double>(), c->yr.as<double>(),
                                 c->yi.as<double>(), de, nmax, c->Xr.as<double>(), c->Xi.as<double>(), g.ld, g.off,
                                 c->num_sms, st));

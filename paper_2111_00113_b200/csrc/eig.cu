@@ -21,12 +21,12 @@ namespace sks {
 
 // Mhat (d x d column-major, ld = d): Hbar[:d,:d] (+ last column += t)
 __global__ void build_mhat_kernel(const double* __restrict__ H, int ldH, int d, const double* __restrict__ t,
-                                  double* __restrict__ Mh) {
+                                  const double* __restrict__ gam, double* __restrict__ Mh) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= d * d) return;
   const int i = idx % d, j = idx / d;
   double v = (i <= j + 1) ? H[i + (int64_t)j * ldH] : 0.0;
-  if (j == d - 1) v += t[i];
+  if (j == d - 1) v += gam[d - 1] * t[i];  // A b_{d-1} = gam w_d + ...
   Mh[idx] = v;
 }
 
@@ -494,8 +494,9 @@ __global__ void srr_rest_kernel(const double* __restrict__ D, const double* __re
 }
 
 // ------------------------------------------------------------------------------
-cudaError_t launch_build_mhat(const double* H, int ldH, int d, const double* t, double* Mh, cudaStream_t st) {
-  build_mhat_kernel<<<(d * d + 255) / 256, 256, 0, st>>>(H, ldH, d, t, Mh);
+cudaError_t launch_build_mhat(const double* H, int ldH, int d, const double* t, const double* gam, double* Mh,
+                              cudaStream_t st) {
+  build_mhat_kernel<<<(d * d + 255) / 256, 256, 0, st>>>(H, ldH, d, t, gam, Mh);
   return cudaGetLastError();
 }
 cudaError_t launch_hqr(double* a, int n, int lda, double* wr, double* wi, int* info, cudaStream_t st) {

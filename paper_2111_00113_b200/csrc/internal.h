@@ -50,7 +50,8 @@ cudaError_t launch_sketch_table(int64_t row_begin, int64_t count, int s, int zet
 
 // smallside.cu
 cudaError_t launch_form_cols(int mode, const double* SW, int s, int j0, int J, int k, const double* H, int ldH,
-                             const double* sigma, double* X, int64_t ldq, int64_t ldj, cudaStream_t st);
+                             const double* sigma, const double* gam, double* X, int64_t ldq, int64_t ldj,
+                             cudaStream_t st);
 cudaError_t launch_utx(const double* U, int ldu, int s, int j0, const double* X, int J, double* Z, double* T,
                        int ldT, int tc0, int tacc, double* ws, int* cnt, cudaStream_t st);
 cudaError_t launch_xmuz(const double* U, int ldu, int s, int j0, double* X, int J, const double* Z, double* ws,
@@ -80,7 +81,8 @@ cudaError_t launch_remap_cols(int64_t nnz, const int32_t* ci_global, int32_t* ci
                               const int64_t* rb_dev, int64_t maxn, cudaStream_t st);
 
 // eig.cu
-cudaError_t launch_build_mhat(const double* H, int ldH, int d, const double* t, double* Mh, cudaStream_t st);
+cudaError_t launch_build_mhat(const double* H, int ldH, int d, const double* t, const double* gam, double* Mh,
+                              cudaStream_t st);
 cudaError_t launch_hqr(double* a, int n, int lda, double* wr, double* wi, int* info, cudaStream_t st);
 cudaError_t launch_select(const double* wr, const double* wi, int n, int nev, int* sel, int* nsel, double* th_re,
                           double* th_im, cudaStream_t st);

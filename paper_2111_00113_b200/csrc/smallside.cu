@@ -20,12 +20,12 @@
 namespace sks {
 
 // X[q*ldq + jj*ldj], columns jj = 0..J-1 correspond to basis index j = j0+jj.
-// mode 0 (SAB):  X[:,jj] = SW[:, j+1] + sum_{i=max(0,j-k+1)}^{j} H[i,j] sigma_i SW[:, i]
+// mode 0 (SAB):  X[:,jj] = gam_j SW[:, j+1] + sum_{i=max(0,j-k+1)}^{j} H[i,j] sigma_i SW[:, i]
 // mode 1 (SB):   X[:,jj] = sigma_j SW[:, j]
 // mode 2 (raw):  X[:,jj] = SW[:, j]
 __global__ void form_cols_kernel(int mode, const double* __restrict__ SW, int s, int j0, int J, int k,
                                  const double* __restrict__ H, int ldH, const double* __restrict__ sigma,
-                                 double* __restrict__ X, int64_t ldq, int64_t ldj) {
+                                 const double* __restrict__ gam, double* __restrict__ X, int64_t ldq, int64_t ldj) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= s * J) return;
   const int q = idx / J, jj = idx % J, j = j0 + jj;
@@ -35,7 +35,7 @@ __global__ void form_cols_kernel(int mode, const double* __restrict__ SW, int s,
   } else if (mode == 2) {
     v = SW[(int64_t)j * s + q];
   } else {
-    v = SW[(int64_t)(j + 1) * s + q];
+    v = gam[j] * SW[(int64_t)(j + 1) * s + q];
     const int lo = max(0, j - k + 1);
     for (int i = lo; i <= j; ++i) v += H[i + (int64_t)j * ldH] * sigma[i] * SW[(int64_t)i * s + q];
   }
@@ -565,9 +565,10 @@ __global__ void remap_cols_kernel(int64_t nnz, const int32_t* __restrict__ cg, i
 
 // ------------------------------------------------------------------------------
 cudaError_t launch_form_cols(int mode, const double* SW, int s, int j0, int J, int k, const double* H, int ldH,
-                             const double* sigma, double* X, int64_t ldq, int64_t ldj, cudaStream_t st) {
+                             const double* sigma, const double* gam, double* X, int64_t ldq, int64_t ldj,
+                             cudaStream_t st) {
   const int tot = s * J;
-  form_cols_kernel<<<(tot + 255) / 256, 256, 0, st>>>(mode, SW, s, j0, J, k, H, ldH, sigma, X, ldq, ldj);
+  form_cols_kernel<<<(tot + 255) / 256, 256, 0, st>>>(mode, SW, s, j0, J, k, H, ldH, sigma, gam, X, ldq, ldj);
   return cudaGetLastError();
 }
 

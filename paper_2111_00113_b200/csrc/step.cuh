@@ -37,6 +37,9 @@ struct StepArgs {
   double* H;        // Hbar, column-major, ld = ldH: Hbar[i, j] = h coefficient of b_i in w_{j+1}
   int ldH;
   double* mnorm;    // ||m_i||
+  double* gam;      // gam_i: A b_i = gam_i w_{i+1} + sum_l H[l, i] b_l  (1 for Arnoldi)
+  int basis;        // 0: k-truncated Arnoldi (Eq. partorth), 1: Chebyshev (Eq. Chebrecurse)
+  double cheb_c, cheb_rho, cheb_e;  // Chebyshev: centre, rho, (dx^2 - dy^2)/(4 rho)
   CtrlBlock* ctrl;
   int64_t ntiles;   // work items
   int tiles_x, tiles_y, zchunk;  // tiling
@@ -91,41 +94,69 @@ __device__ __forceinline__ bool step_prologue(const StepArgs& a, StepCoef* cf, d
     const double N = P[0];
     const double nu = sqrt(N);
     bool bd = !(N > 0.0) || !isfinite(N);
-    if (jm >= 1 && nu <= 1e-14 * a.mnorm[jm - 1]) bd = true;
+    // breakdown (reading O10): ||w_j|| negligible against the scale of the vector it came from
+    // (Arnoldi: ||A b_{j-1}||; Chebyshev: the previous raw vector, raw_0 = b_0 has norm 1)
+    const double ref = (a.basis == 1) ? (jm >= 2 ? 1.0 / a.sigma[jm - 1] : 1.0) : (jm >= 1 ? a.mnorm[jm - 1] : 0.0);
+    if (jm >= 1 && nu <= 1e-14 * ref) bd = true;
     if (cf->ok && bd) {
       cf->ok = 0;
       if (blockIdx.x == 0) {
         a.ctrl->stop_col = jm;
         a.ctrl->breakdown = 1;
-        if (jm >= 1) a.H[jm + (int64_t)(jm - 1) * a.ldH] = nu;
+        if (jm >= 1) a.H[jm + (int64_t)(jm - 1) * a.ldH] = a.gam[jm - 1] * nu;
         if (jm == 0) a.ctrl->rnorm = nu;
       }
     }
     if (cf->ok) {
       const double sg = 1.0 / nu;
       const int lo = max(0, j - k);
-      const double hj = sg * sg * P[1];
       cf->U = a.W + (int64_t)jm * a.ld;
-      cf->alpha = sg;
-      cf->beta_u = -hj * sg;
-      const int nv = jm - lo;
-      cf->nv = nv;
-      for (int l = 0; l < nv; ++l) {
-        const int i = lo + l;
-        const double si = a.sigma[i];
-        const double hi = sg * si * P[3 + i - (j - k)];
-        cf->V[l] = a.W + (int64_t)i * a.ld;
-        cf->c[l] = -hi * si;
-        const int sl = i - (j - k + 1);
-        cf->vslot[l] = (sl >= 0) ? 3 + sl : -1;
-        if (blockIdx.x == 0) a.H[i + (int64_t)jm * a.ldH] = hi;
+      if (a.basis == 1) {
+        // Chebyshev on the raw vectors w: w_1 = (A - cI) b_0 / (2 rho) with
+        // b_0 = sg w_0; w_j = [(A - cI) w_{j-1} - e raw_{j-2}] / rho, raw_0 = b_0 = sigma_0 w_0
+        const double rho = a.cheb_rho, cc0 = a.cheb_c, e = a.cheb_e;
+        const double s0 = (jm == 0) ? sg : 1.0;  // only the first vector is used normalised
+        const double al = (jm == 0) ? s0 / (2.0 * rho) : 1.0 / rho;
+        cf->alpha = al;
+        cf->beta_u = -cc0 * al;
+        cf->nv = (jm >= 1) ? 1 : 0;
+        if (jm >= 1) {
+          cf->V[0] = a.W + (int64_t)(jm - 1) * a.ld;
+          cf->c[0] = -(e / rho) * (jm == 1 ? a.sigma[0] : 1.0);
+          cf->vslot[0] = -1;
+        }
+      } else {
+        const double hj = sg * sg * P[1];
+        cf->alpha = sg;
+        cf->beta_u = -hj * sg;
+        const int nv = jm - lo;
+        cf->nv = nv;
+        for (int l = 0; l < nv; ++l) {
+          const int i = lo + l;
+          const double si = a.sigma[i];
+          const double hi = sg * si * P[3 + i - (j - k)];
+          cf->V[l] = a.W + (int64_t)i * a.ld;
+          cf->c[l] = -hi * si;
+          const int sl = i - (j - k + 1);
+          cf->vslot[l] = (sl >= 0) ? 3 + sl : -1;
+        }
       }
-      cf->uslot = (k >= 2) ? k + 1 : -1;
+      cf->uslot = (a.basis == 0 && k >= 2) ? k + 1 : -1;
       if (blockIdx.x == 0) {
+        // recurrence of column jm (both bases): A b_jm = gam w_j + sum_l H[l, jm] b_l with
+        // gam = sg/alpha, H[jm, jm] = -beta_u/alpha, H[i, jm] = -sg c_i / (alpha sigma_i)
+        const double al = cf->alpha;
+        const double gm = sg / al;
+        a.gam[jm] = gm;
+        a.H[jm + (int64_t)jm * a.ldH] = -cf->beta_u / al;
+        for (int l = 0; l < cf->nv; ++l) {
+          const int i = (a.basis == 1) ? jm - 1 : lo + l;
+          const double si = (a.basis == 1 && i == 0) ? a.sigma[0] : a.sigma[i];
+          a.H[i + (int64_t)jm * a.ldH] = -sg * cf->c[l] / (al * si);
+        }
         a.sigma[jm] = sg;
         a.mnorm[jm] = sg * sqrt(P[2]);
-        a.H[jm + (int64_t)jm * a.ldH] = hj;
-        if (jm >= 1) a.H[jm + (int64_t)(jm - 1) * a.ldH] = nu;
+        if (jm >= 1) a.H[jm + (int64_t)(jm - 1) * a.ldH] = a.gam[jm - 1] * nu;
         if (jm == 0) a.ctrl->rnorm = nu;
       }
     }

@@ -232,3 +232,35 @@ def test_srr_closed_form_full_dimension(ctx):
     assert out["info"]["columns"] == distinct.size
     assert np.abs(out["theta"].imag).max() <= 1e-9 * ev.max()
     np.testing.assert_allclose(np.sort(out["theta"].real), distinct, rtol=1e-9)
+
+
+# ---------------------------------------------------------------- Chebyshev basis (NEXT(1))
+@pytest.mark.parametrize("dim,m,beta,d", [(2, 32, 20.0, 60), (2, 33, 20.0, 60), (3, 24, 30.0, 60), (3, 19, 10.0, 40)])
+def test_sgmres_chebyshev_parity(ctx, dim, m, beta, d):
+    """Eq. Chebrecurse with the closed-form spectral box: same restarts, history
+    and solution as the oracle's Chebyshev sGMRES (even m: TMA kernels, odd m: generic)."""
+    P = _P()
+    n = m ** dim
+    f = rhs_normal(n, 2)
+    Ao = O.stencil_matrix(dim, m, beta)
+    box = O.spectral_box(dim, m, beta)
+    res = ctx.sgmres_solve(P.StencilOperator(dim, m, beta), f, d=d, k=2, s=2 * d, seed=2, tol=1e-8, max_cycles=8,
+                           basis="chebyshev")
+    orc = O.sgmres_solve(lambda x: Ao @ x, f, d, 2, 2 * d, 8, 2, tol=1e-8, max_cycles=8, cheb=box)
+    rel_gpu = np.linalg.norm(f - Ao @ res.x) / np.linalg.norm(f)
+    assert rel_gpu <= 2 * orc["rel_res_true"] and orc["rel_res_true"] <= 2 * rel_gpu
+    assert res.info["cycles"] == orc["cycles"] and res.info["columns"] == orc["columns"]
+    np.testing.assert_allclose(res.hist, orc["hist_est"], rtol=1e-6)
+
+
+def test_srr_chebyshev_parity(ctx):
+    P = _P()
+    m, beta, d = 48, 10.0, 60
+    v0 = start_vector(m * m, 4)
+    Ao = O.stencil_matrix(2, m, beta)
+    box = O.spectral_box(2, m, beta)
+    out = ctx.srr_eigs(P.StencilOperator(2, m, beta), v0, d=d, k=2, s=2 * d, nev=6, seed=4, basis="chebyshev")
+    bas = O.chebyshev_basis(lambda x: Ao @ x, v0, d, *box)
+    orc = O.srr_from_basis(lambda x: Ao @ x, bas["B"], bas["M"], O.sketch_matrix(m * m, 2 * d, 8, 4, 0), 6)
+    assert _match(out["theta"], orc["theta_all"]) <= 1e-8
+    np.testing.assert_allclose(np.sort(out["res_true"]), np.sort(orc["res_true"]), rtol=1e-4)
