@@ -1095,7 +1095,7 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
   SKS_TRY(ensure(c, c->th, sizeof(double) * 64));
   int* d_info = c->sel.as<int>() + 32;
   int* d_nsel = c->sel.as<int>() + 31;
-  SKS_CK(c, cudaMemsetAsync(d_info, 0, sizeof(int), st));
+  SKS_CK(c, cudaMemsetAsync(d_info, 0, sizeof(int) * 5, st));
   SKS_CK(c, launch_hqr(c->Mh2.as<double>(), de, de, c->wr.as<double>(), c->wi.as<double>(), d_info, st));
   double* th_re = c->th.as<double>();
   double* th_im = th_re + 32;
@@ -1179,6 +1179,8 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
   const int* hsel = reinterpret_cast<const int*>(hs + 576);
   const int nsel = hsel[31];
   const int hinfo = hsel[32];
+  if (getenv("SKS_DEBUG_HQR")) fprintf(stderr, "hqr: d=%d sweeps=%d bulge_steps=%d chase_kcyc=%d total_kcyc=%d\n", de, hsel[33],
+                                       hsel[34], hsel[35], hsel[36]);
   if (hinfo != 0) return fail(c, SKS_ENOTCONV, "QR algorithm did not converge on Mhat");
   for (int v = 0; v < nsel; ++v) {
     theta_re[v] = hs[512 + v];

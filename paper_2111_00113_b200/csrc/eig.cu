@@ -7,8 +7,9 @@
 //        Mhat = Hbar[:d, :d] + e_{d-1}-column correction  nu_d T^-1 U^T S b_d,
 //    so Mhat is upper Hessenberg by construction (no Hessenberg reduction needed).
 //  * hqr: Francis double-shift QR iteration on the Hessenberg matrix, eigenvalues only
-//    (one CTA; the scalar bulge set-up on thread 0, row/column updates spread over the
-//    block).
+//    (one CTA; deflation and shift-origin searches over the whole block, the bulge chased by
+//    one warp through 32x32 shared-memory windows, the off-window parts of each window's 29
+//    reflectors applied as one accumulated-Q block update by the whole CTA).
 //  * inverse iteration per selected eigenvalue on (Mhat - theta I) in complex arithmetic
 //    (Hessenberg LU with partial pivoting), one CTA per eigenvalue, giving y_i.
 //  * sketched residual estimate  ||D y - theta C y|| / ||C y||  (Eq. srr-resid-est).
@@ -44,12 +45,48 @@ __device__ __forceinline__ int block_max_int(int v, int* smem) {
   return r;
 }
 
-__global__ void __launch_bounds__(256) hqr_kernel(double* __restrict__ a, int n, int lda, double* __restrict__ wr,
-                                                  double* __restrict__ wi, int* __restrict__ info) {
+// 1/x and 1/sqrt(x) from the hardware approximations plus two Newton steps each (about 1 ulp;
+// used for reflector coefficients, where the IEEE-exact slow paths only add latency)
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y;
+}
+
+// D(8x8) += A(8x4, row) B(4x8, col) in fp64 on the tensor cores; per thread: a = A[lane/4][lane%4],
+// b = B[lane%4][lane/4], d0/d1 = D[lane/4][2(lane%4)], D[lane/4][2(lane%4)+1]
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+constexpr int HQ_R = 32;         // window rows/cols (the bulge region of HQ_W steps plus 3)
+constexpr int HQ_W = HQ_R - 3;   // bulge steps per window
+constexpr int HQ_LD = HQ_R + 1;  // odd pitch: row- and column-wise smem access both conflict-free
+constexpr int HQ_THREADS = 512;
+
+__global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a, int n, int lda,
+                                                         double* __restrict__ wr, double* __restrict__ wi,
+                                                         int* __restrict__ info) {
+  __shared__ double Hw[HQ_LD * (HQ_R + 1)];
+  __shared__ double Qs[HQ_LD * HQ_R];
   __shared__ double red[32];
   __shared__ int ired[32];
-  __shared__ double sp, sq, sr, sx, sy, sz, sw, st;
-  __shared__ int sl, snn, sm, sflag, sits, sdone;
+  __shared__ double sp, sq, sr, sx, sy, sw, st;
+  __shared__ int sl, snn, sm, sflag, sits, sdone, nsweep, nstep;
+  long long cyc_chase = 0, cyc_all = clock64();
   const int tid = threadIdx.x, nt = blockDim.x;
   // anorm
   double loc = 0.0;
@@ -62,6 +99,8 @@ __global__ void __launch_bounds__(256) hqr_kernel(double* __restrict__ a, int n,
     snn = n - 1;
     st = 0.0;
     sdone = 0;
+    nsweep = 0;
+    nstep = 0;
   }
   __syncthreads();
   while (true) {
@@ -183,6 +222,8 @@ __global__ void __launch_bounds__(256) hqr_kernel(double* __restrict__ a, int n,
           double p, q, r, z;
           pqr(best, p, q, r, z);
           sm = best;
+          nsweep += 1;
+          nstep += nn - best;
           sp = p;
           sq = q;
           sr = r;
@@ -197,63 +238,180 @@ __global__ void __launch_bounds__(256) hqr_kernel(double* __restrict__ a, int n,
         }
       }
       __syncthreads();
+      // --- the double-shift sweep k = m .. nn-1, chased through windows of HQ_W steps.
+      //     Window rows/cols R = [k0, r1] (r1 <= k0+31) live in shared memory (Hw, column k0-1
+      //     included for the reflector reads); warp 0 chases the bulge through them with warp-level
+      //     syncs only, applying each 3x3 reflector P_k exactly as the per-element sweep does inside
+      //     the window and accumulating Q = P_k0 ... P_k1-1.  The parts of P_k's row/column
+      //     transformations outside the window are applied afterwards as one block update by the
+      //     whole CTA: H[R, (r1, nn]] <- Q^T H[R, (r1, nn]],  H[[l, k0), R] <- H[[l, k0), R] Q.
+      //     Same reflectors, same order; only the rounding of the far updates differs.
       const int nn = snn, l = sl, m = sm;
-      for (int k = m; k <= nn - 1; ++k) {
-        if (tid == 0) {
-          double p = sp, q = sq, r = sr, x = 0.0;
-          int doit = 0;
-          if (k != m) {
-            p = HA(k, k - 1);
-            q = HA(k + 1, k - 1);
-            r = 0.0;
-            if (k != nn - 1) r = HA(k + 2, k - 1);
-            x = fabs(p) + fabs(q) + fabs(r);
-            if (x != 0.0) {
-              p /= x;
-              q /= x;
-              r /= x;
-            }
-          }
-          const double s = copysign(sqrt(p * p + q * q + r * r), p);
-          if (s != 0.0) {
-            if (k == m) {
-              if (l != m) HA(k, k - 1) = -HA(k, k - 1);
-            } else {
-              HA(k, k - 1) = -s * x;
-            }
-            p += s;
-            sx = p / s;
-            sy = q / s;
-            sz = r / s;
-            sq = q / p;
-            sr = r / p;
-            doit = 1;
-          }
-          sflag = doit;
+      const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+      for (int k0 = m; k0 <= nn - 1; k0 += HQ_W) {
+        const int k1 = min(k0 + HQ_W, nn);  // steps k0 .. k1-1
+        const int r1 = min(k0 + HQ_R - 1, nn);
+        const int nr = r1 - k0 + 1;  // <= 32
+        for (int idx = tid; idx < HQ_R * (HQ_R + 1); idx += nt) {
+          const int i = idx % HQ_R, c = idx / HQ_R;  // local row i = k0+i, local col c = k0-1+c
+          const int gj = k0 - 1 + c;
+          Hw[i + c * HQ_LD] = (i < nr && gj >= 0 && gj <= r1) ? HA(k0 + i, gj) : 0.0;
+        }
+        for (int idx = tid; idx < HQ_R * HQ_R; idx += nt) {
+          const int i = idx % HQ_R, c = idx / HQ_R;
+          Qs[i + c * HQ_LD] = (i == c) ? 1.0 : 0.0;
         }
         __syncthreads();
-        if (sflag) {
-          const double x = sx, y = sy, z = sz, q = sq, r = sr;
-          const bool three = (k != nn - 1);
-          for (int jj = k + tid; jj <= nn; jj += nt) {  // row transformation
-            double p = HA(k, jj) + q * HA(k + 1, jj);
-            if (three) {
-              p += r * HA(k + 2, jj);
-              HA(k + 2, jj) -= p * z;
+        long long tc0 = clock64();
+        if (warp == 0) {
+          for (int k = k0; k < k1; ++k) {
+            const int kk = k - k0;  // local row of k; local col of k is kk+1
+            double p, q, r;
+            if (k == m) {
+              p = sp;
+              q = sq;
+              r = sr;
+            } else {
+              p = Hw[kk + kk * HQ_LD];
+              q = Hw[kk + 1 + kk * HQ_LD];
+              r = (k != nn - 1) ? Hw[kk + 2 + kk * HQ_LD] : 0.0;
             }
-            HA(k + 1, jj) -= p * y;
-            HA(k, jj) -= p * x;
+            // reflector of (p, q, r): s = sign(p) ||(p,q,r)||, u = (p+s, q, r)/s, w = (1, q, r)/(p+s).
+            // The direction is scale-free, so the NR pre-scaling by |p|+|q|+|r| is only needed
+            // outside the safe exponent range; inside it, s and 1/s come from one rsqrt.
+            const double t = fma(p, p, fma(q, q, r * r));
+            __syncwarp();
+            if (t == 0.0) continue;  // uniform over the warp
+            double s, is;
+            if (t > 1e-280 && t < 1e280) {
+              is = rsqrt_nr(t);
+              s = t * is;
+              if (p < 0.0) {
+                s = -s;
+                is = -is;
+              }
+            } else {
+              const double x = fabs(p) + fabs(q) + fabs(r), ix = 1.0 / x;
+              const double ps = p * ix, qs = q * ix, rs = r * ix;
+              s = copysign(x * sqrt(ps * ps + qs * qs + rs * rs), p);
+              is = 1.0 / s;
+            }
+            if (lane == 0) {
+              if (k == m) {
+                if (l != m) Hw[kk + kk * HQ_LD] = -Hw[kk + kk * HQ_LD];
+              } else {
+                Hw[kk + kk * HQ_LD] = -s;
+              }
+            }
+            p += s;
+            const double ip = rcp_nr(p);
+            const double xx = p * is, yy = q * is, zz = r * is, qq = q * ip, rr = r * ip;
+            const bool three = (k != nn - 1);
+            {  // row transformation, columns k .. r1
+              const int c = kk + 1 + lane;
+              if (c <= nr) {
+                double* col = Hw + c * HQ_LD;
+                double pp = col[kk] + qq * col[kk + 1];
+                if (three) {
+                  pp += rr * col[kk + 2];
+                  col[kk + 2] -= pp * zz;
+                }
+                col[kk + 1] -= pp * yy;
+                col[kk] -= pp * xx;
+              }
+            }
+            __syncwarp();
+            {  // column transformation, rows k0 .. min(nn, k+3), and Q <- Q P_k
+              const int imax = min(nn, k + 3) - k0;
+              if (lane <= imax) {
+                double* c0 = Hw + (kk + 1) * HQ_LD;
+                double pp = xx * c0[lane] + yy * c0[lane + HQ_LD];
+                if (three) {
+                  pp += zz * c0[lane + 2 * HQ_LD];
+                  c0[lane + 2 * HQ_LD] -= pp * rr;
+                }
+                c0[lane + HQ_LD] -= pp * qq;
+                c0[lane] -= pp;
+              }
+              double* q0 = Qs + kk * HQ_LD;
+              double pp = xx * q0[lane] + yy * q0[lane + HQ_LD];
+              if (three) {
+                pp += zz * q0[lane + 2 * HQ_LD];
+                q0[lane + 2 * HQ_LD] -= pp * rr;
+              }
+              q0[lane + HQ_LD] -= pp * qq;
+              q0[lane] -= pp;
+            }
+            __syncwarp();
           }
-          __syncthreads();
-          const int mmin = nn < k + 3 ? nn : k + 3;
-          for (int i = l + tid; i <= mmin; i += nt) {  // column transformation
-            double p = x * HA(i, k) + y * HA(i, k + 1);
-            if (three) {
-              p += z * HA(i, k + 2);
-              HA(i, k + 2) -= p * r;
+        }
+        __syncthreads();
+        long long tc1 = clock64();
+        if (tid == 0) cyc_chase += tc1 - tc0;
+        // write the window back; far-right and far-above block updates (disjoint regions)
+        for (int idx = tid; idx < HQ_R * (HQ_R + 1); idx += nt) {
+          const int i = idx % HQ_R, c = idx / HQ_R;
+          const int gj = k0 - 1 + c;
+          if (i < nr && gj >= 0 && gj <= r1) HA(k0 + i, gj) = Hw[i + c * HQ_LD];
+        }
+        // far updates on the FP64 tensor cores (mma.m8n8k4.f64), one warp per 8-vector tile with
+        // the 32x32 Q held as 32 fragments per thread (frag[t][ks] = Q[4ks + lane%4, 8t + lane/4],
+        // which is the A fragment of Q^T and the B fragment of Q):
+        //   far right, 8 columns:  H[R, (r1, nn]]  <- Q^T H[R, (r1, nn]]
+        //   far above, 8 rows:     H[[l, k0), R]   <- H[[l, k0), R] Q
+        {
+          const int lr = lane >> 2, lc = lane & 3;
+          double fq[4][8];
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) fq[t][ks] = Qs[4 * ks + lc + (8 * t + lr) * HQ_LD];
+          const int ncol = nn - r1, nrow = k0 - l;
+          const int ntc = (ncol + 7) >> 3, ntr = (nrow + 7) >> 3;
+          for (int u = warp; u < ntc + ntr; u += nw) {
+            double fx[8], d[4][2];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) d[t][0] = d[t][1] = 0.0;
+            if (u < ntc) {
+              const int c = 8 * u + lr;  // B fragment: H[k0 + 4ks + lc, r1 + 1 + c]
+#pragma unroll
+              for (int ks = 0; ks < 8; ++ks) {
+                const int k = 4 * ks + lc;
+                fx[ks] = (c < ncol && k < nr) ? HA(k0 + k, r1 + 1 + c) : 0.0;
+              }
+#pragma unroll
+              for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+                for (int t = 0; t < 4; ++t) dmma884(d[t][0], d[t][1], fq[t][ks], fx[ks]);
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                const int m = 8 * t + lr;
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                  const int cc = 8 * u + 2 * lc + e;
+                  if (m < nr && cc < ncol) HA(k0 + m, r1 + 1 + cc) = d[t][e];
+                }
+              }
+            } else {
+              const int i = l + 8 * (u - ntc) + lr;  // A fragment: H[i, k0 + 4ks + lc]
+#pragma unroll
+              for (int ks = 0; ks < 8; ++ks) {
+                const int k = 4 * ks + lc;
+                fx[ks] = (i < k0 && k < nr) ? HA(i, k0 + k) : 0.0;
+              }
+#pragma unroll
+              for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+                for (int t = 0; t < 4; ++t) dmma884(d[t][0], d[t][1], fx[ks], fq[t][ks]);
+              const int io = l + 8 * (u - ntc) + lr;
+#pragma unroll
+              for (int t = 0; t < 4; ++t)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                  const int nc = 8 * t + 2 * lc + e;
+                  if (io < k0 && nc < nr) HA(io, k0 + nc) = d[t][e];
+                }
             }
-            HA(i, k + 1) -= p * q;
-            HA(i, k) -= p;
           }
         }
         __syncthreads();
@@ -265,6 +423,12 @@ __global__ void __launch_bounds__(256) hqr_kernel(double* __restrict__ a, int n,
       }
     }
     if (sdone) break;
+  }
+  if (tid == 0) {
+    info[1] = nsweep;  // diagnostics: Francis sweeps, bulge steps
+    info[2] = nstep;
+    info[3] = (int)(cyc_chase >> 10);  // diagnostics: clock cycles / 1024 in the chase, in total
+    info[4] = (int)((clock64() - cyc_all) >> 10);
   }
 }
 
@@ -500,7 +664,7 @@ cudaError_t launch_build_mhat(const double* H, int ldH, int d, const double* t, 
   return cudaGetLastError();
 }
 cudaError_t launch_hqr(double* a, int n, int lda, double* wr, double* wi, int* info, cudaStream_t st) {
-  hqr_kernel<<<1, 256, 0, st>>>(a, n, lda, wr, wi, info);
+  hqr_kernel<<<1, HQ_THREADS, 0, st>>>(a, n, lda, wr, wi, info);
   return cudaGetLastError();
 }
 cudaError_t launch_select(const double* wr, const double* wi, int n, int nev, int* sel, int* nsel, double* th_re,
