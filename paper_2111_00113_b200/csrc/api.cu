@@ -51,7 +51,7 @@ struct sks_ctx {
   // workspaces
   DevBuf W, xb, fb, vb, mr, xg, part, part2, partsk, sigma, H, mnorm, SW, Xp, Zb, U, T, rvec, rho, rest, coef,
       ctrl, small, Mh, Mh2, wr, wi, sel, th, yr, yi, ework, SAB, SB, Xr, Xi, AXr, AXi, rpb, cib, vab, cig, rbd,
-      tmp, bgsw, bgsc, plan, gam;
+      tmp, bgsw, bgsc, plan, gam, rcoef;
   CtrlBlock* h_ctrl = nullptr;   // pinned mirror
   double* h_small = nullptr;     // pinned scratch (4096 doubles)
   int64_t w_zeroed_bytes = 0;
@@ -333,7 +333,7 @@ sks_status sks_destroy(sks_ctx* c) {
                     &c->rho,  &c->rest, &c->coef,  &c->ctrl, &c->small, &c->Mh,  &c->Mh2,   &c->wr,    &c->wi,
                     &c->sel,  &c->th,   &c->yr,    &c->yi,   &c->ework, &c->SAB, &c->SB,    &c->Xr,    &c->Xi,
                     &c->AXr,  &c->AXi,  &c->rpb,   &c->cib,  &c->vab,  &c->cig,  &c->rbd,   &c->tmp,
-                    &c->bgsw, &c->bgsc, &c->plan, &c->gam};
+                    &c->bgsw, &c->bgsc, &c->plan, &c->gam, &c->rcoef};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->comm) ncclCommDestroy(c->comm);
@@ -1088,6 +1088,20 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
   SKS_TRY(ensure(c, c->Mh2, sizeof(double) * (size_t)de * de));
   SKS_CK(c, launch_build_mhat(c->H.as<double>(), b.ldH, de, c->coef.as<double>(), c->gam.as<double>(),
                               c->Mh.as<double>(), st));
+  SKS_CK(c, cudaEventRecord(c->ev_fork, st));
+  SKS_CK(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+  // ---- side stream, concurrent with the one-CTA eigen-solve: C = SB, D = SAB (for the sketched
+  //      residual estimate) and kappa(T)
+  SKS_TRY(ensure(c, c->SAB, sizeof(double) * (size_t)s * de));
+  SKS_TRY(ensure(c, c->SB, sizeof(double) * (size_t)s * de));
+  SKS_CK(c, launch_form_cols(0, c->SW.as<double>(), s, 0, de, b.k, c->H.as<double>(), b.ldH, c->sigma.as<double>(),
+                             c->gam.as<double>(),
+                             c->SAB.as<double>(), 1, s, c->side));
+  SKS_CK(c, launch_form_cols(1, c->SW.as<double>(), s, 0, de, b.k, c->H.as<double>(), b.ldH, c->sigma.as<double>(),
+                             c->gam.as<double>(),
+                             c->SB.as<double>(), 1, s, c->side));
+  SKS_CK(c, launch_cond(c->T.as<double>(), b.ncol, de, 12, nullptr, c->small.as<double>() + 8, c->side));
+  SKS_CK(c, cudaEventRecord(c->ev_join, c->side));
   SKS_CK(c, cudaMemcpyAsync(c->Mh2.p, c->Mh.p, sizeof(double) * (size_t)de * de, cudaMemcpyDeviceToDevice, st));
   SKS_TRY(ensure(c, c->wr, sizeof(double) * de));
   SKS_TRY(ensure(c, c->wi, sizeof(double) * de));
@@ -1108,19 +1122,10 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
   SKS_CK(c, cudaMemsetAsync(c->yi.p, 0, sizeof(double) * (size_t)de * nmax, st));
   SKS_CK(c, launch_inverse_iteration(c->Mh.as<double>(), de, th_re, th_im, d_nsel, nmax, c->ework.as<double>(),
                                      c->yr.as<double>(), c->yi.as<double>(), 3, 0.0, st));
-  // ---- sketched residual estimate with explicit C = SB, D = SAB
-  SKS_TRY(ensure(c, c->SAB, sizeof(double) * (size_t)s * de));
-  SKS_TRY(ensure(c, c->SB, sizeof(double) * (size_t)s * de));
-  SKS_CK(c, launch_form_cols(0, c->SW.as<double>(), s, 0, de, b.k, c->H.as<double>(), b.ldH, c->sigma.as<double>(),
-                             c->gam.as<double>(),
-                             c->SAB.as<double>(), 1, s, st));
-  SKS_CK(c, launch_form_cols(1, c->SW.as<double>(), s, 0, de, b.k, c->H.as<double>(), b.ldH, c->sigma.as<double>(),
-                             c->gam.as<double>(),
-                             c->SB.as<double>(), 1, s, st));
+  SKS_CK(c, cudaStreamWaitEvent(st, c->ev_join, 0));
   double* d_rest = c->small.as<double>() + 128;
   SKS_CK(c, launch_srr_rest(c->SAB.as<double>(), c->SB.as<double>(), s, de, c->yr.as<double>(), c->yi.as<double>(),
                             th_re, th_im, d_nsel, nmax, d_rest, st));
-  SKS_CK(c, launch_cond(c->T.as<double>(), b.ncol, de, 12, nullptr, c->small.as<double>() + 8, st));
   SKS_CK(c, cudaEventRecord(ev_s1, st));
   c->launches += 14;
   // ---- Ritz vectors x_i = B y_i and true residuals ||A x - theta x|| / ||x||
@@ -1130,10 +1135,11 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
   // (the buffers may hold another geometry's data from an earlier call)
   SKS_CK(c, cudaMemsetAsync(c->Xr.p, 0, sizeof(double) * (size_t)g.ld * nmax, st));
   SKS_CK(c, cudaMemsetAsync(c->Xi.p, 0, sizeof(double) * (size_t)g.ld * nmax, st));
+  SKS_TRY(ensure(c, c->rcoef, sizeof(double) * ritz_coef_doubles(de)));
   SKS_CK(c, launch_ritz_vectors(c->W.as<double>(), g.ld, g.off, g.n, de, c->sigma.as<double>(), c->yr.as<double>(),
-                                c->yi.as<double>(), de, nmax, c->Xr.as<double>(), c->Xi.as<double>(), g.ld, g.off,
-                                c->num_sms, st));
-  ++c->launches;
+                                c->yi.as<double>(), de, th_re, th_im, d_nsel, nmax, c->rcoef.as<double>(),
+                                c->Xr.as<double>(), c->Xi.as<double>(), g.ld, g.off, c->num_sms, st));
+  c->launches += 2;
   const int rgrid = c->num_sms * 2;
   double* rpart = c->tmp.as<double>();
   SKS_TRY(ensure(c, c->tmp, sizeof(double) * (size_t)rgrid * nmax * 2 + 64));

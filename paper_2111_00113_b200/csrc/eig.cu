@@ -432,41 +432,84 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
   }
 }
 
-// pick the nev largest |theta| (ties: Im descending, O23) and a split conjugate partner
-__global__ void select_kernel(const double* __restrict__ wr, const double* __restrict__ wi, int n, int nev,
-                              int* __restrict__ sel, int* __restrict__ nsel, double* __restrict__ th_re,
-                              double* __restrict__ th_im) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  int cnt = 0;
+// pick the nev largest |theta| (ties: Im descending, then lowest index; O23) and a split
+// conjugate partner: nev+1 rounds of a block-wide arg-max over the unused eigenvalues
+__device__ __forceinline__ bool sel_better(double m1, double i1, int k1, double m2, double i2, int k2) {
+  if (k2 < 0) return k1 >= 0;
+  if (k1 < 0) return false;
+  if (m1 != m2) return m1 > m2;
+  if (i1 != i2) return i1 > i2;
+  return k1 < k2;
+}
+
+__global__ void __launch_bounds__(1024) select_kernel(const double* __restrict__ wr, const double* __restrict__ wi,
+                                                      int n, int nev, int* __restrict__ sel, int* __restrict__ nsel,
+                                                      double* __restrict__ th_re, double* __restrict__ th_im) {
+  extern __shared__ int used[];  // n
+  __shared__ double rm[32], ri[32];
+  __shared__ int rk[32];
+  __shared__ int cnt_s;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = (blockDim.x + 31) >> 5;
+  for (int i = tid; i < n; i += blockDim.x) used[i] = 0;
+  if (tid == 0) cnt_s = 0;
+  __syncthreads();
   const int want = min(nev, n);
   for (int c = 0; c < want + 1 && c < n; ++c) {
-    int best = -1;
     double bm = -1.0, bi = 0.0;
-    for (int i = 0; i < n; ++i) {
-      bool used = false;
-      for (int t = 0; t < cnt; ++t) used |= (sel[t] == i);
-      if (used) continue;
+    int bk = -1;
+    for (int i = tid; i < n; i += blockDim.x) {
+      if (used[i]) continue;
       const double mg = hypot(wr[i], wi[i]);
-      if (best < 0 || mg > bm || (mg == bm && wi[i] > bi)) {
-        best = i;
+      if (sel_better(mg, wi[i], i, bm, bi, bk)) {
         bm = mg;
         bi = wi[i];
+        bk = i;
       }
     }
-    if (c < want) {
-      sel[cnt++] = best;
-    } else {
-      // position nev splits a conjugate pair?
-      const int last = sel[cnt - 1];
-      if (wi[last] != 0.0 && best >= 0 && fabs(wr[best] - wr[last]) <= 1e-12 * fabs(wr[last]) &&
-          fabs(wi[best] + wi[last]) <= 1e-12 * fabs(wi[last]))
-        sel[cnt++] = best;
+    for (int o = 16; o > 0; o >>= 1) {
+      const double om = __shfl_xor_sync(0xffffffffu, bm, o), oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
+      if (sel_better(om, oi, ok, bm, bi, bk)) {
+        bm = om;
+        bi = oi;
+        bk = ok;
+      }
     }
+    if (lane == 0) {
+      rm[wid] = bm;
+      ri[wid] = bi;
+      rk[wid] = bk;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < nw; ++w)
+        if (sel_better(rm[w], ri[w], rk[w], bm, bi, bk)) {
+          bm = rm[w];
+          bi = ri[w];
+          bk = rk[w];
+        }
+      int cnt = cnt_s;
+      if (c < want) {
+        sel[cnt++] = bk;
+        used[bk] = 1;
+      } else {
+        // position nev splits a conjugate pair?
+        const int last = sel[cnt - 1];
+        if (wi[last] != 0.0 && bk >= 0 && fabs(wr[bk] - wr[last]) <= 1e-12 * fabs(wr[last]) &&
+            fabs(wi[bk] + wi[last]) <= 1e-12 * fabs(wi[last]))
+          sel[cnt++] = bk;
+      }
+      cnt_s = cnt;
+    }
+    __syncthreads();
   }
-  *nsel = cnt;
-  for (int t = 0; t < cnt; ++t) {
-    th_re[t] = wr[sel[t]];
-    th_im[t] = wi[sel[t]];
+  if (tid == 0) {
+    const int cnt = cnt_s;
+    *nsel = cnt;
+    for (int t = 0; t < cnt; ++t) {
+      th_re[t] = wr[sel[t]];
+      th_im[t] = wi[sel[t]];
+    }
   }
 }
 
@@ -669,7 +712,7 @@ cudaError_t launch_hqr(double* a, int n, int lda, double* wr, double* wi, int* i
 }
 cudaError_t launch_select(const double* wr, const double* wi, int n, int nev, int* sel, int* nsel, double* th_re,
                           double* th_im, cudaStream_t st) {
-  select_kernel<<<1, 1, 0, st>>>(wr, wi, n, nev, sel, nsel, th_re, th_im);
+  select_kernel<<<1, 1024, sizeof(int) * n, st>>>(wr, wi, n, nev, sel, nsel, th_re, th_im);
   return cudaGetLastError();
 }
 size_t inverse_iteration_work_doubles(int d, int nmax) {

@@ -67,9 +67,13 @@ cudaError_t launch_cond(const double* T, int ldT, int n, int iters, CtrlBlock* c
                         cudaStream_t st);
 cudaError_t launch_assemble(double* x, const double* W, int64_t ld, int64_t off, int64_t n, const double* coef,
                             const int* ncp, int nc_max, int num_sms, cudaStream_t st);
+size_t ritz_coef_doubles(int nc);
+// Ritz vectors X_v = W diag(sigma) y_v for the nsel selected v (conjugate partners and real y
+// share compact columns); work: ritz_coef_doubles(nc) doubles.  Xr/Xi must be zero on entry.
 cudaError_t launch_ritz_vectors(const double* W, int64_t ld, int64_t off, int64_t n, int nc, const double* sigma,
-                                const double* yr, const double* yi, int ldy, int nvec, double* Xr, double* Xi,
-                                int64_t ldx, int64_t xoff, int num_sms, cudaStream_t st);
+                                const double* yr, const double* yi, int ldy, const double* th_re,
+                                const double* th_im, const int* nsel, int nmax, double* work, double* Xr,
+                                double* Xi, int64_t ldx, int64_t xoff, int num_sms, cudaStream_t st);
 cudaError_t launch_scale_cols(const double* W, int64_t ld, int64_t off, int64_t n, int nc, const double* sigma,
                               double* out, int64_t ldo, cudaStream_t st);
 cudaError_t launch_complex_residual(int64_t n, const double* Axr, const double* Axi, const double* xr,

@@ -459,39 +459,146 @@ __global__ void assemble_kernel(double* __restrict__ x, const double* __restrict
 }
 
 // X_re/X_im[:, v] = sum_{i<nc} W[:, i] * sigma_i * Y(i, v)  (Y complex, yr/yi column-major ld = ldy)
-template <int NV>
-__global__ void ritz_vectors_kernel(const double* __restrict__ W, int64_t ld, int64_t off, int64_t n, int nc,
-                                    const double* __restrict__ sigma, const double* __restrict__ yr,
-                                    const double* __restrict__ yi, int ldy, int nvec, double* __restrict__ Xr,
-                                    double* __restrict__ Xi, int64_t ldx, int64_t xoff) {
-  extern __shared__ double cs[];  // [nc][2*NV]
-  for (int t = threadIdx.x; t < nc * NV; t += blockDim.x) {
-    const int i = t / NV, v = t % NV;
-    cs[i * 2 * NV + v] = v < nvec ? sigma[i] * yr[i + v * ldy] : 0.0;
-    cs[i * 2 * NV + NV + v] = v < nvec ? sigma[i] * yi[i + v * ldy] : 0.0;
-  }
-  __syncthreads();
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
-    double ar[NV], ai[NV];
-#pragma unroll
-    for (int v = 0; v < NV; ++v) ar[v] = ai[v] = 0.0;
-    for (int i = 0; i < nc; ++i) {
-      const double w = W[off + p + (int64_t)i * ld];
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        ar[v] += cs[i * 2 * NV + v] * w;
-        ai[v] += cs[i * 2 * NV + NV + v] * w;
+// ---- Ritz vectors x_v = B y_v = W diag(sigma) y_v (Alg. 2), compacted.
+// A conjugate pair (theta, conj theta) has y_v' = conj(y_v), so X_v' = conj(X_v), and a real theta
+// has a real y: only the distinct real columns Re y, Im y are multiplied with W (C5: 10 instead
+// of 22), each written to up to two outputs with a sign.  ritz_coef_kernel builds the compact
+// coefficient matrix C = diag(sigma) [y columns] (nc x RV_MAXC) and the destination table.
+constexpr int RV_MAXC = 24;
+
+__global__ void ritz_coef_kernel(const double* __restrict__ sigma, const double* __restrict__ yr,
+                                 const double* __restrict__ yi, int ldy, int nc, const double* __restrict__ th_re,
+                                 const double* __restrict__ th_im, const int* __restrict__ nsel, int nmax,
+                                 double* __restrict__ coef, int* __restrict__ meta) {
+  __shared__ int src[RV_MAXC];  // compact column -> (v << 1) | imag
+  __shared__ int ncomp;
+  if (threadIdx.x == 0) {
+    int dst[2 * RV_MAXC];
+    for (int t = 0; t < 2 * RV_MAXC; ++t) dst[t] = 0;
+    int pr[32];  // v -> compact column of Re y_v, or -1; paired flag via -2
+    const int ns = min(*nsel, nmax);
+    int nco = 0;
+    for (int v = 0; v < ns && v < 32; ++v) {
+      pr[v] = -1;
+      if (th_im[v] == 0.0) {
+        if (nco < RV_MAXC) {
+          src[nco] = v << 1;
+          dst[2 * nco] = 2 * v + 1;  // +Xr_v   (out id + 1, signed)
+          pr[v] = nco++;
+        }
+        continue;
+      }
+      int u = -1;
+      for (int w = 0; w < v; ++w)
+        if (pr[w] >= 0 && th_im[w] != 0.0 && fabs(th_re[w] - th_re[v]) <= 1e-12 * fabs(th_re[v]) &&
+            fabs(th_im[w] + th_im[v]) <= 1e-12 * fabs(th_im[v])) {
+          u = w;
+          break;
+        }
+      if (u >= 0) {  // X_v = conj(X_u)
+        const int cr = pr[u];
+        dst[2 * cr + 1] = 2 * v + 1;           // +Xr_v from Re
+        dst[2 * (cr + 1) + 1] = -(2 * v + 2);  // -Xi_v from Im
+        pr[u] = -2;
+        continue;
+      }
+      if (nco + 2 <= RV_MAXC) {
+        src[nco] = v << 1;
+        dst[2 * nco] = 2 * v + 1;
+        src[nco + 1] = (v << 1) | 1;
+        dst[2 * (nco + 1)] = 2 * v + 2;  // +Xi_v
+        pr[v] = nco;
+        nco += 2;
       }
     }
-#pragma unroll
-    for (int v = 0; v < NV; ++v)
-      if (v < nvec) {
-        Xr[xoff + p + v * ldx] = ar[v];
-        Xi[xoff + p + v * ldx] = ai[v];
-      }
+    ncomp = nco;
+    meta[0] = nco;
+    for (int t = 0; t < 2 * RV_MAXC; ++t) meta[1 + t] = dst[t];
+  }
+  __syncthreads();
+  const int nco = ncomp;
+  for (int idx = threadIdx.x; idx < nc * RV_MAXC; idx += blockDim.x) {
+    const int i = idx / RV_MAXC, c = idx % RV_MAXC;
+    double v = 0.0;
+    if (c < nco) {
+      const int sv = src[c] >> 1;
+      v = sigma[i] * ((src[c] & 1) ? yi[i + (int64_t)sv * ldy] : yr[i + (int64_t)sv * ldy]);
+    }
+    coef[idx] = v;
   }
 }
 
+// one pass over W for compact columns [c0, c0 + NC); RB rows per thread
+template <int NC, int RB>
+__device__ __forceinline__ void ritz_body(const double* __restrict__ W, int64_t ld, int64_t off, int64_t n, int nc,
+                                          const double* __restrict__ cs, const int* __restrict__ dst, int c0,
+                                          int nco, double* __restrict__ Xr, double* __restrict__ Xi, int64_t ldx,
+                                          int64_t xoff) {
+  const int64_t rpb = (int64_t)blockDim.x * RB;
+  for (int64_t base = blockIdx.x * rpb; base < n; base += (int64_t)gridDim.x * rpb) {
+    int64_t p[RB];
+    bool ok[RB];
+    double acc[RB][NC];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      p[r] = base + threadIdx.x + (int64_t)r * blockDim.x;
+      ok[r] = p[r] < n;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) acc[r][c] = 0.0;
+    }
+    const double* wp = W + off;
+#pragma unroll 4
+    for (int i = 0; i < nc; ++i) {
+      double w[RB];
+#pragma unroll
+      for (int r = 0; r < RB; ++r) w[r] = ok[r] ? __ldg(wp + p[r] + (int64_t)i * ld) : 0.0;
+      const double2* ci = reinterpret_cast<const double2*>(cs + i * RV_MAXC + c0);
+#pragma unroll
+      for (int c2 = 0; c2 < NC / 2; ++c2) {
+        const double2 cv = ci[c2];
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+          acc[r][2 * c2] = fma(cv.x, w[r], acc[r][2 * c2]);
+          acc[r][2 * c2 + 1] = fma(cv.y, w[r], acc[r][2 * c2 + 1]);
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      if (c0 + c >= nco) break;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int d = dst[2 * (c0 + c) + e];
+        if (d == 0) continue;
+        const int o = (d > 0 ? d : -d) - 1;
+        double* out = ((o & 1) ? Xi : Xr) + xoff + (int64_t)(o >> 1) * ldx;
+        const double sg = d > 0 ? 1.0 : -1.0;
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+          if (ok[r]) out[p[r]] = sg * acc[r][c];
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256, 3) ritz_vectors_kernel(const double* __restrict__ W, int64_t ld, int64_t off,
+                                                              int64_t n, int nc, const double* __restrict__ coef,
+                                                              const int* __restrict__ meta, double* __restrict__ Xr,
+                                                              double* __restrict__ Xi, int64_t ldx, int64_t xoff) {
+  extern __shared__ double cs[];  // [nc][RV_MAXC]
+  __shared__ int dst[2 * RV_MAXC];
+  for (int t = threadIdx.x; t < nc * RV_MAXC; t += blockDim.x) cs[t] = coef[t];
+  if (threadIdx.x < 2 * RV_MAXC) dst[threadIdx.x] = meta[1 + threadIdx.x];
+  const int nco = meta[0];
+  __syncthreads();
+  // C5's ten Ritz vectors need 10-12 compact columns: one pass; more columns take more passes
+  for (int c0 = 0; c0 < nco; c0 += 12) {
+    if (nco - c0 <= 4)
+      ritz_body<4, 2>(W, ld, off, n, nc, cs, dst, c0, nco, Xr, Xi, ldx, xoff);
+    else
+      ritz_body<12, 2>(W, ld, off, n, nc, cs, dst, c0, nco, Xr, Xi, ldx, xoff);
+  }
+}
 
 // out[:, i] = sigma_i W[off:off+n, i]   (normalised basis columns, ld = ldo)
 __global__ void scale_cols_kernel(const double* __restrict__ W, int64_t ld, int64_t off, int64_t n, int nc,
@@ -647,26 +754,22 @@ cudaError_t launch_assemble(double* x, const double* W, int64_t ld, int64_t off,
   return cudaGetLastError();
 }
 
+size_t ritz_coef_doubles(int nc) { return (size_t)nc * RV_MAXC + 64; }
+
 cudaError_t launch_ritz_vectors(const double* W, int64_t ld, int64_t off, int64_t n, int nc, const double* sigma,
-                                const double* yr, const double* yi, int ldy, int nvec, double* Xr, double* Xi,
-                                int64_t ldx, int64_t xoff, int num_sms, cudaStream_t st) {
-  int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms * 4);
+                                const double* yr, const double* yi, int ldy, const double* th_re,
+                                const double* th_im, const int* nsel, int nmax, double* work, double* Xr,
+                                double* Xi, int64_t ldx, int64_t xoff, int num_sms, cudaStream_t st) {
+  double* coef = work;
+  int* meta = reinterpret_cast<int*>(work + (size_t)nc * RV_MAXC);
+  ritz_coef_kernel<<<1, 256, 0, st>>>(sigma, yr, yi, ldy, nc, th_re, th_im, nsel, nmax, coef, meta);
+  const size_t smem = sizeof(double) * (size_t)nc * RV_MAXC;
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute(ritz_vectors_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return cudaGetLastError();
+  int grid = (int)std::min<int64_t>((n + 511) / 512, (int64_t)num_sms * 3);
   if (grid < 1) grid = 1;
-  if (nvec <= 4) {
-    const size_t smem = sizeof(double) * nc * 8;
-    if (smem > 48 * 1024 &&
-        cudaFuncSetAttribute(ritz_vectors_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-      return cudaGetLastError();
-    ritz_vectors_kernel<4><<<grid, 256, smem, st>>>(W, ld, off, n, nc, sigma, yr, yi, ldy, nvec, Xr, Xi, ldx, xoff);
-  } else if (nvec <= 12) {
-    const size_t smem = sizeof(double) * nc * 24;
-    if (smem > 48 * 1024 &&
-        cudaFuncSetAttribute(ritz_vectors_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-      return cudaGetLastError();
-    ritz_vectors_kernel<12><<<grid, 256, smem, st>>>(W, ld, off, n, nc, sigma, yr, yi, ldy, nvec, Xr, Xi, ldx, xoff);
-  } else {
-    return cudaErrorInvalidValue;
-  }
+  ritz_vectors_kernel<<<grid, 256, smem, st>>>(W, ld, off, n, nc, coef, meta, Xr, Xi, ldx, xoff);
   return cudaGetLastError();
 }
 
