@@ -21,6 +21,7 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "common.cuh"
 #include "internal.h"
@@ -139,34 +140,62 @@ __global__ void __launch_bounds__(ZT, 1)
     const bool xyin = wt && (unsigned)gxw < (unsigned)m && (unsigned)gyw < (unsigned)m;
     const bool aw = inner && gxw < m && gyw < m;    // this thread forms A w_j (interior output)
     double* wcol = Wout + (int64_t)(wa - 1) * pl + (int64_t)gyw * m + gxw;  // plane wa-1 of the column
-    int sbw = ZS;  // ring slot of plane p0 (= ((t+1) mod 3) ZS), uniform; plane p0-1 is at sbw-1 (mod R)
-    for (int t = 0; t < nsteps; ++t) {
+    // Fast steps (CTA-uniform: every plane of the step inside the piece and the domain, t >= T0)
+    // run without per-plane predicates; the xy mask is folded into the coefficients (a column
+    // outside the domain gets w = 0 A u + 0 u + 0 v = 0).  The w_j ring has period 3 steps, so
+    // the step body is instantiated for the 3 ring phases and every ring offset is a constant.
+    const double am = xyin ? alpha : 0.0, bm = xyin ? beta_u : 0.0;
+    double clm[KM - 1];
+#pragma unroll
+    for (int l = 0; l < KM - 1; ++l) clm[l] = xyin ? cl[l] : 0.0;
+    constexpr int T0 = ZS == 1 ? 2 : 1;
+    auto step = [&](int t, auto phc) {
+      constexpr int PH = decltype(phc)::value;
+      constexpr int SBW = ((PH + 1) % 3) * ZS;          // ring slot of plane p0
+      constexpr int SBP = SBW == 0 ? R - 1 : SBW - 1;   // ring slot of plane p0-1
       const uint32_t slot = (s0 + (uint32_t)t) & 1u;
       mbar_wait(&bar[slot], (phase >> slot) & 1u);
       phase ^= 1u << slot;
       const double* sU = sm + slot * STG;
       const double* sV = sU + UB;
       const int p0 = wa + t * ZS;
+      const bool fast = t >= T0 && p0 + ZS - 1 <= zb && z0g + p0 + ZS - 1 < m;
       double w[ZS], c[ZS + 2], v[KM - 1][ZS];
-      double* rw = ring + sbw * ZW + cwb;                       // plane p0 (+ i ZW for p0 + i)
-      const double* rp = ring + (sbw == 0 ? R - 1 : sbw - 1) * ZW + cwb;  // plane p0-1
+      double* rw = ring + SBW * ZW + cwb;        // plane p0 (+ i ZW for p0 + i)
+      const double* rp = ring + SBP * ZW + cwb;  // plane p0-1
       // ---- w_j on planes p0 .. p0+ZS-1 (this thread's column)
 #pragma unroll
       for (int k = 0; k < ZS + 2; ++k) c[k] = sU[k * ZUP + cu];
+      if (fast) {
 #pragma unroll
-      for (int i = 0; i < ZS; ++i) {
-        const int p = p0 + i;
+        for (int i = 0; i < ZS; ++i) {
 #pragma unroll
-        for (int l = 0; l < KM - 1; ++l) v[l][i] = (FULL || l < nv) ? sV[l * VB + i * ZVP + cvv] : 0.0;
-        const double* q = sU + (i + 1) * ZUP + cu;
-        const double Au = cc * c[i + 1] + cm * (q[-1] + q[-ZUX] + c[i]) + cp * (q[1] + q[ZUX] + c[i + 2]);
-        double wv = alpha * Au + beta_u * c[i + 1];
+          for (int l = 0; l < KM - 1; ++l) v[l][i] = (FULL || l < nv) ? sV[l * VB + i * ZVP + cvv] : 0.0;
+          const double* q = sU + (i + 1) * ZUP + cu;
+          const double Au = cc * c[i + 1] + cm * (q[-1] + q[-ZUX] + c[i]) + cp * (q[1] + q[ZUX] + c[i + 2]);
+          double wv = am * Au + bm * c[i + 1];
 #pragma unroll
-        for (int l = 0; l < KM - 1; ++l)
-          if (FULL || l < nv) wv += cl[l] * v[l][i];
-        wv = (xyin && (unsigned)(z0g + p) < (unsigned)m && p <= zb) ? wv : 0.0;
-        w[i] = wv;
-        if (wt) rw[i * ZW] = wv;
+          for (int l = 0; l < KM - 1; ++l)
+            if (FULL || l < nv) wv += clm[l] * v[l][i];
+          w[i] = wv;
+          if (wt) rw[i * ZW] = wv;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < ZS; ++i) {
+          const int p = p0 + i;
+#pragma unroll
+          for (int l = 0; l < KM - 1; ++l) v[l][i] = (FULL || l < nv) ? sV[l * VB + i * ZVP + cvv] : 0.0;
+          const double* q = sU + (i + 1) * ZUP + cu;
+          const double Au = cc * c[i + 1] + cm * (q[-1] + q[-ZUX] + c[i]) + cp * (q[1] + q[ZUX] + c[i + 2]);
+          double wv = alpha * Au + beta_u * c[i + 1];
+#pragma unroll
+          for (int l = 0; l < KM - 1; ++l)
+            if (FULL || l < nv) wv += cl[l] * v[l][i];
+          wv = (xyin && (unsigned)(z0g + p) < (unsigned)m && p <= zb) ? wv : 0.0;
+          w[i] = wv;
+          if (wt) rw[i * ZW] = wv;
+        }
       }
       __syncthreads();
       if (tid == 0 && t + 2 < nsteps) issue(t + 2);  // the stage just consumed is free
@@ -176,7 +205,7 @@ __global__ void __launch_bounds__(ZT, 1)
 #pragma unroll
         for (int i = 0; i < ZS; ++i) {
           const int qp = p0 - 1 + i;
-          if (qp >= za && qp < zb) {
+          if (fast || (qp >= za && qp < zb)) {
             const double wq = (i == 0) ? wp1 : w[i - 1];
             const double wqm = (i == 0) ? wp2 : (i == 1 ? wp1 : w[i - 2]);
             const double* r = (i == 0) ? rp : rw + (i - 1) * ZW;
@@ -203,7 +232,11 @@ __global__ void __launch_bounds__(ZT, 1)
 #pragma unroll
       for (int l = 0; l < KM - 1; ++l) vlast[l] = v[l][ZS - 1];
       wcol += (int64_t)ZS * pl;
-      sbw = (sbw + ZS == R) ? 0 : sbw + ZS;
+    };
+    for (int t = 0; t < nsteps; t += 3) {
+      step(t, std::integral_constant<int, 0>{});
+      if (t + 1 < nsteps) step(t + 1, std::integral_constant<int, 1>{});
+      if (t + 2 < nsteps) step(t + 2, std::integral_constant<int, 2>{});
     }
     sidx = s0 + (uint32_t)nsteps;
     __syncthreads();  // ring and stages are reused by the next piece
