@@ -72,16 +72,77 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
                : "d"(a), "d"(b));
 }
 
+// reflector of (p, q, r) in the form of the Francis sweep: s = sign(p) ||(p,q,r)||,
+// u = (p+s, q, r)/s, w = (1, q/(p+s), r/(p+s)), P = I - u w^T; (p,q,r) = 0 gives u = 0 (P = I)
+struct HqRefl {
+  double xx, yy, zz, qq, rr, s;
+  bool valid;
+};
+__device__ __forceinline__ HqRefl hq_refl(double p, double q, double r) {
+  HqRefl R;
+  const double t = fma(p, p, fma(q, q, r * r));
+  double s, is;
+  if (t > 1e-280 && t < 1e280) {
+    is = rsqrt_nr(t);
+    s = t * is;
+  } else {
+    const double x = fabs(p) + fabs(q) + fabs(r);
+    if (x == 0.0) {
+      R.xx = R.yy = R.zz = R.qq = R.rr = R.s = 0.0;
+      R.valid = false;
+      return R;
+    }
+    const double ix = 1.0 / x, ps = p * ix, qs = q * ix, rs = r * ix;
+    s = x * sqrt(ps * ps + qs * qs + rs * rs);
+    is = 1.0 / s;
+  }
+  if (p < 0.0) {
+    s = -s;
+    is = -is;
+  }
+  const double pp = p + s, ip = rcp_nr(pp);
+  R.s = s;
+  R.xx = pp * is;
+  R.yy = q * is;
+  R.zz = r * is;
+  R.qq = q * ip;
+  R.rr = r * ip;
+  R.valid = true;
+  return R;
+}
+
+// branch-free variant for the chase (the matrix is pre-scaled to norm ~1, so p^2+q^2+r^2 cannot
+// overflow; a sub-normal-range bulge is treated as zero, i.e. P = I)
+__device__ __forceinline__ HqRefl hq_refl_fast(double p, double q, double r) {
+  HqRefl R;
+  const double t = fma(p, p, fma(q, q, r * r));
+  const bool ok = t >= 2.3e-308;
+  double is = rsqrt_nr(ok ? t : 1.0);
+  double s = t * is;
+  s = p < 0.0 ? -s : s;
+  is = p < 0.0 ? -is : is;
+  const double pp = p + s, ip = rcp_nr(ok ? pp : 1.0);
+  R.s = s;
+  R.xx = ok ? pp * is : 0.0;
+  R.yy = ok ? q * is : 0.0;
+  R.zz = ok ? r * is : 0.0;
+  R.qq = ok ? q * ip : 0.0;
+  R.rr = ok ? r * ip : 0.0;
+  R.valid = ok;
+  return R;
+}
+
 constexpr int HQ_R = 32;         // window rows/cols (the bulge region of HQ_W steps plus 3)
 constexpr int HQ_W = HQ_R - 3;   // bulge steps per window
 constexpr int HQ_LD = HQ_R + 1;  // odd pitch: row- and column-wise smem access both conflict-free
-constexpr int HQ_THREADS = 512;
+constexpr int HQ_THREADS = 384;
+constexpr int HQ_QSZ = HQ_LD * HQ_R;
 
 __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a, int n, int lda,
                                                          double* __restrict__ wr, double* __restrict__ wi,
                                                          int* __restrict__ info) {
-  __shared__ double Hw[HQ_LD * (HQ_R + 1)];
-  __shared__ double Qs[HQ_LD * HQ_R];
+  __shared__ double Hw[HQ_LD * (HQ_R + 1) + 4 * 32];  // window + per-lane scratch
+  __shared__ double Qsh[2 * HQ_QSZ];  // accumulated Q of the current / previous window
   __shared__ double red[32];
   __shared__ int ired[32];
   __shared__ double sp, sq, sr, sx, sy, sw, st;
@@ -94,7 +155,16 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
     const int i = (int)(idx % n), j = (int)(idx / n);
     if (j >= i - 1) loc += fabs(HA(i, j));
   }
-  const double anorm = block_sum(loc, red);
+  const double anorm0 = block_sum(loc, red);
+  // scale by a power of two so that ||H||_1-ish ~ 1 (exact; the eigenvalues are scaled back at the
+  // end): the reflectors of the sweep then never leave the normal exponent range
+  const double hsc = anorm0 > 0.0 ? ldexp(1.0, -ilogb(anorm0)) : 1.0;
+  const double anorm = anorm0 * hsc;
+  for (int64_t idx = tid; idx < (int64_t)n * n; idx += nt) {
+    const int i = (int)(idx % n), j = (int)(idx / n);
+    HA(i, j) *= hsc;
+  }
+  __syncthreads();
   if (tid == 0) {
     snn = n - 1;
     st = 0.0;
@@ -248,172 +318,234 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
       //     Same reflectors, same order; only the rounding of the far updates differs.
       const int nn = snn, l = sl, m = sm;
       const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-      for (int k0 = m; k0 <= nn - 1; k0 += HQ_W) {
-        const int k1 = min(k0 + HQ_W, nn);  // steps k0 .. k1-1
-        const int r1 = min(k0 + HQ_R - 1, nn);
-        const int nr = r1 - k0 + 1;  // <= 32
+      // Off-window block update with the accumulated Q of a window [wk0, wr1] (FP64 tensor cores,
+      // mma.m8n8k4.f64; a warp per 8-vector tile, the 32x32 Q held as 32 fragments per thread:
+      // frag[t][ks] = Q[4ks + lane%4, 8t + lane/4], the A fragment of Q^T and the B fragment of Q):
+      //   right part, columns (clo, chi]:  H[R, c]  <- Q^T H[R, c]
+      //   above part, rows [alo, ahi):     H[i, R]  <- H[i, R] Q
+      auto far_update = [&](const double* qb, int wk0, int wr1, int clo, int chi, int alo, int ahi, int w0,
+                            int ws) {
+        const int wnr = wr1 - wk0 + 1;
+        const int lr = lane >> 2, lc = lane & 3;
+        const int ncol = chi - clo, nrow = ahi - alo;
+        const int ntc = ncol > 0 ? (ncol + 7) >> 3 : 0, ntr = nrow > 0 ? (nrow + 7) >> 3 : 0;
+        // w0 < 0: deferred mode, workers are the warps off warp 0's scheduler (warp % 4 != 0)
+        int me = warp - w0;
+        if (w0 < 0) {
+          if ((warp & 3) == 0) return;
+          me = warp - (warp >> 2) - 1;
+        }
+        if (me < 0 || me >= ntc + ntr) return;
+        double fq[4][8];
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) fq[t][ks] = qb[4 * ks + lc + (8 * t + lr) * HQ_LD];
+        for (int u = me; u < ntc + ntr; u += ws) {
+          double fx[8], d[4][2];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) d[t][0] = d[t][1] = 0.0;
+          if (u < ntc) {
+            const int c = 8 * u + lr;  // B fragment: H[wk0 + 4ks + lc, clo + 1 + c]
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+              const int k = 4 * ks + lc;
+              fx[ks] = (c < ncol && k < wnr) ? HA(wk0 + k, clo + 1 + c) : 0.0;
+            }
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+              for (int t = 0; t < 4; ++t) dmma884(d[t][0], d[t][1], fq[t][ks], fx[ks]);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const int mm = 8 * t + lr;
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int cc = 8 * u + 2 * lc + e;
+                if (mm < wnr && cc < ncol) HA(wk0 + mm, clo + 1 + cc) = d[t][e];
+              }
+            }
+          } else {
+            const int i = alo + 8 * (u - ntc) + lr;  // A fragment: H[i, wk0 + 4ks + lc]
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+              const int k = 4 * ks + lc;
+              fx[ks] = (i < ahi && k < wnr) ? HA(i, wk0 + k) : 0.0;
+            }
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+              for (int t = 0; t < 4; ++t) dmma884(d[t][0], d[t][1], fx[ks], fq[t][ks]);
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int nc = 8 * t + 2 * lc + e;
+                if (i < ahi && nc < wnr) HA(i, wk0 + nc) = d[t][e];
+              }
+          }
+        }
+      };
+      auto load_window = [&](int wk0, int wr1, double* qb) {
+        const int wnr = wr1 - wk0 + 1;
         for (int idx = tid; idx < HQ_R * (HQ_R + 1); idx += nt) {
-          const int i = idx % HQ_R, c = idx / HQ_R;  // local row i = k0+i, local col c = k0-1+c
-          const int gj = k0 - 1 + c;
-          Hw[i + c * HQ_LD] = (i < nr && gj >= 0 && gj <= r1) ? HA(k0 + i, gj) : 0.0;
+          const int i = idx % HQ_R, c = idx / HQ_R;  // local row i = wk0+i, local col c = wk0-1+c
+          const int gj = wk0 - 1 + c;
+          Hw[i + c * HQ_LD] = (i < wnr && gj >= 0 && gj <= wr1) ? HA(wk0 + i, gj) : 0.0;
         }
         for (int idx = tid; idx < HQ_R * HQ_R; idx += nt) {
           const int i = idx % HQ_R, c = idx / HQ_R;
-          Qs[i + c * HQ_LD] = (i == c) ? 1.0 : 0.0;
+          qb[i + c * HQ_LD] = (i == c) ? 1.0 : 0.0;
         }
-        __syncthreads();
+      };
+      // Pipeline over the windows of the sweep: while warp 0 chases window w, the other warps apply
+      // the deferred off-window update of window w-1 (its columns beyond window w and its rows
+      // above); the part of w's update that window w+1 reads (its columns) is done before w+1 loads.
+      int k0 = m;
+      int k1 = min(k0 + HQ_W, nn), r1 = min(k0 + HQ_R - 1, nn);
+      int cur = 0, pk0 = -1, pr1 = 0;
+      load_window(k0, r1, Qsh);
+      __syncthreads();
+      while (true) {
+        double* Qs = Qsh + cur * HQ_QSZ;
         long long tc0 = clock64();
         if (warp == 0) {
-          for (int k = k0; k < k1; ++k) {
-            const int kk = k - k0;  // local row of k; local col of k is kk+1
-            double p, q, r;
-            if (k == m) {
-              p = sp;
-              q = sq;
-              r = sr;
-            } else {
-              p = Hw[kk + kk * HQ_LD];
-              q = Hw[kk + 1 + kk * HQ_LD];
-              r = (k != nn - 1) ? Hw[kk + 2 + kk * HQ_LD] : 0.0;
-            }
-            // reflector of (p, q, r): s = sign(p) ||(p,q,r)||, u = (p+s, q, r)/s, w = (1, q, r)/(p+s).
-            // The direction is scale-free, so the NR pre-scaling by |p|+|q|+|r| is only needed
-            // outside the safe exponent range; inside it, s and 1/s come from one rsqrt.
-            const double t = fma(p, p, fma(q, q, r * r));
-            __syncwarp();
-            if (t == 0.0) continue;  // uniform over the warp
-            double s, is;
-            if (t > 1e-280 && t < 1e280) {
-              is = rsqrt_nr(t);
-              s = t * is;
-              if (p < 0.0) {
-                s = -s;
-                is = -is;
-              }
-            } else {
-              const double x = fabs(p) + fabs(q) + fabs(r), ix = 1.0 / x;
-              const double ps = p * ix, qs = q * ix, rs = r * ix;
-              s = copysign(x * sqrt(ps * ps + qs * qs + rs * rs), p);
-              is = 1.0 / s;
-            }
-            if (lane == 0) {
-              if (k == m) {
-                if (l != m) Hw[kk + kk * HQ_LD] = -Hw[kk + kk * HQ_LD];
-              } else {
-                Hw[kk + kk * HQ_LD] = -s;
-              }
-            }
-            p += s;
-            const double ip = rcp_nr(p);
-            const double xx = p * is, yy = q * is, zz = r * is, qq = q * ip, rr = r * ip;
-            const bool three = (k != nn - 1);
-            {  // row transformation, columns k .. r1
-              const int c = kk + 1 + lane;
-              if (c <= nr) {
-                double* col = Hw + c * HQ_LD;
-                double pp = col[kk] + qq * col[kk + 1];
-                if (three) {
-                  pp += rr * col[kk + 2];
-                  col[kk + 2] -= pp * zz;
-                }
-                col[kk + 1] -= pp * yy;
-                col[kk] -= pp * xx;
-              }
-            }
-            __syncwarp();
-            {  // column transformation, rows k0 .. min(nn, k+3), and Q <- Q P_k
-              const int imax = min(nn, k + 3) - k0;
-              if (lane <= imax) {
-                double* c0 = Hw + (kk + 1) * HQ_LD;
-                double pp = xx * c0[lane] + yy * c0[lane + HQ_LD];
-                if (three) {
-                  pp += zz * c0[lane + 2 * HQ_LD];
-                  c0[lane + 2 * HQ_LD] -= pp * rr;
-                }
-                c0[lane + HQ_LD] -= pp * qq;
-                c0[lane] -= pp;
-              }
-              double* q0 = Qs + kk * HQ_LD;
-              double pp = xx * q0[lane] + yy * q0[lane + HQ_LD];
-              if (three) {
-                pp += zz * q0[lane + 2 * HQ_LD];
-                q0[lane + 2 * HQ_LD] -= pp * rr;
-              }
-              q0[lane + HQ_LD] -= pp * qq;
-              q0[lane] -= pp;
-            }
-            __syncwarp();
+          // Register-forwarded chase.  Every lane carries the step's reflector and the bulge state
+          // (B = H[k..k+2][k..k+2], C = H[k..k+2][k+3], h3 = H[k+3][k+2], d33 = H[k+3][k+3]) and
+          // derives step k+1's reflector input H[k+1..k+3][k] (and state) from them in registers,
+          // so the dependent chain per step is reflector -> 3x3 update -> reflector; the shared
+          // memory updates of step k (one phase: the 3x3 block rows come from the registers) and
+          // the Q update run alongside.  Entries beyond the window / active block read as 0.
+          auto H_ = [&](int gi, int gj) -> double {
+            return (gi <= r1 && gj <= r1) ? Hw[(gi - k0) + (gj - k0 + 1) * HQ_LD] : 0.0;
+          };
+          int k = k0;
+          double p0_, q0_, r0_;
+          if (k == m) {
+            p0_ = sp;
+            q0_ = sq;
+            r0_ = sr;
+          } else {
+            p0_ = H_(k, k - 1);
+            q0_ = H_(k + 1, k - 1);
+            r0_ = H_(k + 2, k - 1);
           }
+          double B00 = H_(k, k), B01 = H_(k, k + 1), B02 = H_(k, k + 2);
+          double B10 = H_(k + 1, k), B11 = H_(k + 1, k + 1), B12 = H_(k + 1, k + 2);
+          double B20 = H_(k + 2, k), B21 = H_(k + 2, k + 1), B22 = H_(k + 2, k + 2);
+          double C0 = H_(k, k + 3), C1 = H_(k + 1, k + 3), C2 = H_(k + 2, k + 3);
+          double h3 = H_(k + 3, k + 2), d33 = H_(k + 3, k + 3);
+          HqRefl R = hq_refl_fast(p0_, q0_, r0_);
+          double* dmy = Hw + HQ_LD * (HQ_R + 1);  // scratch for masked stores (4 doubles per lane)
+          for (; k < k1; ++k) {
+            const int kk = k - k0;
+            // ---- loads (values after step k-1).  One basic block per step: the shared-memory
+            //      updates of step k interleave with the register chain of step k+1.  Loaded
+            //      values are stored back (updated) only by the lane that loaded them, except
+            //      E0..E2, read by all lanes before lane 1 (column k+4) stores them (same
+            //      warp-converged instruction stream).
+            const double E0 = H_(k, k + 4), E1 = H_(k + 1, k + 4), E2 = H_(k + 2, k + 4), E3 = H_(k + 3, k + 4);
+            const double h4 = H_(k + 4, k + 3), d44 = H_(k + 4, k + 4);
+            const int jr = k + 3 + lane;  // row transformation: this lane's column
+            const bool rok = jr <= r1;
+            double* colr = rok ? Hw + (jr - k0 + 1) * HQ_LD + kk : dmy + 4 * lane;
+            const double a0 = colr[0], a1 = colr[1], a2 = colr[2];
+            const int ir = k0 + lane;  // column transformation: this lane's row
+            const bool cok = ir <= min(nn, k + 3), above = ir < k;
+            double* rowc = (cok && above) ? Hw + lane + (kk + 1) * HQ_LD : dmy + 4 * lane;
+            const double b0 = rowc[0], b1 = rowc[above && cok ? HQ_LD : 1], b2 = rowc[above && cok ? 2 * HQ_LD : 2];
+            double* qc = Qs + lane + kk * HQ_LD;
+            const double g0 = qc[0], g1 = qc[HQ_LD], g2 = qc[2 * HQ_LD];
+            double* hk = (lane == 0 && R.valid) ? Hw + kk + kk * HQ_LD : dmy + 4 * lane + 3;  // H(k, k-1)
+            const double hkv = *hk;
+            const double u0 = R.xx, u1 = R.yy, u2 = R.zz, w1 = R.qq, w2 = R.rr;
+            // ---- forward: H' = (I - u w^T) H on rows k..k+2, then the column update of rows k+1..k+3
+            const double pp0 = fma(w2, B20, fma(w1, B10, B00)), pp1 = fma(w2, B21, fma(w1, B11, B01)),
+                         pp2 = fma(w2, B22, fma(w1, B12, B02)), ppc = fma(w2, C2, fma(w1, C1, C0)),
+                         ppe = fma(w2, E2, fma(w1, E1, E0));
+            const double R10 = fma(-u1, pp0, B10), R11 = fma(-u1, pp1, B11), R12 = fma(-u1, pp2, B12),
+                         R1c = fma(-u1, ppc, C1), R1e = fma(-u1, ppe, E1);
+            const double R20 = fma(-u2, pp0, B20), R21 = fma(-u2, pp1, B21), R22 = fma(-u2, pp2, B22),
+                         R2c = fma(-u2, ppc, C2), R2e = fma(-u2, ppe, E2);
+            const double t1 = fma(u2, R12, fma(u1, R11, u0 * R10));
+            const double t2 = fma(u2, R22, fma(u1, R21, u0 * R20));
+            const double t3 = u2 * h3;
+            const double N10 = R10 - t1, N11 = fma(-t1, w1, R11), N12 = fma(-t1, w2, R12);
+            const double N20 = R20 - t2, N21 = fma(-t2, w1, R21), N22 = fma(-t2, w2, R22);
+            const double N30 = -t3, N31 = -t3 * w1, N32 = fma(-t3, w2, h3);
+            const HqRefl Rn = hq_refl_fast(N10, N20, N30);
+            // ---- shared-memory updates of step k (masked lanes write to their scratch slots)
+            *hk = (k == m) ? ((l != m) ? -hkv : hkv) : -R.s;
+            {
+              const double pr = fma(w2, a2, fma(w1, a1, a0));
+              colr[0] = fma(-u0, pr, a0);
+              colr[1] = fma(-u1, pr, a1);
+              *((k + 2 <= nn) ? colr + 2 : dmy + 4 * lane + 2) = fma(-u2, pr, a2);
+            }
+            {
+              const int d = ir - k;
+              const double X0 = fma(-u0, pp0, B00), X1 = fma(-u0, pp1, B01), X2 = fma(-u0, pp2, B02);
+              const double v0 = above ? b0 : (d == 0 ? X0 : (d == 1 ? R10 : (d == 2 ? R20 : 0.0)));
+              const double v1 = above ? b1 : (d == 0 ? X1 : (d == 1 ? R11 : (d == 2 ? R21 : 0.0)));
+              const double v2 = above ? b2 : (d == 0 ? X2 : (d == 1 ? R12 : (d == 2 ? R22 : h3)));
+              const double tt = fma(u2, v2, fma(u1, v1, u0 * v0));
+              double* rw = Hw + lane + (kk + 1) * HQ_LD;
+              double* sc = dmy + 4 * lane;
+              *(cok ? rw : sc) = v0 - tt;
+              *(cok ? rw + HQ_LD : sc + 1) = fma(-tt, w1, v1);
+              *((cok && k + 2 <= nn) ? rw + 2 * HQ_LD : sc + 2) = fma(-tt, w2, v2);
+            }
+            {
+              const double tq = fma(u2, g2, fma(u1, g1, u0 * g0));
+              qc[0] = g0 - tq;
+              qc[HQ_LD] = fma(-tq, w1, g1);
+              qc[2 * HQ_LD] = fma(-tq, w2, g2);
+            }
+            __syncwarp();
+            R = Rn;
+            B00 = N11;
+            B01 = N12;
+            B02 = R1c;
+            B10 = N21;
+            B11 = N22;
+            B12 = R2c;
+            B20 = N31;
+            B21 = N32;
+            B22 = d33;
+            C0 = R1e;
+            C1 = R2e;
+            C2 = E3;
+            h3 = h4;
+            d33 = d44;
+          }
+        }
+        else if (pk0 >= 0) {
+          far_update(Qsh + (cur ^ 1) * HQ_QSZ, pk0, pr1, r1, nn, l, pk0, -1, nw - (nw >> 2));
         }
         __syncthreads();
         long long tc1 = clock64();
         if (tid == 0) cyc_chase += tc1 - tc0;
-        // write the window back; far-right and far-above block updates (disjoint regions)
-        for (int idx = tid; idx < HQ_R * (HQ_R + 1); idx += nt) {
+        for (int idx = tid; idx < HQ_R * (HQ_R + 1); idx += nt) {  // write the window back
           const int i = idx % HQ_R, c = idx / HQ_R;
           const int gj = k0 - 1 + c;
-          if (i < nr && gj >= 0 && gj <= r1) HA(k0 + i, gj) = Hw[i + c * HQ_LD];
+          if (i <= r1 - k0 && gj >= 0 && gj <= r1) HA(k0 + i, gj) = Hw[i + c * HQ_LD];
         }
-        // far updates on the FP64 tensor cores (mma.m8n8k4.f64), one warp per 8-vector tile with
-        // the 32x32 Q held as 32 fragments per thread (frag[t][ks] = Q[4ks + lane%4, 8t + lane/4],
-        // which is the A fragment of Q^T and the B fragment of Q):
-        //   far right, 8 columns:  H[R, (r1, nn]]  <- Q^T H[R, (r1, nn]]
-        //   far above, 8 rows:     H[[l, k0), R]   <- H[[l, k0), R] Q
-        {
-          const int lr = lane >> 2, lc = lane & 3;
-          double fq[4][8];
-#pragma unroll
-          for (int t = 0; t < 4; ++t)
-#pragma unroll
-            for (int ks = 0; ks < 8; ++ks) fq[t][ks] = Qs[4 * ks + lc + (8 * t + lr) * HQ_LD];
-          const int ncol = nn - r1, nrow = k0 - l;
-          const int ntc = (ncol + 7) >> 3, ntr = (nrow + 7) >> 3;
-          for (int u = warp; u < ntc + ntr; u += nw) {
-            double fx[8], d[4][2];
-#pragma unroll
-            for (int t = 0; t < 4; ++t) d[t][0] = d[t][1] = 0.0;
-            if (u < ntc) {
-              const int c = 8 * u + lr;  // B fragment: H[k0 + 4ks + lc, r1 + 1 + c]
-#pragma unroll
-              for (int ks = 0; ks < 8; ++ks) {
-                const int k = 4 * ks + lc;
-                fx[ks] = (c < ncol && k < nr) ? HA(k0 + k, r1 + 1 + c) : 0.0;
-              }
-#pragma unroll
-              for (int ks = 0; ks < 8; ++ks)
-#pragma unroll
-                for (int t = 0; t < 4; ++t) dmma884(d[t][0], d[t][1], fq[t][ks], fx[ks]);
-#pragma unroll
-              for (int t = 0; t < 4; ++t) {
-                const int m = 8 * t + lr;
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                  const int cc = 8 * u + 2 * lc + e;
-                  if (m < nr && cc < ncol) HA(k0 + m, r1 + 1 + cc) = d[t][e];
-                }
-              }
-            } else {
-              const int i = l + 8 * (u - ntc) + lr;  // A fragment: H[i, k0 + 4ks + lc]
-#pragma unroll
-              for (int ks = 0; ks < 8; ++ks) {
-                const int k = 4 * ks + lc;
-                fx[ks] = (i < k0 && k < nr) ? HA(i, k0 + k) : 0.0;
-              }
-#pragma unroll
-              for (int ks = 0; ks < 8; ++ks)
-#pragma unroll
-                for (int t = 0; t < 4; ++t) dmma884(d[t][0], d[t][1], fx[ks], fq[t][ks]);
-              const int io = l + 8 * (u - ntc) + lr;
-#pragma unroll
-              for (int t = 0; t < 4; ++t)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                  const int nc = 8 * t + 2 * lc + e;
-                  if (io < k0 && nc < nr) HA(io, k0 + nc) = d[t][e];
-                }
-            }
-          }
+        const int k0n = k1;
+        if (k0n > nn - 1) {  // last window: its whole off-window update now
+          far_update(Qs, k0, r1, r1, nn, l, k0, 0, nw);
+          __syncthreads();
+          break;
         }
+        const int r1n = min(k0n + HQ_R - 1, nn);
+        far_update(Qs, k0, r1, r1, r1n, 0, 0, 0, nw);  // the next window's columns
+        __syncthreads();
+        pk0 = k0;
+        pr1 = r1;
+        cur ^= 1;
+        k0 = k0n;
+        k1 = min(k0 + HQ_W, nn);
+        r1 = r1n;
+        load_window(k0, r1, Qsh + cur * HQ_QSZ);
         __syncthreads();
       }
       {
@@ -423,6 +555,12 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
       }
     }
     if (sdone) break;
+  }
+  __syncthreads();
+  const double ihsc = 1.0 / hsc;  // power of two: exact
+  for (int i = tid; i < n; i += nt) {
+    wr[i] *= ihsc;
+    wi[i] *= ihsc;
   }
   if (tid == 0) {
     info[1] = nsweep;  // diagnostics: Francis sweeps, bulge steps
