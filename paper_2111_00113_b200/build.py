@@ -20,6 +20,8 @@ OBJ = os.path.join(HERE, "_build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-warn-spills"]
+# experiments only (e.g. SKS_NVCC_EXTRA="-DZM_ZS_FORCE=2"); part of the build digest
+FLAGS += [f for f in os.environ.get("SKS_NVCC_EXTRA", "").split() if f]
 
 
 def nccl_dir():
