@@ -266,7 +266,9 @@ def main():
                          "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy burst)", "traffic": traffic,
                          "bytes_per_launch_alg": b_step / max(n_step, 1),
                          "avg_launch_us": t_step / max(n_step, 1) * 1e6, "launches_timed": int(n_step),
-                         "share_of_solve": t_step / max(len(infos), 1) / t_dev if t_dev > 0 else None},
+                         # sampled launches (every 16th) -> mean duration x step launches per solve
+                         "share_of_solve": (t_step / max(n_step, 1)) * steps_per_solve / t_dev
+                         if t_dev > 0 else None},
             "cpu_baseline": cpu,
             "e2e": {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": int(16 * (re_ - rb)),
                     "d2h_bytes_per_step": int(8 * (re_ - rb))},
