@@ -230,6 +230,12 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 __host__ __device__ __forceinline__ uint32_t s4_g(uint32_t r) { return r & 31u; }
+// bulk L2 prefetch of the 16-byte-aligned part of [p, p + bytes) (never outside the range)
+__device__ __forceinline__ void l2_prefetch_bulk(const void* p, uint32_t bytes) {
+  const uint64_t a = (reinterpret_cast<uint64_t>(p) + 15ull) & ~15ull;
+  const uint64_t e = (reinterpret_cast<uint64_t>(p) + bytes) & ~15ull;
+  if (e > a) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(e - a)) : "memory");
+}
 __host__ __device__ __forceinline__ int s4_nqp(int s) { return (s + 7) & ~7; }
 // plan strides: entries (u32) and bucket starts (u16) per tile, both 16-byte multiples
 __host__ __device__ __forceinline__ int s5_ent_stride(int s, int zeta) { return (S4_R * zeta + s + 4 + 3) & ~3; }
@@ -425,6 +431,14 @@ __global__ void __launch_bounds__(S4_THREADS, 1) sketch_v5_kernel(SketchArgs a, 
     }
     cp_async_wait_all();
     __syncthreads();
+    // ---- pull the next tile (its J column segments and its plan) into L2 while this one is
+    //      gathered, so that the next staging is served from L2 instead of HBM
+    if (wid == 0 && tile + 1 < t_hi) {
+      const int64_t rn = r0 + S4_R;
+      const int nrn = (int)((a.nrows - rn) < (int64_t)S4_R ? (a.nrows - rn) : (int64_t)S4_R);
+      if (lane < a.J) l2_prefetch_bulk(a.M + (int64_t)lane * a.ldm + rn, (uint32_t)(nrn * 8));
+      if (lane == 31) l2_prefetch_bulk(pent + (tile + 1) * (int64_t)ES, (uint32_t)(ES * 4));
+    }
     // ---- gather: warp-owned buckets, lane = column, two entries per iteration; the bucket
     //      boundaries of the warp come from one load + shuffles
     {
