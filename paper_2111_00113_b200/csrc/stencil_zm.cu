@@ -30,14 +30,23 @@
 
 namespace sks {
 
-constexpr int ZX = 32, ZY = 16;                  // output tile
+#ifndef ZM_TX
+#define ZM_TX 32
+#endif
+#ifndef ZM_TY
+#define ZM_TY 16
+#endif
+#ifndef ZM_CPS
+#define ZM_CPS 1  // resident CTAs per SM
+#endif
+constexpr int ZX = ZM_TX, ZY = ZM_TY;            // output tile
 constexpr int ZWX = ZX + 2, ZWY = ZY + 2;        // W box 34 x 18 (one thread per column)
 constexpr int ZUX = ZX + 4, ZUY = ZY + 4;        // U plane box 36 x 20
 constexpr int ZVX = ZX + 4, ZVY = ZY + 2;        // V plane box 36 x 18 (origin x0-2: 16-byte aligned)
 constexpr int ZUP = ZUX * ZUY;                   // 720 doubles per U plane
 constexpr int ZVP = ZVX * ZVY;                   // 648 doubles per V plane
 constexpr int ZW = ZWX * ZWY;                    // 612
-constexpr int ZT = 640;                          // threads (20 warps; 28 idle in the compute)
+constexpr int ZT = (ZWX * ZWY + 31) / 32 * 32;  // threads: one per W-box column (32 x 16: 640, 20 warps)
 
 struct ZmArgs {
   int ucol;
@@ -61,7 +70,7 @@ __host__ __device__ constexpr size_t zm_smem_bytes() {
 }
 
 template <int KM, int ZS, bool FULL, bool USL>
-__global__ void __launch_bounds__(ZT, 1)
+__global__ void __launch_bounds__(ZT, ZM_CPS)
     step3d_zm_kernel(StepArgs a, ZmArgs z, const __grid_constant__ CUtensorMap tmU,
                      const __grid_constant__ CUtensorMap tmV) {
   extern __shared__ __align__(128) unsigned char smraw_z[];
@@ -281,7 +290,8 @@ struct ZmMaps {
 
 template <int KM>
 constexpr int zm_zs() {
-  return zm_smem_bytes<KM, 4>() <= 200 * 1024 ? 4 : (zm_smem_bytes<KM, 2>() <= 200 * 1024 ? 2 : 1);
+  constexpr size_t cap = (ZM_CPS > 1 ? 226 * 1024 / ZM_CPS - 1024 : 200 * 1024);
+  return zm_smem_bytes<KM, 4>() <= cap ? 4 : (zm_smem_bytes<KM, 2>() <= cap ? 2 : 1);
 }
 
 bool stencil_zm_supported(int dim, int64_t m, int k) {
@@ -296,7 +306,7 @@ void stencil_zm_tiling(int64_t m, int64_t nz, int num_sms, StepArgs* a, int* gri
   a->tiles_y = (int)((m + ZY - 1) / ZY);
   a->zchunk = 0;
   a->ntiles = (int64_t)a->tiles_x * a->tiles_y * nz;  // (tile, plane) units
-  *grid = (int)std::max<int64_t>(1, std::min<int64_t>(a->ntiles, num_sms));
+  *grid = (int)std::max<int64_t>(1, std::min<int64_t>(a->ntiles, (int64_t)num_sms * ZM_CPS));
 }
 
 template <int KM, bool FULL, bool USL>
