@@ -46,7 +46,15 @@ constexpr int ZVX = ZX + 4, ZVY = ZY + 2;        // V plane box 36 x 18 (origin 
 constexpr int ZUP = ZUX * ZUY;                   // 720 doubles per U plane
 constexpr int ZVP = ZVX * ZVY;                   // 648 doubles per V plane
 constexpr int ZW = ZWX * ZWY;                    // 612
-constexpr int ZT = (ZWX * ZWY + 31) / 32 * 32;  // threads: one per W-box column (32 x 16: 640, 20 warps)
+#ifndef ZM_PITCH
+#define ZM_PITCH 0
+#endif
+// ZM_PITCH=1: thread rows and w_j ring rows use the U-plane pitch (36), so every warp touches one
+// contiguous run of shared memory per load (no row-break bank conflicts; 2 idle threads per row).
+// Measured 38.8 us vs 38.1 us at C3 (the conflicts are not the bound), so off by default.
+constexpr int ZRX = ZM_PITCH ? ZUX : ZWX;        // thread-row width = ring row pitch
+constexpr int ZR = ZRX * ZWY;                    // ring plane (648 doubles)
+constexpr int ZT = (ZRX * ZWY + 31) / 32 * 32;  // threads (32 x 16 tile: 672 = 21 warps)
 
 struct ZmArgs {
   int ucol;
@@ -66,7 +74,7 @@ template <int KM, int ZS>
 __host__ __device__ constexpr int zm_stage() { return zm_ublk<KM, ZS>() + (KM - 1) * zm_vblk<KM, ZS>(); }
 template <int KM, int ZS>
 __host__ __device__ constexpr size_t zm_smem_bytes() {
-  return 128 + sizeof(double) * ((size_t)2 * zm_stage<KM, ZS>() + (size_t)(3 * ZS) * ZW);
+  return 128 + sizeof(double) * ((size_t)2 * zm_stage<KM, ZS>() + (size_t)(3 * ZS) * ZR);
 }
 
 template <int KM, int ZS, bool FULL, bool USL>
@@ -103,12 +111,14 @@ __global__ void __launch_bounds__(ZT, ZM_CPS)
   double* Wout = a.W + (a.mode == 0 ? (int64_t)a.j * a.ld : 0) + a.off;
 
   // this thread's W-box column
-  const bool wt = tid < ZW;  // threads past the W box shadow its last column (no stores)
-  const int tcol = wt ? tid : ZW - 1;
-  const int bx = tcol % ZWX, by = tcol / ZWX;
+  // threads past the last thread row shadow the last W column (no stores); threads in the pitch
+  // padding of a row (bx >= ZWX) compute in-bounds garbage and store nothing
+  const int tcol = tid < ZR ? tid : ZR - ZRX + ZWX - 1;
+  const int bx = tcol % ZRX, by = tcol / ZRX;
+  const bool wt = tid < ZR && bx < ZWX;
   const int cu = (by + 1) * ZUX + (bx + 1);  // U-plane offset of the column
   const int cvv = by * ZVX + (bx + 1);       // V-plane offset
-  const int cwb = by * ZWX + bx;             // W-plane offset
+  const int cwb = by * ZRX + bx;             // ring-plane offset
   const bool inner = wt && bx >= 1 && bx <= ZX && by >= 1 && by <= ZY;
 
   double acc[KM + 3];
@@ -170,8 +180,8 @@ __global__ void __launch_bounds__(ZT, ZM_CPS)
       const int p0 = wa + t * ZS;
       const bool fast = t >= T0 && p0 + ZS - 1 <= zb && z0g + p0 + ZS - 1 < m;
       double w[ZS], c[ZS + 2], v[KM - 1][ZS];
-      double* rw = ring + SBW * ZW + cwb;        // plane p0 (+ i ZW for p0 + i)
-      const double* rp = ring + SBP * ZW + cwb;  // plane p0-1
+      double* rw = ring + SBW * ZR + cwb;        // plane p0 (+ i ZR for p0 + i)
+      const double* rp = ring + SBP * ZR + cwb;  // plane p0-1
       // ---- w_j on planes p0 .. p0+ZS-1 (this thread's column)
 #pragma unroll
       for (int k = 0; k < ZS + 2; ++k) c[k] = sU[k * ZUP + cu];
@@ -187,7 +197,7 @@ __global__ void __launch_bounds__(ZT, ZM_CPS)
           for (int l = 0; l < KM - 1; ++l)
             if (FULL || l < nv) wv += clm[l] * v[l][i];
           w[i] = wv;
-          if (wt) rw[i * ZW] = wv;
+          if (wt) rw[i * ZR] = wv;
         }
       } else {
 #pragma unroll
@@ -203,7 +213,7 @@ __global__ void __launch_bounds__(ZT, ZM_CPS)
             if (FULL || l < nv) wv += cl[l] * v[l][i];
           wv = (xyin && (unsigned)(z0g + p) < (unsigned)m && p <= zb) ? wv : 0.0;
           w[i] = wv;
-          if (wt) rw[i * ZW] = wv;
+          if (wt) rw[i * ZR] = wv;
         }
       }
       __syncthreads();
@@ -217,8 +227,8 @@ __global__ void __launch_bounds__(ZT, ZM_CPS)
           if (fast || (qp >= za && qp < zb)) {
             const double wq = (i == 0) ? wp1 : w[i - 1];
             const double wqm = (i == 0) ? wp2 : (i == 1 ? wp1 : w[i - 2]);
-            const double* r = (i == 0) ? rp : rw + (i - 1) * ZW;
-            const double Aw = cc * wq + cm * (r[-1] + r[-ZWX] + wqm) + cp * (r[1] + r[ZWX] + w[i]);
+            const double* r = (i == 0) ? rp : rw + (i - 1) * ZR;
+            const double Aw = cc * wq + cm * (r[-1] + r[-ZRX] + wqm) + cp * (r[1] + r[ZRX] + w[i]);
             *wo = wq;
             acc[0] += wq * wq;
             acc[1] += wq * Aw;
