@@ -1,0 +1,161 @@
+"""GPU edge cases through the C-ABI (-m gpu), each against the oracle or a closed form:
+
+  * argument errors come back as SKS_EINVAL (sks.h): sizes outside the header's
+    ranges, a non-finite right-hand side, bad nev;
+  * the degenerate inputs of the method: a zero right-hand side (x = 0 exactly), a lucky breakdown
+    on an exact eigenvector of A (reading O10: the basis stops, x = f / lambda), an sRR start vector
+    that spans an invariant subspace (fewer than 2 columns: SKS_EINVAL), a single basis column
+    (d = 1), full orthogonalisation k >= d (orthonormal basis, Eq. partorth with the whole window);
+  * the smallest stencil (m = 2) and the largest window (k = 8).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from inputs import rhs_normal, start_vector
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import paper_2111_00113_b200 as P
+    from paper_2111_00113_b200 import build
+    build.build()
+    c = P.Context(0)
+    yield c
+    c.close()
+
+
+def _P():
+    import paper_2111_00113_b200 as P
+    return P
+
+
+def _eigvec_2d(m, beta, p=1):
+    """Closed-form eigenvector of the 2D operator (Kronecker sum of the 1D factor T = tridiag(b, a, c),
+    b, c < 0): u_i = (b/c)^(i/2) sin(i p pi/(m+1)), T u = (a - 2 sqrt(bc) cos(p pi/(m+1))) u;
+    A (u x u) = 2 lambda (u x u)."""
+    a, b, c = O.stencil_coeffs(m, beta)
+    i = np.arange(1, m + 1)
+    u = (b / c) ** (i / 2.0) * np.sin(i * p * np.pi / (m + 1))
+    lam = a - 2.0 * np.sqrt(b * c) * np.cos(p * np.pi / (m + 1))
+    f = np.outer(u, u).ravel()
+    return f / np.linalg.norm(f), 2.0 * lam
+
+
+BAD_SGMRES = [dict(d=0), dict(s=20), dict(s=4096), dict(zeta=0), dict(zeta=17), dict(k=0), dict(k=9),
+              dict(tol=-1.0), dict(max_cycles=0)]
+
+
+@pytest.mark.parametrize("bad", BAD_SGMRES)
+def test_sgmres_rejects_bad_arguments(ctx, bad):
+    P = _P()
+    kw = dict(d=20, k=2, s=40, zeta=8, seed=0, tol=1e-8, max_cycles=2)
+    kw.update(bad)
+    with pytest.raises(P.SksError) as e:
+        ctx.sgmres_solve(P.StencilOperator(2, 16, 5.0), rhs_normal(256, 0), **kw)
+    assert e.value.status == -1 and "SKS_EINVAL" in str(e.value)
+
+
+def test_sgmres_rejects_non_finite_rhs(ctx):
+    P = _P()
+    f = rhs_normal(256, 0)
+    f[17] = np.nan
+    with pytest.raises(P.SksError) as e:
+        ctx.sgmres_solve(P.StencilOperator(2, 16, 5.0), f, d=20, k=2, s=40)
+    assert e.value.status == -1
+
+
+@pytest.mark.parametrize("nev,d", [(0, 20), (12, 40), (5, 1)])
+def test_srr_rejects_bad_arguments(ctx, nev, d):
+    P = _P()
+    with pytest.raises(P.SksError) as e:
+        ctx.srr_eigs(P.StencilOperator(2, 16, 5.0), start_vector(256, 4), d=d, k=2, s=2 * d + 2, nev=nev)
+    assert e.value.status == -1
+
+
+def test_stencil_rejects_m_below_2(ctx):
+    P = _P()
+    with pytest.raises(P.SksError):
+        ctx.sgmres_solve(P.StencilOperator(2, 1, 5.0), np.ones(1), d=1, k=1, s=2)
+
+
+def test_sgmres_zero_rhs_gives_zero(ctx):
+    P = _P()
+    res = ctx.sgmres_solve(P.StencilOperator(2, 16, 5.0), np.zeros(256), d=20, k=2, s=40, max_cycles=3)
+    assert res.converged and np.all(res.x == 0.0)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_sgmres_lucky_breakdown_on_eigenvector(ctx, dim):
+    P = _P()
+    m, beta = 8, 2.0  # small m: the rounding-level w_1 stays far below the 1e-14 breakdown threshold
+    f2, lam2 = _eigvec_2d(m, beta)
+    if dim == 2:
+        f, lam = f2, lam2
+    else:  # u x u x u, eigenvalue 3 lambda_1
+        a, b, c = O.stencil_coeffs(m, beta)
+        i = np.arange(1, m + 1)
+        u = (b / c) ** (i / 2.0) * np.sin(i * np.pi / (m + 1))
+        f = np.einsum("i,j,k->ijk", u, u, u).ravel()
+        f /= np.linalg.norm(f)
+        lam = 3.0 * (a - 2.0 * np.sqrt(b * c) * np.cos(np.pi / (m + 1)))
+    Ao = O.stencil_matrix(dim, m, beta)
+    assert np.linalg.norm(Ao @ f - lam * f) <= 1e-13 * lam           # the closed form is an eigenpair
+    res = ctx.sgmres_solve(P.StencilOperator(dim, m, beta), f, d=10, k=2, s=20, seed=1, tol=1e-8, max_cycles=2)
+    orc = O.sgmres_solve(lambda v: Ao @ v, f, 10, 2, 20, 8, 1, tol=1e-8, max_cycles=2)
+    assert res.info["flags"] & _P()._lib.SKS_WARN_BREAKDOWN and orc["flags"] & 2
+    assert res.converged and res.info["columns"] == orc["columns"] == 1
+    np.testing.assert_allclose(res.x, f / lam, rtol=0, atol=1e-12 * np.abs(f / lam).max())
+    np.testing.assert_allclose(res.x, orc["x"], rtol=0, atol=1e-12 * np.abs(orc["x"]).max())
+
+
+def test_srr_invariant_start_vector_is_rejected(ctx):
+    P = _P()
+    f, _ = _eigvec_2d(8, 2.0)
+    with pytest.raises(P.SksError) as e:
+        ctx.srr_eigs(P.StencilOperator(2, 8, 2.0), f, d=20, k=2, s=40, nev=4)
+    assert e.value.status == -1
+
+
+def test_sgmres_single_column(ctx):
+    P = _P()
+    m, beta = 16, 5.0
+    f = rhs_normal(m * m, 3)
+    Ao = O.stencil_matrix(2, m, beta)
+    res = ctx.sgmres_solve(P.StencilOperator(2, m, beta), f, d=1, k=1, s=4, zeta=4, seed=3, tol=1e-8,
+                           max_cycles=4)
+    orc = O.sgmres_solve(lambda v: Ao @ v, f, 1, 1, 4, 4, 3, tol=1e-8, max_cycles=4)
+    assert res.info["cycles"] == orc["cycles"] == 4
+    np.testing.assert_allclose(res.hist_true, orc["hist_true"], rtol=1e-10)
+    np.testing.assert_allclose(res.x, orc["x"], rtol=0, atol=1e-10 * np.abs(orc["x"]).max())
+
+
+@pytest.mark.parametrize("dim,m", [(2, 20), (3, 10)])
+def test_full_orthogonalisation_k_ge_d(ctx, dim, m):
+    """k = 8 >= d = 8: the truncated recurrence is full Arnoldi, so the basis is orthonormal
+    (oracle pin: ||B^T B - I|| < 1e-12) and equals the oracle's column by column."""
+    P = _P()
+    r0 = rhs_normal(m ** dim, 5)
+    Ao = O.stencil_matrix(dim, m, 3.0)
+    B, H = ctx.basis(P.StencilOperator(dim, m, 3.0), r0, k=8, ncols=8)
+    assert np.abs(B.T @ B - np.eye(8)).max() <= 1e-12
+    ref = O.partial_arnoldi(lambda v: Ao @ v, r0, 8, 8)
+    assert np.abs(B - ref["B"]).max() <= 1e-10 * np.abs(ref["B"]).max()
+
+
+def test_smallest_stencil_m2(ctx):
+    """m = 2 (n = 4 in 2D, 8 in 3D): every point touches the Dirichlet boundary; d = n-1 columns."""
+    P = _P()
+    for dim in (2, 3):
+        n = 2 ** dim
+        f = rhs_normal(n, 7)
+        Ao = O.stencil_matrix(dim, 2, 1.0)
+        res = ctx.sgmres_solve(P.StencilOperator(dim, 2, 1.0), f, d=n - 1, k=2, s=2 * n, seed=7, tol=1e-12,
+                               max_cycles=6)
+        orc = O.sgmres_solve(lambda v: Ao @ v, f, n - 1, 2, 2 * n, 8, 7, tol=1e-12, max_cycles=6)
+        x_exact = np.linalg.solve(Ao.toarray(), f)
+        assert res.info["cycles"] == orc["cycles"]
+        np.testing.assert_allclose(res.x, orc["x"], rtol=0, atol=1e-9 * np.abs(x_exact).max())
+        assert np.linalg.norm(res.x - x_exact) <= 1e-9 * np.linalg.norm(x_exact)
