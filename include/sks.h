@@ -51,7 +51,8 @@ typedef enum {
 enum {
   SKS_WARN_COND = 1,       /* kappa_2(T) > cond_tol (Alg. 1, Alg. 2) */
   SKS_WARN_BREAKDOWN = 2,  /* ||w_j|| <= 1e-14 ||m_{j-1}||: basis stopped early (reading O10) */
-  SKS_WARN_STAGNATION = 4  /* reserved */
+  SKS_WARN_STAGNATION = 4, /* reserved */
+  SKS_INFO_ADAPTIVE_RESTART = 8 /* SKS_OPT_ADAPTIVE_RESTART ended at least one cycle early */
 };
 
 typedef struct sks_ctx sks_ctx;
@@ -138,8 +139,13 @@ enum {
 };
 
 enum {
-  SKS_OPT_TIME_STEPS = 1  /* bracket every basis-step launch with CUDA events on the main stream and
-                             report the summed kernel time in info->t_step_s (measurement only) */
+  SKS_OPT_TIME_STEPS = 1,       /* bracket every basis-step launch with CUDA events on the main stream and
+                                   report the summed kernel time in info->t_step_s (measurement only) */
+  SKS_OPT_ADAPTIVE_RESTART = 2  /* adaptive restarting (Sec. "Adaptive restarting"): when
+                                   first kappa_2(T_j) > cond_tol, the cycle ends with the previous
+                                   solution (j-1 columns) and restarts from its residual (reading O31:
+                                   kappa_2 estimated by power iteration on the device, checked after
+                                   every sketched-QR batch, the first j located by bisection) */
 };
 
 typedef struct {

@@ -22,6 +22,7 @@ from .sketch import sketch_matrix
 
 WARN_COND = 1
 WARN_BREAKDOWN = 2
+INFO_ADAPTIVE = 8   # adaptive restarting ended a cycle early
 
 
 def thin_qr(C):
@@ -48,9 +49,13 @@ def gmres_exact_ls(M, r0):
 
 
 def sgmres_cycle(matvec, f, x, d, k, s, zeta, seed, cycle, tol=1e-8,
-                 early_exit_factor=0.25, cond_tol=1e14, fnorm=None, S=None, cheb=None):
+                 early_exit_factor=0.25, cond_tol=1e14, fnorm=None, S=None, cheb=None, adaptive=False):
     """One cycle; cheb = (c, dx, dy) selects the Chebyshev basis of Eq. Chebrecurse
-     instead of k-truncated Arnoldi."""
+     instead of k-truncated Arnoldi.
+    adaptive: adaptive restarting (Sec. adaptive-restart): "When first
+    kappa_2(T_j) > tol, we recognize that it is time to restart.  We generate the new Krylov
+    subspace using the previous residual r_{j-1} = r_0 - AB_{j-1} y_{j-1}" -- the cycle keeps
+    the solution of j-1 columns (at least one column is always used)."""
     f = np.asarray(f, dtype=np.float64)
     n = f.size
     if fnorm is None:
@@ -73,16 +78,26 @@ def sgmres_cycle(matvec, f, x, d, k, s, zeta, seed, cycle, tol=1e-8,
     thr = early_exit_factor * tol * fnorm
     hits = np.nonzero(r_est <= thr)[0] if early_exit_factor > 0 else np.zeros(0, int)
     jstar = int(hits[0]) + 1 if hits.size else de
+    adapted = False
+    if adaptive:
+        conds = np.array([np.linalg.cond(T[:j, :j]) for j in range(1, de + 1)])   # exact 2-norm
+        over = np.nonzero(conds > cond_tol)[0]
+        if over.size:
+            jfirst = int(over[0]) + 1
+            if max(jfirst - 1, 1) < jstar:
+                jstar = max(jfirst - 1, 1)
+                adapted = True
     yhat = solve_triangular(T[:jstar, :jstar], c[:jstar], lower=False)
     x_new = x + B[:, :jstar] @ yhat
     condT = np.linalg.cond(T[:jstar, :jstar])
-    flags = (WARN_COND if condT > cond_tol else 0) | (WARN_BREAKDOWN if basis["breakdown"] else 0)
+    flags = (WARN_COND if condT > cond_tol else 0) | (WARN_BREAKDOWN if basis["breakdown"] else 0) | \
+        (INFO_ADAPTIVE if adapted else 0)
     return dict(x=x_new, j=jstar, r_est=r_est[:jstar], yhat=yhat, cond_T=condT,
                 flags=flags, basis=basis, C=C, g=g, U=U, T=T)
 
 
 def sgmres_solve(matvec, f, d, k, s, zeta, seed, tol=1e-8, max_cycles=50,
-                 early_exit_factor=0.25, cond_tol=1e14, x0=None, keep_last=False, cheb=None):
+                 early_exit_factor=0.25, cond_tol=1e14, x0=None, keep_last=False, cheb=None, adaptive=False):
     """Restarted sGMRES.  Returns dict(x, cycles, columns, rel_res_true, r_est,
     hist_est (r_est_j/||f|| per column, concatenated), hist_true (per cycle),
     cond_T, flags)."""
@@ -95,7 +110,7 @@ def sgmres_solve(matvec, f, d, k, s, zeta, seed, tol=1e-8, max_cycles=50,
     cycles = 0
     for c in range(max_cycles):
         out = sgmres_cycle(matvec, f, x, d, k, s, zeta, seed, c, tol,
-                           early_exit_factor, cond_tol, fnorm, cheb=cheb)
+                           early_exit_factor, cond_tol, fnorm, cheb=cheb, adaptive=adaptive)
         cycles += 1
         x = out["x"]
         columns += out["j"]

@@ -10,7 +10,7 @@ LIBPATH = os.path.join(HERE, "libsks.so")
 SKS_OK, SKS_EINVAL, SKS_ECUDA, SKS_ENCCL, SKS_ENOMEM, SKS_ENOTCONV, SKS_EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
 STATUS_NAMES = {0: "SKS_OK", -1: "SKS_EINVAL", -2: "SKS_ECUDA", -3: "SKS_ENCCL", -4: "SKS_ENOMEM",
                 -5: "SKS_ENOTCONV", -6: "SKS_EUNSUPPORTED"}
-SKS_WARN_COND, SKS_WARN_BREAKDOWN, SKS_WARN_STAGNATION = 1, 2, 4
+SKS_WARN_COND, SKS_WARN_BREAKDOWN, SKS_WARN_STAGNATION, SKS_INFO_ADAPTIVE_RESTART = 1, 2, 4, 8
 SKS_OP_STENCIL2D, SKS_OP_STENCIL3D, SKS_OP_CSR = 1, 2, 3
 
 # every symbol include/sks.h declares (checked by tests/test_abi.py)
@@ -43,6 +43,7 @@ class SgmresInfo(C.Structure):
 
 
 SKS_OPT_TIME_STEPS = 1
+SKS_OPT_ADAPTIVE_RESTART = 2
 SKS_BASIS_ARNOLDI, SKS_BASIS_CHEBYSHEV = 0, 1
 BASES = {"arnoldi": SKS_BASIS_ARNOLDI, "chebyshev": SKS_BASIS_CHEBYSHEV}
 

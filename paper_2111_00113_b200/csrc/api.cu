@@ -21,6 +21,9 @@
 #include <vector>
 
 #include "../../include/sks.h"
+
+// power-iteration steps of the kappa_2(T_j) estimate behind adaptive restarting
+#define SKS_ADAPT_ITERS 16
 #include "common.cuh"
 #include "internal.h"
 #include "step.cuh"
@@ -800,6 +803,7 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
   SKS_TRY(global_norm(c, b, fb + g.off, &fnorm));
   if (!(fnorm >= 0.0) || !std::isfinite(fnorm)) return fail(c, SKS_EINVAL, "f is not finite");
   const double thr = o->early_exit_factor > 0 ? o->early_exit_factor * o->tol * fnorm : -1.0;
+  const bool adaptive = (o->flags & SKS_OPT_ADAPTIVE_RESTART) != 0;
 
   int cycles = 0, columns = 0, generated = 0, flags = 0;
   int64_t nh = 0, nht = 0;
@@ -839,6 +843,7 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
     SKS_CK(c, cudaEventRecord(c->ev_b0, st));
     int next_sk = 0;    // next column to sketch
     int next_qr = 0;    // next SAB column to append
+    std::vector<int> kq_cols;  // adaptive restarting: QR columns behind each batch's kappa estimate
     const void* plan = nullptr;
     int nbatch = 0;
     int last_col = d;   // columns 0..d are generated (d+1 columns)
@@ -864,6 +869,13 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
         SKS_TRY(qr_append(c, b, 0, next_qr, J, s, 1, d, c->side));
         next_qr += J;
       }
+      // adaptive restarting (O31): kappa_2(T_j) after every batch, j = next_qr
+      if (adaptive && next_qr > 0 && (kq_cols.empty() || kq_cols.back() < next_qr) && kq_cols.size() < 1024) {
+        SKS_CK(c, launch_cond(c->T.as<double>(), b.ncol, next_qr, SKS_ADAPT_ITERS, dctrl,
+                              c->small.as<double>() + 2048 + kq_cols.size(), c->side));
+        kq_cols.push_back(next_qr);
+        ++c->launches;
+      }
       SKS_CK(c, cudaMemcpyAsync(hc, dctrl, sizeof(CtrlBlock), cudaMemcpyDeviceToHost, c->side));
       if (nbatch < (int)c->ev_batch.size()) SKS_CK(c, cudaEventRecord(c->ev_batch[nbatch], c->side));
       ++nbatch;
@@ -882,7 +894,8 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
         // poll the early-exit / breakdown flags of batch nbatch-2 (bounded lag)
         if (nbatch >= 2 && nbatch - 2 < (int)c->ev_batch.size()) {
           SKS_CK(c, cudaEventSynchronize(c->ev_batch[nbatch - 2]));
-          if (hc->exit_cols > 0 || hc->stop_col < INT_MAX || hc->rank_def) {
+          if (hc->exit_cols > 0 || hc->stop_col < INT_MAX || hc->rank_def ||
+              (adaptive && hc->cond > o->cond_tol)) {
             last_col = j;
             break;
           }
@@ -919,6 +932,41 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
       int dmax = d;
       if (hc->stop_col < INT_MAX) dmax = std::min(dmax, hc->stop_col);
       jstar = std::min(dmax, hc->qr_cols);
+    }
+    if (adaptive && !kq_cols.empty()) {
+      // first batch whose kappa estimate exceeds cond_tol, then bisection inside it for the first j
+      // with kappa_2(T_j) > cond_tol (kappa_2 of the leading blocks is non-decreasing in j)
+      const int nk = (int)kq_cols.size();
+      SKS_CK(c, cudaMemcpyAsync(c->h_small + 2048, c->small.as<double>() + 2048, sizeof(double) * nk,
+                                cudaMemcpyDeviceToHost, st));
+      SKS_CK(c, cudaStreamSynchronize(st));
+      int bo = -1;
+      for (int t = 0; t < nk; ++t)
+        if (c->h_small[2048 + t] > o->cond_tol) {
+          bo = t;
+          break;
+        }
+      if (bo >= 0) {
+        int lo = bo == 0 ? 0 : kq_cols[bo - 1], hi = kq_cols[bo];
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) / 2;
+          SKS_CK(c, launch_cond(c->T.as<double>(), b.ncol, mid, SKS_ADAPT_ITERS, nullptr,
+                                c->small.as<double>() + 3072, st));
+          ++c->launches;
+          SKS_CK(c, cudaMemcpyAsync(c->h_small + 3072, c->small.as<double>() + 3072, sizeof(double),
+                                    cudaMemcpyDeviceToHost, st));
+          SKS_CK(c, cudaStreamSynchronize(st));
+          if (c->h_small[3072] > o->cond_tol)
+            hi = mid;
+          else
+            lo = mid;
+        }
+        const int jad = std::max(hi - 1, 1);  // "restart with the previous residual r_{j-1}"
+        if (jad < jstar) {
+          jstar = jad;
+          flags |= SKS_INFO_ADAPTIVE_RESTART;
+        }
+      }
     }
     if (hc->breakdown) flags |= SKS_WARN_BREAKDOWN;
     if (jstar <= 0) {  // nothing usable (r == 0 handled above); stop

@@ -264,3 +264,31 @@ def test_srr_chebyshev_parity(ctx):
     orc = O.srr_from_basis(lambda x: Ao @ x, bas["B"], bas["M"], O.sketch_matrix(m * m, 2 * d, 8, 4, 0), 6)
     assert _match(out["theta"], orc["theta_all"]) <= 1e-8
     np.testing.assert_allclose(np.sort(out["res_true"]), np.sort(orc["res_true"]), rtol=1e-4)
+
+
+# ---------------------------------------------------------------- adaptive restarting (NEXT(2))
+def test_sgmres_adaptive_restart_parity(ctx):
+    """Adaptive restarting (reading O31): the first cycle ends at the same column as the
+    oracle's exact rule -- cond_tol is put at the geometric midpoint of two consecutive kappa_2(T_j)
+    (2.3x apart with a k = 1 basis), so the device's power-iteration estimate cannot straddle it --
+    with the same solution; restarted to 1e-8 it converges (true residual by the oracle's operator)."""
+    from scipy.linalg import svdvals
+    P = _P()
+    m, beta, d, k, s = 32, 20.0, 40, 1, 80
+    A = O.stencil_matrix(2, m, beta)
+    f = rhs_normal(m * m, 0)
+    out = O.sgmres_cycle(lambda v: A @ v, f, np.zeros_like(f), d, k, s, 8, 0, 0, early_exit_factor=0.0)
+    kap = [svdvals(out["C"][:, :j]) for j in (20, 21)]
+    tol_k = float(np.sqrt((kap[0][0] / kap[0][-1]) * (kap[1][0] / kap[1][-1])))
+    Ag = P.StencilOperator(2, m, beta)
+    res = ctx.sgmres_solve(Ag, f, d=d, k=k, s=s, seed=0, tol=1e-8, max_cycles=1, cond_tol=tol_k,
+                           adaptive_restart=True, early_exit_factor=0.0)
+    orc = O.sgmres_solve(lambda v: A @ v, f, d, k, s, 8, 0, tol=1e-8, max_cycles=1, cond_tol=tol_k,
+                         adaptive=True, early_exit_factor=0.0)
+    assert res.info["columns"] == orc["columns"] == 20
+    assert res.info["flags"] & P._lib.SKS_INFO_ADAPTIVE_RESTART and orc["flags"] & O.INFO_ADAPTIVE
+    np.testing.assert_allclose(res.x, orc["x"], rtol=0, atol=1e-8 * np.abs(orc["x"]).max())
+    full = ctx.sgmres_solve(Ag, f, d=d, k=k, s=s, seed=0, tol=1e-8, max_cycles=80, cond_tol=tol_k,
+                            adaptive_restart=True)
+    rel = np.linalg.norm(f - A @ full.x) / np.linalg.norm(f)
+    assert full.converged and rel <= 1e-8
