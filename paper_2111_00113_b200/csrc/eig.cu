@@ -135,13 +135,239 @@ __device__ __forceinline__ HqRefl hq_refl_fast(double p, double q, double r) {
 constexpr int HQ_R = 32;         // window rows/cols (the bulge region of HQ_W steps plus 3)
 constexpr int HQ_W = HQ_R - 3;   // bulge steps per window
 constexpr int HQ_LD = HQ_R + 1;  // odd pitch: row- and column-wise smem access both conflict-free
-constexpr int HQ_THREADS = 384;
+#ifndef HQ_NB
+// bulges per Francis sweep.  HQ_NB=2 (two bulges with the same shift pair, one shared-memory phase per
+// round, hq_chase2) cuts the C5 sweeps 422 -> 269 but one warp then issues both chains: 1835 cycles per
+// round vs 697 per one-bulge step, hqr 40 ms vs 30 ms -- kept as an option, off by default
+#define HQ_NB 1
+#endif
+constexpr int HQ_THREADS = HQ_NB == 2 ? 256 : 384;  // HQ_NB=2 needs the larger register budget
 constexpr int HQ_QSZ = HQ_LD * HQ_R;
+#ifndef HQ_TWO_MIN
+#define HQ_TWO_MIN 12  // minimum nn - m for the second bulge
+#endif
+
+// ---- two-bulge chase (HQ_NB == 2): bulges A (leading) and B (trailing by 4 positions) carry the same
+// double shift (reading: two Francis double-shift steps with one shift pair per sweep; B is introduced
+// at row m from the current matrix once A has moved 4 positions).  P_A (rows/cols kA..kA+2) and P_B
+// (kB..kB+2, kB = kA-4) act on disjoint index sets, so each round applies both in one shared-memory
+// phase: the block rows kB..kB+2 x cols kA..kA+2 (touched by P_B from the left and P_A from the right)
+// is formed by the lanes of A's column transform.  The two reflector chains are independent, so the
+// scheduler overlaps their FP64 latencies.  Window: rows/cols [lo, lo+31] (col lo-1 for reflector
+// reads), rounds kA in [a0, a1); Q accumulates P_A and P_B.
+struct HqBulge {
+  double B00, B01, B02, B10, B11, B12, B20, B21, B22;  // H[k..k+2][k..k+2] before the step
+  double C0, C1, C2, h3, d33;                         // H[k..k+2][k+3], H[k+3][k+2], H[k+3][k+3]
+};
+
+__device__ __forceinline__ void hq_chase2(double* Hw, double* Qs, double* dmy, int lo, int r1, int a0, int a1, int m,
+                                          int nn, int l, double sp, double sq, double sr, double sx, double sy,
+                                          double sw, int lane) {
+  auto H_ = [&](int gi, int gj) -> double {
+    return (gi >= lo && gj >= lo - 1 && gi <= r1 && gj <= r1) ? Hw[(gi - lo) + (gj - lo + 1) * HQ_LD] : 0.0;
+  };
+  auto load_state = [&](int k, HqBulge& S) {
+    S.B00 = H_(k, k); S.B01 = H_(k, k + 1); S.B02 = H_(k, k + 2);
+    S.B10 = H_(k + 1, k); S.B11 = H_(k + 1, k + 1); S.B12 = H_(k + 1, k + 2);
+    S.B20 = H_(k + 2, k); S.B21 = H_(k + 2, k + 1); S.B22 = H_(k + 2, k + 2);
+    S.C0 = H_(k, k + 3); S.C1 = H_(k + 1, k + 3); S.C2 = H_(k + 2, k + 3);
+    S.h3 = H_(k + 3, k + 2); S.d33 = H_(k + 3, k + 3);
+  };
+  // first reflector input of a bulge at row k: the shift polynomial at m (NR's p, q, r; scale-free)
+  // or the bulge column k-1
+  auto intro = [&](int k, double& p, double& q, double& r) {
+    const double z = H_(m, m), rr = sx - z, ss = sy - z;
+    p = (rr * ss - sw) / H_(m + 1, m) + H_(m, m + 1);
+    q = H_(m + 1, m + 1) - z - rr - ss;
+    r = H_(m + 2, m + 1);
+    (void)k;
+  };
+  // the second bulge only on active blocks long enough to hold both (short ones: one bulge)
+  const bool twoB = nn - m >= HQ_TWO_MIN;
+  HqBulge A = {}, Bb = {};
+  HqRefl RA, RB;
+  {
+    const int kA = a0, kB = a0 - 4;
+    double p, q, r;
+    if (kA == m) {
+      p = sp; q = sq; r = sr;
+    } else {
+      p = H_(kA, kA - 1); q = H_(kA + 1, kA - 1); r = H_(kA + 2, kA - 1);
+    }
+    if (kA <= nn - 1) {
+      load_state(kA, A);
+      RA = hq_refl_fast(p, q, r);
+    } else {
+      RA = hq_refl_fast(0.0, 0.0, 0.0);
+    }
+    if (twoB && kB >= m && kB <= nn - 1) {  // B already running: its bulge sits in column kB-1
+      load_state(kB, Bb);
+      RB = hq_refl_fast(H_(kB, kB - 1), H_(kB + 1, kB - 1), H_(kB + 2, kB - 1));
+    } else {
+      RB = hq_refl_fast(0.0, 0.0, 0.0);
+    }
+  }
+  for (int kA = a0; kA < a1; ++kA) {
+    const int kB = kA - 4;
+    const bool actA = kA <= nn - 1, actB = twoB && kB >= m && kB <= nn - 1;
+    if (kB == m && twoB) {  // introduce B from the current matrix (A has moved 4 positions)
+      double p, q, r;
+      intro(kB, p, q, r);
+      load_state(kB, Bb);
+      Bb.B20 = 0.0;  // H[m+2][m]: zeroed by A's step m+1 (shared memory still holds A's stale bulge entry)
+      RB = hq_refl_fast(p, q, r);
+    }
+    // ---- loads (values after the previous round)
+    const double E0 = H_(kA, kA + 4), E1 = H_(kA + 1, kA + 4), E2 = H_(kA + 2, kA + 4), E3 = H_(kA + 3, kA + 4);
+    const double h4 = H_(kA + 4, kA + 3), d44 = H_(kA + 4, kA + 4);
+    if (actB) {  // B's column k+3 and row k+3 are changed by A every round: reload
+      Bb.C0 = H_(kB, kB + 3); Bb.C1 = H_(kB + 1, kB + 3); Bb.C2 = H_(kB + 2, kB + 3);
+      Bb.h3 = H_(kB + 3, kB + 2); Bb.d33 = H_(kB + 3, kB + 3);
+    }
+    double Z[3][3];  // H[kB..kB+2][kA..kA+2]
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) Z[i][j] = H_(kB + i, kA + j);
+    const int ir = lo + lane;  // this lane's row (column transforms, Q)
+    // A row transformation: column kA+3+lane
+    const int jA = kA + 3 + lane;
+    const bool rokA = actA && jA <= r1;
+    double* colA = rokA ? Hw + (jA - lo + 1) * HQ_LD + (kA - lo) : dmy + 16 * lane;
+    const double aA0 = colA[0], aA1 = colA[1], aA2 = colA[2];
+    // B row transformation: column kB+3+lane, except A's columns kA..kA+2 (lanes 1..3)
+    const int jB = kB + 3 + lane;
+    const bool rokB = actB && jB <= r1 && (!actA || lane < 1 || lane > 3);
+    double* colB = rokB ? Hw + (jB - lo + 1) * HQ_LD + (kB - lo) : dmy + 16 * lane + 3;
+    const double aB0 = colB[0], aB1 = colB[1], aB2 = colB[2];
+    // A column transformation of row ir: loaded rows are those above kA outside B's rows
+    const bool cokA = actA && ir <= min(nn, kA + 3);
+    const bool specA = ir >= kB && ir <= kB + 2;
+    const bool ldA = cokA && ir < kA && !specA;
+    double* rowA = Hw + lane + (kA - lo + 1) * HQ_LD;
+    const double bA0 = ldA ? rowA[0] : 0.0, bA1 = ldA ? rowA[HQ_LD] : 0.0, bA2 = ldA ? rowA[2 * HQ_LD] : 0.0;
+    const bool cokB = actB && ir <= min(nn, kB + 3);
+    const bool ldB = cokB && ir < kB;
+    double* rowB = Hw + lane + (kB - lo + 1) * HQ_LD;
+    const double bB0 = ldB ? rowB[0] : 0.0, bB1 = ldB ? rowB[HQ_LD] : 0.0, bB2 = ldB ? rowB[2 * HQ_LD] : 0.0;
+    double* qA = Qs + lane + (actA ? kA - lo : 0) * HQ_LD;
+    double* qB = Qs + lane + (actB ? kB - lo : 0) * HQ_LD;
+    const double gA0 = qA[0], gA1 = qA[HQ_LD], gA2 = qA[2 * HQ_LD];
+    const double gB0 = qB[0], gB1 = qB[HQ_LD], gB2 = qB[2 * HQ_LD];
+    double* hkA = (lane == 0 && actA && RA.valid) ? Hw + (kA - lo) + (kA - lo) * HQ_LD : dmy + 16 * lane + 6;
+    double* hkB = (lane == 0 && actB && RB.valid) ? Hw + (kB - lo) + (kB - lo) * HQ_LD : dmy + 16 * lane + 7;
+    const double hkAv = *hkA, hkBv = *hkB;
+    // ---- forward of A (as in the one-bulge chase)
+    const double u0 = RA.xx, u1 = RA.yy, u2 = RA.zz, w1 = RA.qq, w2 = RA.rr;
+    const double pp0 = fma(w2, A.B20, fma(w1, A.B10, A.B00)), pp1 = fma(w2, A.B21, fma(w1, A.B11, A.B01)),
+                 pp2 = fma(w2, A.B22, fma(w1, A.B12, A.B02)), ppc = fma(w2, A.C2, fma(w1, A.C1, A.C0)),
+                 ppe = fma(w2, E2, fma(w1, E1, E0));
+    const double R10 = fma(-u1, pp0, A.B10), R11 = fma(-u1, pp1, A.B11), R12 = fma(-u1, pp2, A.B12),
+                 R1c = fma(-u1, ppc, A.C1), R1e = fma(-u1, ppe, E1);
+    const double R20 = fma(-u2, pp0, A.B20), R21 = fma(-u2, pp1, A.B21), R22 = fma(-u2, pp2, A.B22),
+                 R2c = fma(-u2, ppc, A.C2), R2e = fma(-u2, ppe, E2);
+    const double t1 = fma(u2, R12, fma(u1, R11, u0 * R10));
+    const double t2 = fma(u2, R22, fma(u1, R21, u0 * R20));
+    const double t3 = u2 * A.h3;
+    const double N10 = R10 - t1, N11 = fma(-t1, w1, R11), N12 = fma(-t1, w2, R12);
+    const double N20 = R20 - t2, N21 = fma(-t2, w1, R21), N22 = fma(-t2, w2, R22);
+    const double N30 = -t3, N31 = -t3 * w1, N32 = fma(-t3, w2, A.h3);
+    const HqRefl RnA = hq_refl_fast(actA && kA + 1 <= nn - 1 ? N10 : 0.0, actA && kA + 1 <= nn - 1 ? N20 : 0.0,
+                                    actA && kA + 1 <= nn - 1 ? N30 : 0.0);
+    // ---- forward of B
+    const double v0 = RB.xx, v1 = RB.yy, v2 = RB.zz, x1 = RB.qq, x2 = RB.rr;
+    const double qq0 = fma(x2, Bb.B20, fma(x1, Bb.B10, Bb.B00)), qq1 = fma(x2, Bb.B21, fma(x1, Bb.B11, Bb.B01)),
+                 qq2 = fma(x2, Bb.B22, fma(x1, Bb.B12, Bb.B02)), qqc = fma(x2, Bb.C2, fma(x1, Bb.C1, Bb.C0));
+    const double S10 = fma(-v1, qq0, Bb.B10), S11 = fma(-v1, qq1, Bb.B11), S12 = fma(-v1, qq2, Bb.B12),
+                 S1c = fma(-v1, qqc, Bb.C1);
+    const double S20 = fma(-v2, qq0, Bb.B20), S21 = fma(-v2, qq1, Bb.B21), S22 = fma(-v2, qq2, Bb.B22),
+                 S2c = fma(-v2, qqc, Bb.C2);
+    const double e1 = fma(v2, S12, fma(v1, S11, v0 * S10));
+    const double e2 = fma(v2, S22, fma(v1, S21, v0 * S20));
+    const double e3 = v2 * Bb.h3;
+    const double M10 = S10 - e1, M11 = fma(-e1, x1, S11), M12 = fma(-e1, x2, S12);
+    const double M20 = S20 - e2, M21 = fma(-e2, x1, S21), M22 = fma(-e2, x2, S22);
+    const double M30 = -e3, M31 = -e3 * x1, M32 = fma(-e3, x2, Bb.h3);
+    const bool nxB = actB && kB + 1 <= nn - 1;
+    const HqRefl RnB = hq_refl_fast(nxB ? M10 : 0.0, nxB ? M20 : 0.0, nxB ? M30 : 0.0);
+    // ---- shared-memory updates of the round (masked lanes write to their scratch slots)
+    *hkA = (kA == m) ? ((l != m) ? -hkAv : hkAv) : -RA.s;
+    *hkB = (kB == m) ? ((l != m) ? -hkBv : hkBv) : -RB.s;
+    {  // row transformations
+      const double prA = fma(w2, aA2, fma(w1, aA1, aA0));
+      colA[0] = fma(-u0, prA, aA0);
+      colA[1] = fma(-u1, prA, aA1);
+      *((rokA && kA + 2 <= nn) ? colA + 2 : dmy + 16 * lane + 2) = fma(-u2, prA, aA2);
+      const double prB = fma(x2, aB2, fma(x1, aB1, aB0));
+      colB[0] = fma(-v0, prB, aB0);
+      colB[1] = fma(-v1, prB, aB1);
+      *((rokB && kB + 2 <= nn) ? colB + 2 : dmy + 16 * lane + 5) = fma(-v2, prB, aB2);
+    }
+    {  // A's column transformation (cols kA..kA+2)
+      const int d = ir - kA, dB = ir - kB;
+      const double X0 = fma(-u0, pp0, A.B00), X1 = fma(-u0, pp1, A.B01), X2 = fma(-u0, pp2, A.B02);
+      // B's rows: P_B from the left on the Z block first
+      const double zz0 = fma(x2, Z[2][0], fma(x1, Z[1][0], Z[0][0]));
+      const double zz1 = fma(x2, Z[2][1], fma(x1, Z[1][1], Z[0][1]));
+      const double zz2 = fma(x2, Z[2][2], fma(x1, Z[1][2], Z[0][2]));
+      const double vb = dB == 0 ? v0 : (dB == 1 ? v1 : v2);
+      const double zr0 = fma(-vb, zz0, dB == 0 ? Z[0][0] : (dB == 1 ? Z[1][0] : Z[2][0]));
+      const double zr1 = fma(-vb, zz1, dB == 0 ? Z[0][1] : (dB == 1 ? Z[1][1] : Z[2][1]));
+      const double zr2 = fma(-vb, zz2, dB == 0 ? Z[0][2] : (dB == 1 ? Z[1][2] : Z[2][2]));
+      const bool own = ir >= kA;
+      const double c0 = specA ? zr0 : (own ? (d == 0 ? X0 : (d == 1 ? R10 : (d == 2 ? R20 : 0.0))) : bA0);
+      const double c1 = specA ? zr1 : (own ? (d == 0 ? X1 : (d == 1 ? R11 : (d == 2 ? R21 : 0.0))) : bA1);
+      const double c2 = specA ? zr2 : (own ? (d == 0 ? X2 : (d == 1 ? R12 : (d == 2 ? R22 : A.h3))) : bA2);
+      const double tt = fma(u2, c2, fma(u1, c1, u0 * c0));
+      // the special block exists only where both columns and rows are real (<= nn, in the window)
+      const bool stA = cokA;
+      double* sc = dmy + 16 * lane;
+      *(stA ? rowA : sc) = c0 - tt;
+      *(stA && kA + 1 <= nn ? rowA + HQ_LD : sc + 1) = fma(-tt, w1, c1);
+      *(stA && kA + 2 <= nn ? rowA + 2 * HQ_LD : sc + 2) = fma(-tt, w2, c2);
+    }
+    {  // B's column transformation (cols kB..kB+2)
+      const int d = ir - kB;
+      const double Y0 = fma(-v0, qq0, Bb.B00), Y1 = fma(-v0, qq1, Bb.B01), Y2 = fma(-v0, qq2, Bb.B02);
+      const bool own = ir >= kB;
+      const double c0 = own ? (d == 0 ? Y0 : (d == 1 ? S10 : (d == 2 ? S20 : 0.0))) : bB0;
+      const double c1 = own ? (d == 0 ? Y1 : (d == 1 ? S11 : (d == 2 ? S21 : 0.0))) : bB1;
+      const double c2 = own ? (d == 0 ? Y2 : (d == 1 ? S12 : (d == 2 ? S22 : Bb.h3))) : bB2;
+      const double tt = fma(v2, c2, fma(v1, c1, v0 * c0));
+      double* sc = dmy + 16 * lane + 3;
+      *(cokB ? rowB : sc) = c0 - tt;
+      *(cokB ? rowB + HQ_LD : sc + 1) = fma(-tt, x1, c1);
+      *((cokB && kB + 2 <= nn) ? rowB + 2 * HQ_LD : sc + 2) = fma(-tt, x2, c2);
+    }
+    {  // Q <- Q P_A P_B (disjoint columns; an inactive bulge's stores go to scratch, not over the other's)
+      double* sq = dmy + 16 * lane + 8;
+      const double tqA = fma(u2, gA2, fma(u1, gA1, u0 * gA0));
+      *(actA ? qA : sq) = gA0 - tqA;
+      *(actA ? qA + HQ_LD : sq + 1) = fma(-tqA, w1, gA1);
+      *(actA ? qA + 2 * HQ_LD : sq + 2) = fma(-tqA, w2, gA2);
+      const double tqB = fma(v2, gB2, fma(v1, gB1, v0 * gB0));
+      *(actB ? qB : sq + 3) = gB0 - tqB;
+      *(actB ? qB + HQ_LD : sq + 4) = fma(-tqB, x1, gB1);
+      *(actB ? qB + 2 * HQ_LD : sq + 5) = fma(-tqB, x2, gB2);
+    }
+    __syncwarp();
+    RA = RnA;
+    A.B00 = N11; A.B01 = N12; A.B02 = R1c;
+    A.B10 = N21; A.B11 = N22; A.B12 = R2c;
+    A.B20 = N31; A.B21 = N32; A.B22 = A.d33;
+    A.C0 = R1e; A.C1 = R2e; A.C2 = E3;
+    A.h3 = h4; A.d33 = d44;
+    RB = RnB;
+    Bb.B00 = M11; Bb.B01 = M12; Bb.B02 = S1c;
+    Bb.B10 = M21; Bb.B11 = M22; Bb.B12 = S2c;
+    Bb.B20 = M31; Bb.B21 = M32; Bb.B22 = Bb.d33;
+  }
+}
 
 __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a, int n, int lda,
                                                          double* __restrict__ wr, double* __restrict__ wi,
                                                          int* __restrict__ info) {
-  __shared__ double Hw[HQ_LD * (HQ_R + 1) + 4 * 32];  // window + per-lane scratch
+  __shared__ double Hw[HQ_LD * (HQ_R + 1) + 16 * 32];  // window + per-lane scratch
   __shared__ double Qsh[2 * HQ_QSZ];  // accumulated Q of the current / previous window
   __shared__ double red[32];
   __shared__ int ired[32];
@@ -178,6 +404,14 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
     if (tid == 0) sits = 0;
     __syncthreads();
     while (true) {
+#ifdef HQ_DEBUG_SWEEPS  // debugging harness: stop after info[7] sweeps (if > 0), H left in place
+      if (info[7] > 0 && nsweep >= info[7]) {
+        __syncthreads();
+        if (tid == 0) sdone = 1;
+        __syncthreads();
+        break;
+      }
+#endif
       // --- find the largest l in [1, nn] with a negligible subdiagonal (all threads, one pass
       //     over the subdiagonal instead of a serial scan with one L2 round trip per element)
       {
@@ -401,14 +635,25 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
       // Pipeline over the windows of the sweep: while warp 0 chases window w, the other warps apply
       // the deferred off-window update of window w-1 (its columns beyond window w and its rows
       // above); the part of w's update that window w+1 reads (its columns) is done before w+1 loads.
-      int k0 = m;
-      int k1 = min(k0 + HQ_W, nn), r1 = min(k0 + HQ_R - 1, nn);
+      int k0 = m;  // window rows/cols [k0, r1]
+#if HQ_NB == 2
+      int a0 = m, a1 = min(k0 + HQ_R - 3, nn + 4);  // rounds: bulge A at kA in [a0, a1), B at kA - 4
+      int k1 = a1;
+#else
+      int k1 = min(k0 + HQ_W, nn);
+#endif
+      int r1 = min(k0 + HQ_R - 1, nn);
       int cur = 0, pk0 = -1, pr1 = 0;
       load_window(k0, r1, Qsh);
       __syncthreads();
       while (true) {
         double* Qs = Qsh + cur * HQ_QSZ;
         long long tc0 = clock64();
+#if HQ_NB == 2
+        if (warp == 0) {
+          hq_chase2(Hw, Qs, Hw + HQ_LD * (HQ_R + 1), k0, r1, a0, a1, m, nn, l, sp, sq, sr, sx, sy, sw, lane);
+        }
+#else
         if (warp == 0) {
           // Register-forwarded chase.  Every lane carries the step's reflector and the bulge state
           // (B = H[k..k+2][k..k+2], C = H[k..k+2][k+3], h3 = H[k+3][k+2], d33 = H[k+3][k+3]) and
@@ -519,6 +764,7 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
             d33 = d44;
           }
         }
+#endif
         else if (pk0 >= 0) {
           far_update(Qsh + (cur ^ 1) * HQ_QSZ, pk0, pr1, r1, nn, l, pk0, -1, nw - (nw >> 2));
         }
@@ -530,8 +776,13 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
           const int gj = k0 - 1 + c;
           if (i <= r1 - k0 && gj >= 0 && gj <= r1) HA(k0 + i, gj) = Hw[i + c * HQ_LD];
         }
+#if HQ_NB == 2
+        const int k0n = a1 - 4;  // the next window starts at bulge B's row
+        if (a1 >= nn + 4) {      // last window: its whole off-window update now
+#else
         const int k0n = k1;
         if (k0n > nn - 1) {  // last window: its whole off-window update now
+#endif
           far_update(Qs, k0, r1, r1, nn, l, k0, 0, nw);
           __syncthreads();
           break;
@@ -543,7 +794,13 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
         pr1 = r1;
         cur ^= 1;
         k0 = k0n;
+#if HQ_NB == 2
+        a0 = a1;
+        a1 = min(k0 + HQ_R - 3, nn + 4);
+        k1 = a1;
+#else
         k1 = min(k0 + HQ_W, nn);
+#endif
         r1 = r1n;
         load_window(k0, r1, Qsh + cur * HQ_QSZ);
         __syncthreads();
