@@ -1,7 +1,7 @@
 """Compare hqr_dbg (GPU, after 1 sweep / to completion) with the Python emulation of the windowed
 two-bulge sweep (/tmp/hq/kern2.py) and with numpy eigenvalues.  usage: python hqr_cmp.py make|check"""
 import sys, struct, numpy as np
-sys.path.insert(0, '/tmp/hq')
+sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.abspath(__file__)))
 from scipy.linalg import hessenberg
 n = 100
 rng = np.random.default_rng(7)
@@ -18,7 +18,7 @@ def rd(p):
     b = open(p, 'rb').read()
     inf = struct.unpack('8i', b[:32]); o = np.frombuffer(b[32:], dtype=np.float64)
     return inf, o[:n * n].reshape(n, n).T, o[n * n:n * n + n], o[n * n + n:]
-import kern2, emul
+import hq_kern2 as kern2, hq_emul as emul
 inf1, H1, _, _ = rd('/root/repo/gpurun_out/hqr_out1.bin')
 nn = n - 1; l = 0
 x = H[nn, nn]; y = H[nn - 1, nn - 1]; w = H[nn, nn - 1] * H[nn - 1, nn]
