@@ -1,6 +1,7 @@
 // common.cuh -- shared device/host helpers of libsks (product side; shares nothing with oracle/).
 #pragma once
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <stdint.h>
 #include <math.h>
 
@@ -129,3 +130,35 @@ struct CtrlBlock {
   double r_est_last;  // r_est at exit / last appended column
   double pad2[3];
 };
+
+namespace sks {
+// ---- programmatic dependent launch (PDL) for the back-to-back basis-step kernels: a step grid may be
+// scheduled while the previous kernel on the stream drains; it runs its set-up (barrier init, tensor
+// map prefetch), then waits for that kernel's completion before reading any of its outputs.
+__device__ __forceinline__ void pdl_wait_and_release() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+}
+inline bool pdl_enabled() {  // SKS_NO_PDL=1 turns it off (A/B measurements)
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("SKS_NO_PDL");
+    on = (e && e[0] == '1') ? 0 : 1;
+  }
+  return on == 1;
+}
+template <typename K, typename... Args>
+inline cudaError_t launch_pdl(K kern, int grid, int block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+}  // namespace sks

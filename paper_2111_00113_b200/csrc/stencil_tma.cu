@@ -57,6 +57,7 @@ __global__ void __launch_bounds__(QT, 1)
     for (int s = 0; s < NST; ++s) mbar_init(&bar[s], 1);
     fence_mbar_init();
   }
+  pdl_wait_and_release();                   // programmatic dependent launch (see stencil_zm.cu)
   if (!step_prologue(a, &cf, red)) return;  // contains __syncthreads
   constexpr int STAGE = QU3 + (KM - 1) * QB3;
   double* sW = smt + NST * STAGE;
@@ -200,6 +201,7 @@ __global__ void __launch_bounds__(QT, 1)
     for (int s = 0; s < NST; ++s) mbar_init(&bar[s], 1);
     fence_mbar_init();
   }
+  pdl_wait_and_release();
   if (!step_prologue(a, &cf, red)) return;
   constexpr int STAGE = QU2 + (KM - 1) * QB2P;
   double* sW = smt + NST * STAGE;
@@ -360,7 +362,7 @@ static cudaError_t launch_t(const StepArgs& a, const TmaCols& tc, const CUtensor
       if (e != cudaSuccess) return e;
       set = true;
     }
-    step3d_tma_kernel<KM, NST><<<grid, QT, smem, st>>>(a, tc, mu, mv);
+    return launch_pdl(step3d_tma_kernel<KM, NST>, grid, QT, smem, st, a, tc, mu, mv);
   } else {
     static bool set = false;
     if (!set) {
@@ -369,7 +371,7 @@ static cudaError_t launch_t(const StepArgs& a, const TmaCols& tc, const CUtensor
       if (e != cudaSuccess) return e;
       set = true;
     }
-    step2d_tma_kernel<KM, NST><<<grid, QT, smem, st>>>(a, tc, mu, mv);
+    return launch_pdl(step2d_tma_kernel<KM, NST>, grid, QT, smem, st, a, tc, mu, mv);
   }
   return cudaGetLastError();
 }

@@ -98,6 +98,9 @@ __global__ void __launch_bounds__(ZT, ZM_CPS)
     mbar_init(&bar[1], 1);
     fence_mbar_init();
   }
+  // PDL: everything above overlaps the previous kernel's tail; its outputs (partials, w_{j-1}) are
+  // read only after this wait.  The next step launch may be scheduled as soon as this grid runs.
+  pdl_wait_and_release();
   if (!step_prologue(a, &cf, red)) return;  // contains __syncthreads
   const int nv = FULL ? KM - 1 : cf.nv;
   const uint32_t sbytes = (uint32_t)(ZUP * (ZS + 2) * 8 + nv * ZVP * ZS * 8);
@@ -334,8 +337,7 @@ static cudaError_t zm_launch_v(const StepArgs& a, const ZmArgs& z, const CUtenso
     }
     set = true;
   }
-  step3d_zm_kernel<KM, ZS, FULL, USL><<<grid, ZT, smem, st>>>(a, z, mu, mv);
-  return cudaGetLastError();
+  return launch_pdl(step3d_zm_kernel<KM, ZS, FULL, USL>, grid, ZT, smem, st, a, z, mu, mv);
 }
 
 template <int KM>
