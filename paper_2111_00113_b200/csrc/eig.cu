@@ -136,12 +136,14 @@ constexpr int HQ_R = 32;         // window rows/cols (the bulge region of HQ_W s
 constexpr int HQ_W = HQ_R - 3;   // bulge steps per window
 constexpr int HQ_LD = HQ_R + 1;  // odd pitch: row- and column-wise smem access both conflict-free
 #ifndef HQ_NB
-// bulges per Francis sweep.  HQ_NB=2 (two bulges with the same shift pair, one shared-memory phase per
-// round, hq_chase2) cuts the C5 sweeps 422 -> 269 but one warp then issues both chains: 1835 cycles per
-// round vs 697 per one-bulge step, hqr 40 ms vs 30 ms -- kept as an option, off by default
-#define HQ_NB 1
+// bulges per Francis sweep / chasing warps:
+//   1: one bulge, one warp (hqr 29 ms at C5, 422 sweeps);
+//   2: two bulges with the same shift pair chased by ONE warp (hq_chase2; 269 sweeps but the warp
+//      issues both chains: 40 ms);
+//   3: the same two bulges on two warps with a 64-thread barrier per round (hq_chase2w; 27 ms).
+#define HQ_NB 3
 #endif
-constexpr int HQ_THREADS = HQ_NB == 2 ? 256 : 384;  // HQ_NB=2 needs the larger register budget
+constexpr int HQ_THREADS = HQ_NB == 2 ? 256 : 384;  // (HQ_NB=3: warps 0, 1 chase)  // HQ_NB=2 needs the larger register budget
 constexpr int HQ_QSZ = HQ_LD * HQ_R;
 #ifndef HQ_TWO_MIN
 #define HQ_TWO_MIN 12  // minimum nn - m for the second bulge
@@ -159,6 +161,228 @@ struct HqBulge {
   double B00, B01, B02, B10, B11, B12, B20, B21, B22;  // H[k..k+2][k..k+2] before the step
   double C0, C1, C2, h3, d33;                         // H[k..k+2][k+3], H[k+3][k+2], H[k+3][k+3]
 };
+
+// ---- two-bulge chase on two warps (HQ_NB == 3): warp 0 chases bulge A, warp 1 bulge B (4 rows
+// behind, same shift pair), one 64-thread named barrier per round.  Within a round the two warps
+// touch disjoint entries: the block rows kB..kB+2 x cols kA..kA+2 is formed by warp 0 (P_B from the
+// left with B's reflector of the round, exchanged through shared memory one round ahead, then P_A);
+// B's row transformation skips those columns; B reloads its column kB+3 and row kB+3 every round
+// (A changes them).  Validated against tools/micro/hq_kern2.py (same arithmetic as hq_chase2).
+__device__ __forceinline__ void hq_bar2() { asm volatile("bar.sync 1, 64;" ::: "memory"); }
+
+__device__ __forceinline__ void hq_chase2w(double* Hw, double* Qs, double* dmy, double* xchg, int lo, int r1, int a0,
+                                           int a1, int m, int nn, int l, double sp, double sq, double sr, double sx,
+                                           double sy, double sw, int lane, int role) {
+  auto H_ = [&](int gi, int gj) -> double {
+    return (gi >= lo && gj >= lo - 1 && gi <= r1 && gj <= r1) ? Hw[(gi - lo) + (gj - lo + 1) * HQ_LD] : 0.0;
+  };
+  auto load_state = [&](int k, HqBulge& S) {
+    S.B00 = H_(k, k); S.B01 = H_(k, k + 1); S.B02 = H_(k, k + 2);
+    S.B10 = H_(k + 1, k); S.B11 = H_(k + 1, k + 1); S.B12 = H_(k + 1, k + 2);
+    S.B20 = H_(k + 2, k); S.B21 = H_(k + 2, k + 1); S.B22 = H_(k + 2, k + 2);
+    S.C0 = H_(k, k + 3); S.C1 = H_(k + 1, k + 3); S.C2 = H_(k + 2, k + 3);
+    S.h3 = H_(k + 3, k + 2); S.d33 = H_(k + 3, k + 3);
+  };
+  auto put = [&](const HqRefl& R, int slot) {  // B's reflector for warp 0
+    if (lane == 0) {
+      double* x = xchg + 8 * slot;
+      x[0] = R.xx; x[1] = R.yy; x[2] = R.zz; x[3] = R.qq; x[4] = R.rr; x[5] = R.s; x[6] = R.valid ? 1.0 : 0.0;
+    }
+  };
+  auto get = [&](int slot) {
+    const double* x = xchg + 8 * slot;
+    HqRefl R;
+    R.xx = x[0]; R.yy = x[1]; R.zz = x[2]; R.qq = x[3]; R.rr = x[4]; R.s = x[5]; R.valid = x[6] != 0.0;
+    return R;
+  };
+  const bool twoB = nn - m >= HQ_TWO_MIN;
+  HqBulge S = {};
+  HqRefl R = hq_refl_fast(0.0, 0.0, 0.0);
+  // ---- window start: each warp its own bulge
+  if (role == 0) {
+    const int kA = a0;
+    if (kA <= nn - 1) {
+      double p, q, r;
+      if (kA == m) {
+        p = sp; q = sq; r = sr;
+      } else {
+        p = H_(kA, kA - 1); q = H_(kA + 1, kA - 1); r = H_(kA + 2, kA - 1);
+      }
+      load_state(kA, S);
+      R = hq_refl_fast(p, q, r);
+    }
+  } else {
+    const int kB = a0 - 4;
+    if (twoB && kB >= m && kB <= nn - 1) {
+      load_state(kB, S);
+      R = hq_refl_fast(H_(kB, kB - 1), H_(kB + 1, kB - 1), H_(kB + 2, kB - 1));
+    } else if (twoB && kB + 1 == m) {  // B enters at the window's first round
+      // (cannot happen: B enters at kA = m+4 inside the sweep's first window)
+    }
+    put(R, a0 & 1);
+  }
+  hq_bar2();
+  for (int kA = a0; kA < a1; ++kA) {
+    const int kB = kA - 4;
+    const bool actA = kA <= nn - 1, actB = twoB && kB >= m && kB <= nn - 1;
+    const int ir = lo + lane;
+    if (role == 0) {
+      const HqRefl RB = get(kA & 1);  // B's reflector of this round (identity if B is not running)
+      const double v0 = RB.xx, v1 = RB.yy, v2 = RB.zz, x1 = RB.qq, x2 = RB.rr;
+      const double E0 = H_(kA, kA + 4), E1 = H_(kA + 1, kA + 4), E2 = H_(kA + 2, kA + 4), E3 = H_(kA + 3, kA + 4);
+      const double h4 = H_(kA + 4, kA + 3), d44 = H_(kA + 4, kA + 4);
+      double Z[3][3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) Z[i][j] = H_(kB + i, kA + j);
+      const int jA = kA + 3 + lane;
+      const bool rokA = actA && jA <= r1;
+      double* colA = rokA ? Hw + (jA - lo + 1) * HQ_LD + (kA - lo) : dmy + 16 * lane;
+      const double aA0 = colA[0], aA1 = colA[1], aA2 = colA[2];
+      const bool cokA = actA && ir <= min(nn, kA + 3);
+      const bool specA = ir >= kB && ir <= kB + 2;
+      const bool ldA = cokA && ir < kA && !specA;
+      double* rowA = Hw + lane + (kA - lo + 1) * HQ_LD;
+      const double bA0 = ldA ? rowA[0] : 0.0, bA1 = ldA ? rowA[HQ_LD] : 0.0, bA2 = ldA ? rowA[2 * HQ_LD] : 0.0;
+      double* qA = Qs + lane + (actA ? kA - lo : 0) * HQ_LD;
+      const double gA0 = qA[0], gA1 = qA[HQ_LD], gA2 = qA[2 * HQ_LD];
+      double* hkA = (lane == 0 && actA && R.valid) ? Hw + (kA - lo) + (kA - lo) * HQ_LD : dmy + 16 * lane + 6;
+      const double hkAv = *hkA;
+      const double u0 = R.xx, u1 = R.yy, u2 = R.zz, w1 = R.qq, w2 = R.rr;
+      const double pp0 = fma(w2, S.B20, fma(w1, S.B10, S.B00)), pp1 = fma(w2, S.B21, fma(w1, S.B11, S.B01)),
+                   pp2 = fma(w2, S.B22, fma(w1, S.B12, S.B02)), ppc = fma(w2, S.C2, fma(w1, S.C1, S.C0)),
+                   ppe = fma(w2, E2, fma(w1, E1, E0));
+      const double R10 = fma(-u1, pp0, S.B10), R11 = fma(-u1, pp1, S.B11), R12 = fma(-u1, pp2, S.B12),
+                   R1c = fma(-u1, ppc, S.C1), R1e = fma(-u1, ppe, E1);
+      const double R20 = fma(-u2, pp0, S.B20), R21 = fma(-u2, pp1, S.B21), R22 = fma(-u2, pp2, S.B22),
+                   R2c = fma(-u2, ppc, S.C2), R2e = fma(-u2, ppe, E2);
+      const double t1 = fma(u2, R12, fma(u1, R11, u0 * R10));
+      const double t2 = fma(u2, R22, fma(u1, R21, u0 * R20));
+      const double t3 = u2 * S.h3;
+      const double N10 = R10 - t1, N11 = fma(-t1, w1, R11), N12 = fma(-t1, w2, R12);
+      const double N20 = R20 - t2, N21 = fma(-t2, w1, R21), N22 = fma(-t2, w2, R22);
+      const double N30 = -t3, N31 = -t3 * w1, N32 = fma(-t3, w2, S.h3);
+      const bool nx = actA && kA + 1 <= nn - 1;
+      const HqRefl Rn = hq_refl_fast(nx ? N10 : 0.0, nx ? N20 : 0.0, nx ? N30 : 0.0);
+      *hkA = (kA == m) ? ((l != m) ? -hkAv : hkAv) : -R.s;
+      {
+        const double pr = fma(w2, aA2, fma(w1, aA1, aA0));
+        colA[0] = fma(-u0, pr, aA0);
+        colA[1] = fma(-u1, pr, aA1);
+        *((rokA && kA + 2 <= nn) ? colA + 2 : dmy + 16 * lane + 2) = fma(-u2, pr, aA2);
+      }
+      {
+        const int d = ir - kA, dB = ir - kB;
+        const double X0 = fma(-u0, pp0, S.B00), X1 = fma(-u0, pp1, S.B01), X2 = fma(-u0, pp2, S.B02);
+        const double zz0 = fma(x2, Z[2][0], fma(x1, Z[1][0], Z[0][0]));
+        const double zz1 = fma(x2, Z[2][1], fma(x1, Z[1][1], Z[0][1]));
+        const double zz2 = fma(x2, Z[2][2], fma(x1, Z[1][2], Z[0][2]));
+        const double vb = dB == 0 ? v0 : (dB == 1 ? v1 : v2);
+        const double zr0 = fma(-vb, zz0, dB == 0 ? Z[0][0] : (dB == 1 ? Z[1][0] : Z[2][0]));
+        const double zr1 = fma(-vb, zz1, dB == 0 ? Z[0][1] : (dB == 1 ? Z[1][1] : Z[2][1]));
+        const double zr2 = fma(-vb, zz2, dB == 0 ? Z[0][2] : (dB == 1 ? Z[1][2] : Z[2][2]));
+        const bool own = ir >= kA;
+        const double c0 = specA ? zr0 : (own ? (d == 0 ? X0 : (d == 1 ? R10 : (d == 2 ? R20 : 0.0))) : bA0);
+        const double c1 = specA ? zr1 : (own ? (d == 0 ? X1 : (d == 1 ? R11 : (d == 2 ? R21 : 0.0))) : bA1);
+        const double c2 = specA ? zr2 : (own ? (d == 0 ? X2 : (d == 1 ? R12 : (d == 2 ? R22 : S.h3))) : bA2);
+        const double tt = fma(u2, c2, fma(u1, c1, u0 * c0));
+        double* sc = dmy + 16 * lane;
+        *(cokA ? rowA : sc) = c0 - tt;
+        *(cokA && kA + 1 <= nn ? rowA + HQ_LD : sc + 1) = fma(-tt, w1, c1);
+        *(cokA && kA + 2 <= nn ? rowA + 2 * HQ_LD : sc + 2) = fma(-tt, w2, c2);
+      }
+      {
+        double* sq2 = dmy + 16 * lane + 8;
+        const double tq = fma(u2, gA2, fma(u1, gA1, u0 * gA0));
+        *(actA ? qA : sq2) = gA0 - tq;
+        *(actA ? qA + HQ_LD : sq2 + 1) = fma(-tq, w1, gA1);
+        *(actA ? qA + 2 * HQ_LD : sq2 + 2) = fma(-tq, w2, gA2);
+      }
+      R = Rn;
+      S.B00 = N11; S.B01 = N12; S.B02 = R1c;
+      S.B10 = N21; S.B11 = N22; S.B12 = R2c;
+      S.B20 = N31; S.B21 = N32; S.B22 = S.d33;
+      S.C0 = R1e; S.C1 = R2e; S.C2 = E3;
+      S.h3 = h4; S.d33 = d44;
+    } else {
+      HqRefl Rnext = hq_refl_fast(0.0, 0.0, 0.0);
+      if (actB) {
+        S.C0 = H_(kB, kB + 3); S.C1 = H_(kB + 1, kB + 3); S.C2 = H_(kB + 2, kB + 3);
+        S.h3 = H_(kB + 3, kB + 2); S.d33 = H_(kB + 3, kB + 3);
+        const int jB = kB + 3 + lane;
+        const bool rokB = jB <= r1 && (!actA || lane < 1 || lane > 3);
+        double* colB = rokB ? Hw + (jB - lo + 1) * HQ_LD + (kB - lo) : dmy + 16 * lane + 3;
+        const double aB0 = colB[0], aB1 = colB[1], aB2 = colB[2];
+        const bool cokB = ir <= min(nn, kB + 3);
+        const bool ldB = cokB && ir < kB;
+        double* rowB = Hw + lane + (kB - lo + 1) * HQ_LD;
+        const double bB0 = ldB ? rowB[0] : 0.0, bB1 = ldB ? rowB[HQ_LD] : 0.0, bB2 = ldB ? rowB[2 * HQ_LD] : 0.0;
+        double* qB = Qs + lane + (kB - lo) * HQ_LD;
+        const double gB0 = qB[0], gB1 = qB[HQ_LD], gB2 = qB[2 * HQ_LD];
+        double* hkB = (lane == 0 && R.valid) ? Hw + (kB - lo) + (kB - lo) * HQ_LD : dmy + 16 * lane + 7;
+        const double hkBv = *hkB;
+        const double v0 = R.xx, v1 = R.yy, v2 = R.zz, x1 = R.qq, x2 = R.rr;
+        const double qq0 = fma(x2, S.B20, fma(x1, S.B10, S.B00)), qq1 = fma(x2, S.B21, fma(x1, S.B11, S.B01)),
+                     qq2 = fma(x2, S.B22, fma(x1, S.B12, S.B02)), qqc = fma(x2, S.C2, fma(x1, S.C1, S.C0));
+        const double S10 = fma(-v1, qq0, S.B10), S11 = fma(-v1, qq1, S.B11), S12 = fma(-v1, qq2, S.B12),
+                     S1c = fma(-v1, qqc, S.C1);
+        const double S20 = fma(-v2, qq0, S.B20), S21 = fma(-v2, qq1, S.B21), S22 = fma(-v2, qq2, S.B22),
+                     S2c = fma(-v2, qqc, S.C2);
+        const double e1 = fma(v2, S12, fma(v1, S11, v0 * S10));
+        const double e2 = fma(v2, S22, fma(v1, S21, v0 * S20));
+        const double e3 = v2 * S.h3;
+        const double M10 = S10 - e1, M11 = fma(-e1, x1, S11), M12 = fma(-e1, x2, S12);
+        const double M20 = S20 - e2, M21 = fma(-e2, x1, S21), M22 = fma(-e2, x2, S22);
+        const double M30 = -e3, M31 = -e3 * x1, M32 = fma(-e3, x2, S.h3);
+        const bool nx = kB + 1 <= nn - 1;
+        Rnext = hq_refl_fast(nx ? M10 : 0.0, nx ? M20 : 0.0, nx ? M30 : 0.0);
+        *hkB = (kB == m) ? ((l != m) ? -hkBv : hkBv) : -R.s;
+        {
+          const double pr = fma(x2, aB2, fma(x1, aB1, aB0));
+          colB[0] = fma(-v0, pr, aB0);
+          colB[1] = fma(-v1, pr, aB1);
+          *((rokB && kB + 2 <= nn) ? colB + 2 : dmy + 16 * lane + 5) = fma(-v2, pr, aB2);
+        }
+        {
+          const int d = ir - kB;
+          const double Y0 = fma(-v0, qq0, S.B00), Y1 = fma(-v0, qq1, S.B01), Y2 = fma(-v0, qq2, S.B02);
+          const bool own = ir >= kB;
+          const double c0 = own ? (d == 0 ? Y0 : (d == 1 ? S10 : (d == 2 ? S20 : 0.0))) : bB0;
+          const double c1 = own ? (d == 0 ? Y1 : (d == 1 ? S11 : (d == 2 ? S21 : 0.0))) : bB1;
+          const double c2 = own ? (d == 0 ? Y2 : (d == 1 ? S12 : (d == 2 ? S22 : S.h3))) : bB2;
+          const double tt = fma(v2, c2, fma(v1, c1, v0 * c0));
+          double* sc = dmy + 16 * lane + 3;
+          *(cokB ? rowB : sc) = c0 - tt;
+          *(cokB ? rowB + HQ_LD : sc + 1) = fma(-tt, x1, c1);
+          *((cokB && kB + 2 <= nn) ? rowB + 2 * HQ_LD : sc + 2) = fma(-tt, x2, c2);
+        }
+        {
+          const double tq = fma(v2, gB2, fma(v1, gB1, v0 * gB0));
+          qB[0] = gB0 - tq;
+          qB[HQ_LD] = fma(-tq, x1, gB1);
+          qB[2 * HQ_LD] = fma(-tq, x2, gB2);
+        }
+        S.B00 = M11; S.B01 = M12; S.B02 = S1c;
+        S.B10 = M21; S.B11 = M22; S.B12 = S2c;
+        S.B20 = M31; S.B21 = M32; S.B22 = S.d33;
+      }
+      if (twoB && kB + 1 == m) {  // B enters next round: its first reflector from the current matrix
+        // (rows/cols m..m+2 are final: A is at m+3 and only touches indices >= m+3)
+        const double z = H_(m, m), rr = sx - z, ss = sy - z;
+        const double p = (rr * ss - sw) / H_(m + 1, m) + H_(m, m + 1);
+        const double q = H_(m + 1, m + 1) - z - rr - ss;
+        const double r = H_(m + 2, m + 1);
+        load_state(m, S);
+        S.B20 = 0.0;  // H[m+2][m]: zeroed by A's step m+1 (shared memory holds A's stale bulge entry)
+        Rnext = hq_refl_fast(p, q, r);
+      }
+      R = Rnext;
+      put(R, (kA + 1) & 1);
+    }
+    hq_bar2();
+  }
+}
 
 __device__ __forceinline__ void hq_chase2(double* Hw, double* Qs, double* dmy, int lo, int r1, int a0, int a1, int m,
                                           int nn, int l, double sp, double sq, double sr, double sx, double sy,
@@ -369,6 +593,7 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
                                                          int* __restrict__ info) {
   __shared__ double Hw[HQ_LD * (HQ_R + 1) + 16 * 32];  // window + per-lane scratch
   __shared__ double Qsh[2 * HQ_QSZ];  // accumulated Q of the current / previous window
+  __shared__ double hq_x[16];         // HQ_NB=3: bulge B's reflector for warp 0, by round parity
   __shared__ double red[32];
   __shared__ int ired[32];
   __shared__ double sp, sq, sr, sx, sy, sw, st;
@@ -563,11 +788,16 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
         const int lr = lane >> 2, lc = lane & 3;
         const int ncol = chi - clo, nrow = ahi - alo;
         const int ntc = ncol > 0 ? (ncol + 7) >> 3 : 0, ntr = nrow > 0 ? (nrow + 7) >> 3 : 0;
-        // w0 < 0: deferred mode, workers are the warps off warp 0's scheduler (warp % 4 != 0)
+        // w0 < 0: deferred mode, workers are the warps off the chasing warps' schedulers
         int me = warp - w0;
         if (w0 < 0) {
+#if HQ_NB == 3
+          if ((warp & 3) < 2) return;  // warps 0, 1 chase; 4, 5, 8, 9 share their schedulers
+          me = (warp >> 2) * 2 + (warp & 3) - 2;
+#else
           if ((warp & 3) == 0) return;
           me = warp - (warp >> 2) - 1;
+#endif
         }
         if (me < 0 || me >= ntc + ntr) return;
         double fq[4][8];
@@ -636,7 +866,7 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
       // the deferred off-window update of window w-1 (its columns beyond window w and its rows
       // above); the part of w's update that window w+1 reads (its columns) is done before w+1 loads.
       int k0 = m;  // window rows/cols [k0, r1]
-#if HQ_NB == 2
+#if HQ_NB >= 2
       int a0 = m, a1 = min(k0 + HQ_R - 3, nn + 4);  // rounds: bulge A at kA in [a0, a1), B at kA - 4
       int k1 = a1;
 #else
@@ -649,7 +879,12 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
       while (true) {
         double* Qs = Qsh + cur * HQ_QSZ;
         long long tc0 = clock64();
-#if HQ_NB == 2
+#if HQ_NB == 3
+        if (warp < 2) {
+          hq_chase2w(Hw, Qs, Hw + HQ_LD * (HQ_R + 1), hq_x, k0, r1, a0, a1, m, nn, l, sp, sq, sr, sx, sy, sw, lane,
+                     warp);
+        }
+#elif HQ_NB == 2
         if (warp == 0) {
           hq_chase2(Hw, Qs, Hw + HQ_LD * (HQ_R + 1), k0, r1, a0, a1, m, nn, l, sp, sq, sr, sx, sy, sw, lane);
         }
@@ -766,7 +1001,8 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
         }
 #endif
         else if (pk0 >= 0) {
-          far_update(Qsh + (cur ^ 1) * HQ_QSZ, pk0, pr1, r1, nn, l, pk0, -1, nw - (nw >> 2));
+          far_update(Qsh + (cur ^ 1) * HQ_QSZ, pk0, pr1, r1, nn, l, pk0, -1,
+                     HQ_NB == 3 ? nw / 2 : nw - (nw >> 2));
         }
         __syncthreads();
         long long tc1 = clock64();
@@ -776,7 +1012,7 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
           const int gj = k0 - 1 + c;
           if (i <= r1 - k0 && gj >= 0 && gj <= r1) HA(k0 + i, gj) = Hw[i + c * HQ_LD];
         }
-#if HQ_NB == 2
+#if HQ_NB >= 2
         const int k0n = a1 - 4;  // the next window starts at bulge B's row
         if (a1 >= nn + 4) {      // last window: its whole off-window update now
 #else
@@ -794,7 +1030,7 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
         pr1 = r1;
         cur ^= 1;
         k0 = k0n;
-#if HQ_NB == 2
+#if HQ_NB >= 2
         a0 = a1;
         a1 = min(k0 + HQ_R - 3, nn + 4);
         k1 = a1;
