@@ -141,6 +141,7 @@ enum {
 enum {
   SKS_OPT_TIME_STEPS = 1,       /* bracket every basis-step launch with CUDA events on the main stream and
                                    report the summed kernel time in info->t_step_s (measurement only) */
+  SKS_OPT_ZERO_X0 = 4,          /* x0 = 0: x is output only (its input content is not read or copied) */
   SKS_OPT_ADAPTIVE_RESTART = 2  /* adaptive restarting (Sec. "Adaptive restarting"): when
                                    first kappa_2(T_j) > cond_tol, the cycle ends with the previous
                                    solution (j-1 columns) and restarts from its residual (reading O31:

@@ -44,6 +44,7 @@ class SgmresInfo(C.Structure):
 
 SKS_OPT_TIME_STEPS = 1
 SKS_OPT_ADAPTIVE_RESTART = 2
+SKS_OPT_ZERO_X0 = 4
 SKS_BASIS_ARNOLDI, SKS_BASIS_CHEBYSHEV = 0, 1
 BASES = {"arnoldi": SKS_BASIS_ARNOLDI, "chebyshev": SKS_BASIS_CHEBYSHEV}
 

@@ -155,15 +155,22 @@ class Context:
     # ---------------------------------------------------------------- sGMRES
     def sgmres_solve(self, A, f, x0=None, *, d, k, s, zeta=8, seed=0, tol=1e-8, max_cycles=50,
                      early_exit_factor=0.25, cond_tol=1e14, sketch_batch=0, hist_cap=None, time_steps=False, time_stride=1,
-                     basis="arnoldi", cheb=None, adaptive_restart=False):
+                     basis="arnoldi", cheb=None, adaptive_restart=False, out=None):
         op, keep = A.struct()
         fa, pf = _prep(f)
         n = fa.shape[0]
-        if x0 is None:
-            if _is_torch(fa):
-                x = torch.zeros_like(fa)
-            else:
-                x = np.zeros(n)
+        zero_x0 = x0 is None
+        if out is not None:
+            # the solution is written into `out` (a pinned host `out` keeps the library's copy at full
+            # DMA speed); x0 (if given and not `out` itself) is copied into it first
+            x = out
+            if x0 is not None and x0 is not out:
+                if _is_torch(x):
+                    x.copy_(x0 if _is_torch(x0) else torch.from_numpy(np.asarray(x0, dtype=np.float64)))
+                else:
+                    x[...] = x0.cpu().numpy() if _is_torch(x0) else x0
+        elif x0 is None:  # x0 = 0 is not copied to the device (SKS_OPT_ZERO_X0)
+            x = torch.empty_like(fa) if _is_torch(fa) else np.empty(n)
         else:
             x = (x0.detach().clone().to(torch.float64).contiguous() if _is_torch(x0)
                  else np.array(x0, dtype=np.float64, copy=True))
@@ -174,7 +181,8 @@ class Context:
         cc, cdx, cdy = cheb if cheb is not None else (0.0, 0.0, 0.0)
         opts = L.SgmresOpts(d, k, s, zeta, seed, tol, max_cycles, sketch_batch, early_exit_factor, cond_tol,
                             (L.SKS_OPT_TIME_STEPS if time_steps else 0)
-                            | (L.SKS_OPT_ADAPTIVE_RESTART if adaptive_restart else 0), time_stride, L.BASES[basis], 0,
+                            | (L.SKS_OPT_ADAPTIVE_RESTART if adaptive_restart else 0)
+                            | (L.SKS_OPT_ZERO_X0 if zero_x0 else 0), time_stride, L.BASES[basis], 0,
                             cc, cdx, cdy)
         info = L.SgmresInfo()
         st = self.lib.sks_sgmres_solve(self.h, C.byref(op), pf, px, C.byref(opts), C.byref(info),

@@ -795,7 +795,10 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
   double* fb = c->fb.as<double>();
   SKS_CK(c, cudaMemsetAsync(xb, 0, sizeof(double) * g.ld, st));
   SKS_CK(c, cudaMemsetAsync(fb, 0, sizeof(double) * g.ld, st));
-  SKS_CK(c, cudaMemcpyAsync(xb + g.off, x, sizeof(double) * g.n, cudaMemcpyDefault, st));
+  if (o->flags & SKS_OPT_ZERO_X0)
+    SKS_CK(c, cudaMemsetAsync(xb + g.off, 0, sizeof(double) * g.n, st));
+  else
+    SKS_CK(c, cudaMemcpyAsync(xb + g.off, x, sizeof(double) * g.n, cudaMemcpyDefault, st));
   SKS_CK(c, cudaMemcpyAsync(fb + g.off, f, sizeof(double) * g.n, cudaMemcpyDefault, st));
   SKS_TRY(halo_exchange(c, g, xb));
   SKS_TRY(halo_exchange(c, g, fb));
