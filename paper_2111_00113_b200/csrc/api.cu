@@ -807,6 +807,8 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
   if (!(fnorm >= 0.0) || !std::isfinite(fnorm)) return fail(c, SKS_EINVAL, "f is not finite");
   const double thr = o->early_exit_factor > 0 ? o->early_exit_factor * o->tol * fnorm : -1.0;
   const bool adaptive = (o->flags & SKS_OPT_ADAPTIVE_RESTART) != 0;
+  int poll_lag = (g.kind == SKS_OP_CSR) ? 1 : 2;
+  if (const char* e = getenv("SKS_POLL_LAG")) poll_lag = std::max(1, atoi(e));
 
   int cycles = 0, columns = 0, generated = 0, flags = 0;
   int64_t nh = 0, nht = 0;
@@ -894,9 +896,11 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
         SKS_TRY(enqueue_side(j + 1, j == d));
         pending_upto = j + 1;
         batch_size = std::min(JB, batch_size * 2);
-        // poll the early-exit / breakdown flags of batch nbatch-2 (bounded lag)
-        if (nbatch >= 2 && nbatch - 2 < (int)c->ev_batch.size()) {
-          SKS_CK(c, cudaEventSynchronize(c->ev_batch[nbatch - 2]));
+        // poll the early-exit / breakdown flags of batch nbatch-lag (bounded lag): 2 for stencils
+        // (cheap columns: keep the GPU fed), 1 for CSR (a column costs a full matrix sweep, more
+        // than the batch's sketched QR, so over-generated columns cost more than the wait)
+        if (nbatch >= poll_lag && nbatch - poll_lag < (int)c->ev_batch.size()) {
+          SKS_CK(c, cudaEventSynchronize(c->ev_batch[nbatch - poll_lag]));
           if (hc->exit_cols > 0 || hc->stop_col < INT_MAX || hc->rank_def ||
               (adaptive && hc->cond > o->cond_tol)) {
             last_col = j;
