@@ -60,6 +60,7 @@ struct sks_ctx {
   int64_t w_zeroed_bytes = 0;
   void* tma_cache = nullptr;   // encoded tensor maps of the stencil step
   void* zm_cache = nullptr;    // encoded tensor maps of the 3D z-march step
+  void* ym_cache = nullptr;    // encoded tensor maps of the 2D y-march step
   int use_tma = 1;             // SKS_NO_TMA=1 forces the generic stencil kernels
   int tma_mask = 7;
   cudaStream_t main() const { return user_main ? user_main : own_main; }
@@ -342,6 +343,7 @@ sks_status sks_destroy(sks_ctx* c) {
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->tma_cache) stencil_tma_free(c->tma_cache);
   if (c->zm_cache) stencil_zm_free(c->zm_cache);
+  if (c->ym_cache) stencil_ym_free(c->ym_cache);
   for (auto& ev : c->ev_batch) cudaEventDestroy(ev);
   for (auto& ev : c->ev_step) cudaEventDestroy(ev);
   cudaEvent_t evs[] = {c->ev_fork, c->ev_join, c->ev_t0, c->ev_t1, c->ev_b0, c->ev_b1};
@@ -377,6 +379,7 @@ struct Basis {
   int step_grid = 0;   // stencil step grid, or CSR grid
   bool tma = false;    // TMA-fed stencil kernels
   bool zm = false;     // 3D z-march kernel (replaces the TMA box kernel)
+  bool ym = false;     // 2D y-march kernel (replaces the TMA box kernel)
   int last_grid = 0;   // grid of the previous step launch (its partial count)
   StepArgs sat;        // step arguments with the TMA tiling
   int tma_grid = 0;
@@ -465,9 +468,14 @@ static sks_status setup_basis(sks_ctx* c, const sks_operator* A, int k, int ncol
     stencil_tiling(g.dim, g.m, g.nz, c->main_sms, &a, &b->step_grid);
     if (b->step_grid > b->pslots) b->step_grid = b->pslots;
     b->zm = c->use_tma && stencil_zm_supported(g.dim, g.m, k);
+    b->ym = !b->zm && c->use_tma && stencil_ym_supported(g.dim, g.m, k);
     if (b->zm) {
       b->tma = true;
       stencil_zm_tiling(g.m, g.nz, c->main_sms, &b->sat, &b->tma_grid);
+      if (b->tma_grid > b->pslots) b->tma_grid = b->pslots;
+    } else if (b->ym) {
+      b->tma = true;
+      stencil_ym_tiling(g.m, g.nz, c->main_sms, &b->sat, &b->tma_grid);
       if (b->tma_grid > b->pslots) b->tma_grid = b->pslots;
     } else if (b->tma) {
       stencil_tma_tiling(g.dim, g.m, g.nz, c->main_sms, &b->sat, &b->tma_grid);
@@ -575,6 +583,9 @@ static sks_status first_column(sks_ctx* c, Basis& b, int mode, const double* xve
     if (use_t && b.zm)
       SKS_CK(c, launch_step_stencil_zm(a, c->W.as<double>(), b.ncol, c->xb.as<double>(), c->fb.as<double>(),
                                        c->vb.as<double>(), b.tma_grid, st, &c->zm_cache));
+    else if (use_t && b.ym)
+      SKS_CK(c, launch_step_stencil_ym(a, c->W.as<double>(), b.ncol, c->xb.as<double>(), c->fb.as<double>(),
+                                       c->vb.as<double>(), b.tma_grid, st, &c->ym_cache));
     else if (use_t)
       SKS_CK(c, launch_step_stencil_tma(a, c->W.as<double>(), b.ncol, c->xb.as<double>(), c->fb.as<double>(),
                                         c->vb.as<double>(), b.tma_grid, st, &c->tma_cache));
@@ -621,6 +632,9 @@ static sks_status step_column(sks_ctx* c, Basis& b, int j) {
     if (use_t && b.zm)
       SKS_CK(c, launch_step_stencil_zm(a, c->W.as<double>(), b.ncol, c->xb.as<double>(), c->fb.as<double>(),
                                        c->vb.as<double>(), b.tma_grid, st, &c->zm_cache));
+    else if (use_t && b.ym)
+      SKS_CK(c, launch_step_stencil_ym(a, c->W.as<double>(), b.ncol, c->xb.as<double>(), c->fb.as<double>(),
+                                       c->vb.as<double>(), b.tma_grid, st, &c->ym_cache));
     else if (use_t)
       SKS_CK(c, launch_step_stencil_tma(a, c->W.as<double>(), b.ncol, c->xb.as<double>(), c->fb.as<double>(),
                                         c->vb.as<double>(), b.tma_grid, st, &c->tma_cache));

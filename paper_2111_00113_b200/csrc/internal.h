@@ -34,6 +34,13 @@ cudaError_t launch_step_stencil_zm(const StepArgs& a, const double* W, int64_t n
                                    const double* fb, const double* vb, int grid, cudaStream_t st, void** cache);
 void stencil_zm_free(void* cache);
 
+// stencil_ym.cu (2D, even m: TMA-fed y-march kernel)
+bool stencil_ym_supported(int dim, int64_t m, int k);
+void stencil_ym_tiling(int64_t m, int64_t nz, int num_sms, StepArgs* a, int* grid);
+cudaError_t launch_step_stencil_ym(const StepArgs& a, const double* W, int64_t ncol, const double* xb,
+                                   const double* fb, const double* vb, int grid, cudaStream_t st, void** cache);
+void stencil_ym_free(void* cache);
+
 // sketch.cu
 int sketch_grid(int num_sms, int64_t nrows);
 size_t sketch_part_doubles(int grid, int J, int s);
