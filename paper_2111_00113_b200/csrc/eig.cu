@@ -14,6 +14,7 @@
 //    (Hessenberg LU with partial pivoting), one CTA per eigenvalue, giving y_i.
 //  * sketched residual estimate  ||D y - theta C y|| / ||C y||  (Eq. srr-resid-est).
 #include <climits>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.h"
@@ -1300,6 +1301,173 @@ __global__ void __launch_bounds__(256) inverse_iteration_kernel(const double* __
   }
 }
 
+// ---- inverse iteration, pipelined: the same algorithm as inverse_iteration_kernel (Hessenberg LU of
+// (Mhat - theta I) with partial pivoting between rows k and k+1, then `iters` solves), organised so that
+// no step waits on an L2 round trip: the original rows of Mhat (strided in the column-major matrix) and
+// the columns of U for the back substitution are staged into shared-memory rings by cp.async several
+// steps ahead.  U is kept column-major in the work buffer.  One CTA per selected eigenvalue.
+constexpr int II_T = 256;
+constexpr int II_RING = 6;
+__device__ __forceinline__ void ii_cp8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void ii_cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void ii_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void ii_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__global__ void __launch_bounds__(II_T) inverse_iteration_pipe_kernel(const double* __restrict__ Mh, int d,
+                                                                      const double* __restrict__ th_re,
+                                                                      const double* __restrict__ th_im,
+                                                                      const int* __restrict__ nsel,
+                                                                      double* __restrict__ work,
+                                                                      double* __restrict__ yr,
+                                                                      double* __restrict__ yi, int iters) {
+  const int v = blockIdx.x;
+  if (v >= *nsel) return;
+  extern __shared__ __align__(16) double smi[];
+  cplx* cur = reinterpret_cast<cplx*>(smi);       // d: the row carried through the elimination
+  cplx* L = cur + d;                              // d: multipliers
+  cplx* b = L + d;                                // d: solve vector
+  cplx* cring = b + d;                            // II_RING x d: columns of U (back substitution)
+  double* rring = reinterpret_cast<double*>(cring + (size_t)II_RING * d);  // II_RING x d: rows of Mhat
+  int* perm = reinterpret_cast<int*>(rring + (size_t)II_RING * d);          // d
+  __shared__ double red[32];
+  __shared__ cplx piv_l, piv_p;
+  __shared__ int swp;
+  __shared__ double runmax;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  cplx* U = reinterpret_cast<cplx*>(work) + (int64_t)v * d * d;  // column-major: U[l + i d], l <= i
+  const cplx th = {th_re[v], th_im[v]};
+  auto issue_row = [&](int r) {  // Mhat row r, columns r-1 .. d-1 (Hessenberg), into ring slot r % RING
+    if (r < d) {
+      double* dst = rring + (size_t)(r % II_RING) * d;
+      for (int j = max(r - 1, 0) + tid; j < d; j += nt) ii_cp8(dst + j, Mh + r + (int64_t)j * d);
+    }
+    ii_commit();
+  };
+  // ring of RING slots, prefetch distance RING-1: rows 1..RING-1 now; iteration k issues row k+RING-1
+  // into the slot of row k-1 (consumed in iteration k-1, free after this iteration's first barrier)
+  for (int r = 1; r <= II_RING - 1; ++r) issue_row(r);
+  for (int j = tid; j < d; j += nt) cur[j] = {Mh[(int64_t)j * d] - (j == 0 ? th.r : 0.0), j == 0 ? -th.i : 0.0};
+  if (tid == 0) runmax = 0.0;
+  // ---- LU: rows k (cur) and k+1 (Mhat row k+1 - theta e_{k+1}) compete for the pivot
+  for (int k = 0; k < d - 1; ++k) {
+    ii_wait<II_RING - 2>();  // row k+1 (group k+1 of RING-1+k) has landed (this thread's copies)
+    __syncthreads();         // ... and everybody's; everybody is past iteration k-1
+    issue_row(k + II_RING - 1);
+    const double* nx = rring + (size_t)((k + 1) % II_RING) * d;
+    if (tid == 0) {
+      const cplx a = cur[k];
+      const cplx bb = {nx[k], 0.0};  // column k of row k+1 (subdiagonal; theta sits on column k+1)
+      runmax = fmax(runmax, fmax(cabs1(a), cabs1(bb)));
+      const int sw = cabs1(bb) > cabs1(a) ? 1 : 0;
+      cplx p = sw ? bb : a;
+      const cplx o = sw ? a : bb;
+      if (cabs1(p) == 0.0) p = {1e-15 * runmax + 1e-300, 0.0};
+      swp = sw;
+      piv_p = p;
+      piv_l = cdiv(o, p);
+      perm[k] = sw;
+      L[k] = piv_l;
+    }
+    __syncthreads();
+    const int sw = swp;
+    const cplx lk = piv_l, pk = piv_p;
+    for (int j = k + tid; j < d; j += nt) {
+      const cplx cj = cur[j];
+      const cplx nj = {nx[j] - (j == k + 1 ? th.r : 0.0), j == k + 1 ? -th.i : 0.0};
+      const cplx pj = (j == k) ? pk : (sw ? nj : cj);
+      const cplx oj = sw ? cj : nj;
+      U[k + (int64_t)j * d] = pj;
+      const cplx pr = cmul(lk, pj);
+      cur[j] = {oj.r - pr.r, oj.i - pr.i};
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    cplx p = cur[d - 1];
+    if (cabs1(p) == 0.0) p = {1e-15 * runmax + 1e-300, 0.0};
+    U[(d - 1) + (int64_t)(d - 1) * d] = p;
+  }
+  ii_wait<0>();
+  __threadfence_block();
+  __syncthreads();
+  for (int i = tid; i < d; i += nt) b[i] = {1.0 / (1.0 + 0.37 * (i % 11)), 0.0};
+  __syncthreads();
+  auto issue_col = [&](int c) {  // column c of U (rows 0..c) into ring slot c % RING
+    if (c >= 0) {
+      cplx* dst = cring + (size_t)(c % II_RING) * d;
+      for (int l = tid; l <= c; l += nt) ii_cp16(dst + l, U + l + (int64_t)c * d);
+    }
+    ii_commit();
+  };
+  for (int it = 0; it < iters; ++it) {
+    for (int c = d - 1; c >= d - II_RING + 1; --c) issue_col(c);  // prefetch distance RING-1
+    if (tid == 0) {  // forward: apply the row swaps and L
+      for (int k = 0; k < d - 1; ++k) {
+        if (perm[k]) {
+          const cplx t = b[k];
+          b[k] = b[k + 1];
+          b[k + 1] = t;
+        }
+        const cplx pr = cmul(L[k], b[k]);
+        b[k + 1].r -= pr.r;
+        b[k + 1].i -= pr.i;
+      }
+    }
+    // backward, column-oriented: y_i = b_i / U_ii, b_l -= U_li y_i (l < i)
+    for (int i = d - 1; i >= 0; --i) {
+      ii_wait<II_RING - 2>();  // column i landed (this thread's copies)
+      __syncthreads();         // everybody's; b_i final; column i+1's slot is free
+      issue_col(i - II_RING + 1);
+      const cplx* col = cring + (size_t)(i % II_RING) * d;
+      const cplx yi_ = cdiv(b[i], col[i]);
+      __syncthreads();  // everybody has read b_i
+      for (int l = tid; l < i; l += nt) {
+        const cplx pr = cmul(col[l], yi_);
+        b[l].r -= pr.r;
+        b[l].i -= pr.i;
+      }
+      if (tid == 0) b[i] = yi_;
+    }
+    ii_wait<0>();
+    __syncthreads();
+    double loc = 0.0;
+    for (int i = tid; i < d; i += nt) loc += b[i].r * b[i].r + b[i].i * b[i].i;
+    const double nr = sqrt(block_sum(loc, red));
+    for (int i = tid; i < d; i += nt) {
+      b[i].r /= nr;
+      b[i].i /= nr;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {  // canonical phase: largest-modulus entry real positive
+    int im = 0;
+    double bm = -1.0;
+    for (int i = 0; i < d; ++i) {
+      const double mg = b[i].r * b[i].r + b[i].i * b[i].i;
+      if (mg > bm) {
+        bm = mg;
+        im = i;
+      }
+    }
+    const double mg = sqrt(bm);
+    piv_l = {b[im].r / mg, -b[im].i / mg};
+  }
+  __syncthreads();
+  const cplx ph = piv_l;
+  for (int i = tid; i < d; i += nt) {
+    const cplx z = cmul(b[i], ph);
+    yr[i + (int64_t)v * d] = z.r;
+    yi[i + (int64_t)v * d] = (th.i == 0.0) ? 0.0 : z.i;
+  }
+}
+
 // r_est[v] = ||D y - theta C y|| / ||C y||, D = SAB (s x d, col-major), C = SB
 __global__ void srr_rest_kernel(const double* __restrict__ D, const double* __restrict__ C, int s, int d,
                                 const double* __restrict__ yr, const double* __restrict__ yi,
@@ -1352,6 +1520,20 @@ size_t inverse_iteration_work_doubles(int d, int nmax) {
 cudaError_t launch_inverse_iteration(const double* Mh, int d, const double* th_re, const double* th_im,
                                      const int* nsel, int nmax, double* work, double* yr, double* yi, int iters,
                                      double anorm, cudaStream_t st) {
+  if (!getenv("SKS_II_OLD")) {  // pipelined version (default); SKS_II_OLD=1 for A/B
+    const size_t smem = sizeof(double) * ((size_t)d * 2 * 3 + (size_t)II_RING * d * 2 + (size_t)II_RING * d) +
+                        sizeof(int) * (size_t)d + 16;
+    static size_t set = 0;
+    if (smem > 48 * 1024 && set < smem) {
+      if (cudaFuncSetAttribute(inverse_iteration_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem) != cudaSuccess)
+        return cudaGetLastError();
+      set = smem;
+    }
+    (void)anorm;
+    inverse_iteration_pipe_kernel<<<nmax, II_T, smem, st>>>(Mh, d, th_re, th_im, nsel, work, yr, yi, iters);
+    return cudaGetLastError();
+  }
   inverse_iteration_kernel<<<nmax, 256, sizeof(double) * 2 * d, st>>>(Mh, d, th_re, th_im, nsel, work, yr, yi,
                                                                        iters, anorm);
   return cudaGetLastError();
