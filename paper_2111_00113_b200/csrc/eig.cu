@@ -114,6 +114,12 @@ __device__ __forceinline__ HqRefl hq_refl(double p, double q, double r) {
 
 // branch-free variant for the chase (the matrix is pre-scaled to norm ~1, so p^2+q^2+r^2 cannot
 // overflow; a sub-normal-range bulge is treated as zero, i.e. P = I)
+__device__ __forceinline__ HqRefl hq_identity() {  // P = I (no arithmetic)
+  HqRefl R;
+  R.xx = R.yy = R.zz = R.qq = R.rr = R.s = 0.0;
+  R.valid = false;
+  return R;
+}
 __device__ __forceinline__ HqRefl hq_refl_fast(double p, double q, double r) {
   HqRefl R;
   const double t = fma(p, p, fma(q, q, r * r));
@@ -147,7 +153,10 @@ constexpr int HQ_LD = HQ_R + 1;  // odd pitch: row- and column-wise smem access 
 constexpr int HQ_THREADS = HQ_NB == 2 ? 256 : 384;  // (HQ_NB=3: warps 0, 1 chase)  // HQ_NB=2 needs the larger register budget
 constexpr int HQ_QSZ = HQ_LD * HQ_R;
 #ifndef HQ_TWO_MIN
-#define HQ_TWO_MIN 12  // minimum nn - m for the second bulge
+#define HQ_TWO_MIN 12  // minimum nn - m per additional bulge
+#endif
+#ifndef HQ_NW
+#define HQ_NW 2  // HQ_NB=3: chase warps (bulges per sweep)
 #endif
 
 // ---- two-bulge chase (HQ_NB == 2): bulges A (leading) and B (trailing by 4 positions) carry the same
@@ -385,6 +394,177 @@ __device__ __forceinline__ void hq_chase2w(double* Hw, double* Qs, double* dmy, 
   }
 }
 
+// ---- NW bulges on NW warps (HQ_NB == 3; HQ_NW = 2 is the two-bulge chase above, generalised): warp w
+// chases bulge w at k_w = kA - 4w with the sweep's shift pair.  Per round, warp w (a) skips the columns
+// k_{w-1}..k_{w-1}+2 of the bulge ahead in its row transformation, (b) forms the block rows
+// k_{w+1}..k_{w+1}+2 x its columns (P_{w+1} from the left with the reflector warp w+1 published one
+// round ahead, then its own P_w), (c) reloads its column k_w+3 and row k_w+3 every round when a bulge
+// runs ahead (warp 0 forwards them in registers).  Bulge w enters at row m once bulge w-1 has moved
+// 4 rows; blocks too short for it (nn - m < HQ_TWO_MIN w) run fewer bulges.
+__device__ __forceinline__ int hq_nbulges(int nn, int m) {
+  int nb = 1;
+  while (nb < HQ_NW && nn - m >= HQ_TWO_MIN * nb) ++nb;
+  return nb;
+}
+
+__device__ __forceinline__ void hq_barw(int nw) { asm volatile("bar.sync 1, %0;" ::"r"(32 * nw) : "memory"); }
+
+__device__ __forceinline__ void hq_chasew(double* Hw, double* Qs, double* dmy, double* xchg, int lo, int r1, int a0,
+                                          int a1, int m, int nn, int l, double sp, double sq, double sr, double sx,
+                                          double sy, double sw, int lane, int w) {
+  auto H_ = [&](int gi, int gj) -> double {
+    return (gi >= lo && gj >= lo - 1 && gi <= r1 && gj <= r1) ? Hw[(gi - lo) + (gj - lo + 1) * HQ_LD] : 0.0;
+  };
+  auto load_state = [&](int k, HqBulge& S) {
+    S.B00 = H_(k, k); S.B01 = H_(k, k + 1); S.B02 = H_(k, k + 2);
+    S.B10 = H_(k + 1, k); S.B11 = H_(k + 1, k + 1); S.B12 = H_(k + 1, k + 2);
+    S.B20 = H_(k + 2, k); S.B21 = H_(k + 2, k + 1); S.B22 = H_(k + 2, k + 2);
+    S.C0 = H_(k, k + 3); S.C1 = H_(k + 1, k + 3); S.C2 = H_(k + 2, k + 3);
+    S.h3 = H_(k + 3, k + 2); S.d33 = H_(k + 3, k + 3);
+  };
+  auto put = [&](const HqRefl& R, int slot) {  // warp w's reflector, for warp w-1
+    if (lane == 0) {
+      double* x = xchg + 16 * w + 8 * slot;
+      x[0] = R.xx; x[1] = R.yy; x[2] = R.zz; x[3] = R.qq; x[4] = R.rr; x[5] = R.s; x[6] = R.valid ? 1.0 : 0.0;
+    }
+  };
+  auto get = [&](int ww, int slot) {
+    const double* x = xchg + 16 * ww + 8 * slot;
+    HqRefl R;
+    R.xx = x[0]; R.yy = x[1]; R.zz = x[2]; R.qq = x[3]; R.rr = x[4]; R.s = x[5]; R.valid = x[6] != 0.0;
+    return R;
+  };
+  const int nb = hq_nbulges(nn, m);
+  const int NWc = HQ_NW;                 // warps in the barrier (all chase warps take part)
+  const bool en = w < nb;                // this warp's bulge runs in this sweep
+  HqBulge S = {};
+  HqRefl R = hq_identity();
+  {  // window start
+    const int k = a0 - 4 * w;
+    if (en && k >= m && k <= nn - 1) {
+      double p, q, r;
+      if (k == m) {
+        p = sp; q = sq; r = sr;  // (only bulge 0 can start a window at m)
+      } else {
+        p = H_(k, k - 1); q = H_(k + 1, k - 1); r = H_(k + 2, k - 1);
+      }
+      load_state(k, S);
+      R = hq_refl_fast(p, q, r);
+    }
+    if (w > 0) put(R, a0 & 1);
+  }
+  hq_barw(NWc);
+  for (int kA = a0; kA < a1; ++kA) {
+    const int k = kA - 4 * w;
+    const bool act = en && k >= m && k <= nn - 1;
+    HqRefl Rn = hq_identity();
+    if (act) {
+      auto cok_pre = [&](int r) { return r <= min(nn, k + 3); };
+      const int ir = lo + lane;
+      // rows of a bulge behind (u = w + jb, rows k_u..k_u+2, k_u = k - 4 jb) x own columns: P_u from the
+      // left (its reflector, published one round ahead) before this warp's P_w
+      const int off = k - ir, jb = (off + 3) >> 2, tb = 4 * jb - off;
+      const bool spec = cok_pre(ir) && off >= 2 && tb <= 2 && w + jb < nb;
+      const HqRefl RB = spec ? get(w + jb, kA & 1) : hq_identity();
+      const double v0 = RB.xx, v1 = RB.yy, v2 = RB.zz, x1 = RB.qq, x2 = RB.rr;
+      const int kb_l = k - 4 * jb;  // this lane's behind-bulge row origin
+      if (w > 0) {  // column k+3 and row k+3 change under the bulge ahead: reload
+        S.C0 = H_(k, k + 3); S.C1 = H_(k + 1, k + 3); S.C2 = H_(k + 2, k + 3);
+        S.h3 = H_(k + 3, k + 2); S.d33 = H_(k + 3, k + 3);
+      }
+      const double E0 = H_(k, k + 4), E1 = H_(k + 1, k + 4), E2 = H_(k + 2, k + 4), E3 = H_(k + 3, k + 4);
+      const double h4 = H_(k + 4, k + 3), d44 = H_(k + 4, k + 4);
+      double Z[3][3];  // this lane's behind-bulge rows x own columns
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) Z[i][j] = spec ? H_(kb_l + i, k + j) : 0.0;
+      // row transformation column k+3+lane; the columns of a running bulge ahead (v = w - ja,
+      // cols k_v..k_v+2, k_v = k + 4 ja <= nn-1) are formed by that bulge's warp
+      const int jc = k + 3 + lane, dc = jc - k, ja = dc >> 2, ta = dc & 3;
+      const bool skip = ja >= 1 && ta <= 2 && w - ja >= 0 && k + 4 * ja <= nn - 1;
+      const bool rok = jc <= r1 && !skip;
+      double* colp = rok ? Hw + (jc - lo + 1) * HQ_LD + (k - lo) : dmy + 16 * lane;
+      const double aa0 = colp[0], aa1 = colp[1], aa2 = colp[2];
+      const bool cok = cok_pre(ir);
+      const bool ld = cok && ir < k && !spec;
+      double* rowp = Hw + lane + (k - lo + 1) * HQ_LD;
+      const double b0 = ld ? rowp[0] : 0.0, b1 = ld ? rowp[HQ_LD] : 0.0, b2 = ld ? rowp[2 * HQ_LD] : 0.0;
+      double* qp = Qs + lane + (k - lo) * HQ_LD;
+      const double g0 = qp[0], g1 = qp[HQ_LD], g2 = qp[2 * HQ_LD];
+      double* hk = (lane == 0 && R.valid) ? Hw + (k - lo) + (k - lo) * HQ_LD : dmy + 16 * lane + 6;
+      const double hkv = *hk;
+      const double u0 = R.xx, u1 = R.yy, u2 = R.zz, w1 = R.qq, w2 = R.rr;
+      const double pp0 = fma(w2, S.B20, fma(w1, S.B10, S.B00)), pp1 = fma(w2, S.B21, fma(w1, S.B11, S.B01)),
+                   pp2 = fma(w2, S.B22, fma(w1, S.B12, S.B02)), ppc = fma(w2, S.C2, fma(w1, S.C1, S.C0)),
+                   ppe = fma(w2, E2, fma(w1, E1, E0));
+      const double R10 = fma(-u1, pp0, S.B10), R11 = fma(-u1, pp1, S.B11), R12 = fma(-u1, pp2, S.B12),
+                   R1c = fma(-u1, ppc, S.C1), R1e = fma(-u1, ppe, E1);
+      const double R20 = fma(-u2, pp0, S.B20), R21 = fma(-u2, pp1, S.B21), R22 = fma(-u2, pp2, S.B22),
+                   R2c = fma(-u2, ppc, S.C2), R2e = fma(-u2, ppe, E2);
+      const double t1 = fma(u2, R12, fma(u1, R11, u0 * R10));
+      const double t2 = fma(u2, R22, fma(u1, R21, u0 * R20));
+      const double t3 = u2 * S.h3;
+      const double N10 = R10 - t1, N11 = fma(-t1, w1, R11), N12 = fma(-t1, w2, R12);
+      const double N20 = R20 - t2, N21 = fma(-t2, w1, R21), N22 = fma(-t2, w2, R22);
+      const double N30 = -t3, N31 = -t3 * w1, N32 = fma(-t3, w2, S.h3);
+      const bool nx = k + 1 <= nn - 1;
+      Rn = hq_refl_fast(nx ? N10 : 0.0, nx ? N20 : 0.0, nx ? N30 : 0.0);
+      *hk = (k == m) ? ((l != m) ? -hkv : hkv) : -R.s;
+      {
+        const double pr = fma(w2, aa2, fma(w1, aa1, aa0));
+        colp[0] = fma(-u0, pr, aa0);
+        colp[1] = fma(-u1, pr, aa1);
+        *((rok && k + 2 <= nn) ? colp + 2 : dmy + 16 * lane + 2) = fma(-u2, pr, aa2);
+      }
+      {
+        const int d = ir - k, dB = tb;
+        const double X0 = fma(-u0, pp0, S.B00), X1 = fma(-u0, pp1, S.B01), X2 = fma(-u0, pp2, S.B02);
+        const double zz0 = fma(x2, Z[2][0], fma(x1, Z[1][0], Z[0][0]));
+        const double zz1 = fma(x2, Z[2][1], fma(x1, Z[1][1], Z[0][1]));
+        const double zz2 = fma(x2, Z[2][2], fma(x1, Z[1][2], Z[0][2]));
+        const double vb = dB == 0 ? v0 : (dB == 1 ? v1 : v2);
+        const double zr0 = fma(-vb, zz0, dB == 0 ? Z[0][0] : (dB == 1 ? Z[1][0] : Z[2][0]));
+        const double zr1 = fma(-vb, zz1, dB == 0 ? Z[0][1] : (dB == 1 ? Z[1][1] : Z[2][1]));
+        const double zr2 = fma(-vb, zz2, dB == 0 ? Z[0][2] : (dB == 1 ? Z[1][2] : Z[2][2]));
+        const bool own = ir >= k;
+        const double c0 = spec ? zr0 : (own ? (d == 0 ? X0 : (d == 1 ? R10 : (d == 2 ? R20 : 0.0))) : b0);
+        const double c1 = spec ? zr1 : (own ? (d == 0 ? X1 : (d == 1 ? R11 : (d == 2 ? R21 : 0.0))) : b1);
+        const double c2 = spec ? zr2 : (own ? (d == 0 ? X2 : (d == 1 ? R12 : (d == 2 ? R22 : S.h3))) : b2);
+        const double tt = fma(u2, c2, fma(u1, c1, u0 * c0));
+        double* sc = dmy + 16 * lane;
+        *(cok ? rowp : sc) = c0 - tt;
+        *(cok && k + 1 <= nn ? rowp + HQ_LD : sc + 1) = fma(-tt, w1, c1);
+        *(cok && k + 2 <= nn ? rowp + 2 * HQ_LD : sc + 2) = fma(-tt, w2, c2);
+      }
+      {
+        const double tq = fma(u2, g2, fma(u1, g1, u0 * g0));
+        qp[0] = g0 - tq;
+        qp[HQ_LD] = fma(-tq, w1, g1);
+        qp[2 * HQ_LD] = fma(-tq, w2, g2);
+      }
+      S.B00 = N11; S.B01 = N12; S.B02 = R1c;
+      S.B10 = N21; S.B11 = N22; S.B12 = R2c;
+      S.B20 = N31; S.B21 = N32; S.B22 = S.d33;
+      S.C0 = R1e; S.C1 = R2e; S.C2 = E3;
+      S.h3 = h4; S.d33 = d44;
+    }
+    if (en && w > 0 && k + 1 == m) {  // this bulge enters next round, from the current matrix
+      // (rows/cols m..m+2 are final: the bulge ahead is at m+3 and only touches indices >= m+3)
+      const double z = H_(m, m), rr = sx - z, ss = sy - z;
+      const double p = (rr * ss - sw) / H_(m + 1, m) + H_(m, m + 1);
+      const double q = H_(m + 1, m + 1) - z - rr - ss;
+      const double r = H_(m + 2, m + 1);
+      load_state(m, S);
+      S.B20 = 0.0;  // H[m+2][m]: zeroed by the bulge ahead (shared memory holds its stale entry)
+      Rn = hq_refl_fast(p, q, r);
+    }
+    R = Rn;
+    if (w > 0) put(R, (kA + 1) & 1);
+    hq_barw(NWc);
+  }
+}
+
 __device__ __forceinline__ void hq_chase2(double* Hw, double* Qs, double* dmy, int lo, int r1, int a0, int a1, int m,
                                           int nn, int l, double sp, double sq, double sr, double sx, double sy,
                                           double sw, int lane) {
@@ -594,7 +774,7 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
                                                          int* __restrict__ info) {
   __shared__ double Hw[HQ_LD * (HQ_R + 1) + 16 * 32];  // window + per-lane scratch
   __shared__ double Qsh[2 * HQ_QSZ];  // accumulated Q of the current / previous window
-  __shared__ double hq_x[16];         // HQ_NB=3: bulge B's reflector for warp 0, by round parity
+  __shared__ double hq_x[16 * 8];     // HQ_NB=3: each chase warp's next reflector, by round parity
   __shared__ double red[32];
   __shared__ int ired[32];
   __shared__ double sp, sq, sr, sx, sy, sw, st;
@@ -793,8 +973,13 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
         int me = warp - w0;
         if (w0 < 0) {
 #if HQ_NB == 3
-          if ((warp & 3) < 2) return;  // warps 0, 1 chase; 4, 5, 8, 9 share their schedulers
-          me = (warp >> 2) * 2 + (warp & 3) - 2;
+          if (HQ_NW <= 2) {
+            if ((warp & 3) < 2) return;  // warps 0, 1 chase; 4, 5, 8, 9 share their schedulers
+            me = (warp >> 2) * 2 + (warp & 3) - 2;
+          } else {  // every scheduler has a chase warp: all other warps work
+            if (warp < HQ_NW) return;
+            me = warp - HQ_NW;
+          }
 #else
           if ((warp & 3) == 0) return;
           me = warp - (warp >> 2) - 1;
@@ -867,8 +1052,13 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
       // the deferred off-window update of window w-1 (its columns beyond window w and its rows
       // above); the part of w's update that window w+1 reads (its columns) is done before w+1 loads.
       int k0 = m;  // window rows/cols [k0, r1]
+#if HQ_NB == 3
+      const int hspan = 4 * (hq_nbulges(nn, m) - 1);  // rows between the first and the last bulge
+#else
+      const int hspan = 4;
+#endif
 #if HQ_NB >= 2
-      int a0 = m, a1 = min(k0 + HQ_R - 3, nn + 4);  // rounds: bulge A at kA in [a0, a1), B at kA - 4
+      int a0 = m, a1 = min(k0 + HQ_R - 3, nn + hspan);  // rounds: bulge 0 at kA in [a0, a1), bulge w at kA - 4w
       int k1 = a1;
 #else
       int k1 = min(k0 + HQ_W, nn);
@@ -881,9 +1071,15 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
         double* Qs = Qsh + cur * HQ_QSZ;
         long long tc0 = clock64();
 #if HQ_NB == 3
-        if (warp < 2) {
-          hq_chase2w(Hw, Qs, Hw + HQ_LD * (HQ_R + 1), hq_x, k0, r1, a0, a1, m, nn, l, sp, sq, sr, sx, sy, sw, lane,
-                     warp);
+        if (warp < HQ_NW) {
+          // two bulges: the role-specialised chase; more: the general one (correct, but every warp then
+          // issues the union of both roles' work: C5 hqr 33 ms at 4 bulges vs 27.6 ms here)
+          if (HQ_NW == 2)
+            hq_chase2w(Hw, Qs, Hw + HQ_LD * (HQ_R + 1), hq_x, k0, r1, a0, a1, m, nn, l, sp, sq, sr, sx, sy, sw, lane,
+                       warp);
+          else
+            hq_chasew(Hw, Qs, Hw + HQ_LD * (HQ_R + 1), hq_x, k0, r1, a0, a1, m, nn, l, sp, sq, sr, sx, sy, sw, lane,
+                      warp);
         }
 #elif HQ_NB == 2
         if (warp == 0) {
@@ -1003,7 +1199,7 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
 #endif
         else if (pk0 >= 0) {
           far_update(Qsh + (cur ^ 1) * HQ_QSZ, pk0, pr1, r1, nn, l, pk0, -1,
-                     HQ_NB == 3 ? nw / 2 : nw - (nw >> 2));
+                     HQ_NB == 3 ? (HQ_NW <= 2 ? nw / 2 : nw - HQ_NW) : nw - (nw >> 2));
         }
         __syncthreads();
         long long tc1 = clock64();
@@ -1014,8 +1210,8 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
           if (i <= r1 - k0 && gj >= 0 && gj <= r1) HA(k0 + i, gj) = Hw[i + c * HQ_LD];
         }
 #if HQ_NB >= 2
-        const int k0n = a1 - 4;  // the next window starts at bulge B's row
-        if (a1 >= nn + 4) {      // last window: its whole off-window update now
+        const int k0n = a1 - hspan;  // the next window starts at the last bulge's row
+        if (a1 >= nn + hspan) {      // last window: its whole off-window update now
 #else
         const int k0n = k1;
         if (k0n > nn - 1) {  // last window: its whole off-window update now
@@ -1033,7 +1229,7 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
         k0 = k0n;
 #if HQ_NB >= 2
         a0 = a1;
-        a1 = min(k0 + HQ_R - 3, nn + 4);
+        a1 = min(k0 + HQ_R - 3, nn + hspan);
         k1 = a1;
 #else
         k1 = min(k0 + HQ_W, nn);
