@@ -23,6 +23,7 @@ from .operators import (  # noqa: F401
 )
 from .sketch import (  # noqa: F401
     sketch_key, sketch_table, sketch_matrix, sketch_apply, fmix64,
+    srft_key, srft_signs, srft_rows, srft_apply, SRFT,
 )
 from .krylov import partial_arnoldi, full_arnoldi, chebyshev_basis  # noqa: F401
 from .sgmres import (  # noqa: F401

@@ -18,7 +18,7 @@ import numpy as np
 from scipy.linalg import solve_triangular
 
 from .krylov import partial_arnoldi, chebyshev_basis
-from .sketch import sketch_matrix
+from .sketch import sketch_matrix, SRFT
 
 WARN_COND = 1
 WARN_BREAKDOWN = 2
@@ -49,7 +49,8 @@ def gmres_exact_ls(M, r0):
 
 
 def sgmres_cycle(matvec, f, x, d, k, s, zeta, seed, cycle, tol=1e-8,
-                 early_exit_factor=0.25, cond_tol=1e14, fnorm=None, S=None, cheb=None, adaptive=False):
+                 early_exit_factor=0.25, cond_tol=1e14, fnorm=None, S=None, cheb=None, adaptive=False,
+                 sketch="sparse"):
     """One cycle; cheb = (c, dx, dy) selects the Chebyshev basis of Eq. Chebrecurse
      instead of k-truncated Arnoldi.
     adaptive: adaptive restarting (Sec. adaptive-restart): "When first
@@ -60,8 +61,8 @@ def sgmres_cycle(matvec, f, x, d, k, s, zeta, seed, cycle, tol=1e-8,
     n = f.size
     if fnorm is None:
         fnorm = np.linalg.norm(f)
-    if S is None:
-        S = sketch_matrix(n, s, zeta, seed, cycle)
+    if S is None:  # sketch: "sparse" (Eq. sparse-map) or "srft" (Eq. SRFT with DCT2, reading O32)
+        S = sketch_matrix(n, s, zeta, seed, cycle) if sketch == "sparse" else SRFT(n, s, seed, cycle)
     r = f - matvec(x)
     if np.linalg.norm(r) == 0.0:
         return dict(x=x.copy(), j=0, r_est=np.zeros(0), yhat=np.zeros(0),
@@ -97,7 +98,8 @@ def sgmres_cycle(matvec, f, x, d, k, s, zeta, seed, cycle, tol=1e-8,
 
 
 def sgmres_solve(matvec, f, d, k, s, zeta, seed, tol=1e-8, max_cycles=50,
-                 early_exit_factor=0.25, cond_tol=1e14, x0=None, keep_last=False, cheb=None, adaptive=False):
+                 early_exit_factor=0.25, cond_tol=1e14, x0=None, keep_last=False, cheb=None, adaptive=False,
+                 sketch="sparse"):
     """Restarted sGMRES.  Returns dict(x, cycles, columns, rel_res_true, r_est,
     hist_est (r_est_j/||f|| per column, concatenated), hist_true (per cycle),
     cond_T, flags)."""
@@ -110,7 +112,7 @@ def sgmres_solve(matvec, f, d, k, s, zeta, seed, tol=1e-8, max_cycles=50,
     cycles = 0
     for c in range(max_cycles):
         out = sgmres_cycle(matvec, f, x, d, k, s, zeta, seed, c, tol,
-                           early_exit_factor, cond_tol, fnorm, cheb=cheb, adaptive=adaptive)
+                           early_exit_factor, cond_tol, fnorm, cheb=cheb, adaptive=adaptive, sketch=sketch)
         cycles += 1
         x = out["x"]
         columns += out["j"]

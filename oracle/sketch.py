@@ -122,3 +122,74 @@ def sketch_apply(M, s: int, zeta: int, seed: int, cycle: int = 0, row_begin: int
         n = row_begin + nl
     S = sketch_matrix(n, s, zeta, seed, cycle, row_begin, row_begin + nl)
     return S @ M
+
+
+# ---------------------------------------------------------------- SRFT
+# Eq. (SRFT): S = sqrt(n/s) D F E with E a random diagonal of unit-modulus entries, F
+# the unitary DFT and D a random projector onto s coordinates; the paper's experiments use
+# F = DCT2, a real orthonormal transform.  Readings (O32): real
+# Rademacher E (as O2), F = orthonormal DCT-II, the s coordinates drawn by Floyd's algorithm
+# (uniform s-subset of {0..n-1}) in draw order = sketch row order, a fresh S per cycle.
+# Hash specification (the CUDA driver implements the same integer spec independently):
+#   key(seed, c) = fmix64( fmix64(seed ^ 0x5352465444435432) + GAMMA*(c+1) )
+#   sign(r)      = -1 if bit 0 of fmix64(key + GAMMA*(2r+1)) else +1        r = 0..n-1
+#   Floyd, t = 0..s-1:  u_t = low 32 bits of fmix64(key + GAMMA*(2t+2));  J = n - s + t;
+#                       v = (u_t * (J+1)) >> 32;  q_t = J if v in {q_0..q_{t-1}} else v
+#   (S x)_t = sqrt(n/s) * DCT2_ortho(E x)[q_t]
+_SRFT_DOMAIN = np.uint64(0x5352465444435432)
+
+
+def srft_key(seed: int, cycle: int) -> np.uint64:
+    with np.errstate(over="ignore"):
+        k0 = fmix64(np.array([np.uint64(seed) ^ _SRFT_DOMAIN], dtype=np.uint64))
+        k = fmix64(k0 + _GAMMA * np.uint64(cycle + 1))
+    return np.uint64(k[0])
+
+
+def srft_signs(n: int, seed: int, cycle: int = 0):
+    key = srft_key(seed, cycle)
+    r = np.arange(n, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        w = fmix64(key + _GAMMA * (np.uint64(2) * r + np.uint64(1)))
+    return np.where((w & np.uint64(1)).astype(bool), -1.0, 1.0)
+
+
+def srft_rows(n: int, s: int, seed: int, cycle: int = 0):
+    """The s sampled DCT coordinates, in sketch-row order (Floyd, plain loop)."""
+    if not (1 <= s <= n < 2 ** 32):
+        raise ValueError("need 1 <= s <= n < 2^32")
+    key = srft_key(seed, cycle)
+    t = np.arange(s, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        u = fmix64(key + _GAMMA * (np.uint64(2) * t + np.uint64(2))) & _MASK32
+    q = []
+    taken = set()
+    for i in range(s):
+        J = n - s + i
+        v = int((int(u[i]) * (J + 1)) >> 32)
+        if v in taken:
+            v = J
+        taken.add(v)
+        q.append(v)
+    return np.array(q, dtype=np.int64)
+
+
+def srft_apply(M, s: int, seed: int, cycle: int = 0):
+    """S M for the SRFT of Eq. (SRFT) with F = orthonormal DCT-II."""
+    from scipy.fft import dct
+    M = np.asarray(M, dtype=np.float64)
+    n = M.shape[0]
+    E = srft_signs(n, seed, cycle)
+    Y = dct(E.reshape((n,) + (1,) * (M.ndim - 1)) * M, type=2, norm="ortho", axis=0)
+    return np.sqrt(n / s) * Y[srft_rows(n, s, seed, cycle)]
+
+
+class SRFT:
+    """S as an operator (S @ x, S @ M) for the sGMRES / sRR oracles."""
+
+    def __init__(self, n: int, s: int, seed: int, cycle: int = 0):
+        self.n, self.s, self.seed, self.cycle = n, s, seed, cycle
+        self.shape = (s, n)
+
+    def __matmul__(self, M):
+        return srft_apply(M, self.s, self.seed, self.cycle)

@@ -16,7 +16,7 @@ from scipy.linalg import solve_triangular
 
 from .krylov import partial_arnoldi
 from .sgmres import thin_qr
-from .sketch import sketch_matrix
+from .sketch import sketch_matrix, SRFT
 
 
 def select_ritz(theta, nev):
@@ -55,11 +55,12 @@ def srr_from_basis(matvec, B, M, S, nev):
                 theta_all=theta)
 
 
-def srr_eigs(matvec, v0, d, k, s, zeta, seed, nev, cycle=0):
+def srr_eigs(matvec, v0, d, k, s, zeta, seed, nev, cycle=0, sketch="sparse"):
+    """sketch: "sparse" (Eq. sparse-map, O1-O7) or "srft" (Eq. SRFT with DCT2, O32)."""
     v0 = np.asarray(v0, dtype=np.float64)
     n = v0.size
     basis = partial_arnoldi(matvec, v0, d, k)
-    S = sketch_matrix(n, s, zeta, seed, cycle)
+    S = sketch_matrix(n, s, zeta, seed, cycle) if sketch == "sparse" else SRFT(n, s, seed, cycle)
     out = srr_from_basis(matvec, basis["B"], basis["M"], S, nev)
     out["basis"] = basis
     return out
