@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SKS_ABI_VERSION 3
+#define SKS_ABI_VERSION 4
 
 typedef enum {
   SKS_OK = 0,
@@ -126,10 +126,18 @@ typedef struct {
   int32_t flags;             /* SKS_OPT_* bits */
   int32_t time_stride;       /* SKS_OPT_TIME_STEPS: time every time_stride-th step launch (0/1 = all) */
   int32_t basis;             /* SKS_BASIS_ARNOLDI (k-truncated, Eq. partorth) or SKS_BASIS_CHEBYSHEV */
-  int32_t reserved1;
+  int32_t sketch;            /* SKS_SKETCH_SPARSE (Eq. sparse-map) or SKS_SKETCH_SRFT (Eq. SRFT, single GPU) */
   double cheb_c, cheb_dx, cheb_dy;  /* Chebyshev: spectrum inside [c +- dx] x [+- i dy];
                                        all 0 = closed-form box of the stencil operator */
 } sks_sgmres_opts;
+
+enum {
+  SKS_SKETCH_SPARSE = 0,  /* sparse sign map, Eq. (sparse-map), hashed (readings O1-O7) */
+  SKS_SKETCH_SRFT = 1     /* SRFT, Eq. (SRFT) P:631-638 with F = orthonormal DCT2 as in the paper's
+                             experiments: S x = sqrt(n/s) DCT2(E x)[q_0..q_{s-1}], hashed signs E
+                             and Floyd-sampled coordinates q (reading O32).  The DCT mixes all rows: nranks = 1
+                             only (SKS_EUNSUPPORTED otherwise).  zeta is ignored. */
+};
 
 enum {
   SKS_BASIS_ARNOLDI = 0,   /* k-partial Arnoldi, Eq. (partorth) */
@@ -184,7 +192,8 @@ typedef struct {
   uint64_t seed;
   double cond_tol;
   int32_t basis;        /* SKS_BASIS_* */
-  int32_t reserved[3];
+  int32_t sketch;       /* SKS_SKETCH_* */
+  int32_t reserved[2];
   double cheb_c, cheb_dx, cheb_dy;  /* as in sks_sgmres_opts */
 } sks_srr_opts;
 
@@ -217,6 +226,12 @@ sks_status sks_srr_eigs(sks_ctx* ctx, const sks_operator* A, const double* v0,
 sks_status sks_sketch_apply(sks_ctx* ctx, int64_t n_global, int64_t row_begin, int64_t row_end,
                             int32_t s, int32_t zeta, uint64_t seed, uint32_t cycle,
                             const double* M, int64_t ldm, int32_t c, double* SM);
+
+/* S M for the SRFT sketch (SKS_SKETCH_SRFT, reading O32) of cycle `cycle`: M is n x c column-major
+ * (host or device), SM is s x c column-major (host or device, caller-owned).  Single rank only.
+ * Errors: SKS_EINVAL (n < 1, s < 1, s > n, c < 1, NULL), SKS_EUNSUPPORTED (nranks > 1). */
+sks_status sks_srft_apply(sks_ctx* ctx, int64_t n, int32_t s, uint64_t seed, uint32_t cycle, const double* M,
+                          int32_t c, double* SM);
 
 /* (row, sign) table of S for global rows [row_begin, row_begin+count), computed ON
  * THE DEVICE by the same code the sketch kernel uses: q[count*zeta] int32 in [0,s),

@@ -16,7 +16,7 @@ SKS_OP_STENCIL2D, SKS_OP_STENCIL3D, SKS_OP_CSR = 1, 2, 3
 # every symbol include/sks.h declares (checked by tests/test_abi.py)
 EXPORTS = ["sks_get_unique_id", "sks_create", "sks_destroy", "sks_last_error", "sks_abi_version",
            "sks_set_stream", "sks_partition", "sks_sgmres_solve", "sks_srr_eigs", "sks_sketch_apply",
-           "sks_sketch_table", "sks_apply_operator", "sks_basis"]
+           "sks_sketch_table", "sks_apply_operator", "sks_basis", "sks_srft_apply"]
 
 
 class Operator(C.Structure):
@@ -30,7 +30,7 @@ class SgmresOpts(C.Structure):
     _fields_ = [("d", C.c_int32), ("k", C.c_int32), ("s", C.c_int32), ("zeta", C.c_int32),
                 ("seed", C.c_uint64), ("tol", C.c_double), ("max_cycles", C.c_int32),
                 ("sketch_batch", C.c_int32), ("early_exit_factor", C.c_double), ("cond_tol", C.c_double),
-                ("flags", C.c_int32), ("time_stride", C.c_int32), ("basis", C.c_int32), ("reserved1", C.c_int32),
+                ("flags", C.c_int32), ("time_stride", C.c_int32), ("basis", C.c_int32), ("sketch", C.c_int32),
                 ("cheb_c", C.c_double), ("cheb_dx", C.c_double), ("cheb_dy", C.c_double)]
 
 
@@ -47,11 +47,14 @@ SKS_OPT_ADAPTIVE_RESTART = 2
 SKS_OPT_ZERO_X0 = 4
 SKS_BASIS_ARNOLDI, SKS_BASIS_CHEBYSHEV = 0, 1
 BASES = {"arnoldi": SKS_BASIS_ARNOLDI, "chebyshev": SKS_BASIS_CHEBYSHEV}
+SKS_SKETCH_SPARSE, SKS_SKETCH_SRFT = 0, 1
+SKETCHES = {"sparse": SKS_SKETCH_SPARSE, "srft": SKS_SKETCH_SRFT}
 
 
 class SrrOpts(C.Structure):
     _fields_ = [("d", C.c_int32), ("k", C.c_int32), ("s", C.c_int32), ("zeta", C.c_int32),
-                ("seed", C.c_uint64), ("cond_tol", C.c_double), ("basis", C.c_int32), ("reserved", C.c_int32 * 3),
+                ("seed", C.c_uint64), ("cond_tol", C.c_double), ("basis", C.c_int32), ("sketch", C.c_int32),
+                ("reserved", C.c_int32 * 2),
                 ("cheb_c", C.c_double), ("cheb_dx", C.c_double), ("cheb_dy", C.c_double)]
 
 
@@ -89,6 +92,7 @@ def load(path: str = LIBPATH):
                                    P, P, P, P, P, P, C.POINTER(SrrInfo)]),
         "sks_sketch_apply": (C.c_int, [P, I64, I64, I64, I32, I32, U64, U32, P, I64, I32, P]),
         "sks_sketch_table": (C.c_int, [P, I64, I64, I32, I32, U64, U32, P, P]),
+        "sks_srft_apply": (C.c_int, [P, I64, I32, U64, U32, P, I32, P]),
         "sks_apply_operator": (C.c_int, [P, C.POINTER(Operator), P, P]),
         "sks_basis": (C.c_int, [P, C.POINTER(Operator), P, I32, I32, P, P]),
     }

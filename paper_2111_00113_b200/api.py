@@ -155,7 +155,7 @@ class Context:
     # ---------------------------------------------------------------- sGMRES
     def sgmres_solve(self, A, f, x0=None, *, d, k, s, zeta=8, seed=0, tol=1e-8, max_cycles=50,
                      early_exit_factor=0.25, cond_tol=1e14, sketch_batch=0, hist_cap=None, time_steps=False, time_stride=1,
-                     basis="arnoldi", cheb=None, adaptive_restart=False, out=None):
+                     basis="arnoldi", cheb=None, adaptive_restart=False, out=None, sketch="sparse"):
         op, keep = A.struct()
         fa, pf = _prep(f)
         n = fa.shape[0]
@@ -182,7 +182,8 @@ class Context:
         opts = L.SgmresOpts(d, k, s, zeta, seed, tol, max_cycles, sketch_batch, early_exit_factor, cond_tol,
                             (L.SKS_OPT_TIME_STEPS if time_steps else 0)
                             | (L.SKS_OPT_ADAPTIVE_RESTART if adaptive_restart else 0)
-                            | (L.SKS_OPT_ZERO_X0 if zero_x0 else 0), time_stride, L.BASES[basis], 0,
+                            | (L.SKS_OPT_ZERO_X0 if zero_x0 else 0), time_stride, L.BASES[basis],
+                            L.SKETCHES[sketch],
                             cc, cdx, cdy)
         info = L.SgmresInfo()
         st = self.lib.sks_sgmres_solve(self.h, C.byref(op), pf, px, C.byref(opts), C.byref(info),
@@ -195,7 +196,7 @@ class Context:
 
     # ---------------------------------------------------------------- sRR
     def srr_eigs(self, A, v0, *, d, k, s, nev, zeta=8, seed=0, cond_tol=1e14, want_vectors=False,
-                 basis="arnoldi", cheb=None):
+                 basis="arnoldi", cheb=None, sketch="sparse"):
         op, keep = A.struct()
         va, pv = _prep(v0)
         n = va.shape[0]
@@ -207,7 +208,8 @@ class Context:
             Xr, pxr = _empty_like_place(va, (cap, n))
             Xi, pxi = _empty_like_place(va, (cap, n))
         cc, cdx, cdy = cheb if cheb is not None else (0.0, 0.0, 0.0)
-        opts = L.SrrOpts(d, k, s, zeta, seed, cond_tol, L.BASES[basis], (C.c_int32 * 3)(), cc, cdx, cdy)
+        opts = L.SrrOpts(d, k, s, zeta, seed, cond_tol, L.BASES[basis], L.SKETCHES[sketch], (C.c_int32 * 2)(),
+                         cc, cdx, cdy)
         info = L.SrrInfo()
         st = self.lib.sks_srr_eigs(self.h, C.byref(op), pv, C.byref(opts), nev, cap, th_re.ctypes.data,
                                    th_im.ctypes.data, rt.ctypes.data, re.ctypes.data, pxr, pxi, C.byref(info))
@@ -232,6 +234,18 @@ class Context:
         SM, psm = _empty_like_place(Ma, (c, s))
         st = self.lib.sks_sketch_apply(self.h, ng, row_begin, row_begin + n, s, zeta, seed, cycle, pm, n, c, psm)
         self._check(st, "sks_sketch_apply")
+        return SM.t() if _is_torch(SM) else SM.T
+
+    def srft_apply(self, M, *, s, seed, cycle=0):
+        """S M for the SRFT sketch (include/sks.h sks_srft_apply, reading O32)."""
+        Ma, _ = _prep(M)
+        if Ma.ndim == 1:
+            Ma = Ma.reshape(-1, 1)
+        n, c = Ma.shape
+        Mt = Ma.t().contiguous() if _is_torch(Ma) else np.ascontiguousarray(Ma.T)
+        pm = Mt.data_ptr() if _is_torch(Mt) else Mt.ctypes.data
+        SM, psm = _empty_like_place(Ma, (c, s))
+        self._check(self.lib.sks_srft_apply(self.h, n, s, seed, cycle, pm, c, psm), "sks_srft_apply")
         return SM.t() if _is_torch(SM) else SM.T
 
     def sketch_table(self, row_begin, count, *, s, zeta, seed, cycle=0):

@@ -54,13 +54,17 @@ struct sks_ctx {
   // workspaces
   DevBuf W, xb, fb, vb, mr, xg, part, part2, partsk, sigma, H, mnorm, SW, Xp, Zb, U, T, rvec, rho, rest, coef,
       ctrl, small, Mh, Mh2, wr, wi, sel, th, yr, yi, ework, SAB, SB, Xr, Xi, AXr, AXi, rpb, cib, vab, cig, rbd,
-      tmp, bgsw, bgsc, plan, gam, rcoef;
+      tmp, bgsw, bgsc, plan, gam, rcoef, srft_q, srft_w;
   CtrlBlock* h_ctrl = nullptr;   // pinned mirror
   double* h_small = nullptr;     // pinned scratch (4096 doubles)
   int64_t w_zeroed_bytes = 0;
   void* tma_cache = nullptr;   // encoded tensor maps of the stencil step
   void* zm_cache = nullptr;    // encoded tensor maps of the 3D z-march step
   void* ym_cache = nullptr;    // encoded tensor maps of the 2D y-march step
+  void* srft_cache = nullptr;  // cuFFT plans of the SRFT sketch
+  int sketch_kind = 0;         // SKS_SKETCH_* of the running call
+  uint64_t sk_seed = 0;        // its seed and current cycle (SRFT key)
+  uint32_t sk_cycle = 0;
   int use_tma = 1;             // SKS_NO_TMA=1 forces the generic stencil kernels
   int tma_mask = 7;
   cudaStream_t main() const { return user_main ? user_main : own_main; }
@@ -337,13 +341,14 @@ sks_status sks_destroy(sks_ctx* c) {
                     &c->rho,  &c->rest, &c->coef,  &c->ctrl, &c->small, &c->Mh,  &c->Mh2,   &c->wr,    &c->wi,
                     &c->sel,  &c->th,   &c->yr,    &c->yi,   &c->ework, &c->SAB, &c->SB,    &c->Xr,    &c->Xi,
                     &c->AXr,  &c->AXi,  &c->rpb,   &c->cib,  &c->vab,  &c->cig,  &c->rbd,   &c->tmp,
-                    &c->bgsw, &c->bgsc, &c->plan, &c->gam, &c->rcoef};
+                    &c->bgsw, &c->bgsc, &c->plan, &c->gam, &c->rcoef, &c->srft_q, &c->srft_w};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->tma_cache) stencil_tma_free(c->tma_cache);
   if (c->zm_cache) stencil_zm_free(c->zm_cache);
   if (c->ym_cache) stencil_ym_free(c->ym_cache);
+  if (c->srft_cache) srft_free(c->srft_cache);
   for (auto& ev : c->ev_batch) cudaEventDestroy(ev);
   for (auto& ev : c->ev_step) cudaEventDestroy(ev);
   cudaEvent_t evs[] = {c->ev_fork, c->ev_join, c->ev_t0, c->ev_t1, c->ev_b0, c->ev_b1};
@@ -698,6 +703,14 @@ static sks_status global_norm(sks_ctx* c, Basis& b, const double* v_interior, do
 static sks_status sketch_plan(sks_ctx* c, const Geo& g, int s, int zeta, uint64_t key, cudaStream_t st,
                               const void** plan) {
   *plan = nullptr;
+  if (c->sketch_kind == SKS_SKETCH_SRFT) {  // the cycle's s sampled DCT coordinates (host Floyd, O32)
+    std::vector<int32_t> q(s);
+    srft_rows_host(g.n, s, srft_key_host(c->sk_seed, c->sk_cycle), q.data());
+    SKS_TRY(ensure(c, c->srft_q, sizeof(int32_t) * (size_t)s));
+    SKS_CK(c, cudaStreamSynchronize(st));  // the previous cycle's sample kernels may still read srft_q
+    SKS_CK(c, cudaMemcpy(c->srft_q.p, q.data(), sizeof(int32_t) * (size_t)s, cudaMemcpyHostToDevice));
+    return SKS_OK;
+  }
   if (!sketch_plan_supported(s, zeta)) return SKS_OK;
   SKS_TRY(ensure(c, c->plan, sketch_plan_bytes(g.n, s, zeta)));
   SKS_CK(c, launch_sketch_plan(g.n, g.row_begin, s, zeta, key, c->plan.p, c->main_sms, st));
@@ -709,8 +722,15 @@ static sks_status sketch_plan(sks_ctx* c, const Geo& g, int s, int zeta, uint64_
 static sks_status sketch_cols(sks_ctx* c, Basis& b, int c0, int J, int s, int zeta, uint64_t key,
                               cudaStream_t st, const void* plan) {
   const Geo& g = b.g;
-  const int grid = sketch_grid(c->main_sms, g.n);
   double* out = c->SW.as<double>() + (int64_t)c0 * s;
+  if (c->sketch_kind == SKS_SKETCH_SRFT) {
+    SKS_TRY(ensure(c, c->srft_w, sizeof(double) * srft_work_doubles(g.n, SKS_JB)));
+    SKS_CK(c, launch_srft(colp(c, b, c0) + g.off, g.ld, g.n, J, s, srft_key_host(c->sk_seed, c->sk_cycle),
+                          c->srft_q.as<int32_t>(), c->srft_w.as<double>(), &c->srft_cache, out, s, c->main_sms, st));
+    c->launches += 3;
+    return SKS_OK;
+  }
+  const int grid = sketch_grid(c->main_sms, g.n);
   SKS_CK(c, launch_sketch(colp(c, b, c0) + g.off, g.ld, g.n, g.row_begin, J, s, zeta, key, c->partsk.as<double>(),
                           grid, out, s, 0, st, &c->launches, plan));
   SKS_TRY(allreduce_sum(c, out, (size_t)J * s, st));
@@ -821,6 +841,11 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
   if (!(fnorm >= 0.0) || !std::isfinite(fnorm)) return fail(c, SKS_EINVAL, "f is not finite");
   const double thr = o->early_exit_factor > 0 ? o->early_exit_factor * o->tol * fnorm : -1.0;
   const bool adaptive = (o->flags & SKS_OPT_ADAPTIVE_RESTART) != 0;
+  if (o->sketch != SKS_SKETCH_SPARSE && o->sketch != SKS_SKETCH_SRFT) return fail(c, SKS_EINVAL, "unknown sketch");
+  if (o->sketch == SKS_SKETCH_SRFT && c->nranks > 1)
+    return fail(c, SKS_EUNSUPPORTED, "the SRFT sketch is single-GPU (the DCT mixes all rows)");
+  c->sketch_kind = o->sketch;
+  c->sk_seed = o->seed;
   int poll_lag = (g.kind == SKS_OP_CSR) ? 1 : 2;
   if (const char* e = getenv("SKS_POLL_LAG")) poll_lag = std::max(1, atoi(e));
 
@@ -857,6 +882,7 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
     if (cyc == o->max_cycles) break;
     ++cycles;
     const uint64_t key = sks_key(o->seed, (uint32_t)cyc);
+    c->sk_cycle = (uint32_t)cyc;
     // ---- basis loop (main) with batched sketch + incremental QR (side)
     const double bytes_first = b.bytes;
     SKS_CK(c, cudaEventRecord(c->ev_b0, st));
@@ -1128,6 +1154,12 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
   ++c->launches;
   SKS_TRY(first_column(c, b, 2, g.kind == SKS_OP_CSR ? vb + g.off : vb, nullptr));
   const uint64_t key = sks_key(o->seed, 0u);
+  if (o->sketch != SKS_SKETCH_SPARSE && o->sketch != SKS_SKETCH_SRFT) return fail(c, SKS_EINVAL, "unknown sketch");
+  if (o->sketch == SKS_SKETCH_SRFT && c->nranks > 1)
+    return fail(c, SKS_EUNSUPPORTED, "the SRFT sketch is single-GPU (the DCT mixes all rows)");
+  c->sketch_kind = o->sketch;
+  c->sk_seed = o->seed;
+  c->sk_cycle = 0;
   float t_basis_ms = 0.f;
   const double bytes0 = b.bytes;
   SKS_TRY(basis_and_sketch(c, b, d, s, zeta, key, JB, true, &t_basis_ms));
@@ -1313,6 +1345,7 @@ extern "C" sks_status sks_sketch_apply(sks_ctx* c, int64_t n_global, int64_t row
   SKS_CK(c, cudaMemcpy2DAsync(c->tmp.p, sizeof(double) * ldd, M, sizeof(double) * ldm, sizeof(double) * n, cc,
                               cudaMemcpyDefault, st));
   const uint64_t key = sks_key(seed, cycle);
+  c->sketch_kind = SKS_SKETCH_SPARSE;
   Geo gq;
   gq.n = n;
   gq.row_begin = row_begin;
@@ -1325,6 +1358,39 @@ extern "C" sks_status sks_sketch_apply(sks_ctx* c, int64_t n_global, int64_t row
                             &c->launches, plan));
   }
   SKS_TRY(allreduce_sum(c, c->SAB.as<double>(), (size_t)s * cc, st));
+  SKS_CK(c, cudaMemcpyAsync(SM, c->SAB.p, sizeof(double) * (size_t)s * cc, cudaMemcpyDefault, st));
+  SKS_CK(c, cudaStreamSynchronize(st));
+  return SKS_OK;
+}
+
+extern "C" sks_status sks_srft_apply(sks_ctx* c, int64_t n, int32_t s, uint64_t seed, uint32_t cycle,
+                                     const double* M, int32_t cc, double* SM) {
+  if (!c) return SKS_EINVAL;
+  c->err.clear();
+  if (!M || !SM || n < 1 || s < 1 || s > n || s > SKS_SMAX || cc < 1 || n >= (int64_t(1) << 31))
+    return fail(c, SKS_EINVAL, "bad srft_apply arguments");
+  if (c->nranks > 1) return fail(c, SKS_EUNSUPPORTED, "the SRFT sketch is single-GPU");
+  cudaSetDevice(c->device);
+  cudaStream_t st = c->main();
+  SKS_TRY(ensure(c, c->tmp, sizeof(double) * (size_t)n * cc));
+  SKS_TRY(ensure(c, c->SAB, sizeof(double) * (size_t)s * cc));
+  SKS_TRY(ensure(c, c->srft_w, sizeof(double) * srft_work_doubles(n, SKS_JB)));
+  SKS_CK(c, cudaMemcpyAsync(c->tmp.p, M, sizeof(double) * (size_t)n * cc, cudaMemcpyDefault, st));
+  c->sketch_kind = SKS_SKETCH_SRFT;
+  c->sk_seed = seed;
+  c->sk_cycle = cycle;
+  Geo gq;
+  gq.n = n;
+  gq.row_begin = 0;
+  const void* plan = nullptr;
+  SKS_TRY(sketch_plan(c, gq, s, 8, 0, st, &plan));
+  const uint64_t key = srft_key_host(seed, cycle);
+  for (int c0 = 0; c0 < cc; c0 += SKS_JB) {
+    const int J = std::min(SKS_JB, cc - c0);
+    SKS_CK(c, launch_srft(c->tmp.as<double>() + (int64_t)c0 * n, n, n, J, s, key, c->srft_q.as<int32_t>(),
+                          c->srft_w.as<double>(), &c->srft_cache, c->SAB.as<double>() + (int64_t)c0 * s, s,
+                          c->num_sms, st));
+  }
   SKS_CK(c, cudaMemcpyAsync(SM, c->SAB.p, sizeof(double) * (size_t)s * cc, cudaMemcpyDefault, st));
   SKS_CK(c, cudaStreamSynchronize(st));
   return SKS_OK;

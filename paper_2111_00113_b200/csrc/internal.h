@@ -41,6 +41,14 @@ cudaError_t launch_step_stencil_ym(const StepArgs& a, const double* W, int64_t n
                                    const double* fb, const double* vb, int grid, cudaStream_t st, void** cache);
 void stencil_ym_free(void* cache);
 
+// srft.cu (SRFT sketch, reading O32)
+uint64_t srft_key_host(uint64_t seed, uint32_t cycle);
+void srft_rows_host(int64_t n, int s, uint64_t key, int32_t* q);
+size_t srft_work_doubles(int64_t n, int J);
+cudaError_t launch_srft(const double* M, int64_t ldm, int64_t n, int J, int s, uint64_t key, const int32_t* q,
+                        double* work, void** cache, double* out, int64_t ldo, int num_sms, cudaStream_t st);
+void srft_free(void* cache);
+
 // sketch.cu
 int sketch_grid(int num_sms, int64_t nrows);
 size_t sketch_part_doubles(int grid, int J, int s);

@@ -292,3 +292,37 @@ def test_sgmres_adaptive_restart_parity(ctx):
                             adaptive_restart=True)
     rel = np.linalg.norm(f - A @ full.x) / np.linalg.norm(f)
     assert full.converged and rel <= 1e-8
+
+
+# ---------------------------------------------------------------- SRFT sketch (NEXT(4), reading O32)
+@pytest.mark.parametrize("n,c,s", [(1024, 1, 120), (777, 5, 40), (50_001, 33, 400), (262_144, 3, 600)])
+def test_srft_apply_parity(ctx, n, c, s):
+    rng = np.random.default_rng(n + c)
+    M = rng.standard_normal((n, c))
+    SM = ctx.srft_apply(M, s=s, seed=3, cycle=2)
+    ref = O.srft_apply(M, s, 3, 2)
+    assert np.linalg.norm(SM - ref) / np.linalg.norm(ref) <= 1e-12
+
+
+def test_sgmres_srft_parity(ctx):
+    P = _P()
+    c = get_config("C1")
+    f = rhs_normal(c.n, c.seed)
+    A = O.stencil_matrix(2, c.m, c.beta)
+    res = ctx.sgmres_solve(P.StencilOperator(2, c.m, c.beta), f, d=c.d, k=c.k, s=c.s, seed=c.seed, tol=1e-8,
+                           max_cycles=6, sketch="srft")
+    orc = O.sgmres_solve(lambda v: A @ v, f, c.d, c.k, c.s, c.zeta, c.seed, tol=1e-8, max_cycles=6, sketch="srft")
+    rel = np.linalg.norm(f - A @ res.x) / np.linalg.norm(f)
+    assert res.converged and rel <= 1e-8
+    assert res.info["cycles"] == orc["cycles"] and res.info["columns"] == orc["columns"]
+    np.testing.assert_allclose(res.hist, orc["hist_est"], rtol=1e-6)
+
+
+def test_srr_srft_parity(ctx):
+    P = _P()
+    m, beta, d = 40, 5.0, 40
+    v0 = start_vector(m * m, 4)
+    A = O.stencil_matrix(2, m, beta)
+    out = ctx.srr_eigs(P.StencilOperator(2, m, beta), v0, d=d, k=2, s=2 * d, nev=6, seed=4, sketch="srft")
+    orc = O.srr_eigs(lambda v: A @ v, v0, d, 2, 2 * d, 8, 4, 6, sketch="srft")
+    assert _match(out["theta"], orc["theta_all"]) <= 1e-8
