@@ -178,44 +178,71 @@ __global__ void __launch_bounds__(1024) panel_kernel(double* __restrict__ X, int
   __syncthreads();
   for (int pass = 0; pass < 3; ++pass) {
     const int Jc = nbad;  // columns still factored
-    // ---- Gram G = X^T X (thread (i, j), i = warp, j = lane)
-    {
-      const int i = tid >> 5, j = tid & 31;
-      double g = 0.0;
-      if (i < Jc && j < Jc && i <= j)
-        for (int q = 0; q < s; ++q) g += sX[q * L + i] * sX[q * L + j];
-      G[i * PL + j] = g;
+    // ---- Gram G = X^T X on the FP64 tensor cores: warp t < 16 owns the 8x8 tile (t/4, t%4),
+    //      mma.m8n8k4 over k = rows of X (A = X^T: A[m][k] = X[k][m]; B = X); columns >= Jc read as 0
+    if (wid < 16) {
+      const int mt = wid >> 2, ntl = wid & 3, lr = lane >> 2, lc = lane & 3;
+      const int mcol = 8 * mt + lr, ncol = 8 * ntl + lr;
+      const bool mok = mcol < Jc, nok = ncol < Jc;
+      double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;  // two accumulator pairs (independent DMMA chains)
+      int q = 0;
+      for (; q + 7 < s; q += 8) {
+        const double a0 = mok ? sX[(q + lc) * L + mcol] : 0.0, b0 = nok ? sX[(q + lc) * L + ncol] : 0.0;
+        const double a1 = mok ? sX[(q + 4 + lc) * L + mcol] : 0.0, b1 = nok ? sX[(q + 4 + lc) * L + ncol] : 0.0;
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                     : "+d"(d0), "+d"(d1) : "d"(a0), "d"(b0));
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                     : "+d"(e0), "+d"(e1) : "d"(a1), "d"(b1));
+      }
+      for (; q < s; q += 4) {
+        const bool kok = q + lc < s;
+        const double a0 = (mok && kok) ? sX[(q + lc) * L + mcol] : 0.0;
+        const double b0 = (nok && kok) ? sX[(q + lc) * L + ncol] : 0.0;
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                     : "+d"(d0), "+d"(d1) : "d"(a0), "d"(b0));
+      }
+      const int gi = 8 * mt + lr, gj = 8 * ntl + 2 * lc;
+      G[gi * PL + gj] = d0 + e0;
+      G[gi * PL + gj + 1] = d1 + e1;
     }
     __syncthreads();
-    // ---- Cholesky G = R^T R (upper R in place), one warp; lane j owns column j
-    if (wid == 0) {
+    // ---- Cholesky G = R^T R (upper R in place), right-looking over the whole CTA: thread (i, j)
+    //      owns G[i][j]; per step one scalar (sqrt), one row scaling, one rank-1 trailing update
+    __shared__ double csh[2];
+    if (tid == 0) {
       double shift = 0.0;
       if (pass == 0) {
-        double tr = lane < Jc ? G[lane * PL + lane] : 0.0;
-        tr = warp_sum(tr);
+        double tr = 0.0;
+        for (int l = 0; l < Jc; ++l) tr += G[l * PL + l];
         shift = 11.0 * ((double)s * Jc + (double)Jc * (Jc + 1)) * 1.1102230246251565e-16 * tr;
-        if (lane < Jc) G[lane * PL + lane] += shift;
       }
-      __syncwarp();
+      csh[0] = shift;
+    }
+    __syncthreads();
+    if (pass == 0 && tid < Jc) G[tid * PL + tid] += csh[0];
+    {
+      const int ci = tid >> 5, cj = tid & 31;
       int bad = Jc;
       for (int k = 0; k < Jc; ++k) {
-        const double d = G[k * PL + k];
-        if (!(d > 0.0) || !isfinite(d)) {
+        __syncthreads();
+        if (tid == 0) {
+          const double d = G[k * PL + k];
+          const bool okd = (d > 0.0) && isfinite(d);
+          const double rk = okd ? sqrt(d) : 1.0;
+          G[k * PL + k] = rk;
+          csh[0] = 1.0 / rk;
+          csh[1] = okd ? 1.0 : 0.0;
+        }
+        __syncthreads();
+        if (csh[1] == 0.0) {
           bad = k;
           break;
         }
-        const double rk = sqrt(d);
-        __syncwarp();
-        if (lane == k) G[k * PL + k] = rk;
-        if (lane > k && lane < Jc) G[k * PL + lane] /= rk;
-        __syncwarp();
-        if (lane > k && lane < Jc) {
-          const double gkj = G[k * PL + lane];
-          for (int i = k + 1; i <= lane; ++i) G[i * PL + lane] -= G[k * PL + i] * gkj;
-        }
-        __syncwarp();
+        if (tid > k && tid < Jc) G[k * PL + tid] *= csh[0];
+        __syncthreads();
+        if (ci > k && ci <= cj && cj < Jc) G[ci * PL + cj] = fma(-G[k * PL + ci], G[k * PL + cj], G[ci * PL + cj]);
       }
-      if (lane == 0) nbad = bad;
+      if (tid == 0) nbad = bad;
     }
     __syncthreads();
     const int Jn = nbad;
@@ -223,9 +250,14 @@ __global__ void __launch_bounds__(1024) panel_kernel(double* __restrict__ X, int
     for (int q = tid; q < s; q += nt) {
       double* xr = sX + q * L;
       for (int j = 0; j < Jn; ++j) {
-        double v = xr[j];
-        for (int i = 0; i < j; ++i) v -= xr[i] * G[i * PL + j];
-        xr[j] = v / G[j * PL + j];
+        double v0 = xr[j], v1 = 0.0;  // two chains
+        int i = 0;
+        for (; i + 1 < j; i += 2) {
+          v0 = fma(-xr[i], G[i * PL + j], v0);
+          v1 = fma(-xr[i + 1], G[(i + 1) * PL + j], v1);
+        }
+        if (i < j) v0 = fma(-xr[i], G[i * PL + j], v0);
+        xr[j] = (v0 + v1) / G[j * PL + j];
       }
     }
     // ---- Rt <- R Rt (upper triangular product)
