@@ -848,6 +848,10 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
   c->sk_seed = o->seed;
   int poll_lag = (g.kind == SKS_OP_CSR) ? 1 : 2;
   if (const char* e = getenv("SKS_POLL_LAG")) poll_lag = std::max(1, atoi(e));
+  // near-exit switch (small batches, lag 1) only where a column costs more than a batch's QR
+  // latency: large local vectors (C3: 54.6 vs 56.9 ms; on C2's 2 MB vectors the waits cost more)
+  double near_factor = (g.n >= (int64_t(1) << 20)) ? 4.0 : 0.0;
+  if (const char* e = getenv("SKS_NEAR_FACTOR")) near_factor = atof(e);
 
   int cycles = 0, columns = 0, generated = 0, flags = 0;
   int64_t nh = 0, nht = 0;
@@ -929,18 +933,27 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
     };
     int batch_size = std::min(8, JB);
     int pending_upto = 0;
+    int lag = poll_lag;
+    bool near = false;  // r_est within a factor of the exit threshold: small batches, lag 1
     for (int j = 1; j <= d; ++j) {
       SKS_TRY(step_column(c, b, j));
       const bool batch_done = (j + 1 - pending_upto >= batch_size) || j == d;
       if (batch_done) {
         SKS_TRY(enqueue_side(j + 1, j == d));
         pending_upto = j + 1;
-        batch_size = std::min(JB, batch_size * 2);
+        batch_size = near ? std::min(8, JB) : std::min(JB, batch_size * 2);
         // poll the early-exit / breakdown flags of batch nbatch-lag (bounded lag): 2 for stencils
         // (cheap columns: keep the GPU fed), 1 for CSR (a column costs a full matrix sweep, more
-        // than the batch's sketched QR, so over-generated columns cost more than the wait)
-        if (nbatch >= poll_lag && nbatch - poll_lag < (int)c->ev_batch.size()) {
-          SKS_CK(c, cudaEventSynchronize(c->ev_batch[nbatch - poll_lag]));
+        // than the batch's sketched QR, so over-generated columns cost more than the wait); once
+        // r_est comes within near_factor of the exit threshold the cycle is about to end, and the
+        // columns run ahead of the check would be discarded: 8-column batches polled with lag 1
+        if (nbatch >= lag && nbatch - lag < (int)c->ev_batch.size()) {
+          SKS_CK(c, cudaEventSynchronize(c->ev_batch[nbatch - lag]));
+          if (!near && thr > 0 && hc->r_est_last > 0 && hc->r_est_last <= near_factor * thr) {
+            near = true;
+            lag = 1;
+            batch_size = std::min(8, JB);
+          }
           if (hc->exit_cols > 0 || hc->stop_col < INT_MAX || hc->rank_def ||
               (adaptive && hc->cond > o->cond_tol)) {
             last_col = j;
