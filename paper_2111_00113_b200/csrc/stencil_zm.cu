@@ -54,7 +54,10 @@ constexpr int ZW = ZWX * ZWY;                    // 612
 // Measured 38.8 us vs 38.1 us at C3 (the conflicts are not the bound), so off by default.
 constexpr int ZRX = ZM_PITCH ? ZUX : ZWX;        // thread-row width = ring row pitch
 constexpr int ZR = ZRX * ZWY;                    // ring plane (648 doubles)
-constexpr int ZT = (ZRX * ZWY + 31) / 32 * 32;  // threads (32 x 16 tile: 672 = 21 warps)
+constexpr int ZT = (ZRX * ZWY + 31) / 32 * 32;
+#ifndef ZM_NPY_DEFAULT
+#define ZM_NPY_DEFAULT 2
+#endif  // threads (32 x 16 tile: 672 = 21 warps)
 
 struct ZmArgs {
   int ucol;
@@ -266,6 +269,239 @@ __global__ void __launch_bounds__(ZT, ZM_CPS)
   step_epilogue<KM>(a, &cf, acc, red);
 }
 
+// ---- paired-column variant (default, SKS_ZM_NPY=2): a thread owns the two y-adjacent W columns
+// (bx, 2g) and (bx, 2g+1), so each column's y neighbour on the other side of the pair comes from
+// registers (6 instead of 8 in-plane shared loads per pair and stencil, for U and for the w_j ring)
+// and each thread carries two independent FMA chains; 320 threads (10 warps) per CTA.  The kernel is
+// latency-bound: measured 36.1 us vs 37.7 us per C3 launch.  Three or six columns per
+// thread (a generic version, kept out of the tree) measured 41.2 / 69.4 us: fewer warps, register
+// pressure and spills outweigh the saved loads.
+static_assert(ZWY % 2 == 0, "the pair kernel needs an even tile height");
+constexpr int ZPT = (ZWX * (ZWY / 2) + 31) / 32 * 32;  // 34 x 9 pairs -> 320 threads
+
+template <int KM, int ZS, bool FULL, bool USL>
+__global__ void __launch_bounds__(ZPT, 1)
+    step3d_zmp_kernel(StepArgs a, ZmArgs z, const __grid_constant__ CUtensorMap tmU,
+                      const __grid_constant__ CUtensorMap tmV) {
+  extern __shared__ __align__(128) unsigned char smraw_p[];
+  double* sm = reinterpret_cast<double*>(smraw_p + ((128u - (smem_u32(smraw_p) & 127u)) & 127u));
+  constexpr int STG = zm_stage<KM, ZS>();
+  constexpr int UB = zm_ublk<KM, ZS>(), VB = zm_vblk<KM, ZS>();
+  constexpr int R = 3 * ZS;
+  double* ring = sm + 2 * STG;
+  __shared__ StepCoef cf;
+  __shared__ double red[SKS_NP * 32];
+  __shared__ __align__(8) uint64_t bar[2];
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    tma_prefetch_desc(&tmU);
+    tma_prefetch_desc(&tmV);
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  pdl_wait_and_release();
+  if (!step_prologue(a, &cf, red)) return;
+  const int nv = FULL ? KM - 1 : cf.nv;
+  const uint32_t sbytes = (uint32_t)(ZUP * (ZS + 2) * 8 + nv * ZVP * ZS * 8);
+  const int m = (int)a.m, nz = (int)a.nz, z0g = (int)a.z0, G = a.G;
+  const int64_t pl = a.plane;
+  const double cc = a.cc, cm = a.cm, cp = a.cp, alpha = cf.alpha, beta_u = cf.beta_u;
+  double cl[KM - 1];
+#pragma unroll
+  for (int l = 0; l < KM - 1; ++l) cl[l] = (l < nv) ? cf.c[l] : 0.0;
+  constexpr bool uslot = USL;
+  double* Wout = a.W + (a.mode == 0 ? (int64_t)a.j * a.ld : 0) + a.off;
+
+  constexpr int NPAIR = ZWX * (ZWY / 2);
+  const bool wt = tid < NPAIR;
+  const int tp = wt ? tid : NPAIR - 1;
+  const int bx = tp % ZWX, by0 = 2 * (tp / ZWX), by1 = by0 + 1;
+  const int cu0 = (by0 + 1) * ZUX + (bx + 1), cu1 = cu0 + ZUX;
+  const int cv0 = by0 * ZVX + (bx + 1), cv1 = cv0 + ZVX;
+  const int cw0 = by0 * ZWX + bx, cw1 = cw0 + ZWX;
+  const bool xin_box = bx >= 1 && bx <= ZX;
+  const bool in0 = wt && xin_box && by0 >= 1 && by0 <= ZY, in1 = wt && xin_box && by1 >= 1 && by1 <= ZY;
+
+  double acc[KM + 3];
+#pragma unroll
+  for (int i = 0; i < KM + 3; ++i) acc[i] = 0.0;
+  uint32_t phase = 0, sidx = 0;
+  const int64_t u_lo = (z.units * blockIdx.x) / gridDim.x, u_hi = (z.units * (blockIdx.x + 1)) / gridDim.x;
+  for (int64_t u = u_lo; u < u_hi;) {
+    const int col = (int)(u / nz);
+    const int za = (int)(u % nz);
+    const int64_t zr = za + (u_hi - u);
+    const int zb = (int)(zr < nz ? zr : nz);
+    u += zb - za;
+    const int tx = col % z.tiles_x, ty = col / z.tiles_x;
+    const int x0 = tx * ZX, y0 = ty * ZY;
+    const int wa = za - 1;
+    const int nsteps = (zb - wa + 1 + ZS - 1) / ZS;
+    const uint32_t s0 = sidx;
+    auto issue = [&](int t) {
+      const uint32_t slot = (s0 + (uint32_t)t) & 1u;
+      double* dst = sm + slot * STG;
+      const int p0 = wa + t * ZS;
+      mbar_arrive_expect_tx(&bar[slot], sbytes);
+      tma_load_4d(dst, &tmU, &bar[slot], x0 - 2, y0 - 2, p0 - 1 + G, z.ucol);
+      for (int l = 0; l < nv; ++l) tma_load_4d(dst + UB + l * VB, &tmV, &bar[slot], x0 - 2, y0 - 1, p0 + G, z.vcol[l]);
+    };
+    if (tid == 0) {
+      issue(0);
+      if (nsteps > 1) issue(1);
+    }
+    double wp1a = 0.0, wp2a = 0.0, wp1b = 0.0, wp2b = 0.0;
+    double vla[KM - 1], vlb[KM - 1];
+#pragma unroll
+    for (int l = 0; l < KM - 1; ++l) vla[l] = vlb[l] = 0.0;
+    const int gx = x0 - 1 + bx, gy0 = y0 - 1 + by0, gy1 = gy0 + 1;
+    const bool xok = wt && (unsigned)gx < (unsigned)m;
+    const bool xy0 = xok && (unsigned)gy0 < (unsigned)m, xy1 = xok && (unsigned)gy1 < (unsigned)m;
+    const bool aw0 = in0 && gx < m && gy0 < m, aw1 = in1 && gx < m && gy1 < m;
+    double* wc0 = Wout + (int64_t)(wa - 1) * pl + (int64_t)gy0 * m + gx;
+    double* wc1 = wc0 + m;
+    const double am0 = xy0 ? alpha : 0.0, bm0 = xy0 ? beta_u : 0.0;
+    const double am1 = xy1 ? alpha : 0.0, bm1 = xy1 ? beta_u : 0.0;
+    double clm0[KM - 1], clm1[KM - 1];
+#pragma unroll
+    for (int l = 0; l < KM - 1; ++l) {
+      clm0[l] = xy0 ? cl[l] : 0.0;
+      clm1[l] = xy1 ? cl[l] : 0.0;
+    }
+    constexpr int T0 = ZS == 1 ? 2 : 1;
+    auto step = [&](int t, auto phc) {
+      constexpr int PH = decltype(phc)::value;
+      constexpr int SBW = ((PH + 1) % 3) * ZS;
+      constexpr int SBP = SBW == 0 ? R - 1 : SBW - 1;
+      const uint32_t slot = (s0 + (uint32_t)t) & 1u;
+      mbar_wait(&bar[slot], (phase >> slot) & 1u);
+      phase ^= 1u << slot;
+      const double* sU = sm + slot * STG;
+      const double* sV = sU + UB;
+      const int p0 = wa + t * ZS;
+      const bool fast = t >= T0 && p0 + ZS - 1 <= zb && z0g + p0 + ZS - 1 < m;
+      double wa_[ZS], wb_[ZS], ca[ZS + 2], cb[ZS + 2], va[KM - 1][ZS], vb[KM - 1][ZS];
+      double* rw0 = ring + SBW * ZW + cw0;
+      double* rw1 = ring + SBW * ZW + cw1;
+      const double* rp0 = ring + SBP * ZW + cw0;
+      const double* rp1 = ring + SBP * ZW + cw1;
+#pragma unroll
+      for (int k = 0; k < ZS + 2; ++k) {
+        ca[k] = sU[k * ZUP + cu0];
+        cb[k] = sU[k * ZUP + cu1];
+      }
+#pragma unroll
+      for (int i = 0; i < ZS; ++i) {
+        const int p = p0 + i;
+#pragma unroll
+        for (int l = 0; l < KM - 1; ++l) {
+          va[l][i] = (FULL || l < nv) ? sV[l * VB + i * ZVP + cv0] : 0.0;
+          vb[l][i] = (FULL || l < nv) ? sV[l * VB + i * ZVP + cv1] : 0.0;
+        }
+        const double* q0 = sU + (i + 1) * ZUP + cu0;
+        const double* q1 = q0 + ZUX;
+        // column a (y = by0): y+1 neighbour is column b's centre; column b: y-1 is column a's centre
+        const double Aua = cc * ca[i + 1] + cm * (q0[-1] + q0[-ZUX] + ca[i]) + cp * (q0[1] + cb[i + 1] + ca[i + 2]);
+        const double Aub = cc * cb[i + 1] + cm * (q1[-1] + ca[i + 1] + cb[i]) + cp * (q1[1] + q1[ZUX] + cb[i + 2]);
+        double w0v, w1v;
+        if (fast) {
+          w0v = am0 * Aua + bm0 * ca[i + 1];
+          w1v = am1 * Aub + bm1 * cb[i + 1];
+#pragma unroll
+          for (int l = 0; l < KM - 1; ++l)
+            if (FULL || l < nv) {
+              w0v += clm0[l] * va[l][i];
+              w1v += clm1[l] * vb[l][i];
+            }
+        } else {
+          w0v = alpha * Aua + beta_u * ca[i + 1];
+          w1v = alpha * Aub + beta_u * cb[i + 1];
+#pragma unroll
+          for (int l = 0; l < KM - 1; ++l)
+            if (FULL || l < nv) {
+              w0v += cl[l] * va[l][i];
+              w1v += cl[l] * vb[l][i];
+            }
+          const bool zok = (unsigned)(z0g + p) < (unsigned)m && p <= zb;
+          w0v = (xy0 && zok) ? w0v : 0.0;
+          w1v = (xy1 && zok) ? w1v : 0.0;
+        }
+        wa_[i] = w0v;
+        wb_[i] = w1v;
+        if (wt) {
+          rw0[i * ZW] = w0v;
+          rw1[i * ZW] = w1v;
+        }
+      }
+      __syncthreads();
+      if (tid == 0 && t + 2 < nsteps) issue(t + 2);
+      if (aw0 || aw1) {
+        double* wo0 = wc0;
+        double* wo1 = wc1;
+#pragma unroll
+        for (int i = 0; i < ZS; ++i) {
+          const int qp = p0 - 1 + i;
+          if (fast || (qp >= za && qp < zb)) {
+            const double wqa = (i == 0) ? wp1a : wa_[i - 1];
+            const double wqb = (i == 0) ? wp1b : wb_[i - 1];
+            const double wma = (i == 0) ? wp2a : (i == 1 ? wp1a : wa_[i - 2]);
+            const double wmb = (i == 0) ? wp2b : (i == 1 ? wp1b : wb_[i - 2]);
+            const double* r0 = (i == 0) ? rp0 : rw0 + (i - 1) * ZW;
+            const double* r1 = (i == 0) ? rp1 : rw1 + (i - 1) * ZW;
+            // the pair's outer y neighbours are read only for an output column (the row past the
+            // last W row lies outside the ring)
+            const double ya = aw0 ? r0[-ZWX] : 0.0, yb = aw1 ? r1[ZWX] : 0.0;
+            const double Awa = cc * wqa + cm * (r0[-1] + ya + wma) + cp * (r0[1] + wqb + wa_[i]);
+            const double Awb = cc * wqb + cm * (r1[-1] + wqa + wmb) + cp * (r1[1] + yb + wb_[i]);
+            if (aw0) {
+              *wo0 = wqa;
+              acc[0] += wqa * wqa;
+              acc[1] += wqa * Awa;
+              acc[2] += Awa * Awa;
+              if (uslot) acc[KM + 2] += ca[i] * Awa;
+#pragma unroll
+              for (int l = 0; l < KM - 1; ++l)
+                if (FULL || l < nv) acc[3 + l] += ((i == 0) ? vla[l] : va[l][i - 1]) * Awa;
+            }
+            if (aw1) {
+              *wo1 = wqb;
+              acc[0] += wqb * wqb;
+              acc[1] += wqb * Awb;
+              acc[2] += Awb * Awb;
+              if (uslot) acc[KM + 2] += cb[i] * Awb;
+#pragma unroll
+              for (int l = 0; l < KM - 1; ++l)
+                if (FULL || l < nv) acc[3 + l] += ((i == 0) ? vlb[l] : vb[l][i - 1]) * Awb;
+            }
+          }
+          wo0 += pl;
+          wo1 += pl;
+        }
+      }
+      wp2a = ZS >= 2 ? wa_[ZS >= 2 ? ZS - 2 : 0] : wp1a;
+      wp2b = ZS >= 2 ? wb_[ZS >= 2 ? ZS - 2 : 0] : wp1b;
+      wp1a = wa_[ZS - 1];
+      wp1b = wb_[ZS - 1];
+#pragma unroll
+      for (int l = 0; l < KM - 1; ++l) {
+        vla[l] = va[l][ZS - 1];
+        vlb[l] = vb[l][ZS - 1];
+      }
+      wc0 += (int64_t)ZS * pl;
+      wc1 += (int64_t)ZS * pl;
+    };
+    for (int t = 0; t < nsteps; t += 3) {
+      step(t, std::integral_constant<int, 0>{});
+      if (t + 1 < nsteps) step(t + 1, std::integral_constant<int, 1>{});
+      if (t + 2 < nsteps) step(t + 2, std::integral_constant<int, 2>{});
+    }
+    sidx = s0 + (uint32_t)nsteps;
+    __syncthreads();
+  }
+  step_epilogue<KM>(a, &cf, acc, red);
+}
+
 // ---------------------------------------------------------------- host side
 static PFN_cuTensorMapEncodeTiled_v12000 g_enc_zm = nullptr;
 
@@ -307,6 +543,32 @@ constexpr int zm_zs() {
   return zm_smem_bytes<KM, 4>() <= cap ? 4 : (zm_smem_bytes<KM, 2>() <= cap ? 2 : 1);
 }
 
+static int zm_npy() {  // W columns per thread: 1 = step3d_zm_kernel, 2 = step3d_zmp_kernel (SKS_ZM_NPY)
+  static int npy = -1;
+  if (npy < 0) {
+    const char* e = getenv("SKS_ZM_NPY");
+    npy = e ? atoi(e) : ZM_NPY_DEFAULT;
+    if (npy != 1 && npy != 2) npy = ZM_NPY_DEFAULT;
+  }
+  return npy;
+}
+
+template <int KM, int ZS, bool FULL, bool USL>
+static cudaError_t zmp_launch(const StepArgs& a, const ZmArgs& z, const CUtensorMap& mu, const CUtensorMap& mv,
+                              int grid, size_t smem, cudaStream_t st) {
+  static bool set = false;
+  if (!set) {
+    cudaError_t e = cudaFuncSetAttribute(step3d_zmp_kernel<KM, ZS, FULL, USL>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return e;
+    }
+    set = true;
+  }
+  return launch_pdl(step3d_zmp_kernel<KM, ZS, FULL, USL>, grid, ZPT, smem, st, a, z, mu, mv);
+}
+
 bool stencil_zm_supported(int dim, int64_t m, int k) {
   if (dim != 3 || m % 2) return false;  // TMA global strides must be multiples of 16 bytes
   const char* e = getenv("SKS_NO_ZM");
@@ -337,6 +599,7 @@ static cudaError_t zm_launch_v(const StepArgs& a, const ZmArgs& z, const CUtenso
     }
     set = true;
   }
+  if (zm_npy() == 2) return zmp_launch<KM, ZS, FULL, USL>(a, z, mu, mv, grid, smem, st);
   return launch_pdl(step3d_zm_kernel<KM, ZS, FULL, USL>, grid, ZT, smem, st, a, z, mu, mv);
 }
 
