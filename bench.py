@@ -261,7 +261,7 @@ def main():
             "basis_sketch": {"columns_per_s": steps_per_solve / t_basis if t_basis > 0 else None,
                              "gbs": gbs, "t_basis_s": t_basis, "t_solve_s": t_dev,
                              "frac_of_hbm": gbs / peak_total},
-            "roofline": {"bound": "hbm", "kernel": "step3d_zm_kernel (fused truncated-Arnoldi step)",
+            "roofline": {"bound": "hbm", "kernel": "step3d_zmp_kernel (fused truncated-Arnoldi step)",
                          "achieved": step_gbs, "peak": peak_total, "unit": "GB/s", "frac": step_gbs / peak_total,
                          "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy burst)", "traffic": traffic,
                          "bytes_per_launch_alg": b_step / max(n_step, 1),

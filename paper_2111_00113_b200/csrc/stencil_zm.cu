@@ -280,7 +280,7 @@ static_assert(ZWY % 2 == 0, "the pair kernel needs an even tile height");
 constexpr int ZPT = (ZWX * (ZWY / 2) + 31) / 32 * 32;  // 34 x 9 pairs -> 320 threads
 
 template <int KM, int ZS, bool FULL, bool USL>
-__global__ void __launch_bounds__(ZPT, 1)
+__global__ void __launch_bounds__(ZPT, ZM_CPS)
     step3d_zmp_kernel(StepArgs a, ZmArgs z, const __grid_constant__ CUtensorMap tmU,
                       const __grid_constant__ CUtensorMap tmV) {
   extern __shared__ __align__(128) unsigned char smraw_p[];
