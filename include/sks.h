@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SKS_ABI_VERSION 4
+#define SKS_ABI_VERSION 5
 
 typedef enum {
   SKS_OK = 0,
@@ -52,7 +52,8 @@ enum {
   SKS_WARN_COND = 1,       /* kappa_2(T) > cond_tol (Alg. 1, Alg. 2) */
   SKS_WARN_BREAKDOWN = 2,  /* ||w_j|| <= 1e-14 ||m_{j-1}||: basis stopped early (reading O10) */
   SKS_WARN_STAGNATION = 4, /* reserved */
-  SKS_INFO_ADAPTIVE_RESTART = 8 /* SKS_OPT_ADAPTIVE_RESTART ended at least one cycle early */
+  SKS_INFO_ADAPTIVE_RESTART = 8, /* SKS_OPT_ADAPTIVE_RESTART ended at least one cycle early */
+  SKS_INFO_STABILIZED = 16  /* sRR solved the truncated-SVD pencil (SKS_SRR_STABILIZE_*, reading O33) */
 };
 
 typedef struct sks_ctx sks_ctx;
@@ -193,15 +194,24 @@ typedef struct {
   double cond_tol;
   int32_t basis;        /* SKS_BASIS_* */
   int32_t sketch;       /* SKS_SKETCH_* */
-  int32_t reserved[2];
+  int32_t stabilize;    /* SKS_SRR_STABILIZE_* (Sec. "Stabilization"; reading O33) */
+  int32_t reserved1;
   double cheb_c, cheb_dx, cheb_dy;  /* as in sks_sgmres_opts */
 } sks_srr_opts;
+
+/* Stabilised sRR (Alg. 2 P:1679-1681 "stabilize and solve (eq:qz)"): truncated SVD
+ * SB = U Sigma V^* + E keeping sigma_i >= sigma_1 / cond_tol (rank r, reported in info->rank), then
+ * the r x r pencil (U^* SAB V) z = theta Sigma z; y = V z, x = B y.  Computed by a one-sided
+ * Jacobi SVD of SB in one CTA, M_r = Sigma_r^-1 U_r^T SAB V_r and the Francis QR of M_r (Sigma_r
+ * is diagonal with kappa <= cond_tol, reading O33).
+ * OFF: never; IF_ILL: when the kappa_2(T) estimate exceeds cond_tol (Alg. 2's test); ALWAYS. */
+enum { SKS_SRR_STABILIZE_OFF = 0, SKS_SRR_STABILIZE_IF_ILL = 1, SKS_SRR_STABILIZE_ALWAYS = 2 };
 
 typedef struct {
   int32_t columns;
   int32_t flags;
   int32_t nev_out;      /* pairs written: nev, or nev+1 when position nev splits a conjugate pair (O23) */
-  int32_t reserved0;
+  int32_t rank;         /* columns of the Rayleigh-Ritz problem: de (unstabilised) or the truncated rank r */
   double cond_SB;       /* kappa_2 estimate of the triangular factor of SB */
   double t_total_s, t_basis_s, t_small_s;
   double bytes_basis;

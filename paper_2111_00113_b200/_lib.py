@@ -11,6 +11,8 @@ SKS_OK, SKS_EINVAL, SKS_ECUDA, SKS_ENCCL, SKS_ENOMEM, SKS_ENOTCONV, SKS_EUNSUPPO
 STATUS_NAMES = {0: "SKS_OK", -1: "SKS_EINVAL", -2: "SKS_ECUDA", -3: "SKS_ENCCL", -4: "SKS_ENOMEM",
                 -5: "SKS_ENOTCONV", -6: "SKS_EUNSUPPORTED"}
 SKS_WARN_COND, SKS_WARN_BREAKDOWN, SKS_WARN_STAGNATION, SKS_INFO_ADAPTIVE_RESTART = 1, 2, 4, 8
+SKS_INFO_STABILIZED = 16
+STABILIZE = {"off": 0, "if_ill": 1, "always": 2}  # SKS_SRR_STABILIZE_*
 SKS_OP_STENCIL2D, SKS_OP_STENCIL3D, SKS_OP_CSR = 1, 2, 3
 
 # every symbol include/sks.h declares (checked by tests/test_abi.py)
@@ -54,12 +56,12 @@ SKETCHES = {"sparse": SKS_SKETCH_SPARSE, "srft": SKS_SKETCH_SRFT}
 class SrrOpts(C.Structure):
     _fields_ = [("d", C.c_int32), ("k", C.c_int32), ("s", C.c_int32), ("zeta", C.c_int32),
                 ("seed", C.c_uint64), ("cond_tol", C.c_double), ("basis", C.c_int32), ("sketch", C.c_int32),
-                ("reserved", C.c_int32 * 2),
+                ("stabilize", C.c_int32), ("reserved1", C.c_int32),
                 ("cheb_c", C.c_double), ("cheb_dx", C.c_double), ("cheb_dy", C.c_double)]
 
 
 class SrrInfo(C.Structure):
-    _fields_ = [("columns", C.c_int32), ("flags", C.c_int32), ("nev_out", C.c_int32), ("reserved0", C.c_int32),
+    _fields_ = [("columns", C.c_int32), ("flags", C.c_int32), ("nev_out", C.c_int32), ("rank", C.c_int32),
                 ("cond_SB", C.c_double), ("t_total_s", C.c_double), ("t_basis_s", C.c_double),
                 ("t_small_s", C.c_double), ("bytes_basis", C.c_double), ("kernel_launches", C.c_int64),
                 ("steps", C.c_int64)]

@@ -196,7 +196,9 @@ class Context:
 
     # ---------------------------------------------------------------- sRR
     def srr_eigs(self, A, v0, *, d, k, s, nev, zeta=8, seed=0, cond_tol=1e14, want_vectors=False,
-                 basis="arnoldi", cheb=None, sketch="sparse"):
+                 basis="arnoldi", cheb=None, sketch="sparse", stabilize="off"):
+        """stabilize: "off", "if_ill" (kappa(T) > cond_tol, Alg. 2) or "always": truncated-SVD
+        pencil of Sec. "Stabilization", keeping sigma_i >= sigma_1 / cond_tol."""
         op, keep = A.struct()
         va, pv = _prep(v0)
         n = va.shape[0]
@@ -208,8 +210,8 @@ class Context:
             Xr, pxr = _empty_like_place(va, (cap, n))
             Xi, pxi = _empty_like_place(va, (cap, n))
         cc, cdx, cdy = cheb if cheb is not None else (0.0, 0.0, 0.0)
-        opts = L.SrrOpts(d, k, s, zeta, seed, cond_tol, L.BASES[basis], L.SKETCHES[sketch], (C.c_int32 * 2)(),
-                         cc, cdx, cdy)
+        opts = L.SrrOpts(d, k, s, zeta, seed, cond_tol, L.BASES[basis], L.SKETCHES[sketch],
+                         L.STABILIZE[stabilize], 0, cc, cdx, cdy)
         info = L.SrrInfo()
         st = self.lib.sks_srr_eigs(self.h, C.byref(op), pv, C.byref(opts), nev, cap, th_re.ctypes.data,
                                    th_im.ctypes.data, rt.ctypes.data, re.ctypes.data, pxr, pxi, C.byref(info))

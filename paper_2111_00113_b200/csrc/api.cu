@@ -53,7 +53,7 @@ struct sks_ctx {
   int64_t launches = 0;
   // workspaces
   DevBuf W, xb, fb, vb, mr, xg, part, part2, partsk, sigma, H, mnorm, SW, Xp, Zb, U, T, rvec, rho, rest, coef,
-      ctrl, small, Mh, Mh2, wr, wi, sel, th, yr, yi, ework, SAB, SB, Xr, Xi, AXr, AXi, rpb, cib, vab, cig, rbd,
+      ctrl, small, Mh, Mh2, wr, wi, sel, th, yr, yi, ework, SAB, SB, svw, svs, svU, svV, svH, y2r, y2i, Xr, Xi, AXr, AXi, rpb, cib, vab, cig, rbd,
       tmp, bgsw, bgsc, plan, gam, rcoef, srft_q, srft_w;
   CtrlBlock* h_ctrl = nullptr;   // pinned mirror
   double* h_small = nullptr;     // pinned scratch (4096 doubles)
@@ -341,7 +341,8 @@ sks_status sks_destroy(sks_ctx* c) {
                     &c->rho,  &c->rest, &c->coef,  &c->ctrl, &c->small, &c->Mh,  &c->Mh2,   &c->wr,    &c->wi,
                     &c->sel,  &c->th,   &c->yr,    &c->yi,   &c->ework, &c->SAB, &c->SB,    &c->Xr,    &c->Xi,
                     &c->AXr,  &c->AXi,  &c->rpb,   &c->cib,  &c->vab,  &c->cig,  &c->rbd,   &c->tmp,
-                    &c->bgsw, &c->bgsc, &c->plan, &c->gam, &c->rcoef, &c->srft_q, &c->srft_w};
+                    &c->bgsw, &c->bgsc, &c->plan, &c->gam, &c->rcoef, &c->srft_q, &c->srft_w,
+                    &c->svw,  &c->svs,  &c->svU,   &c->svV,  &c->svH,  &c->y2r,   &c->y2i};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->comm) ncclCommDestroy(c->comm);
@@ -1148,6 +1149,8 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
   if (d < 2 || k < 1 || k > SKS_KMAX || s < d + 1 || s > SKS_SMAX || zeta < 1 || zeta > std::min(s, SKS_ZETA_MAX))
     return fail(c, SKS_EINVAL, "need d>=2, 1<=k<=8, d+1<=s<=2048, 1<=zeta<=min(s,16)");
   if (nev < 1 || nev > 11 || nev > d || nev_cap < nev + 1) return fail(c, SKS_EINVAL, "need 1<=nev<=min(11,d), nev_cap>=nev+1");
+  if (o->stabilize < SKS_SRR_STABILIZE_OFF || o->stabilize > SKS_SRR_STABILIZE_ALWAYS)
+    return fail(c, SKS_EINVAL, "unknown stabilize mode");
   cudaSetDevice(c->device);
   const int64_t launches0 = c->launches;
   cudaStream_t st = c->main();
@@ -1216,7 +1219,45 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
                              c->SB.as<double>(), 1, s, c->side));
   SKS_CK(c, launch_cond(c->T.as<double>(), b.ncol, de, 12, nullptr, c->small.as<double>() + 8, c->side));
   SKS_CK(c, cudaEventRecord(c->ev_join, c->side));
-  SKS_CK(c, cudaMemcpyAsync(c->Mh2.p, c->Mh.p, sizeof(double) * (size_t)de * de, cudaMemcpyDeviceToDevice, st));
+  // ---- stabilised sRR (reading O33): truncated SVD SB = U Sigma V^T (one-sided Jacobi);
+  //      the r x r problem M_r = Sigma_r^-1 U_r^T SAB V_r replaces Mhat, y = V_r z
+  const double ctol = o->cond_tol > 0 ? o->cond_tol : 1e14;
+  bool stab = o->stabilize == SKS_SRR_STABILIZE_ALWAYS;
+  if (o->stabilize == SKS_SRR_STABILIZE_IF_ILL) {  // Alg. 2: test kappa_2(T) first
+    SKS_CK(c, cudaStreamWaitEvent(st, c->ev_join, 0));
+    SKS_CK(c, cudaMemcpyAsync(c->h_small + 8, c->small.as<double>() + 8, sizeof(double), cudaMemcpyDeviceToHost, st));
+    SKS_CK(c, cudaStreamSynchronize(st));
+    stab = !(c->h_small[8] <= ctol);  // a non-finite estimate counts as ill-conditioned
+  }
+  int rr = de;  // order of the small eigenproblem
+  if (stab) {
+    SKS_TRY(ensure(c, c->svw, sizeof(double) * ((size_t)s * de + (size_t)de * de + de + 16)));
+    SKS_TRY(ensure(c, c->svs, sizeof(double) * ((size_t)de + 64)));
+    SKS_TRY(ensure(c, c->svU, sizeof(double) * (size_t)s * de));
+    SKS_TRY(ensure(c, c->svV, sizeof(double) * (size_t)de * de));
+    SKS_TRY(ensure(c, c->svH, sizeof(double) * (size_t)de * de));
+    double* sig = c->svs.as<double>();
+    int* svout = reinterpret_cast<int*>(sig + de + 8);
+    SKS_CK(c, cudaStreamWaitEvent(st, c->ev_join, 0));  // SB, SAB from the side stream
+    SKS_CK(c, launch_jacobi_svd(c->SB.as<double>(), s, s, de, ctol, 60, c->svw.as<double>(), sig,
+                                c->svU.as<double>(), c->svV.as<double>(), svout, st));
+    int* hsv = reinterpret_cast<int*>(c->h_small + 16);
+    SKS_CK(c, cudaMemcpyAsync(hsv, svout, sizeof(int) * 3, cudaMemcpyDeviceToHost, st));
+    SKS_CK(c, cudaStreamSynchronize(st));
+    rr = hsv[0];
+    if (!hsv[2]) return fail(c, SKS_ENOTCONV, "Jacobi SVD of SB did not converge");
+    if (rr < 2) return fail(c, SKS_EINVAL, "truncated rank of SB below 2");
+    SKS_CK(c, launch_small_gemm(rr, de, s, c->svU.as<double>(), s, 1, c->SAB.as<double>(), s, 0, nullptr, 0,
+                                c->svH.as<double>(), de, st));  // U_r^T SAB
+    SKS_CK(c, launch_small_gemm(rr, rr, de, c->svH.as<double>(), de, 0, c->svV.as<double>(), de, 0, sig, 1,
+                                c->Mh.as<double>(), rr, st));  // Sigma_r^-1 (U_r^T SAB) V_r
+    // Hessenberg form for the eigen-solvers: M_r = Q H Q^T, V_r <- V_r Q (so y = V_r z_H)
+    SKS_CK(c, launch_hess_reduce(c->Mh.as<double>(), rr, rr, c->svV.as<double>(), de, de, st));
+    flags |= SKS_INFO_STABILIZED;
+    c->launches += 4;
+  }
+  const int nev_e = std::min(nev, rr);
+  SKS_CK(c, cudaMemcpyAsync(c->Mh2.p, c->Mh.p, sizeof(double) * (size_t)rr * rr, cudaMemcpyDeviceToDevice, st));
   SKS_TRY(ensure(c, c->wr, sizeof(double) * de));
   SKS_TRY(ensure(c, c->wi, sizeof(double) * de));
   SKS_TRY(ensure(c, c->sel, sizeof(int) * 64, true));
@@ -1224,21 +1265,34 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
   int* d_info = c->sel.as<int>() + 32;
   int* d_nsel = c->sel.as<int>() + 31;
   SKS_CK(c, cudaMemsetAsync(d_info, 0, sizeof(int) * 5, st));
-  SKS_CK(c, launch_hqr(c->Mh2.as<double>(), de, de, c->wr.as<double>(), c->wi.as<double>(), d_info, st));
+  SKS_CK(c, launch_hqr(c->Mh2.as<double>(), rr, rr, c->wr.as<double>(), c->wi.as<double>(), d_info, st));
   double* th_re = c->th.as<double>();
   double* th_im = th_re + 32;
-  SKS_CK(c, launch_select(c->wr.as<double>(), c->wi.as<double>(), de, nev, c->sel.as<int>(), d_nsel, th_re, th_im,
+  SKS_CK(c, launch_select(c->wr.as<double>(), c->wi.as<double>(), rr, nev_e, c->sel.as<int>(), d_nsel, th_re, th_im,
                           st));
   SKS_TRY(ensure(c, c->ework, sizeof(double) * inverse_iteration_work_doubles(de, nmax)));
   SKS_TRY(ensure(c, c->yr, sizeof(double) * (size_t)de * nmax, true));
   SKS_TRY(ensure(c, c->yi, sizeof(double) * (size_t)de * nmax, true));
   SKS_CK(c, cudaMemsetAsync(c->yr.p, 0, sizeof(double) * (size_t)de * nmax, st));
   SKS_CK(c, cudaMemsetAsync(c->yi.p, 0, sizeof(double) * (size_t)de * nmax, st));
-  SKS_CK(c, launch_inverse_iteration(c->Mh.as<double>(), de, th_re, th_im, d_nsel, nmax, c->ework.as<double>(),
+  SKS_CK(c, launch_inverse_iteration(c->Mh.as<double>(), rr, th_re, th_im, d_nsel, nmax, c->ework.as<double>(),
                                      c->yr.as<double>(), c->yi.as<double>(), 3, 0.0, st));
   SKS_CK(c, cudaStreamWaitEvent(st, c->ev_join, 0));
+  const double* ys_r = c->yr.as<double>();
+  const double* ys_i = c->yi.as<double>();
+  if (stab) {  // y = V_r z (de x nmax)
+    SKS_TRY(ensure(c, c->y2r, sizeof(double) * (size_t)de * nmax));
+    SKS_TRY(ensure(c, c->y2i, sizeof(double) * (size_t)de * nmax));
+    SKS_CK(c, launch_small_gemm(de, nmax, rr, c->svV.as<double>(), de, 0, c->yr.as<double>(), rr, 0, nullptr, 0,
+                                c->y2r.as<double>(), de, st));
+    SKS_CK(c, launch_small_gemm(de, nmax, rr, c->svV.as<double>(), de, 0, c->yi.as<double>(), rr, 0, nullptr, 0,
+                                c->y2i.as<double>(), de, st));
+    ys_r = c->y2r.as<double>();
+    ys_i = c->y2i.as<double>();
+    c->launches += 2;
+  }
   double* d_rest = c->small.as<double>() + 128;
-  SKS_CK(c, launch_srr_rest(c->SAB.as<double>(), c->SB.as<double>(), s, de, c->yr.as<double>(), c->yi.as<double>(),
+  SKS_CK(c, launch_srr_rest(c->SAB.as<double>(), c->SB.as<double>(), s, de, ys_r, ys_i,
                             th_re, th_im, d_nsel, nmax, d_rest, st));
   SKS_CK(c, cudaEventRecord(ev_s1, st));
   c->launches += 14;
@@ -1250,8 +1304,8 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
   SKS_CK(c, cudaMemsetAsync(c->Xr.p, 0, sizeof(double) * (size_t)g.ld * nmax, st));
   SKS_CK(c, cudaMemsetAsync(c->Xi.p, 0, sizeof(double) * (size_t)g.ld * nmax, st));
   SKS_TRY(ensure(c, c->rcoef, sizeof(double) * ritz_coef_doubles(de)));
-  SKS_CK(c, launch_ritz_vectors(c->W.as<double>(), g.ld, g.off, g.n, de, c->sigma.as<double>(), c->yr.as<double>(),
-                                c->yi.as<double>(), de, th_re, th_im, d_nsel, nmax, c->rcoef.as<double>(),
+  SKS_CK(c, launch_ritz_vectors(c->W.as<double>(), g.ld, g.off, g.n, de, c->sigma.as<double>(), ys_r,
+                                ys_i, de, th_re, th_im, d_nsel, nmax, c->rcoef.as<double>(),
                                 c->Xr.as<double>(), c->Xi.as<double>(), g.ld, g.off, c->num_sms, st));
   c->launches += 2;
   const int rgrid = c->num_sms * 2;
@@ -1302,6 +1356,7 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
   if (getenv("SKS_DEBUG_HQR")) fprintf(stderr, "hqr: d=%d sweeps=%d bulge_steps=%d chase_kcyc=%d total_kcyc=%d\n", de, hsel[33],
                                        hsel[34], hsel[35], hsel[36]);
   if (hinfo != 0) return fail(c, SKS_ENOTCONV, "QR algorithm did not converge on Mhat");
+  if (getenv("SKS_DEBUG_SRR") && stab) fprintf(stderr, "srr stabilised: rank %d of %d\n", rr, de);
   for (int v = 0; v < nsel; ++v) {
     theta_re[v] = hs[512 + v];
     theta_im[v] = hs[512 + 32 + v];
@@ -1322,6 +1377,7 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
     info->columns = de;
     info->flags = flags | (hs[8] > (o->cond_tol > 0 ? o->cond_tol : 1e14) ? SKS_WARN_COND : 0);
     info->nev_out = nsel;
+    info->rank = rr;
     info->cond_SB = hs[8];
     float ms = 0.f;
     cudaEventElapsedTime(&ms, c->ev_t0, c->ev_t1);

@@ -109,6 +109,12 @@ size_t inverse_iteration_work_doubles(int d, int nmax);
 cudaError_t launch_inverse_iteration(const double* Mh, int d, const double* th_re, const double* th_im,
                                      const int* nsel, int nmax, double* work, double* yr, double* yi, int iters,
                                      double anorm, cudaStream_t st);
+// svd.cu: stabilised sRR (reading O33)
+cudaError_t launch_jacobi_svd(const double* M, int ldm, int rows, int n, double tol, int max_sweeps, double* work,
+                              double* sigma, double* Ut, double* Vs, int* out, cudaStream_t st);
+cudaError_t launch_hess_reduce(double* M, int n, int ldm, double* V, int vrows, int ldv, cudaStream_t st);
+cudaError_t launch_small_gemm(int M, int N, int K, const double* A, int lda, int ta, const double* B, int ldb,
+                              int tb, const double* rs, int rs_inv, double* C, int ldc, cudaStream_t st);
 cudaError_t launch_srr_rest(const double* D, const double* C, int s, int d, const double* yr, const double* yi,
                             const double* th_re, const double* th_im, const int* nsel, int nmax, double* rest,
                             cudaStream_t st);

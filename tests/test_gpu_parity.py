@@ -326,3 +326,55 @@ def test_srr_srft_parity(ctx):
     out = ctx.srr_eigs(P.StencilOperator(2, m, beta), v0, d=d, k=2, s=2 * d, nev=6, seed=4, sketch="srft")
     orc = O.srr_eigs(lambda v: A @ v, v0, d, 2, 2 * d, 8, 4, 6, sketch="srft")
     assert _match(out["theta"], orc["theta_all"]) <= 1e-8
+
+
+# ---------------------------------------------------------------- stabilised sRR (NEXT(2), reading O33)
+def test_srr_stabilized_without_truncation(ctx):
+    """stabilize="always" on a well-conditioned basis (kappa(T) ~ 1e1 << tol = 1e14): rank r = d, and
+    the pencil Sigma^-1 U^T SAB V is similar to Mhat, so the Ritz values equal the unstabilised
+    device run's and the oracle's (QZ) ones."""
+    P = _P()
+    m, beta, d = 32, 10.0, 40
+    v0 = start_vector(m * m, 4)
+    A = O.stencil_matrix(2, m, beta)
+    op = P.StencilOperator(2, m, beta)
+    plain = ctx.srr_eigs(op, v0, d=d, k=2, s=2 * d, nev=8, seed=4)
+    out = ctx.srr_eigs(op, v0, d=d, k=2, s=2 * d, nev=8, seed=4, stabilize="always")
+    orc = O.srr_eigs(lambda v: A @ v, v0, d, 2, 2 * d, 8, 4, 8, stabilize="always", tol=1e14)
+    assert out["info"]["flags"] & P._lib.SKS_INFO_STABILIZED and not plain["info"]["flags"] & P._lib.SKS_INFO_STABILIZED
+    assert out["info"]["rank"] == d == orc["rank"] and plain["info"]["rank"] == d
+    assert _match(out["theta"], plain["theta"]) <= 1e-10
+    assert _match(out["theta"], orc["theta_all"]) <= 1e-8
+    np.testing.assert_allclose(np.sort(out["res_true"]), np.sort(orc["res_true"]), rtol=1e-4)
+    np.testing.assert_allclose(np.sort(out["res_est"]), np.sort(orc["res_est"]), rtol=1e-4)
+
+
+@pytest.mark.parametrize("mode", ["always", "if_ill"])
+def test_srr_stabilized_ill_conditioned_basis(ctx, mode):
+    """k = 1 basis with kappa_2(T) ~ 1e17: truncation at tol = 1e8 keeps the same rank
+    as the oracle's SVD (its kept / dropped singular values sit a factor >= 1.2 from the threshold,
+    far above the rounding-level differences of the two bases), and the dominant Ritz values agree
+    to 1e-6: the truncated subspace moves by ~u sigma_1 / (sigma_r - sigma_r+1) ~ 1e-8 between the
+    two runs, times the Ritz values' condition numbers."""
+    P = _P()
+    m, beta, d, k, s, tol = 24, 10.0, 200, 1, 420, 1e8
+    v0 = start_vector(m * m, 4)
+    A = O.stencil_matrix(2, m, beta)
+    out = ctx.srr_eigs(P.StencilOperator(2, m, beta), v0, d=d, k=k, s=s, nev=2, seed=4, cond_tol=tol,
+                       stabilize=mode)
+    orc = O.srr_eigs(lambda v: A @ v, v0, d, k, s, 8, 4, 2, stabilize="always", tol=tol)
+    assert out["info"]["flags"] & P._lib.SKS_INFO_STABILIZED
+    assert out["info"]["rank"] == orc["rank"] < d
+    np.testing.assert_allclose(out["theta"], orc["theta"], rtol=1e-6)
+    ev = np.linalg.eigvals(A.toarray())
+    lam1 = ev[np.argmax(np.abs(ev))]
+    assert abs(out["theta"][0] - lam1) <= 1e-5 * abs(lam1)
+    assert out["res_true"][0] <= 1e-5 * abs(lam1)
+
+
+def test_srr_stabilize_if_ill_leaves_well_conditioned_runs_alone(ctx):
+    P = _P()
+    m, beta, d = 32, 10.0, 40
+    v0 = start_vector(m * m, 4)
+    out = ctx.srr_eigs(P.StencilOperator(2, m, beta), v0, d=d, k=2, s=2 * d, nev=4, seed=4, stabilize="if_ill")
+    assert not out["info"]["flags"] & P._lib.SKS_INFO_STABILIZED and out["info"]["rank"] == d

@@ -10,18 +10,21 @@ import paper_2111_00113_b200 as P  # noqa: E402
 from inputs import get_config, start_vector  # noqa: E402
 
 
-def main(name="C5", reps=1):
+def main(name="C5", reps=1, stabilize="off"):
     cfg = get_config(name)
     ctx = P.Context(0)
     v0 = torch.from_numpy(start_vector(cfg.n, cfg.seed)).cuda()
     A = P.StencilOperator(2, cfg.m, cfg.beta)
     for _ in range(reps):
-        out = ctx.srr_eigs(A, v0, d=cfg.d, k=cfg.k, s=cfg.s, nev=cfg.nev, zeta=cfg.zeta, seed=cfg.seed)
+        out = ctx.srr_eigs(A, v0, d=cfg.d, k=cfg.k, s=cfg.s, nev=cfg.nev, zeta=cfg.zeta, seed=cfg.seed,
+                           stabilize=stabilize)
     torch.cuda.synchronize()
     i = out["info"]
-    print(name, "t_total_ms", i["t_total_s"] * 1e3, "t_small_ms", i["t_small_s"] * 1e3, flush=True)
+    print(name, "stabilize", stabilize, "rank", i["rank"], "t_total_ms", i["t_total_s"] * 1e3, "t_small_ms",
+          i["t_small_s"] * 1e3, "theta", out["theta"][:3], "res_true", out["res_true"][:3], flush=True)
     ctx.close()
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "C5", int(sys.argv[2]) if len(sys.argv) > 2 else 1)
+    main(sys.argv[1] if len(sys.argv) > 1 else "C5", int(sys.argv[2]) if len(sys.argv) > 2 else 1,
+         sys.argv[3] if len(sys.argv) > 3 else "off")
