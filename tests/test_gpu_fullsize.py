@@ -99,3 +99,19 @@ def test_full_size_srr_ritz_residuals(ctx):
     # the top Ritz value approximates the largest eigenvalue of A (closed form, Kronecker sum)
     lam_max = O.closed_form_eigs(2, cfg.m, cfg.beta).max()
     assert abs(th[0].real - lam_max) <= 1e-3 * lam_max
+
+
+def test_full_size_srr_stabilized_matches_unstabilised(ctx):
+    """C5 with stabilize="always" (O33): kappa(SB) ~ 27 << cond_tol, so the truncated
+    SVD keeps all d columns and the pencil is similar to Mhat -- the Ritz values and residuals equal
+    the unstabilised run's (the two small problems differ only by rounding: 1e-10 relative)."""
+    cfg = get_config("C5")
+    A, _, _ = _op(cfg)
+    v0 = start_vector(cfg.n, cfg.seed)
+    kw = dict(d=cfg.d, k=cfg.k, s=cfg.s, nev=cfg.nev, zeta=cfg.zeta, seed=cfg.seed)
+    plain = ctx.srr_eigs(A, v0, **kw)
+    stab = ctx.srr_eigs(A, v0, stabilize="always", **kw)
+    assert stab["info"]["rank"] == cfg.d and stab["info"]["flags"] & 16
+    assert len(stab["theta"]) == len(plain["theta"])
+    np.testing.assert_allclose(stab["theta"], plain["theta"], rtol=1e-10)
+    np.testing.assert_allclose(stab["res_true"], plain["res_true"], rtol=1e-6)
