@@ -540,6 +540,9 @@ struct ZmMaps {
 template <int KM>
 constexpr int zm_zs() {
   constexpr size_t cap = (ZM_CPS > 1 ? 226 * 1024 / ZM_CPS - 1024 : 200 * 1024);
+#ifdef ZM_ZS  // experiment: planes per step (falls back when the stages do not fit)
+  if (zm_smem_bytes<KM, ZM_ZS>() <= 226 * 1024 / ZM_CPS - 1024) return ZM_ZS;
+#endif
   return zm_smem_bytes<KM, 4>() <= cap ? 4 : (zm_smem_bytes<KM, 2>() <= cap ? 2 : 1);
 }
 
