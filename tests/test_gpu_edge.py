@@ -159,3 +159,48 @@ def test_smallest_stencil_m2(ctx):
         assert res.info["cycles"] == orc["cycles"]
         np.testing.assert_allclose(res.x, orc["x"], rtol=0, atol=1e-9 * np.abs(x_exact).max())
         assert np.linalg.norm(res.x - x_exact) <= 1e-9 * np.linalg.norm(x_exact)
+
+
+def test_srr_rejects_unknown_stabilize_mode(ctx):
+    """opts.stabilize outside SKS_SRR_STABILIZE_* is an argument error (sks.h), checked in the C ABI."""
+    import ctypes as C
+    P = _P()
+    L = P._lib
+    A = P.StencilOperator(2, 16, 5.0)
+    op, keep = A.struct()
+    v0 = np.ascontiguousarray(start_vector(256, 4))
+    opts = L.SrrOpts(20, 2, 40, 8, 4, 1e14, 0, 0, 7, 0, 0.0, 0.0, 0.0)
+    out = [np.zeros(5) for _ in range(4)]
+    info = L.SrrInfo()
+    st = ctx.lib.sks_srr_eigs(ctx.h, C.byref(op), v0.ctypes.data, C.byref(opts), 4, 5, out[0].ctypes.data,
+                              out[1].ctypes.data, out[2].ctypes.data, out[3].ctypes.data, None, None, C.byref(info))
+    assert st == -1
+
+
+def test_srr_stabilized_rank_below_two_is_rejected(ctx):
+    """cond_tol = 1 keeps only sigma_1 (rank 1): no 2-column Rayleigh-Ritz problem -> SKS_EINVAL."""
+    P = _P()
+    with pytest.raises(P.SksError) as e:
+        ctx.srr_eigs(P.StencilOperator(2, 16, 5.0), start_vector(256, 4), d=20, k=2, s=40, nev=4, seed=4,
+                     cond_tol=1.0, stabilize="always")
+    assert e.value.status == -1
+
+
+def test_srr_stabilized_rank_below_nev(ctx):
+    """Truncation to rank 3 < nev = 4 (tol placed between sigma_1/sigma_3 and sigma_1/sigma_4 of the
+    oracle's SB): at most rank (+ a conjugate partner) pairs come back, equal to the oracle's rank-3
+    pencil (QZ)."""
+    P = _P()
+    m, beta, d = 16, 5.0, 20
+    v0 = start_vector(m * m, 4)
+    A = O.stencil_matrix(2, m, beta)
+    ref = O.srr_eigs(lambda v: A @ v, v0, d, 2, 2 * d, 8, 4, 4, stabilize="always", tol=1e14)
+    sig = ref["sigma"]
+    tol = np.sqrt((sig[0] / sig[2]) * (sig[0] / sig[3]))
+    orc = O.srr_eigs(lambda v: A @ v, v0, d, 2, 2 * d, 8, 4, 4, stabilize="always", tol=tol)
+    assert orc["rank"] == 3
+    out = ctx.srr_eigs(P.StencilOperator(2, m, beta), v0, d=d, k=2, s=2 * d, nev=4, seed=4, cond_tol=tol,
+                       stabilize="always")
+    assert out["info"]["rank"] == 3 and 1 <= out["info"]["nev_out"] <= 4
+    err = max(np.abs(orc["theta_all"] - t).min() / np.abs(t) for t in out["theta"])
+    assert err <= 1e-8
