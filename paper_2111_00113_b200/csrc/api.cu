@@ -1252,7 +1252,8 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
     SKS_CK(c, launch_small_gemm(rr, rr, de, c->svH.as<double>(), de, 0, c->svV.as<double>(), de, 0, sig, 1,
                                 c->Mh.as<double>(), rr, st));  // Sigma_r^-1 (U_r^T SAB) V_r
     // Hessenberg form for the eigen-solvers: M_r = Q H Q^T, V_r <- V_r Q (so y = V_r z_H)
-    SKS_CK(c, launch_hess_reduce(c->Mh.as<double>(), rr, rr, c->svV.as<double>(), de, de, st));
+    SKS_CK(c, launch_hess_reduce(c->Mh.as<double>(), rr, rr, c->svV.as<double>(), de, de,
+                                 reinterpret_cast<unsigned*>(sig + de + 16), st));
     flags |= SKS_INFO_STABILIZED;
     c->launches += 4;
   }

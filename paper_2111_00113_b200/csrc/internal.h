@@ -112,7 +112,8 @@ cudaError_t launch_inverse_iteration(const double* Mh, int d, const double* th_r
 // svd.cu: stabilised sRR (reading O33)
 cudaError_t launch_jacobi_svd(const double* M, int ldm, int rows, int n, double tol, int max_sweeps, double* work,
                               double* sigma, double* Ut, double* Vs, int* out, cudaStream_t st);
-cudaError_t launch_hess_reduce(double* M, int n, int ldm, double* V, int vrows, int ldv, cudaStream_t st);
+cudaError_t launch_hess_reduce(double* M, int n, int ldm, double* V, int vrows, int ldv, unsigned* scratch,
+                               cudaStream_t st);
 cudaError_t launch_small_gemm(int M, int N, int K, const double* A, int lda, int ta, const double* B, int ldb,
                               int tb, const double* rs, int rs_inv, double* C, int ldc, cudaStream_t st);
 cudaError_t launch_srr_rest(const double* D, const double* C, int s, int d, const double* yr, const double* yi,

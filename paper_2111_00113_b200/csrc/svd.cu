@@ -166,12 +166,15 @@ __global__ void __launch_bounds__(SV_THREADS, 1)
   }
 }
 
-// ---- multi-CTA version (rows <= 32 * JR_RPL): the pairs of a round are spread over every warp of a
+// ---- multi-CTA version (rows, n <= 32 * JR_RPL): the pairs of a round are spread over every warp of a
 // cooperative grid (one grid barrier per round); each warp holds its two columns in registers for
 // the dots and the rotation (one pass over A per pair).  Same pair order, reductions and criterion
 // and per-pair arithmetic as jacobi_svd_kernel.
 constexpr int JR_RPL = 24;         // rows per lane held in registers (rows <= 768)
-constexpr int JC_THREADS = 256;    // 8 warps per CTA
+#ifndef JC_THREADS_DEF
+#define JC_THREADS_DEF 64
+#endif
+constexpr int JC_THREADS = JC_THREADS_DEF;  // warps per CTA x 32
 constexpr int JC_WARPS = JC_THREADS / 32;
 
 __device__ __forceinline__ void jc_grid_barrier(unsigned* count, volatile unsigned* gen, unsigned nblocks) {
@@ -273,10 +276,19 @@ __global__ void __launch_bounds__(JC_THREADS)
         }
         double* vp = Vw + (int64_t)p * n;
         double* vq = Vw + (int64_t)q * n;
-        for (int r = lane; r < n; r += 32) {
-          const double a = vp[r], b = vq[r];
-          vp[r] = cs * a - sn * b;
-          vq[r] = sn * a + cs * b;
+#pragma unroll
+        for (int u = 0; u < JR_RPL; ++u) {  // all loads in flight before the stores
+          const int r = lane + 32 * u;
+          x[u] = r < n ? vp[r] : 0.0;
+          y[u] = r < n ? vq[r] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < JR_RPL; ++u) {
+          const int r = lane + 32 * u;
+          if (r < n) {
+            vp[r] = cs * x[u] - sn * y[u];
+            vq[r] = sn * x[u] + cs * y[u];
+          }
         }
         if (lane == 0) atomicOr(sync + 2 + (sweep & 1), 1u);
       }
@@ -358,7 +370,7 @@ cudaError_t launch_jacobi_svd(const double* M, int ldm, int rows, int n, double 
     e = cudaFuncSetAttribute(jacobi_svd_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  if (rows > 32 * JR_RPL || force_single) {
+  if (rows > 32 * JR_RPL || n > 32 * JR_RPL || force_single) {
     jacobi_svd_kernel<<<1, SV_THREADS, smem, st>>>(M, ldm, rows, n, tol, max_sweeps, work, sigma, Ut, Vs, out);
     return cudaGetLastError();
   }
@@ -445,13 +457,118 @@ __global__ void __launch_bounds__(SV_THREADS, 1)
   }
 }
 
-cudaError_t launch_hess_reduce(double* M, int n, int ldm, double* V, int vrows, int ldv, cudaStream_t st) {
+// ---- multi-CTA Householder reduction (same reflectors and update order per element as
+// hess_reduce_kernel): every CTA forms the reflector of column j redundantly from global memory (no
+// broadcast), the left update is spread over the grid's warps by column, the right update over its
+// CTAs by 32-row blocks; two grid barriers per column.
+constexpr int HC_THREADS = 256;
+constexpr int HC_WARPS = HC_THREADS / 32;
+__global__ void __launch_bounds__(HC_THREADS)
+    hess_reduce_coop_kernel(double* __restrict__ M, int n, int ldm, double* __restrict__ V, int vrows, int ldv,
+                            unsigned* __restrict__ sync) {
+  extern __shared__ double hcv[];  // [n] reflector
+  __shared__ double red[HC_WARPS];
+  __shared__ double hpart[HC_WARPS * 32];
+  __shared__ double sh_beta, sh_alpha;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int gw = blockIdx.x * HC_WARPS + wid, nwg = gridDim.x * HC_WARPS;
+  const unsigned nb = gridDim.x;
+  for (int j = 0; j + 2 < n; ++j) {
+    const int m0 = j + 1, len = n - m0;
+    double ss = 0.0;
+    for (int i = tid; i < len; i += HC_THREADS) {
+      const double x = M[(m0 + i) + (int64_t)j * ldm];
+      hcv[i] = x;
+      ss = fma(x, x, ss);
+    }
+    ss = sv_warp_sum(ss);
+    if (lane == 0) red[wid] = ss;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int q = 0; q < HC_WARPS; ++q) t += red[q];
+      const double x0 = hcv[0];
+      if (t - x0 * x0 <= 0.0) {
+        sh_beta = 0.0;
+      } else {
+        const double nx = sqrt(t);
+        const double alpha = x0 >= 0.0 ? -nx : nx;
+        hcv[0] = x0 - alpha;
+        sh_alpha = alpha;
+        sh_beta = 1.0 / (nx * (nx + fabs(x0)));
+      }
+    }
+    __syncthreads();
+    const double beta = sh_beta;
+    if (beta != 0.0) {  // grid-uniform (every CTA computed the same value)
+      for (int c = j + 1 + gw; c < n; c += nwg) {
+        double* col = M + (int64_t)c * ldm + m0;
+        double t = 0.0;
+        for (int i = lane; i < len; i += 32) t = fma(hcv[i], col[i], t);
+        t = sv_warp_sum(t) * beta;
+        for (int i = lane; i < len; i += 32) col[i] = fma(-t, hcv[i], col[i]);
+      }
+    }
+    jc_grid_barrier(sync, sync + 1, nb);  // column j read by every CTA; left update done
+    if (beta != 0.0) {
+      if (blockIdx.x == 0)
+        for (int i = tid; i < len; i += HC_THREADS) M[(m0 + i) + (int64_t)j * ldm] = (i == 0) ? sh_alpha : 0.0;
+      // right update by 32-row blocks (lane = row, coalesced): the CTA's warps split the reflector
+      // length into HC_WARPS chunks, partial sums combined in a fixed order in shared memory
+      const int nrb = (n + vrows + 31) / 32;
+      const int chunk = (len + HC_WARPS - 1) / HC_WARPS;
+      const int i0 = wid * chunk, i1 = min(len, i0 + chunk);
+      for (int rb = blockIdx.x; rb < nrb; rb += gridDim.x) {
+        const int r = rb * 32 + lane;
+        const bool ok = r < n + vrows;
+        double* base = r < n ? M + r : V + (ok ? r - n : 0);
+        const int64_t ld = r < n ? ldm : ldv;
+        double t = 0.0;
+        if (ok)
+          for (int i = i0; i < i1; ++i) t = fma(base[(int64_t)(m0 + i) * ld], hcv[i], t);
+        hpart[wid * 32 + lane] = t;
+        __syncthreads();
+        double tr = 0.0;
+#pragma unroll
+        for (int w = 0; w < HC_WARPS; ++w) tr += hpart[w * 32 + lane];
+        tr *= beta;
+        if (ok)
+          for (int i = i0; i < i1; ++i) base[(int64_t)(m0 + i) * ld] = fma(-tr, hcv[i], base[(int64_t)(m0 + i) * ld]);
+        __syncthreads();
+      }
+    }
+    jc_grid_barrier(sync, sync + 1, nb);
+  }
+}
+
+// scratch: 8 unsigned of device memory for the grid barrier (NULL: single-CTA kernel)
+cudaError_t launch_hess_reduce(double* M, int n, int ldm, double* V, int vrows, int ldv, unsigned* scratch,
+                               cudaStream_t st) {
   const size_t smem = sizeof(double) * n;
+  static int force_single = -1;
+  if (force_single < 0) force_single = getenv("SKS_HESS_SINGLE") ? 1 : 0;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(hess_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(hess_reduce_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
   }
-  hess_reduce_kernel<<<1, SV_THREADS, smem, st>>>(M, n, ldm, V, vrows, ldv);
+  if (scratch == nullptr || force_single) {
+    hess_reduce_kernel<<<1, SV_THREADS, smem, st>>>(M, n, ldm, V, vrows, ldv);
+    return cudaGetLastError();
+  }
+  int dev = 0, nsm = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hess_reduce_coop_kernel, HC_THREADS, smem);
+  // a CTA per 32-row block of the right update, enough warps for the columns of the left update
+  int grid = std::max((n + vrows + 31) / 32, (n + HC_WARPS - 1) / HC_WARPS);
+  grid = std::max(1, std::min(grid, nsm * std::max(per_sm, 1)));
+  cudaError_t e = cudaMemsetAsync(scratch, 0, 8 * sizeof(unsigned), st);
+  if (e != cudaSuccess) return e;
+  void* args[] = {(void*)&M, (void*)&n, (void*)&ldm, (void*)&V, (void*)&vrows, (void*)&ldv, (void*)&scratch};
+  e = cudaLaunchCooperativeKernel((const void*)hess_reduce_coop_kernel, dim3(grid), dim3(HC_THREADS), args, smem, st);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
