@@ -55,6 +55,9 @@ constexpr int ZW = ZWX * ZWY;                    // 612
 constexpr int ZRX = ZM_PITCH ? ZUX : ZWX;        // thread-row width = ring row pitch
 constexpr int ZR = ZRX * ZWY;                    // ring plane (648 doubles)
 constexpr int ZT = (ZRX * ZWY + 31) / 32 * 32;
+#ifndef ZM_EARLY
+#define ZM_EARLY 1  // pair kernel: issue the first two stages before the prologue's reduction
+#endif
 #ifndef ZM_NPY_DEFAULT
 #define ZM_NPY_DEFAULT 2
 #endif  // threads (32 x 16 tile: 672 = 21 warps)
@@ -301,10 +304,32 @@ __global__ void __launch_bounds__(ZPT, ZM_CPS)
     fence_mbar_init();
   }
   pdl_wait_and_release();
-  if (!step_prologue(a, &cf, red)) return;
-  const int nv = FULL ? KM - 1 : cf.nv;
+  const int nv = FULL ? KM - 1 : z.nv;  // = cf.nv (host-known), so the first stages can go out now
   const uint32_t sbytes = (uint32_t)(ZUP * (ZS + 2) * 8 + nv * ZVP * ZS * 8);
   const int m = (int)a.m, nz = (int)a.nz, z0g = (int)a.z0, G = a.G;
+  const int64_t u_lo = (z.units * blockIdx.x) / gridDim.x, u_hi = (z.units * (blockIdx.x + 1)) / gridDim.x;
+  // the first piece's first two stages are issued before the partials reduction of the prologue:
+  // their inputs (w_{j-1} and the window) were complete at the PDL wait
+  int pre = 0;
+  if (ZM_EARLY && tid == 0 && u_lo < u_hi) {
+    const int col = (int)(u_lo / nz), za = (int)(u_lo % nz);
+    const int64_t zr = za + (u_hi - u_lo);
+    const int zb = (int)(zr < nz ? zr : nz);
+    const int x0 = (col % z.tiles_x) * ZX, y0 = (col / z.tiles_x) * ZY, wa = za - 1;
+    const int nsteps = (zb - wa + 1 + ZS - 1) / ZS;
+    for (int t = 0; t < 2 && t < nsteps; ++t) {
+      double* dst = sm + t * STG;
+      const int p0 = wa + t * ZS;
+      mbar_arrive_expect_tx(&bar[t], sbytes);
+      tma_load_4d(dst, &tmU, &bar[t], x0 - 2, y0 - 2, p0 - 1 + G, z.ucol);
+      for (int l = 0; l < nv; ++l) tma_load_4d(dst + UB + l * VB, &tmV, &bar[t], x0 - 2, y0 - 1, p0 + G, z.vcol[l]);
+      pre = t + 1;
+    }
+  }
+  if (!step_prologue(a, &cf, red)) {
+    for (int t = 0; t < pre; ++t) mbar_wait(&bar[t], 0u);  // no bulk copy may outlive the CTA
+    return;
+  }
   const int64_t pl = a.plane;
   const double cc = a.cc, cm = a.cm, cp = a.cp, alpha = cf.alpha, beta_u = cf.beta_u;
   double cl[KM - 1];
@@ -327,7 +352,7 @@ __global__ void __launch_bounds__(ZPT, ZM_CPS)
 #pragma unroll
   for (int i = 0; i < KM + 3; ++i) acc[i] = 0.0;
   uint32_t phase = 0, sidx = 0;
-  const int64_t u_lo = (z.units * blockIdx.x) / gridDim.x, u_hi = (z.units * (blockIdx.x + 1)) / gridDim.x;
+  bool first = true;
   for (int64_t u = u_lo; u < u_hi;) {
     const int col = (int)(u / nz);
     const int za = (int)(u % nz);
@@ -347,10 +372,11 @@ __global__ void __launch_bounds__(ZPT, ZM_CPS)
       tma_load_4d(dst, &tmU, &bar[slot], x0 - 2, y0 - 2, p0 - 1 + G, z.ucol);
       for (int l = 0; l < nv; ++l) tma_load_4d(dst + UB + l * VB, &tmV, &bar[slot], x0 - 2, y0 - 1, p0 + G, z.vcol[l]);
     };
-    if (tid == 0) {
+    if (tid == 0 && !(ZM_EARLY && first)) {
       issue(0);
       if (nsteps > 1) issue(1);
     }
+    first = false;
     double wp1a = 0.0, wp2a = 0.0, wp1b = 0.0, wp2b = 0.0;
     double vla[KM - 1], vlb[KM - 1];
 #pragma unroll
