@@ -55,6 +55,9 @@ constexpr int ZW = ZWX * ZWY;                    // 612
 constexpr int ZRX = ZM_PITCH ? ZUX : ZWX;        // thread-row width = ring row pitch
 constexpr int ZR = ZRX * ZWY;                    // ring plane (648 doubles)
 constexpr int ZT = (ZRX * ZWY + 31) / 32 * 32;
+#ifndef ZM_NEXT
+#define ZM_NEXT 1  // pair kernel: prefetch the next piece's first stages during this piece's last steps
+#endif
 #ifndef ZM_EARLY
 #define ZM_EARLY 1  // pair kernel: issue the first two stages before the prologue's reduction
 #endif
@@ -352,7 +355,7 @@ __global__ void __launch_bounds__(ZPT, ZM_CPS)
 #pragma unroll
   for (int i = 0; i < KM + 3; ++i) acc[i] = 0.0;
   uint32_t phase = 0, sidx = 0;
-  bool first = true;
+  int carried = pre;  // stages of the coming piece already in flight (thread 0's count)
   for (int64_t u = u_lo; u < u_hi;) {
     const int col = (int)(u / nz);
     const int za = (int)(u % nz);
@@ -372,11 +375,25 @@ __global__ void __launch_bounds__(ZPT, ZM_CPS)
       tma_load_4d(dst, &tmU, &bar[slot], x0 - 2, y0 - 2, p0 - 1 + G, z.ucol);
       for (int l = 0; l < nv; ++l) tma_load_4d(dst + UB + l * VB, &tmV, &bar[slot], x0 - 2, y0 - 1, p0 + G, z.vcol[l]);
     };
-    if (tid == 0 && !(ZM_EARLY && first)) {
-      issue(0);
-      if (nsteps > 1) issue(1);
-    }
-    first = false;
+    // the next piece (if any): its first two stages go out in the slots freed by this piece's last
+    // two steps, so its pipeline fill overlaps this piece's tail
+    const bool has_next = u < u_hi;
+    const int ncol = has_next ? (int)(u / nz) : 0, nza = has_next ? (int)(u % nz) : 0;
+    const int64_t nzr = nza + (u_hi - u);
+    const int nzb = (int)(nzr < nz ? nzr : nz);
+    const int nx0 = (ncol % z.tiles_x) * ZX, ny0 = (ncol / z.tiles_x) * ZY, nwa = nza - 1;
+    const int nnsteps = has_next ? (nzb - nwa + 1 + ZS - 1) / ZS : 0;
+    auto issue_next = [&](int tn) {
+      const uint32_t slot = (s0 + (uint32_t)nsteps + (uint32_t)tn) & 1u;
+      double* dst = sm + slot * STG;
+      const int p0 = nwa + tn * ZS;
+      mbar_arrive_expect_tx(&bar[slot], sbytes);
+      tma_load_4d(dst, &tmU, &bar[slot], nx0 - 2, ny0 - 2, p0 - 1 + G, z.ucol);
+      for (int l = 0; l < nv; ++l) tma_load_4d(dst + UB + l * VB, &tmV, &bar[slot], nx0 - 2, ny0 - 1, p0 + G, z.vcol[l]);
+    };
+    if (tid == 0)
+      for (int t = carried; t < 2 && t < nsteps; ++t) issue(t);
+    carried = 0;
     double wp1a = 0.0, wp2a = 0.0, wp1b = 0.0, wp2b = 0.0;
     double vla[KM - 1], vlb[KM - 1];
 #pragma unroll
@@ -461,7 +478,17 @@ __global__ void __launch_bounds__(ZPT, ZM_CPS)
         }
       }
       __syncthreads();
-      if (tid == 0 && t + 2 < nsteps) issue(t + 2);
+      if (tid == 0) {
+        if (t + 2 < nsteps) {
+          issue(t + 2);
+        } else if (ZM_NEXT && has_next && nsteps >= 2) {
+          const int tn = t + 2 - nsteps;  // 0 after step nsteps-2, 1 after step nsteps-1
+          if (tn < nnsteps) {
+            issue_next(tn);
+            carried = tn + 1;
+          }
+        }
+      }
       if (aw0 || aw1) {
         double* wo0 = wc0;
         double* wo1 = wc1;
