@@ -19,6 +19,7 @@
 //     window dots in registers.
 #include <cudaTypedefs.h>
 
+#include <climits>
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
@@ -55,6 +56,9 @@ constexpr int ZW = ZWX * ZWY;                    // 612
 constexpr int ZRX = ZM_PITCH ? ZUX : ZWX;        // thread-row width = ring row pitch
 constexpr int ZR = ZRX * ZWY;                    // ring plane (648 doubles)
 constexpr int ZT = (ZRX * ZWY + 31) / 32 * 32;
+#ifndef ZM_BALANCE_DEFAULT
+#define ZM_BALANCE_DEFAULT 1
+#endif
 #ifndef ZM_NEXT
 #define ZM_NEXT 1  // pair kernel: prefetch the next piece's first stages during this piece's last steps
 #endif
@@ -65,6 +69,7 @@ constexpr int ZT = (ZRX * ZWY + 31) / 32 * 32;
 #define ZM_NPY_DEFAULT 2
 #endif  // threads (32 x 16 tile: 672 = 21 warps)
 
+constexpr int ZM_MAXG = 2 * 148;  // CTAs covered by the partition table
 struct ZmArgs {
   int ucol;
   int vcol[SKS_KMAX];
@@ -72,6 +77,8 @@ struct ZmArgs {
   int tiles_x;
   int64_t units;   // ncolxy * nz
   int nv;          // window vectors of this launch (= StepCoef::nv, known on the host)
+  int use_ub;      // 1: CTA b owns units [ub[b], ub[b+1]) (step-balanced partition), else proportional
+  int32_t ub[ZM_MAXG + 1];
 };
 
 __host__ __device__ constexpr int zm_al16(int d) { return (d + 15) & ~15; }  // 128-byte multiple (doubles)
@@ -139,7 +146,8 @@ __global__ void __launch_bounds__(ZT, ZM_CPS)
 
   uint32_t phase = 0;  // parity bits of the two stage barriers
   uint32_t sidx = 0;   // global stage counter (slot = sidx & 1)
-  const int64_t u_lo = (z.units * blockIdx.x) / gridDim.x, u_hi = (z.units * (blockIdx.x + 1)) / gridDim.x;
+  const int64_t u_lo = z.use_ub ? (int64_t)z.ub[blockIdx.x] : (z.units * blockIdx.x) / gridDim.x;
+  const int64_t u_hi = z.use_ub ? (int64_t)z.ub[blockIdx.x + 1] : (z.units * (blockIdx.x + 1)) / gridDim.x;
   for (int64_t u = u_lo; u < u_hi;) {
     const int col = (int)(u / nz);
     const int za = (int)(u % nz);
@@ -310,7 +318,8 @@ __global__ void __launch_bounds__(ZPT, ZM_CPS)
   const int nv = FULL ? KM - 1 : z.nv;  // = cf.nv (host-known), so the first stages can go out now
   const uint32_t sbytes = (uint32_t)(ZUP * (ZS + 2) * 8 + nv * ZVP * ZS * 8);
   const int m = (int)a.m, nz = (int)a.nz, z0g = (int)a.z0, G = a.G;
-  const int64_t u_lo = (z.units * blockIdx.x) / gridDim.x, u_hi = (z.units * (blockIdx.x + 1)) / gridDim.x;
+  const int64_t u_lo = z.use_ub ? (int64_t)z.ub[blockIdx.x] : (z.units * blockIdx.x) / gridDim.x;
+  const int64_t u_hi = z.use_ub ? (int64_t)z.ub[blockIdx.x + 1] : (z.units * (blockIdx.x + 1)) / gridDim.x;
   // the first piece's first two stages are issued before the partials reduction of the prologue:
   // their inputs (w_{j-1} and the window) were complete at the PDL wait
   int pre = 0;
@@ -588,6 +597,9 @@ static bool zm_encode(CUtensorMap* out, const double* base, int64_t m, int64_t n
 struct ZmMaps {
   CUtensorMap WU, WV, XU, FV, VU;
   const void* key[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  int64_t part_key = -1;  // step-balanced partition cache
+  bool part_ok = false;
+  int32_t ub[ZM_MAXG + 1];
 };
 
 template <int KM>
@@ -630,6 +642,39 @@ bool stencil_zm_supported(int dim, int64_t m, int k) {
   const char* e = getenv("SKS_NO_ZM");
   if (e && e[0] == '1') return false;
   return zm_encode_fn();
+}
+
+// Step-balanced partition of the (tile, plane) units over the grid: a piece of len planes costs
+// ceil((len + 2) / zs) steps (two halo planes), so the proportional split leaves the CTAs whose range
+// crosses a column boundary up to a step behind.  Greedy fill with a cap of C steps per CTA, C the
+// smallest cap that covers every unit (binary search); pieces end at column boundaries as in the kernel.
+static bool zm_partition(int64_t units, int64_t nz, int grid, int zs, int32_t* ub) {
+  if (grid > ZM_MAXG || units > INT32_MAX) return false;
+  auto fill = [&](int64_t C, bool write) -> bool {
+    int64_t u = 0;
+    if (write) ub[0] = 0;
+    for (int b = 0; b < grid; ++b) {
+      int64_t k = C;
+      while (u < units && k > 0) {
+        const int64_t rem = nz - (u % nz);
+        const int64_t cap = zs * k - 2;
+        if (cap < 1) break;
+        const int64_t len = std::min(rem, cap);
+        u += len;
+        k -= (len + 2 + zs - 1) / zs;
+      }
+      if (write) ub[b + 1] = (int32_t)u;
+    }
+    return u >= units;
+  };
+  int64_t lo = 1, hi = units + 2;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    if (fill(mid, false)) hi = mid;
+    else lo = mid + 1;
+  }
+  fill(lo, true);
+  return ub[grid] == units;
 }
 
 void stencil_zm_tiling(int64_t m, int64_t nz, int num_sms, StepArgs* a, int* grid) {
@@ -695,6 +740,24 @@ cudaError_t launch_step_stencil_zm(const StepArgs& a, const double* W, int64_t n
   z.ncolxy = a.tiles_x * a.tiles_y;
   z.units = a.ntiles;
   z.nv = (a.mode == 0) ? std::min(a.j, a.k) - 1 : (a.mode == 1 ? 1 : 0);
+  {  // step-balanced partition, cached per (units, nz, grid, zs)
+    static int bal = -1;
+    if (bal < 0) {
+      const char* e = getenv("SKS_ZM_BALANCE");
+      bal = e ? (e[0] == '1') : ZM_BALANCE_DEFAULT;
+    }
+    if (bal) {
+      const int64_t pk = z.units * 1000003 + a.nz * 131 + grid * 7 + zs;
+      if (mp->part_key != pk) {
+        mp->part_ok = zm_partition(z.units, a.nz, grid, zs, mp->ub);
+        mp->part_key = pk;
+      }
+      if (mp->part_ok) {
+        z.use_ub = 1;
+        memcpy(z.ub, mp->ub, sizeof(int32_t) * (grid + 1));
+      }
+    }
+  }
   const CUtensorMap* mu;
   const CUtensorMap* mv;
   if (a.mode == 0) {
