@@ -24,6 +24,7 @@ namespace sks {
 struct TmaCols {
   int ucol;
   int vcol[SKS_KMAX];
+  int nv;  // window vectors of this launch (= StepCoef::nv, known on the host)
 };
 
 // ---------------------------------------------------------------- 3D
@@ -202,21 +203,13 @@ __global__ void __launch_bounds__(QT, 1)
     fence_mbar_init();
   }
   pdl_wait_and_release();
-  if (!step_prologue(a, &cf, red)) return;
   constexpr int STAGE = QU2 + (KM - 1) * QB2P;
   double* sW = smt + NST * STAGE;
-  const int nv = cf.nv;
+  const int nv = tc.nv;  // = cf.nv: the first tiles' loads go out before the prologue's reduction
   const uint32_t bytes = (uint32_t)(QU2 * 8 + nv * QB2 * 8);
-  const int64_t m = a.m, nz = a.nz;
-  const int G = a.G;
-  const double cc = a.cc, cm = a.cm, cp = a.cp, alpha = cf.alpha, beta_u = cf.beta_u;
-  double cl[KM - 1];
-#pragma unroll
-  for (int l = 0; l < KM - 1; ++l) cl[l] = (l < nv) ? cf.c[l] : 0.0;
-  double* Wout = a.W + (a.mode == 0 ? (int64_t)a.j * a.ld : 0) + a.off;
   const int ntx = a.tiles_x;
   const int64_t ntiles = a.ntiles;
-
+  const int G = a.G;
   auto issue = [&](int64_t tile, int s) {
     const int tx = (int)(tile % ntx);
     const int ty = (int)(tile / ntx);
@@ -226,16 +219,34 @@ __global__ void __launch_bounds__(QT, 1)
     for (int l = 0; l < nv; ++l)
       tma_load_3d(base + QU2 + l * QB2P, &tmV, &bar[s], tx * Q2X - 2, ty * Q2Y - 1 + G, tc.vcol[l]);
   };
+  const int64_t first = blockIdx.x, stride = gridDim.x;
+  int pre = 0;
+  if (tid == 0 && first < ntiles) {
+    issue(first, 0);
+    pre = 1;
+    if (NST == 2 && first + stride < ntiles) {
+      issue(first + stride, 1);
+      pre = 2;
+    }
+  }
+  if (!step_prologue(a, &cf, red)) {
+    for (int s = 0; s < pre; ++s) mbar_wait(&bar[s], 0u);  // no bulk copy may outlive the CTA
+    return;
+  }
+  const int64_t m = a.m, nz = a.nz;
+  const double cc = a.cc, cm = a.cm, cp = a.cp, alpha = cf.alpha, beta_u = cf.beta_u;
+  double cl[KM - 1];
+#pragma unroll
+  for (int l = 0; l < KM - 1; ++l) cl[l] = (l < nv) ? cf.c[l] : 0.0;
+  double* Wout = a.W + (a.mode == 0 ? (int64_t)a.j * a.ld : 0) + a.off;
 
   double acc[KM + 3];
 #pragma unroll
   for (int i = 0; i < KM + 3; ++i) acc[i] = 0.0;
-  const int64_t first = blockIdx.x, stride = gridDim.x;
-  if (tid == 0 && first < ntiles) issue(first, 0);
   int it = 0;
   for (int64_t tile = first; tile < ntiles; tile += stride, ++it) {
     const int s = (NST == 2) ? (it & 1) : 0;
-    if (NST == 2 && tid == 0 && tile + stride < ntiles) issue(tile + stride, s ^ 1);
+    if (NST == 2 && tid == 0 && it >= 1 && tile + stride < ntiles) issue(tile + stride, s ^ 1);
     const int64_t x0 = (tile % ntx) * Q2X, yt0 = (tile / ntx) * Q2Y;
     const double* sU = smt + s * STAGE;
     const double* sV = sU + QU2;
@@ -421,6 +432,7 @@ cudaError_t launch_step_stencil_tma(const StepArgs& a, const double* W, int64_t 
   };
   TmaCols tc;
   memset(&tc, 0, sizeof(tc));
+  tc.nv = (a.mode == 0) ? std::min(a.j, a.k) - 1 : (a.mode == 1 ? 1 : 0);  // = StepCoef::nv
   const CUtensorMap* mu;
   const CUtensorMap* mv;
   if (a.mode == 0) {
