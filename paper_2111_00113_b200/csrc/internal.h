@@ -109,6 +109,8 @@ size_t inverse_iteration_work_doubles(int d, int nmax);
 cudaError_t launch_inverse_iteration(const double* Mh, int d, const double* th_re, const double* th_im,
                                      const int* nsel, int nmax, double* work, double* yr, double* yi, int iters,
                                      double anorm, cudaStream_t st);
+// stencil_zm.cu: step-balanced partition of (tile, plane|line) units over `grid` CTAs (ub[grid+1])
+bool step_partition(int64_t units, int64_t nz, int grid, int zs, int maxg, int32_t* ub);
 // svd.cu: stabilised sRR (reading O33)
 cudaError_t launch_jacobi_svd(const double* M, int ldm, int rows, int n, double tol, int max_sweeps, double* work,
                               double* sigma, double* Ut, double* Vs, int* out, cudaStream_t st);

@@ -32,12 +32,15 @@ constexpr int YUX = YX + 4;     // U / V line box (2-point halo; TMA box dimensi
 constexpr int YT = 256;         // threads (254 W columns + 2 idle)
 constexpr int YCPS = 2;         // resident CTAs per SM (register budget: 128 per thread)
 
+constexpr int YM_MAXG = 2 * 148;  // CTAs covered by the partition table
 struct YmArgs {
   int ucol;
   int vcol[SKS_KMAX];
   int tiles_x;
   int64_t units;  // tiles_x * nz
   int nv;
+  int use_ub;     // 1: CTA b owns units [ub[b], ub[b+1]) (step-balanced partition), else proportional
+  int32_t ub[YM_MAXG + 1];
 };
 
 __host__ __device__ constexpr int ym_al16(int d) { return (d + 15) & ~15; }
@@ -74,10 +77,32 @@ __global__ void __launch_bounds__(YT, YCPS)
     fence_mbar_init();
   }
   pdl_wait_and_release();                   // programmatic dependent launch (see stencil_zm.cu)
-  if (!step_prologue(a, &cf, red)) return;  // contains __syncthreads
-  const int nv = FULL ? KM - 1 : cf.nv;
+  const int nv = FULL ? KM - 1 : z.nv;      // = cf.nv (host-known)
   const uint32_t sbytes = (uint32_t)(YUX * (ZS + 2) * 8 + nv * YUX * ZS * 8);
   const int m = (int)a.m, nz = (int)a.nz, z0g = (int)a.z0, G = a.G;
+  const int64_t u_lo = z.use_ub ? (int64_t)z.ub[blockIdx.x] : (z.units * blockIdx.x) / gridDim.x;
+  const int64_t u_hi = z.use_ub ? (int64_t)z.ub[blockIdx.x + 1] : (z.units * (blockIdx.x + 1)) / gridDim.x;
+  // the first piece's first two stages go out before the prologue's partials reduction
+  int pre = 0;
+  if (tid == 0 && u_lo < u_hi) {
+    const int col = (int)(u_lo / nz), za = (int)(u_lo % nz);
+    const int64_t zr = za + (u_hi - u_lo);
+    const int zb = (int)(zr < nz ? zr : nz);
+    const int x0 = col * YX, wa = za - 1;
+    const int nsteps = (zb - wa + 1 + ZS - 1) / ZS;
+    for (int t = 0; t < 2 && t < nsteps; ++t) {
+      double* dst = sm + t * STG;
+      const int p0 = wa + t * ZS;
+      mbar_arrive_expect_tx(&bar[t], sbytes);
+      tma_load_3d(dst, &tmU, &bar[t], x0 - 2, p0 - 1 + G, z.ucol);
+      for (int l = 0; l < nv; ++l) tma_load_3d(dst + UB + l * VB, &tmV, &bar[t], x0 - 2, p0 + G, z.vcol[l]);
+      pre = t + 1;
+    }
+  }
+  if (!step_prologue(a, &cf, red)) {  // contains __syncthreads
+    for (int t = 0; t < pre; ++t) mbar_wait(&bar[t], 0u);  // no bulk copy may outlive the CTA
+    return;
+  }
   const int64_t pl = a.plane;  // = m (a line)
   const double cc = a.cc, cm = a.cm, cp = a.cp, alpha = cf.alpha, beta_u = cf.beta_u;
   double cl[KM - 1];
@@ -97,7 +122,7 @@ __global__ void __launch_bounds__(YT, YCPS)
 
   uint32_t phase = 0;
   uint32_t sidx = 0;
-  const int64_t u_lo = (z.units * blockIdx.x) / gridDim.x, u_hi = (z.units * (blockIdx.x + 1)) / gridDim.x;
+  bool first = true;
   for (int64_t u = u_lo; u < u_hi;) {
     const int col = (int)(u / nz);
     const int za = (int)(u % nz);
@@ -116,10 +141,11 @@ __global__ void __launch_bounds__(YT, YCPS)
       tma_load_3d(dst, &tmU, &bar[slot], x0 - 2, p0 - 1 + G, z.ucol);
       for (int l = 0; l < nv; ++l) tma_load_3d(dst + UB + l * VB, &tmV, &bar[slot], x0 - 2, p0 + G, z.vcol[l]);
     };
-    if (tid == 0) {
+    if (tid == 0 && !first) {
       issue(0);
       if (nsteps > 1) issue(1);
     }
+    first = false;
     double wp1 = 0.0, wp2 = 0.0;
     double vlast[KM - 1];
 #pragma unroll
@@ -251,6 +277,9 @@ static bool ym_encode(CUtensorMap* out, const double* base, int64_t m, int64_t n
 struct YmMaps {
   CUtensorMap WU, WV, XU, FV, VU;
   const void* key[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  int64_t part_key = -1;  // step-balanced partition cache
+  bool part_ok = false;
+  int32_t ub[YM_MAXG + 1];
 };
 
 template <int KM>
@@ -328,6 +357,24 @@ cudaError_t launch_step_stencil_ym(const StepArgs& a, const double* W, int64_t n
   z.tiles_x = a.tiles_x;
   z.units = a.ntiles;
   z.nv = (a.mode == 0) ? std::min(a.j, a.k) - 1 : (a.mode == 1 ? 1 : 0);
+  {  // step-balanced partition (stencil_zm.cu), cached per (units, nz, grid, zs)
+    static int bal = -1;
+    if (bal < 0) {
+      const char* e = getenv("SKS_ZM_BALANCE");
+      bal = e ? (e[0] == '1') : 1;
+    }
+    if (bal) {
+      const int64_t pk = z.units * 1000003 + a.nz * 131 + grid * 7 + zs;
+      if (mp->part_key != pk) {
+        mp->part_ok = step_partition(z.units, a.nz, grid, zs, YM_MAXG, mp->ub);
+        mp->part_key = pk;
+      }
+      if (mp->part_ok) {
+        z.use_ub = 1;
+        memcpy(z.ub, mp->ub, sizeof(int32_t) * (grid + 1));
+      }
+    }
+  }
   const CUtensorMap* mu;
   const CUtensorMap* mv;
   if (a.mode == 0) {

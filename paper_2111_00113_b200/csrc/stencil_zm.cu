@@ -648,8 +648,8 @@ bool stencil_zm_supported(int dim, int64_t m, int k) {
 // ceil((len + 2) / zs) steps (two halo planes), so the proportional split leaves the CTAs whose range
 // crosses a column boundary up to a step behind.  Greedy fill with a cap of C steps per CTA, C the
 // smallest cap that covers every unit (binary search); pieces end at column boundaries as in the kernel.
-static bool zm_partition(int64_t units, int64_t nz, int grid, int zs, int32_t* ub) {
-  if (grid > ZM_MAXG || units > INT32_MAX) return false;
+bool step_partition(int64_t units, int64_t nz, int grid, int zs, int maxg, int32_t* ub) {
+  if (grid > maxg || units > INT32_MAX) return false;
   auto fill = [&](int64_t C, bool write) -> bool {
     int64_t u = 0;
     if (write) ub[0] = 0;
@@ -749,7 +749,7 @@ cudaError_t launch_step_stencil_zm(const StepArgs& a, const double* W, int64_t n
     if (bal) {
       const int64_t pk = z.units * 1000003 + a.nz * 131 + grid * 7 + zs;
       if (mp->part_key != pk) {
-        mp->part_ok = zm_partition(z.units, a.nz, grid, zs, mp->ub);
+        mp->part_ok = step_partition(z.units, a.nz, grid, zs, ZM_MAXG, mp->ub);
         mp->part_key = pk;
       }
       if (mp->part_ok) {
