@@ -33,15 +33,6 @@ def thin_qr(C):
     return Q * sgn[None, :], R * sgn[:, None]
 
 
-def sketched_lsq(U, T, g, j):
-    """(yhat_j, r_est_j) of Eqs. sgmres-yhat / sgmres-rhat for the first j columns."""
-    Uj = U[:, :j]
-    c = Uj.T @ g
-    y = solve_triangular(T[:j, :j], c, lower=False)
-    r_est = np.linalg.norm(g - Uj @ c)
-    return y, r_est
-
-
 def gmres_exact_ls(M, r0):
     """GMRES problem over the same basis: min ||AB y - r0|| (Eq. gmres)."""
     y, *_ = np.linalg.lstsq(M, r0, rcond=None)

@@ -42,6 +42,19 @@ def _prep(a, dtype=np.float64):
     return arr, arr.ctypes.data
 
 
+def _check_out(out, n):
+    """`out` receives n float64 values through its raw pointer: it must be a contiguous float64
+    array of exactly n elements (torch tensor on any device, or numpy)."""
+    if _is_torch(out):
+        ok = out.dtype == torch.float64 and out.is_contiguous() and out.numel() == n and out.dim() == 1
+    elif isinstance(out, np.ndarray):
+        ok = out.dtype == np.float64 and out.flags["C_CONTIGUOUS"] and out.size == n and out.ndim == 1
+    else:
+        ok = False
+    if not ok:
+        raise ValueError(f"out must be a contiguous 1-D float64 array of length {n}")
+
+
 def _empty_like_place(ref, shape, dtype=np.float64):
     if _is_torch(ref):
         tdt = {np.float64: torch.float64, np.int32: torch.int32, np.int8: torch.int8}[dtype]
@@ -162,7 +175,9 @@ class Context:
         zero_x0 = x0 is None
         if out is not None:
             # the solution is written into `out` (a pinned host `out` keeps the library's copy at full
-            # DMA speed); x0 (if given and not `out` itself) is copied into it first
+            # DMA speed); x0 (if given and not `out` itself) is copied into it first.  The library writes
+            # n doubles through the raw pointer, so `out` must be exactly that.
+            _check_out(out, n)
             x = out
             if x0 is not None and x0 is not out:
                 if _is_torch(x):

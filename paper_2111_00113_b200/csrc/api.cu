@@ -13,6 +13,9 @@
 #include <nccl.h>
 
 #include <climits>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <cstdlib>
 #include <cmath>
 #include <cstdio>
@@ -29,6 +32,26 @@
 #include "step.cuh"
 
 using namespace sks;
+
+namespace sks {
+cudaError_t set_smem_attr_raw(const void* fn, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = done[{fn, dev}];
+  if (cur >= smem) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return e;
+  }
+  cur = smem;
+  return cudaSuccess;
+}
+}  // namespace sks
 
 // ------------------------------------------------------------------------------------
 struct DevBuf {
@@ -197,6 +220,17 @@ static sks_status allreduce_sum(sks_ctx* c, double* buf, size_t cnt, cudaStream_
   if (c->nranks == 1) return SKS_OK;
   SKS_NC(c, ncclAllReduce(buf, buf, cnt, ncclDouble, ncclSum, c->comm, st));
   return SKS_OK;
+}
+
+// Per-CTA partial sums [grid][SKS_NP] of a step launch at nranks > 1: reduced on the device, in a
+// fixed order, into row 0 (in place: thread i reads only component i), then the SKS_NP scalars
+// (k + 3 dots and norms, 88 bytes) are all-reduced.  The consumer then reads grid_prev = 1 row, so
+// ranks whose step grids differ (uneven slabs) never see stale rows of the ping-pong slot.
+static sks_status reduce_partials(sks_ctx* c, double* slot, int grid, cudaStream_t st) {
+  if (c->nranks == 1) return SKS_OK;
+  SKS_CK(c, launch_sum_partials(slot, grid, SKS_NP, SKS_NP, slot, st));
+  ++c->launches;
+  return allreduce_sum(c, slot, SKS_NP, st);
 }
 
 // CSR: make w (n_local rows) available as the gathered vector for the SpMV
@@ -612,7 +646,7 @@ static sks_status first_column(sks_ctx* c, Basis& b, int mode, const double* xve
     ++c->launches;
     b.bytes += (mode == 1) ? 12.0 * b.nnz + 4.0 * (g.n + 1) + 8.0 * 3 * g.n : 16.0 * g.n;
   }
-  SKS_TRY(allreduce_sum(c, p0, (size_t)b.pslots * SKS_NP, st));
+  SKS_TRY(reduce_partials(c, p0, b.last_grid, st));
   SKS_TRY(halo_exchange(c, g, colp(c, b, 0)));
   ++b.steps;
   return SKS_OK;
@@ -622,7 +656,7 @@ static sks_status first_column(sks_ctx* c, Basis& b, int mode, const double* xve
 static sks_status step_column(sks_ctx* c, Basis& b, int j) {
   cudaStream_t st = c->main();
   const Geo& g = b.g;
-  const int grid_prev = c->nranks > 1 ? b.pslots : b.step_grid;
+  const int grid_prev = c->nranks > 1 ? 1 : b.step_grid;
   const int nwin = std::min(b.k, j);
   if (g.kind != SKS_OP_CSR) {
     const bool use_t = b.tma && (c->tma_mask & 1);
@@ -632,7 +666,7 @@ static sks_status step_column(sks_ctx* c, Basis& b, int j) {
     const bool tm = b.time_steps && j % b.time_stride == 0 && 2 * b.ntimed + 1 < (int)c->ev_step.size();
     if (tm) SKS_CK(c, cudaEventRecord(c->ev_step[2 * b.ntimed], st));
     a.partials_in = pslot(c, b, c->part, j - 1);
-    a.grid_prev = c->nranks > 1 ? b.pslots : b.last_grid;
+    a.grid_prev = c->nranks > 1 ? 1 : b.last_grid;
     a.partials_out = pslot(c, b, c->part, j);
     b.last_grid = use_t ? b.tma_grid : b.step_grid;
     if (use_t && b.zm)
@@ -652,7 +686,7 @@ static sks_status step_column(sks_ctx* c, Basis& b, int j) {
       ++b.ntimed;
       b.bytes_timed += 8.0 * g.n * (nwin + 1);
     }
-    SKS_TRY(allreduce_sum(c, a.partials_out, (size_t)b.pslots * SKS_NP, st));
+    SKS_TRY(reduce_partials(c, a.partials_out, b.last_grid, st));
     SKS_TRY(halo_exchange(c, g, colp(c, b, j)));
     b.bytes += 8.0 * g.n * (nwin + 1);
   } else {
@@ -664,12 +698,12 @@ static sks_status step_column(sks_ctx* c, Basis& b, int j) {
     double* pd = c->part2.as<double>();  // spmv partials (single slot)
     SKS_CK(c, launch_csr_spmv(g.n, b.rp, b.ci, b.va, xg, c->mr.as<double>(), nullptr, 0, c->W.as<double>(), g.ld,
                               lo, nw, b.k, pd, b.step_grid, st, c->ctrl.as<CtrlBlock>()));
-    SKS_TRY(allreduce_sum(c, pd, (size_t)b.pslots * SKS_NP, st));
+    SKS_TRY(reduce_partials(c, pd, b.step_grid, st));
     SKS_CK(c, launch_csr_orth(g.n, j, b.k, c->W.as<double>(), g.ld, c->mr.as<double>(), pslot(c, b, c->part, j - 1),
                               grid_prev, pd, grid_prev, pslot(c, b, c->part, j), c->sigma.as<double>(),
                               c->H.as<double>(), b.ldH, c->mnorm.as<double>(), c->ctrl.as<CtrlBlock>(),
                               b.step_grid, st));
-    SKS_TRY(allreduce_sum(c, pslot(c, b, c->part, j), (size_t)b.pslots * SKS_NP, st));
+    SKS_TRY(reduce_partials(c, pslot(c, b, c->part, j), b.step_grid, st));
     c->launches += 2;
     if (tm) {
       SKS_CK(c, cudaEventRecord(c->ev_step[2 * b.ntimed + 1], st));
@@ -869,7 +903,7 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
     ++c->launches;
     b.bytes = 0;  // per-cycle accounting of the basis loop below
     SKS_TRY(first_column(c, b, 1, xb, fb));
-    SKS_CK(c, launch_sum_partials(pslot(c, b, c->part, 0), c->nranks > 1 ? b.pslots : b.last_grid, SKS_NP, 1,
+    SKS_CK(c, launch_sum_partials(pslot(c, b, c->part, 0), c->nranks > 1 ? 1 : b.last_grid, SKS_NP, 1,
                                   c->small.as<double>(), st));
     ++c->launches;
     SKS_CK(c, cudaMemcpyAsync(c->h_small, c->small.p, sizeof(double), cudaMemcpyDeviceToHost, st));

@@ -147,6 +147,25 @@ inline bool pdl_enabled() {  // SKS_NO_PDL=1 turns it off (A/B measurements)
   }
   return on == 1;
 }
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device function attribute: set_smem_attr
+// remembers, per (kernel, current device), the largest size already set (api.cu; thread-safe).
+cudaError_t set_smem_attr_raw(const void* fn, size_t smem);
+template <typename K>
+inline cudaError_t set_smem_attr(K* kern, size_t smem) {
+  return set_smem_attr_raw(reinterpret_cast<const void*>(kern), smem);
+}
+
+// identity of an encoded CUtensorMap: every field that enters the encoding, compared exactly
+struct MapKey {
+  const void* base = nullptr;
+  int64_t ld = -1, nz = -1, m = -1, ncol = -1;
+  int G = -1, depth = -1, kind = -1;
+  bool operator==(const MapKey& o) const {
+    return base == o.base && ld == o.ld && nz == o.nz && m == o.m && ncol == o.ncol && G == o.G &&
+           depth == o.depth && kind == o.kind;
+  }
+};
+
 template <typename K, typename... Args>
 inline cudaError_t launch_pdl(K kern, int grid, int block, size_t smem, cudaStream_t st, Args... args) {
   cudaLaunchConfig_t cfg = {};

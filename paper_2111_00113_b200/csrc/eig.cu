@@ -1719,12 +1719,9 @@ cudaError_t launch_inverse_iteration(const double* Mh, int d, const double* th_r
   if (!getenv("SKS_II_OLD")) {  // pipelined version (default); SKS_II_OLD=1 for A/B
     const size_t smem = sizeof(double) * ((size_t)d * 2 * 3 + (size_t)II_RING * d * 2 + (size_t)II_RING * d) +
                         sizeof(int) * (size_t)d + 16;
-    static size_t set = 0;
-    if (smem > 48 * 1024 && set < smem) {
-      if (cudaFuncSetAttribute(inverse_iteration_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem) != cudaSuccess)
-        return cudaGetLastError();
-      set = smem;
+    if (smem > 48 * 1024) {
+      cudaError_t e = set_smem_attr(inverse_iteration_pipe_kernel, smem);
+      if (e != cudaSuccess) return e;
     }
     (void)anorm;
     inverse_iteration_pipe_kernel<<<nmax, II_T, smem, st>>>(Mh, d, th_re, th_im, nsel, work, yr, yi, iters);

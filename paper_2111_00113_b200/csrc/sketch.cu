@@ -523,16 +523,8 @@ static size_t sketch_smem(int s) {
 template <int QPW, int ZETA>
 static cudaError_t launch_sk(const SketchArgs& a, int grid, cudaStream_t st) {
   const size_t smem = sketch_smem(a.s);
-  static size_t set = 0;
-  if (set < smem) {
-    cudaError_t e = cudaFuncSetAttribute(sketch_batch_kernel<QPW, ZETA>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      return e;
-    }
-    set = smem;
-  }
+  cudaError_t e = set_smem_attr(sketch_batch_kernel<QPW, ZETA>, smem);
+  if (e != cudaSuccess) return e;
   sketch_batch_kernel<QPW, ZETA><<<grid, SK_THREADS, smem, st>>>(a);
   return cudaGetLastError();
 }
@@ -570,15 +562,8 @@ size_t sketch_plan_bytes(int64_t nrows, int s, int zeta) {
 }
 
 template <typename K>
-static cudaError_t set_smem(K kern, size_t smem, size_t* set) {
-  if (*set >= smem) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    return e;
-  }
-  *set = smem;
-  return cudaSuccess;
+static cudaError_t set_smem(K kern, size_t smem) {
+  return set_smem_attr(kern, smem);
 }
 
 cudaError_t launch_sketch_plan(int64_t nrows, int64_t row_begin, int s, int zeta, uint64_t key, void* plan,
@@ -591,12 +576,10 @@ cudaError_t launch_sketch_plan(int64_t nrows, int64_t row_begin, int s, int zeta
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)num_sms * 2));
   cudaError_t e;
   if (zeta == 8) {
-    static size_t set8 = 0;
-    if ((e = set_smem(sketch_plan_kernel<8>, smem, &set8)) != cudaSuccess) return e;
+    if ((e = set_smem(sketch_plan_kernel<8>, smem)) != cudaSuccess) return e;
     sketch_plan_kernel<8><<<grid, S4_THREADS, smem, st>>>(nrows, row_begin, s, zeta, key, tiles, pent, pkst);
   } else {
-    static size_t set0 = 0;
-    if ((e = set_smem(sketch_plan_kernel<0>, smem, &set0)) != cudaSuccess) return e;
+    if ((e = set_smem(sketch_plan_kernel<0>, smem)) != cudaSuccess) return e;
     sketch_plan_kernel<0><<<grid, S4_THREADS, smem, st>>>(nrows, row_begin, s, zeta, key, tiles, pent, pkst);
   }
   return cudaGetLastError();
@@ -605,8 +588,7 @@ cudaError_t launch_sketch_plan(int64_t nrows, int64_t row_begin, int s, int zeta
 template <int QPW>
 static cudaError_t launch_v5(const SketchArgs& a, const void* plan, int grid, cudaStream_t st) {
   const size_t smem = sketch_v5_smem(a.s, a.zeta);
-  static size_t set = 0;
-  cudaError_t e = set_smem(sketch_v5_kernel<QPW>, smem, &set);
+  cudaError_t e = set_smem(sketch_v5_kernel<QPW>, smem);
   if (e != cudaSuccess) return e;
   const int ES = s5_ent_stride(a.s, a.zeta), KS = s5_kst_stride(a.s);
   const uint32_t* pent = reinterpret_cast<const uint32_t*>(plan);

@@ -755,12 +755,8 @@ cudaError_t launch_panel(double* X, int s, int J, int j0, double* U, int ldu, do
                          double* rho, double* rest, CtrlBlock* ctrl, int track_res, int max_cols,
                          cudaStream_t st) {
   const size_t smem = panel_smem(s, J);
-  static size_t set = 0;
-  if (set < smem) {
-    cudaError_t e = cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    set = smem;
-  }
+  cudaError_t e = set_smem_attr(panel_kernel, smem);
+  if (e != cudaSuccess) return e;
   panel_kernel<<<1, 1024, smem, st>>>(X, s, J, j0, U, ldu, T, ldT, rvec, rho, rest, ctrl, track_res, max_cols);
   return cudaGetLastError();
 }

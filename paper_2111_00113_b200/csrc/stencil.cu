@@ -317,18 +317,10 @@ template <int KM>
 static cudaError_t launch_step_t(const StepArgs& a, int grid, cudaStream_t st) {
   const size_t smem = step_smem_bytes(a.dim, KM);
   if (a.dim == 2) {
-    static bool set = false;
-    if (!set) {
-      cudaFuncSetAttribute(step2d_kernel<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      set = true;
-    }
+    if (cudaError_t e = set_smem_attr(step2d_kernel<KM>, smem)) return e;
     step2d_kernel<KM><<<grid, 256, smem, st>>>(a);
   } else {
-    static bool set = false;
-    if (!set) {
-      cudaFuncSetAttribute(step3d_kernel<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      set = true;
-    }
+    if (cudaError_t e = set_smem_attr(step3d_kernel<KM>, smem)) return e;
     step3d_kernel<KM><<<grid, 256, smem, st>>>(a);
   }
   return cudaGetLastError();

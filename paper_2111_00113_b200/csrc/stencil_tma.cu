@@ -334,7 +334,7 @@ static bool encode_map(CUtensorMap* out, int dim, const double* base, int64_t m,
 
 struct StencilMaps {
   CUtensorMap WU, WV, XU, FV, VU;
-  const void* key[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  MapKey key[6];
 };
 
 static size_t tma_smem(int dim, int KM, int NST) {
@@ -366,22 +366,10 @@ static cudaError_t launch_t(const StepArgs& a, const TmaCols& tc, const CUtensor
                             int grid, cudaStream_t st) {
   const size_t smem = tma_smem(a.dim, KM, NST);
   if (a.dim == 3) {
-    static bool set = false;
-    if (!set) {
-      cudaError_t e = cudaFuncSetAttribute(step3d_tma_kernel<KM, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
-      if (e != cudaSuccess) return e;
-      set = true;
-    }
+    if (cudaError_t e = set_smem_attr(step3d_tma_kernel<KM, NST>, smem)) return e;
     return launch_pdl(step3d_tma_kernel<KM, NST>, grid, QT, smem, st, a, tc, mu, mv);
   } else {
-    static bool set = false;
-    if (!set) {
-      cudaError_t e = cudaFuncSetAttribute(step2d_tma_kernel<KM, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
-      if (e != cudaSuccess) return e;
-      set = true;
-    }
+    if (cudaError_t e = set_smem_attr(step2d_tma_kernel<KM, NST>, smem)) return e;
     return launch_pdl(step2d_tma_kernel<KM, NST>, grid, QT, smem, st, a, tc, mu, mv);
   }
   return cudaGetLastError();
@@ -421,10 +409,16 @@ cudaError_t launch_step_stencil_tma(const StepArgs& a, const double* W, int64_t 
     *cache = mp;
   }
   auto upd = [&](CUtensorMap* mpp, int slot, const double* base, int64_t nc, bool ub) -> bool {
-    // re-encode when the base pointer or the geometry changes (key includes ld and nz in a hash)
-    const void* key = reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(base) ^
-                                                    (uintptr_t)(a.ld * 1315423911ull + a.nz * 2654435761ull +
-                                                                a.m * 97ull + nc * 7ull + a.dim));
+    // re-encode when the base pointer or any field of the geometry changes (exact comparison)
+    MapKey key;
+    key.base = base;
+    key.ld = a.ld;
+    key.nz = a.nz;
+    key.m = a.m;
+    key.ncol = nc;
+    key.G = a.G;
+    key.depth = a.dim;
+    key.kind = ub ? 1 : 0;
     if (mp->key[slot] == key) return true;
     if (!encode_map(mpp, a.dim, base, a.m, a.nz, a.G, a.ld, nc, ub)) return false;
     mp->key[slot] = key;

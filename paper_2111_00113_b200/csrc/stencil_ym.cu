@@ -276,7 +276,7 @@ static bool ym_encode(CUtensorMap* out, const double* base, int64_t m, int64_t n
 
 struct YmMaps {
   CUtensorMap WU, WV, XU, FV, VU;
-  const void* key[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  MapKey key[5];
   int64_t part_key = -1;  // step-balanced partition cache
   bool part_ok = false;
   int32_t ub[YM_MAXG + 1];
@@ -309,16 +309,7 @@ static cudaError_t ym_launch_v(const StepArgs& a, const YmArgs& z, const CUtenso
                                int grid, cudaStream_t st) {
   constexpr int ZS = ym_zs<KM>();
   const size_t smem = ym_smem_bytes<KM, ZS>();
-  static bool set = false;
-  if (!set) {
-    cudaError_t e = cudaFuncSetAttribute(step2d_ym_kernel<KM, ZS, FULL, USL>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      return e;
-    }
-    set = true;
-  }
+  if (cudaError_t e = set_smem_attr(step2d_ym_kernel<KM, ZS, FULL, USL>, smem)) return e;
   return launch_pdl(step2d_ym_kernel<KM, ZS, FULL, USL>, grid, YT, smem, st, a, z, mu, mv);
 }
 
@@ -344,9 +335,15 @@ cudaError_t launch_step_stencil_ym(const StepArgs& a, const double* W, int64_t n
   const int km = step_km(a.k);
   const int zs = km == 2 ? ym_zs<2>() : (km == 4 ? ym_zs<4>() : ym_zs<8>());
   auto upd = [&](CUtensorMap* mpp, int slot, const double* base, int64_t nc, bool ub) -> bool {
-    const void* key = reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(base) ^
-                                                    (uintptr_t)(a.ld * 1315423911ull + a.nz * 2654435761ull +
-                                                                a.m * 97ull + nc * 7ull + zs * 31ull + (ub ? 5 : 0)));
+    MapKey key;
+    key.base = base;
+    key.ld = a.ld;
+    key.nz = a.nz;
+    key.m = a.m;
+    key.ncol = nc;
+    key.G = a.G;
+    key.depth = ub ? zs + 2 : zs;
+    key.kind = ub ? 1 : 0;
     if (mp->key[slot] == key) return true;
     if (!ym_encode(mpp, base, a.m, a.nz, a.G, a.ld, nc, ub ? zs + 2 : zs)) return false;
     mp->key[slot] = key;

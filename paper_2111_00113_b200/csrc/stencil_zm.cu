@@ -596,7 +596,7 @@ static bool zm_encode(CUtensorMap* out, const double* base, int64_t m, int64_t n
 
 struct ZmMaps {
   CUtensorMap WU, WV, XU, FV, VU;
-  const void* key[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  MapKey key[5];
   int64_t part_key = -1;  // step-balanced partition cache
   bool part_ok = false;
   int32_t ub[ZM_MAXG + 1];
@@ -624,16 +624,7 @@ static int zm_npy() {  // W columns per thread: 1 = step3d_zm_kernel, 2 = step3d
 template <int KM, int ZS, bool FULL, bool USL>
 static cudaError_t zmp_launch(const StepArgs& a, const ZmArgs& z, const CUtensorMap& mu, const CUtensorMap& mv,
                               int grid, size_t smem, cudaStream_t st) {
-  static bool set = false;
-  if (!set) {
-    cudaError_t e = cudaFuncSetAttribute(step3d_zmp_kernel<KM, ZS, FULL, USL>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      return e;
-    }
-    set = true;
-  }
+  if (cudaError_t e = set_smem_attr(step3d_zmp_kernel<KM, ZS, FULL, USL>, smem)) return e;
   return launch_pdl(step3d_zmp_kernel<KM, ZS, FULL, USL>, grid, ZPT, smem, st, a, z, mu, mv);
 }
 
@@ -690,16 +681,7 @@ static cudaError_t zm_launch_v(const StepArgs& a, const ZmArgs& z, const CUtenso
                                int grid, cudaStream_t st) {
   constexpr int ZS = zm_zs<KM>();
   const size_t smem = zm_smem_bytes<KM, ZS>();
-  static bool set = false;
-  if (!set) {
-    cudaError_t e = cudaFuncSetAttribute(step3d_zm_kernel<KM, ZS, FULL, USL>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      return e;
-    }
-    set = true;
-  }
+  if (cudaError_t e = set_smem_attr(step3d_zm_kernel<KM, ZS, FULL, USL>, smem)) return e;
   if (zm_npy() == 2) return zmp_launch<KM, ZS, FULL, USL>(a, z, mu, mv, grid, smem, st);
   return launch_pdl(step3d_zm_kernel<KM, ZS, FULL, USL>, grid, ZT, smem, st, a, z, mu, mv);
 }
@@ -726,9 +708,15 @@ cudaError_t launch_step_stencil_zm(const StepArgs& a, const double* W, int64_t n
   const int km = step_km(a.k);
   const int zs = km == 2 ? zm_zs<2>() : (km == 4 ? zm_zs<4>() : zm_zs<8>());
   auto upd = [&](CUtensorMap* mpp, int slot, const double* base, int64_t nc, bool ub) -> bool {
-    const void* key = reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(base) ^
-                                                    (uintptr_t)(a.ld * 1315423911ull + a.nz * 2654435761ull +
-                                                                a.m * 97ull + nc * 7ull + zs * 31ull));
+    MapKey key;
+    key.base = base;
+    key.ld = a.ld;
+    key.nz = a.nz;
+    key.m = a.m;
+    key.ncol = nc;
+    key.G = a.G;
+    key.depth = ub ? zs + 2 : zs;
+    key.kind = ub ? 1 : 0;
     if (mp->key[slot] == key) return true;
     if (!zm_encode(mpp, base, a.m, a.nz, a.G, a.ld, nc, ub, ub ? zs + 2 : zs)) return false;
     mp->key[slot] = key;
