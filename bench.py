@@ -91,27 +91,100 @@ def dist_env():
     return ws, rank, local
 
 
-def oracle_sample(cfg, columns_total, cycles):
-    """Time the oracle (as it stands) on a bounded sample of the same workload: the first
-    `nc` basis columns of cycle 0 (residual, k-truncated Arnoldi, sketch, thin QR, LS),
-    extrapolated linearly to the GPU solve's column count.  Returns (seconds, sample text, cores)."""
-    from threadpoolctl import threadpool_limits
-    import oracle as O
-    with threadpool_limits(limits=1):
+class OracleSampler:
+    """The CPU oracle (oracle/, as it stands, never tuned) timed on BOUNDED samples of the bench workload at its
+    real sizes (C3: n = 4,096,000, d = 300, s = 600), one component at a time; the cost of one restart cycle of
+    oracle.sgmres_cycle is the sum of the components and the solve is `cycles` of them (the oracle always builds
+    all d columns of a cycle; its cycle count at this config is tests/golden/oracle_C3.json's, 3):
+
+      S       sketch_matrix(n, s, zeta, seed, c)                       (once per cycle)
+      basis   partial_arnoldi at the real d (its n x d arrays, strided column access), stopped after 8 matvecs:
+              per column = median interval between successive matvec calls 3..8 (one Arnoldi column: window
+              dots, update, norm, strided stores, SpMV); first cost = time to the 2nd call (allocation and page
+              faults of B and AB) minus one column
+      SM      S @ AB on 32 of the d columns (scipy CSR x dense), x d/32
+      rest    thin_qr + LS of an s x d problem, B y on 32 columns x d/32, the true-residual SpMV
+
+    The BLAS pool is left at its default (all host cores); scipy's sparse products are single-threaded.
+    tools/time_oracle_cycle.py measures one FULL cycle (1 thread and all cores) to check this sum
+    (profiles/r02/oracle_cycle_c3.json)."""
+
+    COMPONENTS = ("S", "basis", "SM", "rest")
+
+    def __init__(self, cfg):
+        import oracle as O
+        self.O, self.cfg = O, cfg
         dim = 3 if cfg.op == "stencil3d" else 2
-        A = O.stencil_matrix(dim, cfg.m, cfg.beta)
-        f = rhs_normal(cfg.n, cfg.seed)
-        nc = 12
+        self.A = O.stencil_matrix(dim, cfg.m, cfg.beta)
+        self.f = rhs_normal(cfg.n, cfg.seed)
+        self.t = {}
+        self.cores = len(os.sched_getaffinity(0))
+        self.cycles = 3
+        gp = os.path.join(ROOT, "tests", "golden", f"oracle_{cfg.name}.json")
+        if os.path.exists(gp):
+            self.cycles = int(json.load(open(gp))["cycles"])
+        self._S = None
+
+    def _basis(self, nmv):
+        class Stop(Exception):
+            pass
+        stamps = []
+        A = self.A
+
+        def mv(v):
+            stamps.append(time.perf_counter())
+            if len(stamps) > nmv:
+                raise Stop
+            return A @ v
         t0 = time.perf_counter()
-        O.sgmres_cycle(lambda v: A @ v, f, np.zeros(cfg.n), nc, cfg.k, 2 * nc, cfg.zeta, cfg.seed, 0,
-                       early_exit_factor=0.0)
-        t1 = time.perf_counter()
-    per_col = (t1 - t0) / nc
-    est = per_col * columns_total
-    sample = (f"oracle sgmres_cycle on {cfg.name} full n={cfg.n}, first {nc} columns of cycle 0 "
-              f"(residual+basis+sketch+QR+LS) in {t1 - t0:.2f}s, extrapolated x{columns_total}/{nc} "
-              f"columns ({cycles} cycles); scipy/numpy single-threaded")
-    return est, sample, 1
+        try:
+            self.O.partial_arnoldi(mv, self.f, self.cfg.d, self.cfg.k)
+        except Stop:
+            pass
+        iv = np.diff(stamps[1:])                      # calls 2..nmv+1: one Arnoldi column each
+        per_col = float(np.median(iv))
+        self.per_col = per_col
+        self.first = max(stamps[1] - t0 - per_col, 0.0)
+
+    def measure(self, comp):
+        cfg, O = self.cfg, self.O
+        t0 = time.perf_counter()
+        if comp == "S":
+            self._S = O.sketch_matrix(cfg.n, cfg.s, cfg.zeta, cfg.seed, 0)
+        elif comp == "basis":
+            self._basis(8)
+        else:
+            S = self._S if self._S is not None else O.sketch_matrix(cfg.n, cfg.s, cfg.zeta, cfg.seed, 0)
+            self._S = S
+            M = np.ones((cfg.n, 32))
+            t0 = time.perf_counter()
+            if comp == "SM":
+                S @ M
+            else:
+                C = np.random.default_rng(0).standard_normal((cfg.s, cfg.d))
+                U, T = O.thin_qr(C)
+                np.linalg.solve(T, U.T @ C[:, 0])
+                M @ np.ones(32)
+                x = np.zeros(cfg.n)
+                np.linalg.norm(self.f - self.A @ x)
+        dt = time.perf_counter() - t0
+        self.t[comp] = dt
+        return dt
+
+    def estimate(self):
+        t, d = self.t, self.cfg.d
+        per_col, first = self.per_col, self.first
+        cycle = t["S"] + first + per_col * d + t["SM"] * d / 32 + t["rest"] * d / 32
+        return self.cycles * cycle, cycle, per_col
+
+    def text(self):
+        tot, cyc, pc = self.estimate()
+        ms = ", ".join(f"{k} {v:.2f}s" for k, v in self.t.items())
+        ms += f"; basis first cost {self.first:.2f}s"
+        return (f"oracle (numpy/scipy, BLAS on {self.cores} host cores, sparse products 1 thread) on {self.cfg.name} "
+                f"full n={self.cfg.n}, d={self.cfg.d}, s={self.cfg.s}: measured components [{ms}] -> "
+                f"{pc:.3f} s per basis column, {cyc:.1f} s per cycle x {self.cycles} cycles (oracle golden) = "
+                f"{tot:.1f} s per solve (extrapolated from the bounded samples; see bench.py OracleSampler)")
 
 
 def main():
@@ -135,18 +208,27 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
-        # the oracle as it stands, on the host cores; each step is a bounded sample
-        times, samples = [], None
-        for i in range(args.warmup + args.steps):
-            t, samples, cores = oracle_sample(cfg, columns_total=cfg.d * 3, cycles=3)
-            if i >= args.warmup:
-                times.append(t)
-        v = statistics.mean(times)
+        # the oracle as it stands, on the host cores: each step times ONE bounded component of the workload
+        # (OracleSampler), the warm-up covers all of them; every timed step reports the full-solve estimate
+        # from the latest measurement of each component
+        smp = OracleSampler(cfg)
+        comps = OracleSampler.COMPONENTS
+        for i in range(max(args.warmup, len(comps))):
+            smp.measure(comps[i % len(comps)])
+        vals, walls = [], []
+        for i in range(args.steps):
+            walls.append(smp.measure(comps[i % len(comps)]))
+            vals.append(smp.estimate()[0])
+        v = statistics.mean(vals)
+        wall = statistics.mean(walls)
         line = {"impl": "reference", "metric": metric, "value": v, "unit": "s", "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3, "higher_is_better": False,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": workload, "parallelism": "cpu-oracle"},
-                "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "oracle", "sample": samples},
+                "config": {"workload": workload, "parallelism": "cpu-oracle",
+                           "step": "one bounded oracle component per step (ms_per_step = its measured wall "
+                                   "time); value = the full-solve estimate from all components"},
+                "cpu_baseline": {"value": v, "unit": "s", "cores": smp.cores, "kind": "oracle",
+                                 "sample": smp.text()},
                 "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return 0
@@ -236,8 +318,18 @@ def main():
         cpu = None
         if not args.no_oracle:
             try:
-                v, sample, cores = oracle_sample(cfg, info["columns_generated"], info["cycles"])
-                cpu = {"value": v, "unit": "s", "cores": cores, "kind": "oracle", "sample": sample}
+                smp = OracleSampler(cfg)
+                for comp in OracleSampler.COMPONENTS:
+                    smp.measure(comp)
+                v = smp.estimate()[0]
+                cpu = {"value": v, "unit": "s", "cores": smp.cores, "kind": "oracle", "sample": smp.text()}
+                cp = os.path.join(ROOT, "profiles", "r02", "oracle_cycle_c3.json")
+                if cfg.name == "C3" and os.path.exists(cp):
+                    mc = json.load(open(cp))
+                    cpu["measured_full_cycle"] = {
+                        "runs": mc["runs"], "cpu_model": mc["cpu_model"], "host_cores": mc["host_cores"],
+                        "x_cycles_estimate_s": [r["seconds"] * smp.cycles for r in mc["runs"]],
+                        "source": "profiles/r02/oracle_cycle_c3.json (tools/time_oracle_cycle.py on the GPU box)"}
             except Exception as e:  # pragma: no cover
                 cpu = {"value": None, "unit": "s", "cores": 0, "kind": "oracle", "sample": f"failed: {e}"}
         traffic = None

@@ -10,6 +10,7 @@ from .configs import CONFIGS, Config, get_config  # noqa: F401
 from .generators import (  # noqa: F401
     rhs_normal,
     start_vector,
+    start_block,
     random_csr_c4,
     partition_rows,
 )

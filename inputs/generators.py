@@ -21,6 +21,13 @@ def start_vector(n: int, seed: int) -> np.ndarray:
     return np.random.default_rng(seed).standard_normal(n)
 
 
+def start_block(n: int, b: int, seed: int) -> np.ndarray:
+    """Start block Omega (n x b) of the block Krylov sRR ("drawn at random from a standard
+    normal distribution"): column i is the i-th chunk of n draws of default_rng(seed) (F-ordered, so each
+    column is contiguous)."""
+    return np.asfortranarray(np.random.default_rng(seed).standard_normal((b, n)).T)
+
+
 def random_csr_c4(n: int, seed: int = 3, nnz_off: int = 16, diag: float = 6.0):
     """Return (row_ptr int32[n+1], col_idx int32[nnz], val f64[nnz], f f64[n])."""
     rng = np.random.default_rng(seed)

@@ -25,8 +25,8 @@ from .sketch import (  # noqa: F401
     sketch_key, sketch_table, sketch_matrix, sketch_apply, fmix64,
     srft_key, srft_signs, srft_rows, srft_apply, SRFT,
 )
-from .krylov import partial_arnoldi, full_arnoldi, chebyshev_basis  # noqa: F401
+from .krylov import partial_arnoldi, full_arnoldi, chebyshev_basis, block_chebyshev_basis  # noqa: F401
 from .sgmres import (  # noqa: F401
     thin_qr, sgmres_cycle, sgmres_solve, gmres_exact_ls, WARN_COND, WARN_BREAKDOWN, INFO_ADAPTIVE,
 )
-from .srr import srr_eigs, select_ritz, srr_from_basis  # noqa: F401
+from .srr import srr_eigs, select_ritz, srr_from_basis, srr_eigs_block  # noqa: F401

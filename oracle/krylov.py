@@ -123,3 +123,32 @@ def chebyshev_basis(matvec, r, d: int, c: float, dx: float, dy: float = 0.0):
         if j >= 1:
             H[j - 1, j] = e * nu[j - 1] / nu[j]
     return dict(B=B, M=M, raw=raw, H=H, d_eff=d, rho=rho, rnorm=rnorm, breakdown=False, nu=nu)
+
+
+def block_chebyshev_basis(matvec, Omega, p: int, c: float, dx: float, dy: float = 0.0):
+    """Block Chebyshev basis for the block Krylov space K_p(A; Omega), Sec. "Block Chebyshev recurrence"
+    (P:1983-2008), written out exactly as displayed:
+        B_1 = Omega;   B_2 = (2 rho)^-1 (A - c I) Omega;
+        B_j = rho^-1 [ (A - c I) B_{j-1} - (dx^2 - dy^2)/(4 rho) B_{j-2} ],   j = 3..p,
+    rho = max(dx, dy), for a spectrum inside [c +- dx, +- i dy].  No inner products, no orthogonalisation and
+    no rescaling (the paper's display has none; sRR is invariant to column scaling of B).
+    Omega: n x b.  Returns dict(B (n x bp; block j in columns [(j-1) b, j b)), M = A B computed column by
+    column with the operator (the plain definition of AB), b, p, rho)."""
+    Omega = np.asarray(Omega, dtype=np.float64)
+    if Omega.ndim == 1:
+        Omega = Omega[:, None]
+    n, b = Omega.shape
+    rho = max(dx, dy)
+    e = (dx * dx - dy * dy) / (4.0 * rho)
+
+    def apply(X):
+        return np.stack([matvec(X[:, i]) for i in range(X.shape[1])], axis=1)
+
+    blocks = [Omega.copy()]
+    if p >= 2:
+        blocks.append((apply(blocks[0]) - c * blocks[0]) / (2.0 * rho))
+    for j in range(2, p):
+        blocks.append((apply(blocks[j - 1]) - c * blocks[j - 1] - e * blocks[j - 2]) / rho)
+    B = np.concatenate(blocks, axis=1)
+    M = apply(B)
+    return dict(B=B, M=M, b=b, p=p, rho=rho, e=e)

@@ -20,7 +20,7 @@ stabilize = "off" | "if_ill" (kappa_2(T) > tol, Alg. 2's test) | "always".
 import numpy as np
 from scipy.linalg import eig as qz_eig, solve_triangular
 
-from .krylov import partial_arnoldi
+from .krylov import partial_arnoldi, block_chebyshev_basis
 from .sgmres import thin_qr
 from .sketch import sketch_matrix, SRFT
 
@@ -87,4 +87,17 @@ def srr_eigs(matvec, v0, d, k, s, zeta, seed, nev, cycle=0, sketch="sparse", sta
     S = sketch_matrix(n, s, zeta, seed, cycle) if sketch == "sparse" else SRFT(n, s, seed, cycle)
     out = srr_from_basis(matvec, basis["B"], basis["M"], S, nev, stabilize, tol)
     out["basis"] = basis
+    return out
+
+
+def srr_eigs_block(matvec, Omega, p, c, dx, dy, s, zeta, seed, nev, cycle=0, stabilize="off", tol=1e14):
+    """sRR with the block Chebyshev basis of Sec. "Block Krylov subspaces" / "Block Chebyshev recurrence"
+    (P:1867-1896): B = [B_1 ... B_p] from the start block Omega (n x b, "drawn at random from a
+    standard normal distribution"), then Alg. 2's sketch, QR, Mhat, eigenpairs and residuals
+    (srr_from_basis, one shared S) exactly as for the single-vector basis (d = b p)."""
+    bas = block_chebyshev_basis(matvec, Omega, p, c, dx, dy)
+    n = bas["B"].shape[0]
+    S = sketch_matrix(n, s, zeta, seed, cycle)
+    out = srr_from_basis(matvec, bas["B"], bas["M"], S, nev, stabilize, tol)
+    out["basis"] = bas
     return out

@@ -77,6 +77,7 @@ struct ZmArgs {
   int tiles_x;
   int64_t units;   // ncolxy * nz
   int nv;          // window vectors of this launch (= StepCoef::nv, known on the host)
+  int vdot;        // bit l: the dot <V_l, A w_j> is needed by the next step (its partial slot is used)
   int use_ub;      // 1: CTA b owns units [ub[b], ub[b+1]) (step-balanced partition), else proportional
   int32_t ub[ZM_MAXG + 1];
 };
@@ -564,6 +565,329 @@ __global__ void __launch_bounds__(ZPT, ZM_CPS)
   step_epilogue<KM>(a, &cf, acc, red);
 }
 
+
+// ---- warp-specialised variant (default; SKS_ZM_WS=0 selects the pair kernel above).
+// The pair kernel runs its two phases -- (A) w_j on the W box from the staged U/V planes, (B) A w_j and the
+// next step's dot products on the interior -- on the same 10 warps with a CTA barrier between them, so each
+// phase's FP64 and shared-memory latencies are exposed (ncu r01j: 'wait' and 'short_scoreboard' stalls, issue
+// active 29%).  Here the phases run on two warp groups, one step apart, handing the w_j ring over through
+// mbarriers (no CTA-wide barrier inside the march):
+//   group A (10 warps, pairs of the 34 x 18 W box): waits for the stage (TMA) and for the ring segment to be
+//     free, forms w_j for ZS planes, writes the ring segment and the interior w_j to global memory;
+//   group B (8 warps, pairs of the 32 x 16 interior): waits for the ring segment, forms A w_j from the ring
+//     (z neighbours carried in registers) and accumulates ||w||^2, <w,Aw>, ||Aw||^2, <U,Aw>, <V_l,Aw>;
+//     its warp 0 refills the stage once all 18 warps have released it.
+// Stages: NST = 3 when they fit (k = 2), else 2.  Ring: 3 segments of ZS planes; segment g mod 3 is written
+// by A at global step g and read by B at steps g and g+1, so A may run up to two steps ahead of B.
+constexpr int WA_T = 320;                 // group A threads (34 x 9 = 306 pairs used)
+constexpr int WB_T = 256;                 // group B threads (32 x 8 pairs)
+constexpr int WS_T = WA_T + WB_T;         // 18 warps
+template <int KM, int ZS, int NST>
+__host__ __device__ constexpr size_t zws_smem_bytes() {
+  return 128 + sizeof(double) * ((size_t)NST * zm_stage<KM, ZS>() + (size_t)(3 * ZS) * ZW);
+}
+
+struct ZPiece {
+  int za, zb, x0, y0, wa, nsteps;
+};
+template <int ZS>
+__device__ __forceinline__ ZPiece zws_piece(const ZmArgs& z, int nz, int64_t u, int64_t u_hi) {
+  ZPiece p;
+  const int col = (int)(u / nz);
+  p.za = (int)(u % nz);
+  const int64_t zr = p.za + (u_hi - u);
+  p.zb = (int)(zr < nz ? zr : nz);
+  p.x0 = (col % z.tiles_x) * ZX;
+  p.y0 = (col / z.tiles_x) * ZY;
+  p.wa = p.za - 1;
+  p.nsteps = (p.zb - p.wa + 1 + ZS - 1) / ZS;
+  return p;
+}
+// walks the (piece, step) sequence of one CTA
+template <int ZS>
+struct ZCursor {
+  int64_t u, u_hi;
+  ZPiece pc;
+  int t;
+  bool valid;
+  __device__ __forceinline__ void init(const ZmArgs& z, int nz, int64_t lo, int64_t hi) {
+    u = lo;
+    u_hi = hi;
+    t = 0;
+    valid = u < u_hi;
+    if (valid) pc = zws_piece<ZS>(z, nz, u, u_hi);
+  }
+  __device__ __forceinline__ void next_piece(const ZmArgs& z, int nz) {
+    u += pc.zb - pc.za;
+    t = 0;
+    valid = u < u_hi;
+    if (valid) pc = zws_piece<ZS>(z, nz, u, u_hi);
+  }
+  __device__ __forceinline__ void next(const ZmArgs& z, int nz) {
+    if (++t >= pc.nsteps) next_piece(z, nz);
+  }
+};
+
+template <int KM, int ZS, int NST, bool FULL, bool USL>
+__global__ void __launch_bounds__(WS_T, 1)
+    step3d_zws_kernel(StepArgs a, ZmArgs z, const __grid_constant__ CUtensorMap tmU,
+                      const __grid_constant__ CUtensorMap tmV) {
+  extern __shared__ __align__(128) unsigned char smraw_w[];
+  double* sm = reinterpret_cast<double*>(smraw_w + ((128u - (smem_u32(smraw_w) & 127u)) & 127u));
+  constexpr int STG = zm_stage<KM, ZS>();
+  constexpr int UB = zm_ublk<KM, ZS>(), VB = zm_vblk<KM, ZS>();
+  constexpr int SEG = ZS * ZW;  // doubles per ring segment
+  double* ring = sm + NST * STG;
+  __shared__ StepCoef cf;
+  __shared__ double red[SKS_NP * 32];
+  __shared__ __align__(8) uint64_t full[NST], sempty[NST], rfull[3], rempty[3];
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) {
+    tma_prefetch_desc(&tmU);
+    tma_prefetch_desc(&tmV);
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&sempty[i], WS_T / 32);
+    }
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(&rfull[i], WA_T / 32);
+      mbar_init(&rempty[i], WB_T / 32);
+    }
+    fence_mbar_init();
+  }
+  pdl_wait_and_release();
+  const int nv = FULL ? KM - 1 : z.nv;
+  const uint32_t sbytes = (uint32_t)(ZUP * (ZS + 2) * 8 + nv * ZVP * ZS * 8);
+  const int m = (int)a.m, nz = (int)a.nz, z0g = (int)a.z0, G = a.G;
+  const int64_t u_lo = z.use_ub ? (int64_t)z.ub[blockIdx.x] : (z.units * blockIdx.x) / gridDim.x;
+  const int64_t u_hi = z.use_ub ? (int64_t)z.ub[blockIdx.x + 1] : (z.units * (blockIdx.x + 1)) / gridDim.x;
+  auto issue = [&](const ZCursor<ZS>& c, int slot) {
+    double* dst = sm + slot * STG;
+    const int p0 = c.pc.wa + c.t * ZS;
+    mbar_arrive_expect_tx(&full[slot], sbytes);
+    tma_load_4d(dst, &tmU, &full[slot], c.pc.x0 - 2, c.pc.y0 - 2, p0 - 1 + G, z.ucol);
+    for (int l = 0; l < nv; ++l)
+      tma_load_4d(dst + UB + l * VB, &tmV, &full[slot], c.pc.x0 - 2, c.pc.y0 - 1, p0 + G, z.vcol[l]);
+  };
+  // the first NST stages go out before the prologue's partials reduction (inputs complete at the PDL wait)
+  int pre = 0;
+  if (tid == 0) {
+    ZCursor<ZS> c;
+    c.init(z, nz, u_lo, u_hi);
+    for (; pre < NST && c.valid; ++pre) {
+      issue(c, pre);
+      c.next(z, nz);
+    }
+  }
+  if (!step_prologue(a, &cf, red)) {
+    if (tid == 0)
+      for (int t = 0; t < pre; ++t) mbar_wait(&full[t], 0u);  // no bulk copy may outlive the CTA
+    return;
+  }
+  const double cc = a.cc, cm = a.cm, cp = a.cp;
+  double acc[KM + 3];
+#pragma unroll
+  for (int i = 0; i < KM + 3; ++i) acc[i] = 0.0;
+
+  if (tid < WA_T) {
+    // ======================= group A: w_j on the W box ========================================
+    const int64_t pl = a.plane;
+    const double alpha = cf.alpha, beta_u = cf.beta_u;
+    double cl[KM - 1];
+#pragma unroll
+    for (int l = 0; l < KM - 1; ++l) cl[l] = (l < nv) ? cf.c[l] : 0.0;
+    double* Wout = a.W + (a.mode == 0 ? (int64_t)a.j * a.ld : 0) + a.off;
+    constexpr int NPAIR = ZWX * (ZWY / 2);
+    const bool wt = tid < NPAIR;
+    const int tp = wt ? tid : NPAIR - 1;
+    const int bx = tp % ZWX, by0 = 2 * (tp / ZWX), by1 = by0 + 1;
+    const int cu0 = (by0 + 1) * ZUX + (bx + 1), cu1 = cu0 + ZUX;
+    const int cv0 = by0 * ZVX + (bx + 1), cv1 = cv0 + ZVX;
+    const int cw0 = by0 * ZWX + bx, cw1 = cw0 + ZWX;
+    const bool xin_box = bx >= 1 && bx <= ZX;
+    const bool in0 = wt && xin_box && by0 >= 1 && by0 <= ZY, in1 = wt && xin_box && by1 >= 1 && by1 <= ZY;
+    uint32_t g = 0;
+    ZCursor<ZS> cur;
+    cur.init(z, nz, u_lo, u_hi);
+    while (cur.valid) {
+      const ZPiece pc = cur.pc;
+      const int gx = pc.x0 - 1 + bx, gy0 = pc.y0 - 1 + by0, gy1 = gy0 + 1;
+      const bool xok = wt && (unsigned)gx < (unsigned)m;
+      const bool xy0 = xok && (unsigned)gy0 < (unsigned)m, xy1 = xok && (unsigned)gy1 < (unsigned)m;
+      const bool st0 = in0 && gx < m && gy0 < m, st1 = in1 && gx < m && gy1 < m;
+      double* wc0 = Wout + (int64_t)gy0 * m + gx;
+      double* wc1 = wc0 + m;
+      const double am0 = xy0 ? alpha : 0.0, bm0 = xy0 ? beta_u : 0.0;
+      const double am1 = xy1 ? alpha : 0.0, bm1 = xy1 ? beta_u : 0.0;
+      double clm0[KM - 1], clm1[KM - 1];
+#pragma unroll
+      for (int l = 0; l < KM - 1; ++l) {
+        clm0[l] = xy0 ? cl[l] : 0.0;
+        clm1[l] = xy1 ? cl[l] : 0.0;
+      }
+      constexpr int T0 = ZS == 1 ? 2 : 1;
+      for (int t = 0; t < pc.nsteps; ++t, ++g) {
+        const int slot = (int)(g % NST), seg = (int)(g % 3);
+        mbar_wait(&full[slot], (g / NST) & 1u);
+        if (g >= 3) mbar_wait(&rempty[seg], ((g / 3) - 1) & 1u);
+        const double* sU = sm + slot * STG;
+        const double* sV = sU + UB;
+        const int p0 = pc.wa + t * ZS;
+        const bool fast = t >= T0 && p0 + ZS - 1 <= pc.zb && z0g + p0 + ZS - 1 < m;
+        double ca[ZS + 2], cb[ZS + 2];
+        double* rw0 = ring + seg * SEG + cw0;
+        double* rw1 = ring + seg * SEG + cw1;
+#pragma unroll
+        for (int k = 0; k < ZS + 2; ++k) {
+          ca[k] = sU[k * ZUP + cu0];
+          cb[k] = sU[k * ZUP + cu1];
+        }
+#pragma unroll
+        for (int i = 0; i < ZS; ++i) {
+          const int p = p0 + i;
+          double va[KM - 1], vb[KM - 1];
+#pragma unroll
+          for (int l = 0; l < KM - 1; ++l) {
+            va[l] = (FULL || l < nv) ? sV[l * VB + i * ZVP + cv0] : 0.0;
+            vb[l] = (FULL || l < nv) ? sV[l * VB + i * ZVP + cv1] : 0.0;
+          }
+          const double* q0 = sU + (i + 1) * ZUP + cu0;
+          const double* q1 = q0 + ZUX;
+          const double Aua = cc * ca[i + 1] + cm * (q0[-1] + q0[-ZUX] + ca[i]) + cp * (q0[1] + cb[i + 1] + ca[i + 2]);
+          const double Aub = cc * cb[i + 1] + cm * (q1[-1] + ca[i + 1] + cb[i]) + cp * (q1[1] + q1[ZUX] + cb[i + 2]);
+          double w0v, w1v;
+          if (fast) {
+            w0v = am0 * Aua + bm0 * ca[i + 1];
+            w1v = am1 * Aub + bm1 * cb[i + 1];
+#pragma unroll
+            for (int l = 0; l < KM - 1; ++l)
+              if (FULL || l < nv) {
+                w0v += clm0[l] * va[l];
+                w1v += clm1[l] * vb[l];
+              }
+          } else {
+            w0v = alpha * Aua + beta_u * ca[i + 1];
+            w1v = alpha * Aub + beta_u * cb[i + 1];
+#pragma unroll
+            for (int l = 0; l < KM - 1; ++l)
+              if (FULL || l < nv) {
+                w0v += cl[l] * va[l];
+                w1v += cl[l] * vb[l];
+              }
+            const bool zok = (unsigned)(z0g + p) < (unsigned)m && p <= pc.zb;
+            w0v = (xy0 && zok) ? w0v : 0.0;
+            w1v = (xy1 && zok) ? w1v : 0.0;
+          }
+          if (wt) {
+            rw0[i * ZW] = w0v;
+            rw1[i * ZW] = w1v;
+          }
+          // the output planes [za, zb) of w_j (a fast step has p >= za; only its last plane can be zb)
+          if (fast ? (i < ZS - 1 || p < pc.zb) : (p >= pc.za && p < pc.zb)) {
+            if (st0) wc0[(int64_t)p * pl] = w0v;
+            if (st1) wc1[(int64_t)p * pl] = w1v;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&rfull[seg]);
+          mbar_arrive(&sempty[slot]);
+        }
+      }
+      cur.next_piece(z, nz);
+    }
+  } else {
+    // ======================= group B: A w_j and the next step's dot products =====================
+    const int tb = tid - WA_T, wb = tb >> 5;
+    const int bx = 1 + tb % ZX, by0 = 1 + 2 * (tb / ZX);
+    const int cu0 = (by0 + 1) * ZUX + (bx + 1), cu1 = cu0 + ZUX;
+    const int cv0 = by0 * ZVX + (bx + 1), cv1 = cv0 + ZVX;
+    const int cw0 = by0 * ZWX + bx, cw1 = cw0 + ZWX;
+    const int vdot = z.vdot;
+    uint32_t g = 0;
+    ZCursor<ZS> cur, ahead;  // ahead: the stage warp 0 issues next (global step g + NST)
+    cur.init(z, nz, u_lo, u_hi);
+    const bool producer = wb == 0 && lane == 0;
+    if (producer) {
+      ahead.init(z, nz, u_lo, u_hi);
+      for (int i = 0; i < NST && ahead.valid; ++i) ahead.next(z, nz);
+    }
+    while (cur.valid) {
+      const ZPiece pc = cur.pc;
+      const int gx = pc.x0 - 1 + bx, gy0 = pc.y0 - 1 + by0, gy1 = gy0 + 1;
+      const bool aw0 = gx < m && gy0 < m, aw1 = gx < m && gy1 < m;
+      double wm1a = 0.0, w0a = 0.0, wm1b = 0.0, w0b = 0.0;  // w_j at planes p0-2, p0-1 (carried)
+      double vla[KM - 1], vlb[KM - 1];
+#pragma unroll
+      for (int l = 0; l < KM - 1; ++l) vla[l] = vlb[l] = 0.0;
+      constexpr int T0 = ZS == 1 ? 2 : 1;
+      for (int t = 0; t < pc.nsteps; ++t, ++g) {
+        const int slot = (int)(g % NST), seg = (int)(g % 3), sprev = (int)((g + 2) % 3);
+        mbar_wait(&full[slot], (g / NST) & 1u);
+        mbar_wait(&rfull[seg], (g / 3) & 1u);
+        const double* sU = sm + slot * STG;
+        const double* sV = sU + UB;
+        const int p0 = pc.wa + t * ZS;
+        const bool fast = t >= T0 && p0 + ZS - 1 <= pc.zb && z0g + p0 + ZS - 1 < m;
+        const double* rs = ring + seg * SEG;
+#pragma unroll
+        for (int i = 0; i < ZS; ++i) {
+          const int qp = p0 - 1 + i;
+          const double* rq = (i == 0) ? ring + sprev * SEG + (ZS - 1) * ZW : rs + (i - 1) * ZW;  // plane qp
+          const double wp1a = rs[i * ZW + cw0], wp1b = rs[i * ZW + cw1];                       // plane qp + 1
+          const double Awa = cc * w0a + cm * (rq[cw0 - 1] + rq[cw0 - ZWX] + wm1a) + cp * (rq[cw0 + 1] + w0b + wp1a);
+          const double Awb = cc * w0b + cm * (rq[cw1 - 1] + w0a + wm1b) + cp * (rq[cw1 + 1] + rq[cw1 + ZWX] + wp1b);
+          if (fast || (qp >= pc.za && qp < pc.zb)) {
+            if (aw0) {
+              acc[0] += w0a * w0a;
+              acc[1] += w0a * Awa;
+              acc[2] += Awa * Awa;
+              if (USL) acc[KM + 2] += sU[i * ZUP + cu0] * Awa;
+#pragma unroll
+              for (int l = 0; l < KM - 1; ++l)
+                if ((FULL || l < nv) && ((vdot >> l) & 1))
+                  acc[3 + l] += ((i == 0) ? vla[l] : sV[l * VB + (i - 1) * ZVP + cv0]) * Awa;
+            }
+            if (aw1) {
+              acc[0] += w0b * w0b;
+              acc[1] += w0b * Awb;
+              acc[2] += Awb * Awb;
+              if (USL) acc[KM + 2] += sU[i * ZUP + cu1] * Awb;
+#pragma unroll
+              for (int l = 0; l < KM - 1; ++l)
+                if ((FULL || l < nv) && ((vdot >> l) & 1))
+                  acc[3 + l] += ((i == 0) ? vlb[l] : sV[l * VB + (i - 1) * ZVP + cv1]) * Awb;
+            }
+          }
+          wm1a = w0a;
+          w0a = wp1a;
+          wm1b = w0b;
+          w0b = wp1b;
+        }
+#pragma unroll
+        for (int l = 0; l < KM - 1; ++l)
+          if ((FULL || l < nv) && ((vdot >> l) & 1)) {
+            vla[l] = sV[l * VB + (ZS - 1) * ZVP + cv0];
+            vlb[l] = sV[l * VB + (ZS - 1) * ZVP + cv1];
+          }
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&sempty[slot]);
+          if (g >= 1) mbar_arrive(&rempty[sprev]);
+        }
+        if (producer && ahead.valid) {  // refill this slot with global step g + NST once all warps left it
+          mbar_wait(&sempty[slot], (g / NST) & 1u);
+          issue(ahead, slot);
+          ahead.next(z, nz);
+        }
+      }
+      cur.next_piece(z, nz);
+    }
+  }
+  __syncthreads();
+  step_epilogue<KM>(a, &cf, acc, red);
+}
+
 // ---------------------------------------------------------------- host side
 static PFN_cuTensorMapEncodeTiled_v12000 g_enc_zm = nullptr;
 
@@ -619,6 +943,15 @@ static int zm_npy() {  // W columns per thread: 1 = step3d_zm_kernel, 2 = step3d
     if (npy != 1 && npy != 2) npy = ZM_NPY_DEFAULT;
   }
   return npy;
+}
+
+static bool zm_ws() {  // warp-specialised step kernel (default); SKS_ZM_WS=0 -> pair / single-column kernels
+  static int ws = -1;
+  if (ws < 0) {
+    const char* e = getenv("SKS_ZM_WS");
+    ws = e ? (e[0] == '1') : 1;
+  }
+  return ws == 1;
 }
 
 template <int KM, int ZS, bool FULL, bool USL>
@@ -682,6 +1015,12 @@ static cudaError_t zm_launch_v(const StepArgs& a, const ZmArgs& z, const CUtenso
   constexpr int ZS = zm_zs<KM>();
   const size_t smem = zm_smem_bytes<KM, ZS>();
   if (cudaError_t e = set_smem_attr(step3d_zm_kernel<KM, ZS, FULL, USL>, smem)) return e;
+  if (zm_ws()) {
+    constexpr int NST = zws_smem_bytes<KM, ZS, 3>() <= 226 * 1024 ? 3 : 2;
+    constexpr size_t wsm = zws_smem_bytes<KM, ZS, NST>();
+    if (cudaError_t e = set_smem_attr(step3d_zws_kernel<KM, ZS, NST, FULL, USL>, wsm)) return e;
+    return launch_pdl(step3d_zws_kernel<KM, ZS, NST, FULL, USL>, grid, WS_T, wsm, st, a, z, mu, mv);
+  }
   if (zm_npy() == 2) return zmp_launch<KM, ZS, FULL, USL>(a, z, mu, mv, grid, smem, st);
   return launch_pdl(step3d_zm_kernel<KM, ZS, FULL, USL>, grid, ZT, smem, st, a, z, mu, mv);
 }
@@ -728,6 +1067,12 @@ cudaError_t launch_step_stencil_zm(const StepArgs& a, const double* W, int64_t n
   z.ncolxy = a.tiles_x * a.tiles_y;
   z.units = a.ntiles;
   z.nv = (a.mode == 0) ? std::min(a.j, a.k) - 1 : (a.mode == 1 ? 1 : 0);
+  z.vdot = 0;
+  if (a.mode == 0 && a.basis == 0) {  // step_prologue: vslot[l] = 3 + (lo + l) - (j - k + 1) if >= 0
+    const int lo = std::max(0, a.j - a.k);
+    for (int l = 0; l < z.nv; ++l)
+      if (lo + l - (a.j - a.k + 1) >= 0) z.vdot |= 1 << l;
+  }
   {  // step-balanced partition, cached per (units, nz, grid, zs)
     static int bal = -1;
     if (bal < 0) {
