@@ -78,6 +78,7 @@ struct ZmArgs {
   int64_t units;   // ncolxy * nz
   int nv;          // window vectors of this launch (= StepCoef::nv, known on the host)
   int vdot;        // bit l: the dot <V_l, A w_j> is needed by the next step (its partial slot is used)
+  int store_b;     // warp-specialised kernel: w_j is stored by group B (1) or group A (0)
   int use_ub;      // 1: CTA b owns units [ub[b], ub[b+1]) (step-balanced partition), else proportional
   int32_t ub[ZM_MAXG + 1];
 };
@@ -566,7 +567,8 @@ __global__ void __launch_bounds__(ZPT, ZM_CPS)
 }
 
 
-// ---- warp-specialised variant (default; SKS_ZM_WS=0 selects the pair kernel above).
+// ---- warp-specialised variant (SKS_ZM_WS=1; measured 37.5 us vs 35.1 us for the pair kernel at C3, so the
+// pair kernel stays the default -- DESIGN.md section 11).
 // The pair kernel runs its two phases -- (A) w_j on the W box from the staged U/V planes, (B) A w_j and the
 // next step's dot products on the interior -- on the same 10 warps with a CTA barrier between them, so each
 // phase's FP64 and shared-memory latencies are exposed (ncu r01j: 'wait' and 'short_scoreboard' stalls, issue
@@ -574,11 +576,19 @@ __global__ void __launch_bounds__(ZPT, ZM_CPS)
 // mbarriers (no CTA-wide barrier inside the march):
 //   group A (10 warps, pairs of the 34 x 18 W box): waits for the stage (TMA) and for the ring segment to be
 //     free, forms w_j for ZS planes, writes the ring segment and the interior w_j to global memory;
+//     it also accumulates <U, A w_j> as <A^T U, w_j> (A^T u from the same neighbour sums as A u, reading O35)
+//     and its thread 0 refills a stage once all group-A warps have released it;
 //   group B (8 warps, pairs of the 32 x 16 interior): waits for the ring segment, forms A w_j from the ring
-//     (z neighbours carried in registers) and accumulates ||w||^2, <w,Aw>, ||Aw||^2, <U,Aw>, <V_l,Aw>;
-//     its warp 0 refills the stage once all 18 warps have released it.
+//     (z neighbours carried in registers) and accumulates ||w||^2, <w,Aw>, ||Aw||^2 and the window dots
+//     <V_l,Aw> (read from the stage; none for k = 2, where group B never touches the stages).
 // Stages: NST = 3 when they fit (k = 2), else 2.  Ring: 3 segments of ZS planes; segment g mod 3 is written
 // by A at global step g and read by B at steps g and g+1, so A may run up to two steps ahead of B.
+#ifndef ZWS_SLEEP_B
+#define ZWS_SLEEP_B 0  // suspend-time hint (ns) of group B's ring wait (0: plain try_wait)
+#endif
+#ifndef ZWS_SLEEP_A
+#define ZWS_SLEEP_A 0
+#endif
 constexpr int WA_T = 320;                 // group A threads (34 x 9 = 306 pairs used)
 constexpr int WB_T = 256;                 // group B threads (32 x 8 pairs)
 constexpr int WS_T = WA_T + WB_T;         // 18 warps
@@ -647,7 +657,7 @@ __global__ void __launch_bounds__(WS_T, 1)
     tma_prefetch_desc(&tmV);
     for (int i = 0; i < NST; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&sempty[i], WS_T / 32);
+      mbar_init(&sempty[i], (WA_T + (z.vdot ? WB_T : 0)) / 32);
     }
     for (int i = 0; i < 3; ++i) {
       mbar_init(&rfull[i], WA_T / 32);
@@ -707,8 +717,13 @@ __global__ void __launch_bounds__(WS_T, 1)
     const bool xin_box = bx >= 1 && bx <= ZX;
     const bool in0 = wt && xin_box && by0 >= 1 && by0 <= ZY, in1 = wt && xin_box && by1 >= 1 && by1 <= ZY;
     uint32_t g = 0;
-    ZCursor<ZS> cur;
+    ZCursor<ZS> cur, ahead;  // ahead: the stage warp 0 issues next (global step g + NST)
     cur.init(z, nz, u_lo, u_hi);
+    const bool producer = tid == 0;
+    if (producer) {
+      ahead.init(z, nz, u_lo, u_hi);
+      for (int i = 0; i < NST && ahead.valid; ++i) ahead.next(z, nz);
+    }
     while (cur.valid) {
       const ZPiece pc = cur.pc;
       const int gx = pc.x0 - 1 + bx, gy0 = pc.y0 - 1 + by0, gy1 = gy0 + 1;
@@ -729,7 +744,7 @@ __global__ void __launch_bounds__(WS_T, 1)
       for (int t = 0; t < pc.nsteps; ++t, ++g) {
         const int slot = (int)(g % NST), seg = (int)(g % 3);
         mbar_wait(&full[slot], (g / NST) & 1u);
-        if (g >= 3) mbar_wait(&rempty[seg], ((g / 3) - 1) & 1u);
+        if (g >= 3) mbar_wait_sleep(&rempty[seg], ((g / 3) - 1) & 1u, ZWS_SLEEP_A);
         const double* sU = sm + slot * STG;
         const double* sV = sU + UB;
         const int p0 = pc.wa + t * ZS;
@@ -753,8 +768,13 @@ __global__ void __launch_bounds__(WS_T, 1)
           }
           const double* q0 = sU + (i + 1) * ZUP + cu0;
           const double* q1 = q0 + ZUX;
-          const double Aua = cc * ca[i + 1] + cm * (q0[-1] + q0[-ZUX] + ca[i]) + cp * (q0[1] + cb[i + 1] + ca[i + 2]);
-          const double Aub = cc * cb[i + 1] + cm * (q1[-1] + ca[i + 1] + cb[i]) + cp * (q1[1] + q1[ZUX] + cb[i + 2]);
+          // minus / plus neighbour sums of U; A u = cc u + cm sM + cp sP and (transposed convection)
+          // A^T u = cc u + cp sM + cm sP, so <U, A w> = <A^T U, w> is accumulated here, on the points this
+          // thread stores, and group B never reads the stage (reading O35)
+          const double sMa = q0[-1] + q0[-ZUX] + ca[i], sPa = q0[1] + cb[i + 1] + ca[i + 2];
+          const double sMb = q1[-1] + ca[i + 1] + cb[i], sPb = q1[1] + q1[ZUX] + cb[i + 2];
+          const double Aua = cc * ca[i + 1] + cm * sMa + cp * sPa;
+          const double Aub = cc * cb[i + 1] + cm * sMb + cp * sPb;
           double w0v, w1v;
           if (fast) {
             w0v = am0 * Aua + bm0 * ca[i + 1];
@@ -784,8 +804,14 @@ __global__ void __launch_bounds__(WS_T, 1)
           }
           // the output planes [za, zb) of w_j (a fast step has p >= za; only its last plane can be zb)
           if (fast ? (i < ZS - 1 || p < pc.zb) : (p >= pc.za && p < pc.zb)) {
-            if (st0) wc0[(int64_t)p * pl] = w0v;
-            if (st1) wc1[(int64_t)p * pl] = w1v;
+            if (st0) {
+              if (!z.store_b) wc0[(int64_t)p * pl] = w0v;
+              if (USL) acc[KM + 2] += (cc * ca[i + 1] + cp * sMa + cm * sPa) * w0v;
+            }
+            if (st1) {
+              if (!z.store_b) wc1[(int64_t)p * pl] = w1v;
+              if (USL) acc[KM + 2] += (cc * cb[i + 1] + cp * sMb + cm * sPb) * w1v;
+            }
           }
         }
         __syncwarp();
@@ -793,29 +819,32 @@ __global__ void __launch_bounds__(WS_T, 1)
           mbar_arrive(&rfull[seg]);
           mbar_arrive(&sempty[slot]);
         }
+        if (producer && ahead.valid) {  // refill this slot with global step g + NST once it is released
+          mbar_wait(&sempty[slot], (g / NST) & 1u);
+          issue(ahead, slot);
+          ahead.next(z, nz);
+        }
       }
       cur.next_piece(z, nz);
     }
   } else {
     // ======================= group B: A w_j and the next step's dot products =====================
-    const int tb = tid - WA_T, wb = tb >> 5;
+    const int tb = tid - WA_T;
     const int bx = 1 + tb % ZX, by0 = 1 + 2 * (tb / ZX);
     const int cu0 = (by0 + 1) * ZUX + (bx + 1), cu1 = cu0 + ZUX;
     const int cv0 = by0 * ZVX + (bx + 1), cv1 = cv0 + ZVX;
     const int cw0 = by0 * ZWX + bx, cw1 = cw0 + ZWX;
     const int vdot = z.vdot;
     uint32_t g = 0;
-    ZCursor<ZS> cur, ahead;  // ahead: the stage warp 0 issues next (global step g + NST)
+    ZCursor<ZS> cur;
     cur.init(z, nz, u_lo, u_hi);
-    const bool producer = wb == 0 && lane == 0;
-    if (producer) {
-      ahead.init(z, nz, u_lo, u_hi);
-      for (int i = 0; i < NST && ahead.valid; ++i) ahead.next(z, nz);
-    }
     while (cur.valid) {
       const ZPiece pc = cur.pc;
       const int gx = pc.x0 - 1 + bx, gy0 = pc.y0 - 1 + by0, gy1 = gy0 + 1;
       const bool aw0 = gx < m && gy0 < m, aw1 = gx < m && gy1 < m;
+      const bool sb = z.store_b != 0;
+      double* wo0 = a.W + (a.mode == 0 ? (int64_t)a.j * a.ld : 0) + a.off + (int64_t)gy0 * m + gx;
+      double* wo1 = wo0 + m;
       double wm1a = 0.0, w0a = 0.0, wm1b = 0.0, w0b = 0.0;  // w_j at planes p0-2, p0-1 (carried)
       double vla[KM - 1], vlb[KM - 1];
 #pragma unroll
@@ -823,8 +852,8 @@ __global__ void __launch_bounds__(WS_T, 1)
       constexpr int T0 = ZS == 1 ? 2 : 1;
       for (int t = 0; t < pc.nsteps; ++t, ++g) {
         const int slot = (int)(g % NST), seg = (int)(g % 3), sprev = (int)((g + 2) % 3);
-        mbar_wait(&full[slot], (g / NST) & 1u);
-        mbar_wait(&rfull[seg], (g / 3) & 1u);
+        if (vdot) mbar_wait(&full[slot], (g / NST) & 1u);  // the stage is read only for window dots
+        mbar_wait_sleep(&rfull[seg], (g / 3) & 1u, ZWS_SLEEP_B);
         const double* sU = sm + slot * STG;
         const double* sV = sU + UB;
         const int p0 = pc.wa + t * ZS;
@@ -838,11 +867,14 @@ __global__ void __launch_bounds__(WS_T, 1)
           const double Awa = cc * w0a + cm * (rq[cw0 - 1] + rq[cw0 - ZWX] + wm1a) + cp * (rq[cw0 + 1] + w0b + wp1a);
           const double Awb = cc * w0b + cm * (rq[cw1 - 1] + w0a + wm1b) + cp * (rq[cw1 + 1] + rq[cw1 + ZWX] + wp1b);
           if (fast || (qp >= pc.za && qp < pc.zb)) {
+            if (sb) {
+              if (aw0) wo0[(int64_t)qp * a.plane] = w0a;
+              if (aw1) wo1[(int64_t)qp * a.plane] = w0b;
+            }
             if (aw0) {
               acc[0] += w0a * w0a;
               acc[1] += w0a * Awa;
               acc[2] += Awa * Awa;
-              if (USL) acc[KM + 2] += sU[i * ZUP + cu0] * Awa;
 #pragma unroll
               for (int l = 0; l < KM - 1; ++l)
                 if ((FULL || l < nv) && ((vdot >> l) & 1))
@@ -852,7 +884,6 @@ __global__ void __launch_bounds__(WS_T, 1)
               acc[0] += w0b * w0b;
               acc[1] += w0b * Awb;
               acc[2] += Awb * Awb;
-              if (USL) acc[KM + 2] += sU[i * ZUP + cu1] * Awb;
 #pragma unroll
               for (int l = 0; l < KM - 1; ++l)
                 if ((FULL || l < nv) && ((vdot >> l) & 1))
@@ -872,13 +903,8 @@ __global__ void __launch_bounds__(WS_T, 1)
           }
         __syncwarp();
         if (lane == 0) {
-          mbar_arrive(&sempty[slot]);
+          if (vdot) mbar_arrive(&sempty[slot]);
           if (g >= 1) mbar_arrive(&rempty[sprev]);
-        }
-        if (producer && ahead.valid) {  // refill this slot with global step g + NST once all warps left it
-          mbar_wait(&sempty[slot], (g / NST) & 1u);
-          issue(ahead, slot);
-          ahead.next(z, nz);
         }
       }
       cur.next_piece(z, nz);
@@ -945,11 +971,13 @@ static int zm_npy() {  // W columns per thread: 1 = step3d_zm_kernel, 2 = step3d
   return npy;
 }
 
-static bool zm_ws() {  // warp-specialised step kernel (default); SKS_ZM_WS=0 -> pair / single-column kernels
+// warp-specialised step kernel: SKS_ZM_WS=1 (measured slower than the pair kernel, DESIGN.md section 11,
+// profiles/r02/zws_ab_r02c.txt; kept for A/B)
+static bool zm_ws() {
   static int ws = -1;
   if (ws < 0) {
     const char* e = getenv("SKS_ZM_WS");
-    ws = e ? (e[0] == '1') : 1;
+    ws = e ? (e[0] == '1') : 0;
   }
   return ws == 1;
 }
@@ -1068,6 +1096,14 @@ cudaError_t launch_step_stencil_zm(const StepArgs& a, const double* W, int64_t n
   z.units = a.ntiles;
   z.nv = (a.mode == 0) ? std::min(a.j, a.k) - 1 : (a.mode == 1 ? 1 : 0);
   z.vdot = 0;
+  {
+    static int sbv = -1;  // SKS_ZWS_STORE_B=1: group B stores w_j (A/B switch)
+    if (sbv < 0) {
+      const char* e = getenv("SKS_ZWS_STORE_B");
+      sbv = e ? (e[0] == '1') : 0;
+    }
+    z.store_b = sbv;
+  }
   if (a.mode == 0 && a.basis == 0) {  // step_prologue: vslot[l] = 3 + (lo + l) - (j - k + 1) if >= 0
     const int lo = std::max(0, a.j - a.k);
     for (int l = 0; l < z.nv; ++l)
