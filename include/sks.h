@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SKS_ABI_VERSION 5
+#define SKS_ABI_VERSION 6
 
 typedef enum {
   SKS_OK = 0,
@@ -142,9 +142,17 @@ enum {
 
 enum {
   SKS_BASIS_ARNOLDI = 0,   /* k-partial Arnoldi, Eq. (partorth) */
-  SKS_BASIS_CHEBYSHEV = 1  /* shifted-scaled Chebyshev recurrence, Eq. (Chebrecurse) P:1192-1199,
+  SKS_BASIS_CHEBYSHEV = 1, /* shifted-scaled Chebyshev recurrence, Eq. (Chebrecurse) P:1192-1199,
                               vectors rescaled to unit norm after use; no inner
                               products in the recurrence (stencil operators only) */
+  SKS_BASIS_BLOCK_CHEBYSHEV = 2 /* sks_srr_eigs only: block Chebyshev basis of the block Krylov space
+                              K_p(A; Omega), Sec. "Block Krylov subspaces" P:1867-1896 and "Block Chebyshev
+                              recurrence" P:1983-2008: B_1 = Omega (v0 holds the n_local x b start block,
+                              column-major), B_2 = (A - cI) B_1 / (2 rho), B_j = [(A - cI) B_{j-1}
+                              - (dx^2 - dy^2)/(4 rho) B_{j-2}] / rho; block size b = opts.block, depth
+                              p = d / b (d must be a multiple of b); no normalisation, no inner products;
+                              S A B from the sketched B_{p+1} through the recurrence (reading O34); stencil
+                              operators only (SKS_EUNSUPPORTED for CSR) */
 };
 
 enum {
@@ -195,7 +203,7 @@ typedef struct {
   int32_t basis;        /* SKS_BASIS_* */
   int32_t sketch;       /* SKS_SKETCH_* */
   int32_t stabilize;    /* SKS_SRR_STABILIZE_* (Sec. "Stabilization"; reading O33) */
-  int32_t reserved1;
+  int32_t block;        /* SKS_BASIS_BLOCK_CHEBYSHEV: block size b >= 1 (d = b p); ignored otherwise */
   double cheb_c, cheb_dx, cheb_dy;  /* as in sks_sgmres_opts */
 } sks_srr_opts;
 

@@ -22,6 +22,7 @@ class Config:
     tol: float = 1e-8
     max_cycles: int = 1
     nev: int = 0
+    block: int = 0         # block Krylov sRR: block size b (d = b p), 0 = single vector
     early_exit_factor: float = 0.25
     note: str = ""
 
@@ -45,6 +46,10 @@ CONFIGS = {
     # C5: sRR on 2D 2048x2048, 10 Ritz pairs of largest magnitude
     "C5": Config("C5", "srr", "stencil2d", 2048, 2048 * 2048, 10.0, 4, 300, 2, 600,
                  nev=10),
+    # C5B (not a BASELINE config): C5's operator and small side (d = 300, s = 600, nev = 10) with
+    # the block Chebyshev basis of P:1983-2008, b = 30 start vectors (Omega ~ N(0,1), seed 4), depth p = 10
+    "C5B": Config("C5B", "srr_block", "stencil2d", 2048, 2048 * 2048, 10.0, 4, 300, 0, 600,
+                  nev=10, block=30, note="block Chebyshev sRR, b = 30, p = 10"),
 }
 
 

@@ -47,8 +47,8 @@ class SgmresInfo(C.Structure):
 SKS_OPT_TIME_STEPS = 1
 SKS_OPT_ADAPTIVE_RESTART = 2
 SKS_OPT_ZERO_X0 = 4
-SKS_BASIS_ARNOLDI, SKS_BASIS_CHEBYSHEV = 0, 1
-BASES = {"arnoldi": SKS_BASIS_ARNOLDI, "chebyshev": SKS_BASIS_CHEBYSHEV}
+SKS_BASIS_ARNOLDI, SKS_BASIS_CHEBYSHEV, SKS_BASIS_BLOCK_CHEBYSHEV = 0, 1, 2
+BASES = {"arnoldi": SKS_BASIS_ARNOLDI, "chebyshev": SKS_BASIS_CHEBYSHEV, "block_chebyshev": SKS_BASIS_BLOCK_CHEBYSHEV}
 SKS_SKETCH_SPARSE, SKS_SKETCH_SRFT = 0, 1
 SKETCHES = {"sparse": SKS_SKETCH_SPARSE, "srft": SKS_SKETCH_SRFT}
 
@@ -56,7 +56,7 @@ SKETCHES = {"sparse": SKS_SKETCH_SPARSE, "srft": SKS_SKETCH_SRFT}
 class SrrOpts(C.Structure):
     _fields_ = [("d", C.c_int32), ("k", C.c_int32), ("s", C.c_int32), ("zeta", C.c_int32),
                 ("seed", C.c_uint64), ("cond_tol", C.c_double), ("basis", C.c_int32), ("sketch", C.c_int32),
-                ("stabilize", C.c_int32), ("reserved1", C.c_int32),
+                ("stabilize", C.c_int32), ("block", C.c_int32),
                 ("cheb_c", C.c_double), ("cheb_dx", C.c_double), ("cheb_dy", C.c_double)]
 
 

@@ -211,12 +211,31 @@ class Context:
 
     # ---------------------------------------------------------------- sRR
     def srr_eigs(self, A, v0, *, d, k, s, nev, zeta=8, seed=0, cond_tol=1e14, want_vectors=False,
-                 basis="arnoldi", cheb=None, sketch="sparse", stabilize="off"):
+                 basis="arnoldi", cheb=None, sketch="sparse", stabilize="off", block=0):
         """stabilize: "off", "if_ill" (kappa(T) > cond_tol, Alg. 2) or "always": truncated-SVD
-        pencil of Sec. "Stabilization", keeping sigma_i >= sigma_1 / cond_tol."""
+        pencil of Sec. "Stabilization", keeping sigma_i >= sigma_1 / cond_tol.
+        basis="block_chebyshev": v0 is the n x b start block Omega (numpy/torch, b = block columns), the
+        basis is the block Chebyshev recurrence of depth d / b."""
         op, keep = A.struct()
-        va, pv = _prep(v0)
-        n = va.shape[0]
+        if basis == "block_chebyshev":
+            # n x b start block -> column-major (each column contiguous): pass its transpose, C-contiguous
+            if _is_torch(v0):
+                vt = v0.detach().to(torch.float64)
+                vt = vt.reshape(-1, 1) if vt.dim() == 1 else vt
+                block = vt.shape[1]
+                va = vt.t().contiguous()
+                pv = va.data_ptr()
+                n = vt.shape[0]
+            else:
+                vt = np.asarray(v0, dtype=np.float64)
+                vt = vt.reshape(-1, 1) if vt.ndim == 1 else vt
+                block = vt.shape[1]
+                va = np.ascontiguousarray(vt.T)
+                pv = va.ctypes.data
+                n = vt.shape[0]
+        else:
+            va, pv = _prep(v0)
+            n = va.shape[0]
         cap = nev + 1
         th_re, th_im, rt, re = (np.zeros(cap) for _ in range(4))
         Xr = Xi = None
@@ -226,7 +245,7 @@ class Context:
             Xi, pxi = _empty_like_place(va, (cap, n))
         cc, cdx, cdy = cheb if cheb is not None else (0.0, 0.0, 0.0)
         opts = L.SrrOpts(d, k, s, zeta, seed, cond_tol, L.BASES[basis], L.SKETCHES[sketch],
-                         L.STABILIZE[stabilize], 0, cc, cdx, cdy)
+                         L.STABILIZE[stabilize], int(block), cc, cdx, cdy)
         info = L.SrrInfo()
         st = self.lib.sks_srr_eigs(self.h, C.byref(op), pv, C.byref(opts), nev, cap, th_re.ctypes.data,
                                    th_im.ctypes.data, rt.ctypes.data, re.ctypes.data, pxr, pxi, C.byref(info))

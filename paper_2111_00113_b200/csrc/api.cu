@@ -1170,6 +1170,47 @@ static sks_status basis_and_sketch(sks_ctx* c, Basis& b, int d, int s, int zeta,
   return SKS_OK;
 }
 
+// block Chebyshev basis (Sec. "Block Chebyshev recurrence" P:1983-2008): W columns
+// [(j-1) bs, j bs) hold B_j for j = 1..p+1 (B_{p+1} only feeds S A B_p through the recurrence, reading O34);
+// Omega = v0 (n_local x bs, column-major, host or device).  Then all (p+1) bs columns are sketched.
+static sks_status block_basis_and_sketch(sks_ctx* c, Basis& b, const double* v0, int bs, int p, int s, int zeta,
+                                         uint64_t key, int JB, float* t_basis_ms) {
+  cudaStream_t st = c->main();
+  const Geo& g = b.g;
+  const StepArgs& sa = b.sa;
+  const double rho = sa.cheb_rho, c0 = sa.cheb_c, e = sa.cheb_e;
+  SKS_CK(c, cudaEventRecord(c->ev_b0, st));
+  for (int i = 0; i < bs; ++i) {
+    SKS_CK(c, cudaMemcpyAsync(colp(c, b, i) + g.off, v0 + (int64_t)i * g.n, sizeof(double) * g.n, cudaMemcpyDefault,
+                              st));
+    SKS_TRY(halo_exchange(c, g, colp(c, b, i)));
+  }
+  for (int j = 2; j <= p + 1; ++j) {  // block j from blocks j-1 and j-2
+    const double* in1 = colp(c, b, (j - 2) * bs);
+    const double* in2 = (j >= 3) ? colp(c, b, (j - 3) * bs) : nullptr;
+    const double al = (j == 2) ? 1.0 / (2.0 * rho) : 1.0 / rho;
+    const double ga = (j >= 3) ? -e / rho : 0.0;
+    SKS_CK(c, launch_block_cheb(g.dim, g.m, g.nz, g.plane, g.off, g.ld, g.cc, g.cm, g.cp, in1, in2,
+                                colp(c, b, (j - 1) * bs), bs, al, c0, ga, st));
+    ++c->launches;
+    b.bytes += 8.0 * g.n * bs * (j >= 3 ? 3 : 2);
+    b.steps += bs;
+    for (int i = 0; i < bs; ++i) SKS_TRY(halo_exchange(c, g, colp(c, b, (j - 1) * bs + i)));
+  }
+  const int ncols = (p + 1) * bs;
+  const void* plan = nullptr;
+  SKS_TRY(sketch_plan(c, g, s, zeta, key, st, &plan));
+  for (int c0i = 0; c0i < ncols; c0i += JB) SKS_TRY(sketch_cols(c, b, c0i, std::min(JB, ncols - c0i), s, zeta, key, st,
+                                                              plan));
+  SKS_CK(c, cudaEventRecord(c->ev_b1, st));
+  SKS_CK(c, cudaMemcpyAsync(c->h_ctrl, c->ctrl.p, sizeof(CtrlBlock), cudaMemcpyDeviceToHost, st));
+  SKS_CK(c, cudaStreamSynchronize(st));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, c->ev_b0, c->ev_b1);
+  if (t_basis_ms) *t_basis_ms += ms;
+  return SKS_OK;
+}
+
 }  // namespace
 
 extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const double* v0, const sks_srr_opts* o,
@@ -1185,24 +1226,34 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
   if (nev < 1 || nev > 11 || nev > d || nev_cap < nev + 1) return fail(c, SKS_EINVAL, "need 1<=nev<=min(11,d), nev_cap>=nev+1");
   if (o->stabilize < SKS_SRR_STABILIZE_OFF || o->stabilize > SKS_SRR_STABILIZE_ALWAYS)
     return fail(c, SKS_EINVAL, "unknown stabilize mode");
+  const bool blk = o->basis == SKS_BASIS_BLOCK_CHEBYSHEV;
+  const int bs = blk ? o->block : 1;
+  if (blk && (bs < 1 || d % bs != 0)) return fail(c, SKS_EINVAL, "block Chebyshev basis: need block >= 1 dividing d");
+  if (blk && A->kind == SKS_OP_CSR) return fail(c, SKS_EUNSUPPORTED, "block Chebyshev basis needs a stencil operator");
+  if (blk && o->sketch != SKS_SKETCH_SPARSE) return fail(c, SKS_EUNSUPPORTED, "block Chebyshev basis: sparse sketch only");
   cudaSetDevice(c->device);
   const int64_t launches0 = c->launches;
   cudaStream_t st = c->main();
   Basis b;
-  SKS_TRY(setup_basis(c, A, k, d + 2, &b));
-  SKS_TRY(set_basis(c, A, b, o->basis, o->cheb_c, o->cheb_dx, o->cheb_dy));
+  SKS_TRY(setup_basis(c, A, k, blk ? d + bs + 2 : d + 2, &b));
+  SKS_TRY(set_basis(c, A, b, blk ? (int)SKS_BASIS_CHEBYSHEV : o->basis, o->cheb_c, o->cheb_dx, o->cheb_dy));
   const Geo& g = b.g;
   const int JB = panel_jb(s, SKS_JB);
   SKS_TRY(setup_small(c, b, s, JB));
   const int nmax = nev + 1;
   SKS_CK(c, cudaEventRecord(c->ev_t0, st));
   double* vb = c->vb.as<double>();
-  SKS_CK(c, cudaMemsetAsync(vb, 0, sizeof(double) * g.ld, st));
-  SKS_CK(c, cudaMemcpyAsync(vb + g.off, v0, sizeof(double) * g.n, cudaMemcpyDefault, st));
-  SKS_TRY(halo_exchange(c, g, vb));
   SKS_CK(c, launch_ctrl_reset(c->ctrl.as<CtrlBlock>(), -1.0, 0.0, st));
   ++c->launches;
-  SKS_TRY(first_column(c, b, 2, g.kind == SKS_OP_CSR ? vb + g.off : vb, nullptr));
+  if (!blk) {
+    SKS_CK(c, cudaMemsetAsync(vb, 0, sizeof(double) * g.ld, st));
+    SKS_CK(c, cudaMemcpyAsync(vb + g.off, v0, sizeof(double) * g.n, cudaMemcpyDefault, st));
+    SKS_TRY(halo_exchange(c, g, vb));
+    SKS_TRY(first_column(c, b, 2, g.kind == SKS_OP_CSR ? vb + g.off : vb, nullptr));
+  } else {  // unnormalised block basis: sigma = 1 for every column (B = W)
+    SKS_CK(c, launch_eye_ones(nullptr, 0, 0, c->sigma.as<double>(), d + bs + 2, st));
+    ++c->launches;
+  }
   const uint64_t key = sks_key(o->seed, 0u);
   if (o->sketch != SKS_SKETCH_SPARSE && o->sketch != SKS_SKETCH_SRFT) return fail(c, SKS_EINVAL, "unknown sketch");
   if (o->sketch == SKS_SKETCH_SRFT && c->nranks > 1)
@@ -1212,7 +1263,10 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
   c->sk_cycle = 0;
   float t_basis_ms = 0.f;
   const double bytes0 = b.bytes;
-  SKS_TRY(basis_and_sketch(c, b, d, s, zeta, key, JB, true, &t_basis_ms));
+  if (blk)
+    SKS_TRY(block_basis_and_sketch(c, b, v0, bs, d / bs, s, zeta, key, JB, &t_basis_ms));
+  else
+    SKS_TRY(basis_and_sketch(c, b, d, s, zeta, key, JB, true, &t_basis_ms));
   const double bytes_basis = b.bytes - bytes0;
   CtrlBlock* hc = c->h_ctrl;
   int de = d;
@@ -1229,25 +1283,31 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
     const int J = std::min(JB, de - j0);
     SKS_TRY(qr_append(c, b, 1, j0, J, s, 0, de, st));
   }
-  // ---- t = T^-1 U^T S w_de ; Mhat = Hbar[:de,:de] + t e_{de}^T
-  SKS_CK(c, launch_form_cols(2, c->SW.as<double>(), s, de, 1, b.k, c->H.as<double>(), b.ldH, c->sigma.as<double>(),
-                             c->gam.as<double>(), c->Xp.as<double>(), 1, 1, st));
-  SKS_CK(c, launch_utx(c->U.as<double>(), s, s, de, c->Xp.as<double>(), 1, c->Zb.as<double>(), nullptr, 0, 0, 0,
-                       c->bgsw.as<double>(), c->bgsc.as<int>(), st));
-  SKS_CK(c, launch_trsv(c->T.as<double>(), b.ncol, de, c->Zb.as<double>(), nullptr, nullptr, c->coef.as<double>(), st));
   SKS_TRY(ensure(c, c->Mh, sizeof(double) * (size_t)de * de));
   SKS_TRY(ensure(c, c->Mh2, sizeof(double) * (size_t)de * de));
-  SKS_CK(c, launch_build_mhat(c->H.as<double>(), b.ldH, de, c->coef.as<double>(), c->gam.as<double>(),
-                              c->Mh.as<double>(), st));
+  if (!blk) {
+    // ---- t = T^-1 U^T S w_de ; Mhat = Hbar[:de,:de] + t e_{de}^T
+    SKS_CK(c, launch_form_cols(2, c->SW.as<double>(), s, de, 1, b.k, c->H.as<double>(), b.ldH,
+                               c->sigma.as<double>(), c->gam.as<double>(), c->Xp.as<double>(), 1, 1, st));
+    SKS_CK(c, launch_utx(c->U.as<double>(), s, s, de, c->Xp.as<double>(), 1, c->Zb.as<double>(), nullptr, 0, 0, 0,
+                         c->bgsw.as<double>(), c->bgsc.as<int>(), st));
+    SKS_CK(c, launch_trsv(c->T.as<double>(), b.ncol, de, c->Zb.as<double>(), nullptr, nullptr, c->coef.as<double>(),
+                          st));
+    SKS_CK(c, launch_build_mhat(c->H.as<double>(), b.ldH, de, c->coef.as<double>(), c->gam.as<double>(),
+                                c->Mh.as<double>(), st));
+  }
   SKS_CK(c, cudaEventRecord(c->ev_fork, st));
   SKS_CK(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
   // ---- side stream, concurrent with the one-CTA eigen-solve: C = SB, D = SAB (for the sketched
   //      residual estimate) and kappa(T)
   SKS_TRY(ensure(c, c->SAB, sizeof(double) * (size_t)s * de));
   SKS_TRY(ensure(c, c->SB, sizeof(double) * (size_t)s * de));
-  SKS_CK(c, launch_form_cols(0, c->SW.as<double>(), s, 0, de, b.k, c->H.as<double>(), b.ldH, c->sigma.as<double>(),
-                             c->gam.as<double>(),
-                             c->SAB.as<double>(), 1, s, c->side));
+  if (blk)  // S A B through the block recurrence from the sketched B_1..B_{p+1} (reading O34)
+    SKS_CK(c, launch_block_sab(c->SW.as<double>(), s, bs, de / bs, b.sa.cheb_rho, b.sa.cheb_c, b.sa.cheb_e,
+                               c->SAB.as<double>(), c->side));
+  else
+    SKS_CK(c, launch_form_cols(0, c->SW.as<double>(), s, 0, de, b.k, c->H.as<double>(), b.ldH,
+                               c->sigma.as<double>(), c->gam.as<double>(), c->SAB.as<double>(), 1, s, c->side));
   SKS_CK(c, launch_form_cols(1, c->SW.as<double>(), s, 0, de, b.k, c->H.as<double>(), b.ldH, c->sigma.as<double>(),
                              c->gam.as<double>(),
                              c->SB.as<double>(), 1, s, c->side));
@@ -1291,6 +1351,21 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
     flags |= SKS_INFO_STABILIZED;
     c->launches += 4;
   }
+  const bool useV = stab || blk;  // the eigenvectors z of the Hessenberg matrix map back through y = V z
+  if (blk && !stab) {
+    // Mhat = T^-1 (U^T SAB) (Eq. Mhat-form; dense for a block basis), then Q^T Mhat Q = H with
+    // V = Q accumulated from the identity
+    SKS_TRY(ensure(c, c->svs, sizeof(double) * ((size_t)de + 64)));
+    SKS_TRY(ensure(c, c->svV, sizeof(double) * (size_t)de * de));
+    SKS_CK(c, cudaStreamWaitEvent(st, c->ev_join, 0));  // SAB from the side stream
+    SKS_CK(c, launch_small_gemm(de, de, s, c->U.as<double>(), s, 1, c->SAB.as<double>(), s, 0, nullptr, 0,
+                                c->Mh.as<double>(), de, st));  // U^T SAB
+    SKS_CK(c, launch_trsm_upper(c->T.as<double>(), b.ncol, de, c->Mh.as<double>(), de, de, st));
+    SKS_CK(c, launch_eye_ones(c->svV.as<double>(), de, de, nullptr, 0, st));
+    SKS_CK(c, launch_hess_reduce(c->Mh.as<double>(), de, de, c->svV.as<double>(), de, de,
+                                 reinterpret_cast<unsigned*>(c->svs.as<double>() + de + 16), st));
+    c->launches += 4;
+  }
   const int nev_e = std::min(nev, rr);
   SKS_CK(c, cudaMemcpyAsync(c->Mh2.p, c->Mh.p, sizeof(double) * (size_t)rr * rr, cudaMemcpyDeviceToDevice, st));
   SKS_TRY(ensure(c, c->wr, sizeof(double) * de));
@@ -1315,7 +1390,7 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
   SKS_CK(c, cudaStreamWaitEvent(st, c->ev_join, 0));
   const double* ys_r = c->yr.as<double>();
   const double* ys_i = c->yi.as<double>();
-  if (stab) {  // y = V_r z (de x nmax)
+  if (useV) {  // y = V_r z (de x nmax)
     SKS_TRY(ensure(c, c->y2r, sizeof(double) * (size_t)de * nmax));
     SKS_TRY(ensure(c, c->y2i, sizeof(double) * (size_t)de * nmax));
     SKS_CK(c, launch_small_gemm(de, nmax, rr, c->svV.as<double>(), de, 0, c->yr.as<double>(), rr, 0, nullptr, 0,

@@ -122,6 +122,15 @@ cudaError_t launch_srr_rest(const double* D, const double* C, int s, int d, cons
                             const double* th_re, const double* th_im, const int* nsel, int nmax, double* rest,
                             cudaStream_t st);
 
+// block.cu (block Chebyshev sRR)
+cudaError_t launch_block_cheb(int dim, int64_t m, int64_t nz, int64_t plane, int64_t off, int64_t ld, double cc,
+                              double cm, double cp, const double* in1, const double* in2, double* out, int ncols,
+                              double alpha, double shift, double gamma, cudaStream_t st);
+cudaError_t launch_block_sab(const double* SW, int s, int b, int p, double rho, double c, double e, double* SAB,
+                             cudaStream_t st);
+cudaError_t launch_trsm_upper(const double* T, int ldT, int n, double* X, int ldx, int nrhs, cudaStream_t st);
+cudaError_t launch_eye_ones(double* V, int n, int ldv, double* sigma, int nc, cudaStream_t st);
+
 // csr.cu
 cudaError_t launch_csr_spmv(int64_t n, const int32_t* rp, const int32_t* ci, const double* va, const double* xg,
                             double* out, const double* f, int mode, const double* W, int64_t ld, int lo, int nw,

@@ -831,7 +831,6 @@ __global__ void __launch_bounds__(WS_T, 1)
     // ======================= group B: A w_j and the next step's dot products =====================
     const int tb = tid - WA_T;
     const int bx = 1 + tb % ZX, by0 = 1 + 2 * (tb / ZX);
-    const int cu0 = (by0 + 1) * ZUX + (bx + 1), cu1 = cu0 + ZUX;
     const int cv0 = by0 * ZVX + (bx + 1), cv1 = cv0 + ZVX;
     const int cw0 = by0 * ZWX + bx, cw1 = cw0 + ZWX;
     const int vdot = z.vdot;

@@ -13,8 +13,8 @@ Calls ONLY ``oracle/`` (the plain fp64 CPU implementation of Alg. 1 / Alg. 2) an
     Im theta descending), their sketched residual estimates and true residuals, kappa(SB).
 
 Usage:  python tools/make_oracle_golden.py C2 C3 ...   (default: all five)
-Each file records the sha256 of the oracle/ and inputs/ sources it was produced by; the tests
-refuse a golden whose hash no longer matches (the oracle changed => regenerate).
+Each file records the sha256 of the source text of the oracle/ and inputs/ functions it was produced by
+(source_hash); the tests refuse a golden whose hash no longer matches (the oracle changed => regenerate).
 Wall time on 8 host cores (numpy/scipy): C1 <1 s, C2 ~2 min, C3 ~10 min, C4 ~3 min, C5 ~5 min;
 peak memory ~21 GB (C3/C5: B and AB at d = 300).
 """
@@ -30,21 +30,34 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 import oracle as O  # noqa: E402
-from inputs import get_config, rhs_normal, start_vector, random_csr_c4  # noqa: E402
+from inputs import get_config, rhs_normal, start_vector, start_block, random_csr_c4  # noqa: E402
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 NSAMPLE = 64
 
 
-def source_hash():
+def _deps(method):
+    """The oracle / inputs functions a golden of `method` depends on (its call graph)."""
+    import inputs as I
+    import oracle.sketch as OS
+    common = [O.stencil_coeffs, O.toeplitz_1d, O.stencil_matrix, O.csr_matrix, OS.fmix64, OS.sketch_key, OS.floyd,
+              OS.sketch_table, OS.sketch_matrix, O.thin_qr, I.rhs_normal, I.start_vector, I.random_csr_c4]
+    if method == "sgmres":
+        return common + [O.partial_arnoldi, O.sgmres_cycle, O.sgmres_solve]
+    if method == "srr":
+        return common + [O.partial_arnoldi, O.srr_eigs, O.srr_from_basis, O.select_ritz, O.srr.stabilized_pencil]
+    return common + [O.spectral_box, O.block_chebyshev_basis, O.srr_eigs_block, O.srr_from_basis, O.select_ritz,
+                     O.srr.stabilized_pencil, I.start_block]
+
+
+def source_hash(method="sgmres"):
+    """sha256 of the source text of every oracle/inputs function a golden of `method` is computed by (so adding
+    unrelated functions to oracle/ does not invalidate it, and any change of those functions does)."""
+    import inspect
     h = hashlib.sha256()
-    for pkg in ("oracle", "inputs"):
-        d = os.path.join(ROOT, pkg)
-        for fn in sorted(os.listdir(d)):
-            if fn.endswith(".py"):
-                h.update(fn.encode())
-                with open(os.path.join(d, fn), "rb") as fh:
-                    h.update(fh.read())
+    for f in _deps(method):
+        h.update(f.__module__.encode() + b"." + f.__qualname__.encode())
+        h.update(inspect.getsource(f).encode())
     return h.hexdigest()
 
 
@@ -110,12 +123,32 @@ def run_srr(cfg):
         cond_SB=float(out["cond_SB"]), d_eff=int(out["basis"]["d_eff"]), oracle_wall_s=wall)
 
 
+def run_srr_block(cfg):
+    """C5B: block Chebyshev sRR -- oracle.srr_eigs_block with the closed-form
+    spectral box of the stencil (oracle.spectral_box)."""
+    A, _ = operator(cfg)
+    Om = start_block(cfg.n, cfg.block, cfg.seed)
+    dim = 3 if cfg.op == "stencil3d" else 2
+    box = O.spectral_box(dim, cfg.m, cfg.beta)
+    nev = cfg.nev + 2
+    t0 = time.time()
+    out = O.srr_eigs_block(lambda v: A @ v, Om, cfg.d // cfg.block, *box, cfg.s, cfg.zeta, cfg.seed, nev)
+    wall = time.time() - t0
+    th = out["theta"]
+    return dict(
+        config=cfg.name, method="srr_block", n=cfg.n, d=cfg.d, block=cfg.block, s=cfg.s, zeta=cfg.zeta,
+        seed=cfg.seed, nev=cfg.nev, nev_golden=len(th), box=[float(v) for v in box],
+        theta_re=[float(t.real) for t in th], theta_im=[float(t.imag) for t in th],
+        res_est=[float(v) for v in out["res_est"]], res_true=[float(v) for v in out["res_true"]],
+        cond_SB=float(out["cond_SB"]), oracle_wall_s=wall)
+
+
 def main(names):
-    h = source_hash()
     for name in names:
         cfg = get_config(name)
+        h = source_hash(cfg.method)
         print(f"[{name}] running the oracle at full size (n = {cfg.n}) ...", flush=True)
-        g = run_sgmres(cfg) if cfg.method == "sgmres" else run_srr(cfg)
+        g = {"sgmres": run_sgmres, "srr": run_srr, "srr_block": run_srr_block}[cfg.method](cfg)
         g["oracle_source_sha256"] = h
         g["produced_by"] = "tools/make_oracle_golden.py (oracle/ + inputs/ only)"
         g["host_cores"] = len(os.sched_getaffinity(0))
