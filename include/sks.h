@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SKS_ABI_VERSION 6
+#define SKS_ABI_VERSION 7
 
 typedef enum {
   SKS_OK = 0,
@@ -69,6 +69,18 @@ sks_status sks_get_unique_id(unsigned char id[128]);
 sks_status sks_create(sks_ctx** ctx, int device, int rank, int nranks,
                       const unsigned char* id);
 sks_status sks_destroy(sks_ctx* ctx);
+
+/* Single-process LOOPBACK transport (multi-rank testing with fewer GPUs than ranks): nranks
+ * contexts in ONE process, one host thread per rank, all on one device, exchange their halos, all-reductions and
+ * all-gathers by device-to-device copies ordered with CUDA events and host barriers instead of NCCL (the
+ * library's own partition, ghost-plane and replicated-small-side code runs unchanged).  Every rank must call the
+ * same entry points in the same order from its own thread, as with NCCL.  The group is owned by the caller:
+ * create it once (nranks <= 16), create one context per rank with sks_create_loopback, destroy every context
+ * before the group.  Errors: SKS_EINVAL (NULL, nranks out of range), SKS_ENOMEM, SKS_ECUDA. */
+typedef struct sks_loopback sks_loopback;
+sks_status sks_loopback_create(int nranks, sks_loopback** group);
+sks_status sks_loopback_destroy(sks_loopback* group);
+sks_status sks_create_loopback(sks_ctx** ctx, int device, int rank, sks_loopback* group);
 const char* sks_last_error(const sks_ctx* ctx);   /* never NULL */
 int sks_abi_version(void);
 

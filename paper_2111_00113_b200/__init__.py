@@ -5,9 +5,9 @@ hand-written sm_100a CUDA kernels behind the C-ABI of include/sks.h (libsks.so).
 package is the thin Python binding (marshalling only).  No CPU fallback.
 """
 from .api import (  # noqa: F401
-    Context, StencilOperator, CsrOperator, SgmresResult, SksError, partition, get_unique_id,
+    Context, StencilOperator, CsrOperator, SgmresResult, SksError, partition, get_unique_id, LoopbackGroup,
 )
 from ._lib import load, LIBPATH, EXPORTS  # noqa: F401
 
-__all__ = ["Context", "StencilOperator", "CsrOperator", "SgmresResult", "SksError", "partition",
+__all__ = ["Context", "LoopbackGroup", "StencilOperator", "CsrOperator", "SgmresResult", "SksError", "partition",
            "get_unique_id", "load", "LIBPATH", "EXPORTS"]

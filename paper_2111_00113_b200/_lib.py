@@ -18,7 +18,8 @@ SKS_OP_STENCIL2D, SKS_OP_STENCIL3D, SKS_OP_CSR = 1, 2, 3
 # every symbol include/sks.h declares (checked by tests/test_abi.py)
 EXPORTS = ["sks_get_unique_id", "sks_create", "sks_destroy", "sks_last_error", "sks_abi_version",
            "sks_set_stream", "sks_partition", "sks_sgmres_solve", "sks_srr_eigs", "sks_sketch_apply",
-           "sks_sketch_table", "sks_apply_operator", "sks_basis", "sks_srft_apply"]
+           "sks_sketch_table", "sks_apply_operator", "sks_basis", "sks_srft_apply", "sks_loopback_create",
+           "sks_loopback_destroy", "sks_create_loopback"]
 
 
 class Operator(C.Structure):
@@ -84,6 +85,9 @@ def load(path: str = LIBPATH):
         "sks_get_unique_id": (C.c_int, [P]),
         "sks_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int, P]),
         "sks_destroy": (C.c_int, [P]),
+        "sks_loopback_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+        "sks_loopback_destroy": (C.c_int, [P]),
+        "sks_create_loopback": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int, P]),
         "sks_last_error": (C.c_char_p, [P]),
         "sks_abi_version": (C.c_int, []),
         "sks_set_stream": (C.c_int, [P, P]),

@@ -123,15 +123,38 @@ def get_unique_id() -> bytes:
     return bytes(buf)
 
 
+class LoopbackGroup:
+    """sks_loopback: `nranks` contexts of ONE process (one thread per rank, one device) exchanging through
+    device-to-device copies instead of NCCL (include/sks.h).  Destroy every Context before the group."""
+
+    def __init__(self, nranks: int):
+        self.lib = L.load()
+        self.h = C.c_void_p()
+        st = self.lib.sks_loopback_create(nranks, C.byref(self.h))
+        if st != 0:
+            raise SksError(st, "sks_loopback_create")
+        self.nranks = nranks
+
+    def close(self):
+        if self.h:
+            self.lib.sks_loopback_destroy(self.h)
+            self.h = C.c_void_p()
+
+
 class Context:
-    def __init__(self, device: int = 0, rank: int = 0, nranks: int = 1, nccl_id: bytes = None):
+    def __init__(self, device: int = 0, rank: int = 0, nranks: int = 1, nccl_id: bytes = None,
+                 loopback: LoopbackGroup = None):
         self.lib = L.load()
         self.h = C.c_void_p()
         idp = None
         if nccl_id is not None:
             self._id = (C.c_ubyte * 128).from_buffer_copy(nccl_id)
             idp = C.addressof(self._id)
-        st = self.lib.sks_create(C.byref(self.h), device, rank, nranks, idp)
+        if loopback is not None:
+            nranks = loopback.nranks
+            st = self.lib.sks_create_loopback(C.byref(self.h), device, rank, loopback.h)
+        else:
+            st = self.lib.sks_create(C.byref(self.h), device, rank, nranks, idp)
         if st != 0:
             raise SksError(st, self.lib.sks_last_error(None).decode())
         self.device, self.rank, self.nranks = device, rank, nranks

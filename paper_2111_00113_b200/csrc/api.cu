@@ -27,6 +27,7 @@
 
 // power-iteration steps of the kappa_2(T_j) estimate behind adaptive restarting
 #define SKS_ADAPT_ITERS 16
+#include "comm.h"
 #include "common.cuh"
 #include "internal.h"
 #include "step.cuh"
@@ -72,6 +73,7 @@ struct sks_ctx {
   std::vector<cudaEvent_t> ev_batch;
   std::vector<cudaEvent_t> ev_step;  // SKS_OPT_TIME_STEPS: [2 i] before / [2 i + 1] after step launch i
   ncclComm_t comm = nullptr;
+  LoopGroup* loop = nullptr;   // single-process loopback transport (comm.cu) instead of NCCL
   std::string err = "";
   int64_t launches = 0;
   // workspaces
@@ -201,6 +203,10 @@ static sks_status make_geo(sks_ctx* c, const sks_operator* A, Geo* g) {
 // communication (nranks > 1): halo planes of a ghost-layout vector, allreduce of partials
 static sks_status halo_exchange(sks_ctx* c, const Geo& g, double* vec) {
   if (c->nranks == 1 || g.G == 0) return SKS_OK;
+  if (c->loop) {
+    SKS_CK(c, loop_halo(c->loop, c->rank, vec, g.off, g.nz, g.plane, (int)g.G, c->main()));
+    return SKS_OK;
+  }
   const size_t cnt = (size_t)(g.G * g.plane);
   const int lo = c->rank - 1, hi = c->rank + 1;
   SKS_NC(c, ncclGroupStart());
@@ -218,6 +224,10 @@ static sks_status halo_exchange(sks_ctx* c, const Geo& g, double* vec) {
 
 static sks_status allreduce_sum(sks_ctx* c, double* buf, size_t cnt, cudaStream_t st) {
   if (c->nranks == 1) return SKS_OK;
+  if (c->loop) {
+    SKS_CK(c, loop_allreduce(c->loop, c->rank, buf, cnt, st));
+    return SKS_OK;
+  }
   SKS_NC(c, ncclAllReduce(buf, buf, cnt, ncclDouble, ncclSum, c->comm, st));
   return SKS_OK;
 }
@@ -240,6 +250,11 @@ static sks_status csr_gather(sks_ctx* c, const Geo& g, const double* w, const do
     return SKS_OK;
   }
   double* dst = c->xg.as<double>();
+  if (c->loop) {
+    SKS_CK(c, loop_allgather(c->loop, c->rank, w, dst, maxn, c->main()));
+    *xg = dst;
+    return SKS_OK;
+  }
   SKS_NC(c, ncclAllGather(w, dst, (size_t)maxn, ncclDouble, c->comm, c->main()));
   *xg = dst;
   return SKS_OK;
@@ -292,7 +307,32 @@ sks_status sks_partition(int kind, int64_t m, int64_t n_global, int nranks, int 
   return SKS_OK;
 }
 
+static sks_status create_ctx(sks_ctx** out, int device, int rank, int nranks, const unsigned char* id,
+                             LoopGroup* loop);
+
 sks_status sks_create(sks_ctx** out, int device, int rank, int nranks, const unsigned char* id) {
+  return create_ctx(out, device, rank, nranks, id, nullptr);
+}
+
+sks_status sks_loopback_create(int nranks, sks_loopback** group) {
+  if (!group || nranks < 1 || nranks > LOOP_MAXR) return SKS_EINVAL;
+  *group = reinterpret_cast<sks_loopback*>(loop_group_create(nranks));
+  return *group ? SKS_OK : SKS_ENOMEM;
+}
+
+sks_status sks_loopback_destroy(sks_loopback* group) {
+  if (group) loop_group_destroy(reinterpret_cast<LoopGroup*>(group));
+  return SKS_OK;
+}
+
+sks_status sks_create_loopback(sks_ctx** out, int device, int rank, sks_loopback* group) {
+  if (!group) return SKS_EINVAL;
+  LoopGroup* g = reinterpret_cast<LoopGroup*>(group);
+  return create_ctx(out, device, rank, loop_group_size(g), nullptr, g);
+}
+
+static sks_status create_ctx(sks_ctx** out, int device, int rank, int nranks, const unsigned char* id,
+                             LoopGroup* loop) {
   if (!out) return SKS_EINVAL;
   *out = nullptr;
   if (nranks < 1 || rank < 0 || rank >= nranks) return SKS_EINVAL;
@@ -341,7 +381,14 @@ sks_status sks_create(sks_ctx** out, int device, int rank, int nranks, const uns
     delete c;
     return SKS_ENOMEM;
   }
-  if (nranks > 1) {
+  if (loop) {
+    c->loop = loop;
+    if (loop_rank_init(loop, rank) != cudaSuccess) {
+      snprintf(g_err, sizeof(g_err), "loopback rank init failed");
+      delete c;
+      return SKS_ECUDA;
+    }
+  } else if (nranks > 1) {
     if (!id) {
       snprintf(g_err, sizeof(g_err), "nranks > 1 needs the NCCL unique id");
       delete c;
@@ -380,6 +427,7 @@ sks_status sks_destroy(sks_ctx* c) {
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->comm) ncclCommDestroy(c->comm);
+  if (c->loop) loop_rank_fini(c->loop, c->rank);
   if (c->tma_cache) stencil_tma_free(c->tma_cache);
   if (c->zm_cache) stencil_zm_free(c->zm_cache);
   if (c->ym_cache) stencil_ym_free(c->ym_cache);
