@@ -79,7 +79,7 @@ struct sks_ctx {
   // workspaces
   DevBuf W, xb, fb, vb, mr, xg, part, part2, partsk, sigma, H, mnorm, SW, Xp, Zb, U, T, rvec, rho, rest, coef,
       ctrl, small, Mh, Mh2, wr, wi, sel, th, yr, yi, ework, SAB, SB, svw, svs, svU, svV, svH, y2r, y2i, Xr, Xi, AXr, AXi, rpb, cib, vab, cig, rbd,
-      tmp, bgsw, bgsc, plan, gam, rcoef, srft_q, srft_w;
+      tmp, bgsw, bgsc, plan, gam, rcoef, srft_q, srft_w, partc, partcs;
   CtrlBlock* h_ctrl = nullptr;   // pinned mirror
   double* h_small = nullptr;     // pinned scratch (4096 doubles)
   int64_t w_zeroed_bytes = 0;
@@ -422,7 +422,7 @@ sks_status sks_destroy(sks_ctx* c) {
                     &c->rho,  &c->rest, &c->coef,  &c->ctrl, &c->small, &c->Mh,  &c->Mh2,   &c->wr,    &c->wi,
                     &c->sel,  &c->th,   &c->yr,    &c->yi,   &c->ework, &c->SAB, &c->SB,    &c->Xr,    &c->Xi,
                     &c->AXr,  &c->AXi,  &c->rpb,   &c->cib,  &c->vab,  &c->cig,  &c->rbd,   &c->tmp,
-                    &c->bgsw, &c->bgsc, &c->plan, &c->gam, &c->rcoef, &c->srft_q, &c->srft_w,
+                    &c->bgsw, &c->bgsc, &c->plan, &c->gam, &c->rcoef, &c->srft_q, &c->srft_w, &c->partc, &c->partcs,
                     &c->svw,  &c->svs,  &c->svU,   &c->svV,  &c->svH,  &c->y2r,   &c->y2i};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
@@ -472,6 +472,9 @@ struct Basis {
   StepArgs sat;        // step arguments with the TMA tiling
   int tma_grid = 0;
   int pslots = 0;      // partial slots (fixed across ranks)
+  bool defer = false;  // deferred Chebyshev bookkeeping (StepArgs::defer)
+  int fin_next = 2;    // first column whose deferred bookkeeping is pending
+  int defer_grid = 0;  // step grid of the deferred launches (per-column partial rows)
   StepArgs sa;
   // CSR
   const int32_t* rp = nullptr;
@@ -636,7 +639,14 @@ static sks_status set_basis(sks_ctx* c, const sks_operator* A, Basis& b, int bas
   }
   const double rho = std::max(bdx, bdy);
   if (!(rho > 0.0) || !std::isfinite(rho) || !std::isfinite(bc_)) return fail(c, SKS_EINVAL, "bad Chebyshev box");
+  const char* sync = getenv("SKS_CHEB_SYNC");  // 1: per-column reduction as for Arnoldi (A/B)
+  b.defer = !(sync && sync[0] == '1') && b.g.kind != SKS_OP_CSR;
+  if (b.defer) {
+    SKS_TRY(ensure(c, c->partc, sizeof(double) * (size_t)(b.ncol + 2) * b.pslots * SKS_NP));
+    SKS_TRY(ensure(c, c->partcs, sizeof(double) * (size_t)(b.ncol + 2) * SKS_NP));
+  }
   for (StepArgs* a : {&b.sa, &b.sat}) {
+    a->defer = b.defer ? 1 : 0;
     a->basis = 1;
     a->k = 2;
     a->cheb_c = bc_;
@@ -715,8 +725,10 @@ static sks_status step_column(sks_ctx* c, Basis& b, int j) {
     if (tm) SKS_CK(c, cudaEventRecord(c->ev_step[2 * b.ntimed], st));
     a.partials_in = pslot(c, b, c->part, j - 1);
     a.grid_prev = c->nranks > 1 ? 1 : b.last_grid;
-    a.partials_out = pslot(c, b, c->part, j);
+    const bool dcol = b.defer && j >= 2;  // this column's partials go to its own slot (cheb_finalize)
+    a.partials_out = dcol ? c->partc.as<double>() + (size_t)j * b.pslots * SKS_NP : pslot(c, b, c->part, j);
     b.last_grid = use_t ? b.tma_grid : b.step_grid;
+    if (dcol) b.defer_grid = b.last_grid;
     if (use_t && b.zm)
       SKS_CK(c, launch_step_stencil_zm(a, c->W.as<double>(), b.ncol, c->xb.as<double>(), c->fb.as<double>(),
                                        c->vb.as<double>(), b.tma_grid, st, &c->zm_cache));
@@ -734,7 +746,7 @@ static sks_status step_column(sks_ctx* c, Basis& b, int j) {
       ++b.ntimed;
       b.bytes_timed += 8.0 * g.n * (nwin + 1);
     }
-    SKS_TRY(reduce_partials(c, a.partials_out, b.last_grid, st));
+    if (!dcol) SKS_TRY(reduce_partials(c, a.partials_out, b.last_grid, st));  // deferred: once per batch
     SKS_TRY(halo_exchange(c, g, colp(c, b, j)));
     b.bytes += 8.0 * g.n * (nwin + 1);
   } else {
@@ -761,6 +773,23 @@ static sks_status step_column(sks_ctx* c, Basis& b, int j) {
     b.bytes += 12.0 * b.nnz + 4.0 * (g.n + 1) + 8.0 * g.n * (nwin + 1);
   }
   ++b.steps;
+  return SKS_OK;
+}
+
+// deferred Chebyshev bookkeeping of the complete columns [fin_next, upto): per-column fixed-order sums, ONE
+// all-reduce of (upto - fin_next) x SKS_NP scalars for the batch at nranks > 1, then sigma / H / gam / breakdown
+static sks_status cheb_finalize(sks_ctx* c, Basis& b, int upto, cudaStream_t st) {
+  if (!b.defer) return SKS_OK;
+  const int j0 = std::max(b.fin_next, 2), j1 = std::min(upto, b.ncol);
+  if (j1 <= j0) return SKS_OK;
+  double* sums = c->partcs.as<double>();
+  SKS_CK(c, launch_cheb_colsum(c->partc.as<double>(), b.defer_grid, b.pslots, j0, j1, sums, st));
+  SKS_TRY(allreduce_sum(c, sums + (size_t)j0 * SKS_NP, (size_t)(j1 - j0) * SKS_NP, st));
+  SKS_CK(c, launch_cheb_finalize(sums, j0, j1, b.sa.cheb_rho, b.sa.cheb_c, b.sa.cheb_e, c->sigma.as<double>(),
+                                 c->H.as<double>(), b.ldH, c->mnorm.as<double>(), c->gam.as<double>(),
+                                 c->ctrl.as<CtrlBlock>(), st));
+  c->launches += 2;
+  b.fin_next = j1;
   return SKS_OK;
 }
 
@@ -982,7 +1011,9 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
     SKS_CK(c, cudaMemsetAsync(c->rvec.p, 0, sizeof(double) * s, st));
     // the sketch batches run on the main stream (bandwidth kernels, all SMs but the reserved
     // ones); the sketched QR (latency kernels) on the side stream, on the reserved SMs
+    b.fin_next = 2;
     auto enqueue_side = [&](int upto /* columns [0, upto) are complete */, bool final_) -> sks_status {
+      SKS_TRY(cheb_finalize(c, b, upto, st));
       while (next_sk < upto) {
         const int J = std::min(JB, upto - next_sk);
         if (next_sk == 0) SKS_TRY(sketch_plan(c, g, s, zeta, key, st, &plan));
@@ -1191,7 +1222,9 @@ static sks_status basis_and_sketch(sks_ctx* c, Basis& b, int d, int s, int zeta,
   int next_sk = 0;
   const void* plan = nullptr;
   SKS_CK(c, cudaEventRecord(c->ev_b0, st));
+  b.fin_next = 2;
   auto side = [&](int upto) -> sks_status {
+    SKS_TRY(cheb_finalize(c, b, upto, st));
     if (!do_sketch) return SKS_OK;
     while (next_sk < upto) {  // sketch batches on the main stream (see sks_sgmres_solve)
       const int J = std::min(JB, upto - next_sk);

@@ -168,4 +168,59 @@ cudaError_t launch_eye_ones(double* V, int n, int ldv, double* sigma, int nc, cu
   return cudaGetLastError();
 }
 
+// ---- deferred Chebyshev bookkeeping (see StepArgs::defer): the per-column partial sums of a
+// batch, reduced in a fixed order to SKS_NP scalars per column (then all-reduced once per batch at P > 1) ...
+__global__ void cheb_colsum_kernel(const double* __restrict__ part, int grid, int pstride, int j0, int j1,
+                                   double* __restrict__ sums) {
+  const int j = j0 + blockIdx.x;
+  if (j >= j1) return;
+  const double* p = part + (int64_t)j * pstride * SKS_NP;
+  for (int i = threadIdx.x; i < SKS_NP; i += blockDim.x) {
+    double t = 0.0;
+    for (int b = 0; b < grid; ++b) t += p[(int64_t)b * SKS_NP + i];
+    sums[(int64_t)j * SKS_NP + i] = t;
+  }
+}
+
+// ... and the recurrence bookkeeping of columns [j0, j1) in order, exactly what step_prologue does for one column
+// (A b_j = gam_j w_{j+1} + sum_l H[l, j] b_l; sigma_j = 1/||w_j||; breakdown, reading O10)
+__global__ void cheb_finalize_kernel(const double* __restrict__ sums, int j0, int j1, double rho, double c0, double e,
+                                     double* sigma, double* H, int ldH, double* mnorm, double* gam, CtrlBlock* ctrl) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int jm = j0; jm < j1; ++jm) {
+    if (ctrl->stop_col <= jm) return;
+    const double N = sums[(int64_t)jm * SKS_NP + 0];
+    const double nu = sqrt(N);
+    const double ref = 1.0 / sigma[jm - 1];  // the previous raw vector's norm
+    if (!(N > 0.0) || !isfinite(N) || nu <= 1e-14 * ref) {
+      ctrl->stop_col = jm;
+      ctrl->breakdown = 1;
+      H[jm + (int64_t)(jm - 1) * ldH] = gam[jm - 1] * nu;
+      return;
+    }
+    const double sg = 1.0 / nu;
+    const double al = 1.0 / rho;  // alpha of launch jm + 1 (jm >= 2)
+    gam[jm] = sg / al;
+    H[jm + (int64_t)jm * ldH] = c0;                                   // -beta_u / alpha
+    H[(jm - 1) + (int64_t)jm * ldH] = -sg * (-e / rho) / (al * sigma[jm - 1]);
+    sigma[jm] = sg;
+    mnorm[jm] = sg * sqrt(sums[(int64_t)jm * SKS_NP + 2]);
+    H[jm + (int64_t)(jm - 1) * ldH] = gam[jm - 1] * nu;
+  }
+}
+
+cudaError_t launch_cheb_colsum(const double* part, int grid, int pstride, int j0, int j1, double* sums,
+                               cudaStream_t st) {
+  if (j1 <= j0) return cudaSuccess;
+  cheb_colsum_kernel<<<j1 - j0, 32, 0, st>>>(part, grid, pstride, j0, j1, sums);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cheb_finalize(const double* sums, int j0, int j1, double rho, double c0, double e, double* sigma,
+                                 double* H, int ldH, double* mnorm, double* gam, CtrlBlock* ctrl, cudaStream_t st) {
+  if (j1 <= j0) return cudaSuccess;
+  cheb_finalize_kernel<<<1, 32, 0, st>>>(sums, j0, j1, rho, c0, e, sigma, H, ldH, mnorm, gam, ctrl);
+  return cudaGetLastError();
+}
+
 }  // namespace sks

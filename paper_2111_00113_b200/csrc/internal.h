@@ -130,6 +130,10 @@ cudaError_t launch_block_sab(const double* SW, int s, int b, int p, double rho, 
                              cudaStream_t st);
 cudaError_t launch_trsm_upper(const double* T, int ldT, int n, double* X, int ldx, int nrhs, cudaStream_t st);
 cudaError_t launch_eye_ones(double* V, int n, int ldv, double* sigma, int nc, cudaStream_t st);
+cudaError_t launch_cheb_colsum(const double* part, int grid, int pstride, int j0, int j1, double* sums,
+                               cudaStream_t st);
+cudaError_t launch_cheb_finalize(const double* sums, int j0, int j1, double rho, double c0, double e, double* sigma,
+                                 double* H, int ldH, double* mnorm, double* gam, CtrlBlock* ctrl, cudaStream_t st);
 
 // csr.cu
 cudaError_t launch_csr_spmv(int64_t n, const int32_t* rp, const int32_t* ci, const double* va, const double* xg,

@@ -40,6 +40,9 @@ struct StepArgs {
   double* gam;      // gam_i: A b_i = gam_i w_{i+1} + sum_l H[l, i] b_l  (1 for Arnoldi)
   int basis;        // 0: k-truncated Arnoldi (Eq. partorth), 1: Chebyshev (Eq. Chebrecurse)
   double cheb_c, cheb_rho, cheb_e;  // Chebyshev: centre, rho, (dx^2 - dy^2)/(4 rho)
+  int defer;        // Chebyshev: from column 2 on the recurrence coefficients are constants, so
+                    // launches j >= 3 skip the previous launch's partials; the norms, sigma and the recurrence
+                    // bookkeeping of a whole batch are finalised at once (cheb_finalize_kernel)
   CtrlBlock* ctrl;
   int64_t ntiles;   // work items
   int tiles_x, tiles_y, zchunk;  // tiling
@@ -75,6 +78,25 @@ __device__ __forceinline__ bool step_prologue(const StepArgs& a, StepCoef* cf, d
     }
     __syncthreads();
     return true;
+  }
+  if (a.defer && a.basis == 1 && a.j >= 3) {
+    // deferred Chebyshev step: w_j = [(A - cI) w_{j-1} - e w_{j-2}] / rho on the raw vectors (Eq. Chebrecurse
+    // P:1192-1199), no dependence on the norms -- no reduction, no grid-wide synchronisation per column
+    if (tid == 0) {
+      const int jm = a.j - 1;
+      cf->ok = (a.ctrl->stop_col > jm && a.ctrl->exit_cols == 0) ? 1 : 0;
+      const double rho = a.cheb_rho;
+      cf->U = a.W + (int64_t)jm * a.ld;
+      cf->alpha = 1.0 / rho;
+      cf->beta_u = -a.cheb_c / rho;
+      cf->nv = 1;
+      cf->V[0] = a.W + (int64_t)(jm - 1) * a.ld;
+      cf->c[0] = -a.cheb_e / rho;
+      cf->vslot[0] = -1;
+      cf->uslot = -1;
+    }
+    __syncthreads();
+    return cf->ok != 0;
   }
   // fixed-order reduction of the previous launch's partials
   double p[SKS_NP];

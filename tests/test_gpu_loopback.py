@@ -126,3 +126,18 @@ def test_loopback_srr_matches_single_rank():
         rel = np.abs(o["theta"] - ref["theta"]) / np.abs(ref["theta"])
         assert rel.max() <= 1e-10, rel
         np.testing.assert_allclose(o["res_true"], ref["res_true"], rtol=1e-8)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_loopback_chebyshev_deferred_matches_single_rank(P):
+    """Chebyshev basis: per column only the halo exchange; the norms and recurrence bookkeeping of
+    a batch are reduced once per batch (one all-reduce of batch x (k+3) scalars).  Same x as P = 1 to 1e-10."""
+    m = 48
+    n = m ** 3
+    f = np.random.default_rng(9).standard_normal(n)
+    kw = dict(d=40, k=2, s=80, zeta=8, seed=4, tol=1e-10, max_cycles=3, basis="chebyshev")
+    ref = _solve("stencil3d", m, n, 20.0, f, 1, kw)[0]
+    outs = _solve("stencil3d", m, n, 20.0, f, P, kw)
+    x = np.concatenate([o.x for o in outs])
+    assert all(o.info["columns"] == ref.info["columns"] for o in outs)
+    assert np.abs(x - ref.x).max() <= 1e-10 * np.abs(ref.x).max()
