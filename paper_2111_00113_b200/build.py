@@ -74,7 +74,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs = list(ex.map(comp, srcs))
     libdir = os.path.join(nd, "lib")
     cmd = [NVCC] + ARCH + ["-shared", "-cudart", "shared", "-o", OUT + ".tmp"] + objs + [
-        "-L" + libdir, "-l:libnccl.so.2", "-L/usr/local/cuda/lib64", "-l:libcufft.so.11",
+        "-L" + libdir, "-l:libnccl.so.2", "-L/usr/local/cuda/lib64",
         "-Xlinker", "-rpath=" + libdir, "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
