@@ -27,6 +27,7 @@ from .sketch import (  # noqa: F401
 )
 from .krylov import partial_arnoldi, full_arnoldi, chebyshev_basis, block_chebyshev_basis  # noqa: F401
 from .sgmres import (  # noqa: F401
-    thin_qr, sgmres_cycle, sgmres_solve, gmres_exact_ls, WARN_COND, WARN_BREAKDOWN, INFO_ADAPTIVE,
+    thin_qr, sgmres_cycle, sgmres_solve, gmres_exact_ls, whitened_basis, WARN_COND, WARN_BREAKDOWN, INFO_ADAPTIVE,
+    INFO_WHITEN,
 )
 from .srr import srr_eigs, select_ritz, srr_from_basis, srr_eigs_block  # noqa: F401

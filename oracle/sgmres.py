@@ -23,6 +23,7 @@ from .sketch import sketch_matrix, SRFT
 WARN_COND = 1
 WARN_BREAKDOWN = 2
 INFO_ADAPTIVE = 8   # adaptive restarting ended a cycle early
+INFO_WHITEN = 32    # the basis was whitened at least once (Fact "Whitening" P:598-612)
 
 
 def thin_qr(C):
@@ -33,6 +34,61 @@ def thin_qr(C):
     return Q * sgn[None, :], R * sgn[:, None]
 
 
+def whitened_basis(matvec, r, d, k, S, cond_tol, breakdown_tol=1e-14, record=False):
+    """k-truncated Arnoldi (Eq. partorth) with WHITENING instead of restarting (P:1398-1400:
+    "instead of restarting, we could approximately orthogonalize B by replacing it with B T^{-1}, whose
+    condition number is constant"; Fact "Whitening" P:598-612), reading O36:
+      after each new column b_j, thin QR  S [A b_0 ... A b_j] = U T;  when first kappa_2(T) > cond_tol, the
+      columns b_0..b_{j-1} (those before the new one, J = j of them) are replaced by B_J T_J^{-1} (and A B_J by
+      A B_J T_J^{-1}, the same linear map), the new column is discarded, and the recurrence continues from the
+      whitened columns (b_J regenerated from A b_{J-1} against the last k whitened columns).  If the threshold is
+      crossed again at the same J (no progress since the last whitening), generation stops with J columns.
+    The whitened columns are rescaled to unit 2-norm, like every basis vector (the sketched QR's
+    kappa_2(T) is not invariant to column scaling, and a unit new column next to whitened columns of norm
+    ~ 1/||A|| would cross the threshold through scaling alone).  T_J^{-1} is applied with a triangular solve.  Returns dict(B, M = A B, d_eff, events (the J of each
+    whitening), breakdown, stopped, snapshots: [(J, A B_J T_J^{-1})] when record)."""
+    r = np.asarray(r, dtype=np.float64)
+    rho = np.linalg.norm(r)
+    B = [r / rho]
+    M = [matvec(B[0])]
+    events, snaps = [], []
+    last, breakdown, stopped = -1, False, False
+    while len(B) < d:
+        j = len(B)
+        lo = max(0, j - k)
+        W = np.stack(B[lo:j], axis=1)
+        m = M[j - 1]
+        h = W.T @ m                        # classical Gram-Schmidt from the same m (reading O8)
+        w = m - W @ h
+        nu = np.linalg.norm(w)
+        if nu <= breakdown_tol * np.linalg.norm(m):
+            breakdown = True
+            break
+        B.append(w / nu)
+        M.append(matvec(B[-1]))
+        _, T = thin_qr(S @ np.stack(M, axis=1))
+        if np.linalg.cond(T) > cond_tol:
+            B.pop()
+            M.pop()
+            if j <= last:
+                stopped = True
+                break
+            Tinv = solve_triangular(T[:j, :j], np.eye(j), lower=False)
+            Bw = np.stack(B, axis=1) @ Tinv
+            Mw = np.stack(M, axis=1) @ Tinv
+            if record:
+                snaps.append((j, Mw.copy()))   # A B_J T_J^{-1}, before the rescaling
+            nrm = np.linalg.norm(Bw, axis=0)   # unit columns, as every basis vector (P:1200-1201)
+            Bw /= nrm[None, :]
+            Mw /= nrm[None, :]
+            B = [Bw[:, i] for i in range(j)]
+            M = [Mw[:, i] for i in range(j)]
+            events.append(j)
+            last = j
+    return dict(B=np.stack(B, axis=1), M=np.stack(M, axis=1), d_eff=len(B), events=events, breakdown=breakdown,
+                stopped=stopped, snapshots=snaps)
+
+
 def gmres_exact_ls(M, r0):
     """GMRES problem over the same basis: min ||AB y - r0|| (Eq. gmres)."""
     y, *_ = np.linalg.lstsq(M, r0, rcond=None)
@@ -41,13 +97,14 @@ def gmres_exact_ls(M, r0):
 
 def sgmres_cycle(matvec, f, x, d, k, s, zeta, seed, cycle, tol=1e-8,
                  early_exit_factor=0.25, cond_tol=1e14, fnorm=None, S=None, cheb=None, adaptive=False,
-                 sketch="sparse"):
+                 sketch="sparse", whiten=False):
     """One cycle; cheb = (c, dx, dy) selects the Chebyshev basis of Eq. Chebrecurse
      instead of k-truncated Arnoldi.
     adaptive: adaptive restarting (Sec. adaptive-restart): "When first
     kappa_2(T_j) > tol, we recognize that it is time to restart.  We generate the new Krylov
     subspace using the previous residual r_{j-1} = r_0 - AB_{j-1} y_{j-1}" -- the cycle keeps
-    the solution of j-1 columns (at least one column is always used)."""
+    the solution of j-1 columns (at least one column is always used).
+    whiten: whitening instead of restarting (whitened_basis, reading O36)."""
     f = np.asarray(f, dtype=np.float64)
     n = f.size
     if fnorm is None:
@@ -59,7 +116,10 @@ def sgmres_cycle(matvec, f, x, d, k, s, zeta, seed, cycle, tol=1e-8,
         return dict(x=x.copy(), j=0, r_est=np.zeros(0), yhat=np.zeros(0),
                     cond_T=1.0, flags=0, basis=None, C=None, g=None)
     g = S @ r
-    basis = partial_arnoldi(matvec, r, d, k) if cheb is None else chebyshev_basis(matvec, r, d, *cheb)
+    if whiten:
+        basis = whitened_basis(matvec, r, d, k, S, cond_tol)
+    else:
+        basis = partial_arnoldi(matvec, r, d, k) if cheb is None else chebyshev_basis(matvec, r, d, *cheb)
     B, M, de = basis["B"], basis["M"], basis["d_eff"]
     C = S @ M
     U, T = thin_qr(C)
@@ -83,14 +143,14 @@ def sgmres_cycle(matvec, f, x, d, k, s, zeta, seed, cycle, tol=1e-8,
     x_new = x + B[:, :jstar] @ yhat
     condT = np.linalg.cond(T[:jstar, :jstar])
     flags = (WARN_COND if condT > cond_tol else 0) | (WARN_BREAKDOWN if basis["breakdown"] else 0) | \
-        (INFO_ADAPTIVE if adapted else 0)
+        (INFO_ADAPTIVE if adapted else 0) | (INFO_WHITEN if basis.get("events") else 0)
     return dict(x=x_new, j=jstar, r_est=r_est[:jstar], yhat=yhat, cond_T=condT,
                 flags=flags, basis=basis, C=C, g=g, U=U, T=T)
 
 
 def sgmres_solve(matvec, f, d, k, s, zeta, seed, tol=1e-8, max_cycles=50,
                  early_exit_factor=0.25, cond_tol=1e14, x0=None, keep_last=False, cheb=None, adaptive=False,
-                 sketch="sparse"):
+                 sketch="sparse", whiten=False):
     """Restarted sGMRES.  Returns dict(x, cycles, columns, rel_res_true, r_est,
     hist_est (r_est_j/||f|| per column, concatenated), hist_true (per cycle),
     cond_T, flags)."""
@@ -103,7 +163,8 @@ def sgmres_solve(matvec, f, d, k, s, zeta, seed, tol=1e-8, max_cycles=50,
     cycles = 0
     for c in range(max_cycles):
         out = sgmres_cycle(matvec, f, x, d, k, s, zeta, seed, c, tol,
-                           early_exit_factor, cond_tol, fnorm, cheb=cheb, adaptive=adaptive, sketch=sketch)
+                           early_exit_factor, cond_tol, fnorm, cheb=cheb, adaptive=adaptive, sketch=sketch,
+                           whiten=whiten)
         cycles += 1
         x = out["x"]
         columns += out["j"]
