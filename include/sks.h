@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SKS_ABI_VERSION 7
+#define SKS_ABI_VERSION 8
 
 typedef enum {
   SKS_OK = 0,
@@ -53,7 +53,8 @@ enum {
   SKS_WARN_BREAKDOWN = 2,  /* ||w_j|| <= 1e-14 ||m_{j-1}||: basis stopped early (reading O10) */
   SKS_WARN_STAGNATION = 4, /* reserved */
   SKS_INFO_ADAPTIVE_RESTART = 8, /* SKS_OPT_ADAPTIVE_RESTART ended at least one cycle early */
-  SKS_INFO_STABILIZED = 16  /* sRR solved the truncated-SVD pencil (SKS_SRR_STABILIZE_*, reading O33) */
+  SKS_INFO_STABILIZED = 16, /* sRR solved the truncated-SVD pencil (SKS_SRR_STABILIZE_*, reading O33) */
+  SKS_INFO_WHITEN = 32      /* SKS_OPT_WHITEN whitened the basis at least once */
 };
 
 typedef struct sks_ctx sks_ctx;
@@ -171,6 +172,12 @@ enum {
   SKS_OPT_TIME_STEPS = 1,       /* bracket every basis-step launch with CUDA events on the main stream and
                                    report the summed kernel time in info->t_step_s (measurement only) */
   SKS_OPT_ZERO_X0 = 4,          /* x0 = 0: x is output only (its input content is not read or copied) */
+  SKS_OPT_WHITEN = 8,           /* whitening instead of restarting (Fact "Whitening" P:598-612; P:1398-1400
+                                   "approximately orthogonalize B by replacing it with B T^{-1}"; reading O36):
+                                   when first kappa_2(T_j) > cond_tol, the first J = j-1 columns become
+                                   B_J T_J^{-1} (unit columns), T_J its diagonal, and the basis continues from
+                                   them; a second crossing at the same J ends the cycle.  k-truncated Arnoldi on
+                                   stencil operators (SKS_EUNSUPPORTED otherwise); info->flags SKS_INFO_WHITEN */
   SKS_OPT_ADAPTIVE_RESTART = 2  /* adaptive restarting (Sec. "Adaptive restarting"): when
                                    first kappa_2(T_j) > cond_tol, the cycle ends with the previous
                                    solution (j-1 columns) and restarts from its residual (reading O31:

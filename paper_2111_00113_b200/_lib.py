@@ -47,6 +47,8 @@ class SgmresInfo(C.Structure):
 
 SKS_OPT_TIME_STEPS = 1
 SKS_OPT_ADAPTIVE_RESTART = 2
+SKS_OPT_WHITEN = 8
+SKS_INFO_WHITEN = 32
 SKS_OPT_ZERO_X0 = 4
 SKS_BASIS_ARNOLDI, SKS_BASIS_CHEBYSHEV, SKS_BASIS_BLOCK_CHEBYSHEV = 0, 1, 2
 BASES = {"arnoldi": SKS_BASIS_ARNOLDI, "chebyshev": SKS_BASIS_CHEBYSHEV, "block_chebyshev": SKS_BASIS_BLOCK_CHEBYSHEV}

@@ -191,7 +191,7 @@ class Context:
     # ---------------------------------------------------------------- sGMRES
     def sgmres_solve(self, A, f, x0=None, *, d, k, s, zeta=8, seed=0, tol=1e-8, max_cycles=50,
                      early_exit_factor=0.25, cond_tol=1e14, sketch_batch=0, hist_cap=None, time_steps=False, time_stride=1,
-                     basis="arnoldi", cheb=None, adaptive_restart=False, out=None, sketch="sparse"):
+                     basis="arnoldi", cheb=None, adaptive_restart=False, out=None, sketch="sparse", whiten=False):
         op, keep = A.struct()
         fa, pf = _prep(f)
         n = fa.shape[0]
@@ -220,6 +220,7 @@ class Context:
         opts = L.SgmresOpts(d, k, s, zeta, seed, tol, max_cycles, sketch_batch, early_exit_factor, cond_tol,
                             (L.SKS_OPT_TIME_STEPS if time_steps else 0)
                             | (L.SKS_OPT_ADAPTIVE_RESTART if adaptive_restart else 0)
+                            | (L.SKS_OPT_WHITEN if whiten else 0)
                             | (L.SKS_OPT_ZERO_X0 if zero_x0 else 0), time_stride, L.BASES[basis],
                             L.SKETCHES[sketch],
                             cc, cdx, cdy)

@@ -79,7 +79,7 @@ struct sks_ctx {
   // workspaces
   DevBuf W, xb, fb, vb, mr, xg, part, part2, partsk, sigma, H, mnorm, SW, Xp, Zb, U, T, rvec, rho, rest, coef,
       ctrl, small, Mh, Mh2, wr, wi, sel, th, yr, yi, ework, SAB, SB, svw, svs, svU, svV, svH, y2r, y2i, Xr, Xi, AXr, AXi, rpb, cib, vab, cig, rbd,
-      tmp, bgsw, bgsc, plan, gam, rcoef, srft_q, srft_w, partc, partcs;
+      tmp, bgsw, bgsc, plan, gam, rcoef, srft_q, srft_w, partc, partcs, wz, wn, wpart, gsave;
   CtrlBlock* h_ctrl = nullptr;   // pinned mirror
   double* h_small = nullptr;     // pinned scratch (4096 doubles)
   int64_t w_zeroed_bytes = 0;
@@ -422,7 +422,7 @@ sks_status sks_destroy(sks_ctx* c) {
                     &c->rho,  &c->rest, &c->coef,  &c->ctrl, &c->small, &c->Mh,  &c->Mh2,   &c->wr,    &c->wi,
                     &c->sel,  &c->th,   &c->yr,    &c->yi,   &c->ework, &c->SAB, &c->SB,    &c->Xr,    &c->Xi,
                     &c->AXr,  &c->AXi,  &c->rpb,   &c->cib,  &c->vab,  &c->cig,  &c->rbd,   &c->tmp,
-                    &c->bgsw, &c->bgsc, &c->plan, &c->gam, &c->rcoef, &c->srft_q, &c->srft_w, &c->partc, &c->partcs,
+                    &c->bgsw, &c->bgsc, &c->plan, &c->gam, &c->rcoef, &c->srft_q, &c->srft_w, &c->partc, &c->partcs, &c->wz, &c->wn, &c->wpart, &c->gsave,
                     &c->svw,  &c->svs,  &c->svU,   &c->svV,  &c->svH,  &c->y2r,   &c->y2i};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
@@ -793,6 +793,63 @@ static sks_status cheb_finalize(sks_ctx* c, Basis& b, int upto, cudaStream_t st)
   return SKS_OK;
 }
 
+// Whitening (Fact "Whitening" P:598-612; reading O36): the first J basis columns
+// are replaced by B_J T_J^{-1}, rescaled to unit norm (stored raw with sigma_i = 1/||.||), S W and T follow
+// (S A B_J T_J^{-1} = U_J: T_J becomes diag(sigma)), and the partial sums the next step (column J) needs are
+// recomputed for the whitened column J-1.  Called with the streams joined.
+static sks_status whiten_columns(sks_ctx* c, Basis& b, int J, int s) {
+  cudaStream_t st = c->main();
+  const Geo& g = b.g;
+  const int ldT = b.ncol;
+  SKS_TRY(ensure(c, c->wz, sizeof(double) * (size_t)J * J));
+  SKS_TRY(ensure(c, c->wn, sizeof(double) * (size_t)g.ld * J));
+  const int ngroups = (int)std::max<int64_t>(1, std::min<int64_t>((g.n + 63) / 64, (int64_t)c->num_sms * 4));
+  SKS_TRY(ensure(c, c->wpart, sizeof(double) * ((size_t)ngroups * J + J + (size_t)s * J)));
+  double* Z = c->wz.as<double>();
+  double* part = c->wpart.as<double>();
+  double* sums = part + (size_t)ngroups * J;
+  double* swt = sums + J;
+  // Z = diag(sigma) T_J^{-1}
+  SKS_CK(c, launch_eye_ones(Z, J, J, nullptr, 0, st));
+  SKS_CK(c, launch_trsm_upper(c->T.as<double>(), ldT, J, Z, J, J, st));
+  SKS_CK(c, launch_scale_rows(Z, J, J, c->sigma.as<double>(), st));
+  // W_J <- W_J Z (out of place, interior rows) and the squared column norms
+  SKS_CK(c, launch_whiten_gemm(c->W.as<double>(), g.ld, g.off, g.n, J, Z, J, c->wn.as<double>(), part, ngroups, st));
+  SKS_CK(c, launch_colsum(part, ngroups, J, sums, st));
+  SKS_TRY(allreduce_sum(c, sums, (size_t)J, st));
+  SKS_CK(c, cudaMemcpy2DAsync(c->W.as<double>() + g.off, sizeof(double) * g.ld, c->wn.as<double>() + g.off,
+                              sizeof(double) * g.ld, sizeof(double) * g.n, J, cudaMemcpyDeviceToDevice, st));
+  // S W_J <- S W_J Z (the sketch is linear; replicated on every rank)
+  SKS_CK(c, launch_small_gemm(s, J, J, c->SW.as<double>(), s, 0, Z, J, 0, nullptr, 0, swt, s, st));
+  SKS_CK(c, cudaMemcpyAsync(c->SW.p, swt, sizeof(double) * (size_t)s * J, cudaMemcpyDeviceToDevice, st));
+  // sigma_i = 1/||w_i||, T_J = diag(sigma), control block at J QR'd columns
+  SKS_CK(c, launch_whiten_finish(sums, J, c->sigma.as<double>(), c->T.as<double>(), ldT, c->ctrl.as<CtrlBlock>(),
+                                 st));
+  // the sketched residual g - U_J U_J^T g (the columns QR'd past J are discarded)
+  SKS_CK(c, launch_resid_restore(c->rvec.as<double>(), c->gsave.as<double>(), c->U.as<double>(), s,
+                                 c->rho.as<double>(), J, s, st));
+  SKS_TRY(halo_exchange(c, g, colp(c, b, J - 1)));
+  // partial sums of the whitened w_{J-1} for the step that regenerates column J (step_prologue slot layout)
+  const double* v[SKS_KMAX];
+  int slot[SKS_KMAX];
+  int nv = 0;
+  for (int i = std::max(0, J - b.k); i < J - 1; ++i) {
+    v[nv] = colp(c, b, i) + g.off;
+    slot[nv] = 3 + i - (J - b.k);
+    ++nv;
+  }
+  const int grid = c->num_sms * 2;
+  double* p0 = pslot(c, b, c->part, J - 1);
+  SKS_CK(c, launch_whiten_partials(colp(c, b, J - 1) + g.off, v, slot, nv, g.n, g.plane, g.m, g.dim, g.cc, g.cm, g.cp,
+                                   p0, grid, st));
+  b.last_grid = grid;
+  SKS_TRY(reduce_partials(c, p0, grid, st));
+  if (J >= 2) SKS_CK(c, cudaMemsetAsync(c->mnorm.as<double>() + (J - 2), 0, sizeof(double), st));
+  c->launches += 9;
+  b.bytes += 16.0 * g.n * J;
+  return SKS_OK;
+}
+
 // ||v||_2 of this rank's interior, reduced over ranks, returned on the host (syncs)
 static sks_status global_norm(sks_ctx* c, Basis& b, const double* v_interior, double* out) {
   cudaStream_t st = c->main();
@@ -953,6 +1010,10 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
   if (!(fnorm >= 0.0) || !std::isfinite(fnorm)) return fail(c, SKS_EINVAL, "f is not finite");
   const double thr = o->early_exit_factor > 0 ? o->early_exit_factor * o->tol * fnorm : -1.0;
   const bool adaptive = (o->flags & SKS_OPT_ADAPTIVE_RESTART) != 0;
+  const bool whiten = (o->flags & SKS_OPT_WHITEN) != 0;
+  const bool watch = adaptive || whiten;  // kappa_2(T_j) estimate after every sketched-QR batch
+  if (whiten && (g.kind == SKS_OP_CSR || o->basis != SKS_BASIS_ARNOLDI))
+    return fail(c, SKS_EUNSUPPORTED, "whitening: k-truncated Arnoldi basis on a stencil operator only");
   if (o->sketch != SKS_SKETCH_SPARSE && o->sketch != SKS_SKETCH_SRFT) return fail(c, SKS_EINVAL, "unknown sketch");
   if (o->sketch == SKS_SKETCH_SRFT && c->nranks > 1)
     return fail(c, SKS_EUNSUPPORTED, "the SRFT sketch is single-GPU (the DCT mixes all rows)");
@@ -1020,6 +1081,10 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
         SKS_TRY(sketch_cols(c, b, next_sk, J, s, zeta, key, st, plan));
         if (next_sk == 0) {  // g = S r = S w_0 starts the residual vector
           SKS_CK(c, cudaMemcpyAsync(c->rvec.p, c->SW.p, sizeof(double) * s, cudaMemcpyDeviceToDevice, st));
+          if (whiten) {  // kept for the residual vector after a whitening event
+            SKS_TRY(ensure(c, c->gsave, sizeof(double) * s));
+            SKS_CK(c, cudaMemcpyAsync(c->gsave.p, c->SW.p, sizeof(double) * s, cudaMemcpyDeviceToDevice, st));
+          }
         }
         next_sk += J;
       }
@@ -1033,7 +1098,7 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
         next_qr += J;
       }
       // adaptive restarting (O31): kappa_2(T_j) after every batch, j = next_qr
-      if (adaptive && next_qr > 0 && (kq_cols.empty() || kq_cols.back() < next_qr) && kq_cols.size() < 1024) {
+      if (watch && next_qr > 0 && (kq_cols.empty() || kq_cols.back() < next_qr) && kq_cols.size() < 1024) {
         SKS_CK(c, launch_cond(c->T.as<double>(), b.ncol, next_qr, SKS_ADAPT_ITERS, dctrl,
                               c->small.as<double>() + 2048 + kq_cols.size(), c->side));
         kq_cols.push_back(next_qr);
@@ -1045,11 +1110,17 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
       (void)final_;
       return SKS_OK;
     };
+    int j_begin = 1;     // first column of this basis segment (after a whitening event: J)
+    int white_at = -1;   // J of the last whitening event of this cycle
+    bool near = false;   // r_est within a factor of the exit threshold: small batches, lag 1
+    int jstar = 0;
+    for (;;) {  // basis segments: one, or one more after every whitening event (reading O36)
     int batch_size = std::min(8, JB);
-    int pending_upto = 0;
-    int lag = poll_lag;
-    bool near = false;  // r_est within a factor of the exit threshold: small batches, lag 1
-    for (int j = 1; j <= d; ++j) {
+    int pending_upto = j_begin;
+    int lag = near ? 1 : poll_lag;
+    last_col = d;
+    if (j_begin > 1) SKS_CK(c, cudaEventRecord(c->ev_b0, st));
+    for (int j = j_begin; j <= d; ++j) {
       SKS_TRY(step_column(c, b, j));
       const bool batch_done = (j + 1 - pending_upto >= batch_size) || j == d;
       if (batch_done) {
@@ -1069,7 +1140,7 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
             batch_size = std::min(8, JB);
           }
           if (hc->exit_cols > 0 || hc->stop_col < INT_MAX || hc->rank_def ||
-              (adaptive && hc->cond > o->cond_tol)) {
+              (watch && hc->cond > o->cond_tol)) {
             last_col = j;
             break;
           }
@@ -1098,8 +1169,7 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
       b.bytes_timed = 0.0;
     }
     bytes_basis_total += b.bytes - bytes_first;
-    generated += last_col + 1;
-    int jstar;
+    generated += last_col + 1 - (j_begin - 1);
     if (hc->exit_cols > 0) {
       jstar = hc->exit_cols;
     } else {
@@ -1107,7 +1177,8 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
       if (hc->stop_col < INT_MAX) dmax = std::min(dmax, hc->stop_col);
       jstar = std::min(dmax, hc->qr_cols);
     }
-    if (adaptive && !kq_cols.empty()) {
+    int jfirst = -1;  // first j with kappa_2(T_j) > cond_tol (watch mode)
+    if (watch && !kq_cols.empty()) {
       // first batch whose kappa estimate exceeds cond_tol, then bisection inside it for the first j
       // with kappa_2(T_j) > cond_tol (kappa_2 of the leading blocks is non-decreasing in j)
       const int nk = (int)kq_cols.size();
@@ -1135,13 +1206,33 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
           else
             lo = mid;
         }
-        const int jad = std::max(hi - 1, 1);  // "restart with the previous residual r_{j-1}"
-        if (jad < jstar) {
-          jstar = jad;
-          flags |= SKS_INFO_ADAPTIVE_RESTART;
+        jfirst = hi;
+        if (adaptive) {
+          const int jad = std::max(hi - 1, 1);  // "restart with the previous residual r_{j-1}"
+          if (jad < jstar) {
+            jstar = jad;
+            flags |= SKS_INFO_ADAPTIVE_RESTART;
+          }
         }
       }
     }
+    if (whiten && jfirst > 0 && hc->exit_cols == 0 && !hc->breakdown && !hc->rank_def) {
+      const int J = jfirst - 1;  // columns kept: kappa_2(T_J) <= cond_tol
+      if (J >= 1 && J > white_at) {  // whiten B_J <- B_J T_J^{-1} (unit columns) and continue from column J
+        SKS_TRY(whiten_columns(c, b, J, s));
+        white_at = J;
+        flags |= SKS_INFO_WHITEN;
+        j_begin = J;
+        next_sk = J;
+        next_qr = J;
+        kq_cols.clear();
+        hc->cond = 0.0;
+        continue;
+      }
+      jstar = std::min(jstar, std::max(J, 1));  // no progress since the last whitening: the cycle ends here
+    }
+    break;
+    }  // basis segments
     if (hc->breakdown) flags |= SKS_WARN_BREAKDOWN;
     if (jstar <= 0) {  // nothing usable (r == 0 handled above); stop
       break;

@@ -12,6 +12,8 @@
 // registers; the in-plane neighbours come through L1 (they were loaded as plane centres by the neighbouring
 // threads).  Columns use the basis layout of api.cu (ghost planes zero at a Dirichlet boundary, filled by the halo
 // exchange between ranks).
+#include <cstring>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -220,6 +222,224 @@ cudaError_t launch_cheb_finalize(const double* sums, int j0, int j1, double rho,
                                  double* H, int ldH, double* mnorm, double* gam, CtrlBlock* ctrl, cudaStream_t st) {
   if (j1 <= j0) return cudaSuccess;
   cheb_finalize_kernel<<<1, 32, 0, st>>>(sums, j0, j1, rho, c0, e, sigma, H, ldH, mnorm, gam, ctrl);
+  return cudaGetLastError();
+}
+
+// ---- whitening (Fact "Whitening" P:598-612; reading O36) ---------------------------
+// Wn[:, i] = sum_{l <= i} W[:, l] Z[l, i] for i < J (Z = diag(sigma) T_J^{-1}, upper triangular), interior rows of
+// the basis layout (pitch ld, first interior point at off), into a separate buffer with the same layout; per
+// (row-block group, column) sums of squares of the outputs in part[blockIdx.y][i] (fixed-order, no atomics).
+constexpr int WG_R = 64, WG_C = 32, WG_K = 32;
+__global__ void __launch_bounds__(256) whiten_gemm_kernel(const double* __restrict__ W, int64_t ld, int64_t off,
+                                                          int64_t n, int J, const double* __restrict__ Z, int ldz,
+                                                          double* __restrict__ Wn, double* __restrict__ part) {
+  __shared__ double As[WG_K][WG_R + 1];
+  __shared__ double Bs[WG_K][WG_C + 1];
+  const int tid = threadIdx.x, lane = tid & 31, cg = tid >> 5;  // rows lane, lane + 32; columns 4 cg .. 4 cg + 3
+  const int i0 = blockIdx.x * WG_C;
+  double ss[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t rb = blockIdx.y; rb * WG_R < n; rb += gridDim.y) {
+    const int64_t r0 = rb * WG_R;
+    double acc[2][4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    const int lend = min(J, i0 + WG_C);  // Z[l, i] = 0 for l > i
+    for (int l0 = 0; l0 < lend; l0 += WG_K) {
+      __syncthreads();
+      for (int e = tid; e < WG_K * WG_R; e += 256) {
+        const int l = e / WG_R, r = e - l * WG_R;
+        As[l][r] = (l0 + l < J && r0 + r < n) ? W[(int64_t)(l0 + l) * ld + off + r0 + r] : 0.0;
+      }
+      for (int e = tid; e < WG_K * WG_C; e += 256) {
+        const int l = e / WG_C, c = e - l * WG_C;
+        const int gl = l0 + l, gi = i0 + c;
+        Bs[l][c] = (gl < J && gi < J && gl <= gi) ? Z[gl + (int64_t)gi * ldz] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll 8
+      for (int l = 0; l < WG_K; ++l) {
+        const double a0 = As[l][lane], a1 = As[l][lane + 32];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const double z = Bs[l][4 * cg + b];
+          acc[0][b] = fma(a0, z, acc[0][b]);
+          acc[1][b] = fma(a1, z, acc[1][b]);
+        }
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      const int64_t r = r0 + lane + 32 * a;
+      if (r < n) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int i = i0 + 4 * cg + b;
+          if (i < J) {
+            Wn[(int64_t)i * ld + off + r] = acc[a][b];
+            ss[b] = fma(acc[a][b], acc[a][b], ss[b]);
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    double v = ss[b];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int i = i0 + 4 * cg + b;
+    if (lane == 0 && i < J) part[(int64_t)blockIdx.y * J + i] = v;
+  }
+}
+
+// sums[i] = sum over the row-block groups of part[g][i], fixed order
+__global__ void colsum_kernel(const double* __restrict__ part, int ng, int J, double* __restrict__ sums) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= J) return;
+  double t = 0.0;
+  for (int g = 0; g < ng; ++g) t += part[(int64_t)g * J + i];
+  sums[i] = t;
+}
+
+// after the whitening: sigma_i = 1/||Wn_i|| (unit basis columns, reading O36), T[:J, :J] = diag(sigma), the
+// control block continues at J QR'd columns
+__global__ void whiten_finish_kernel(const double* __restrict__ sums, int J, double* sigma, double* T, int ldT,
+                                     CtrlBlock* ctrl) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx < (int64_t)J * J) {
+    const int i = (int)(idx % J), j = (int)(idx / J);
+    T[i + (int64_t)j * ldT] = (i == j) ? 1.0 / sqrt(sums[i]) : 0.0;
+  }
+  if (idx < J) sigma[idx] = 1.0 / sqrt(sums[idx]);
+  if (idx == 0) {
+    ctrl->qr_cols = J;
+    ctrl->cond = 0.0;
+    ctrl->exit_cols = 0;
+  }
+}
+
+// Z[l, i] *= sigma[l]  (Z = diag(sigma) T^{-1})
+__global__ void scale_rows_kernel(double* Z, int J, int ldz, const double* __restrict__ sigma) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)J * J) return;
+  const int l = (int)(idx % J), i = (int)(idx / J);
+  Z[l + (int64_t)i * ldz] *= sigma[l];
+}
+
+// partial sums the step after a whitening needs (step_prologue of launch J, the whitened column J-1 as w_{J-1}):
+// [0] ||u||^2, [1] <u, A u>, [2] ||A u||^2, [3 + slot_l] <v_l, A u>; stencil operator, ghost planes valid
+struct WpArgs {
+  const double* u;
+  const double* v[SKS_KMAX];
+  int slot[SKS_KMAX];
+  int nv;
+  int64_t n, plane, m;
+  int dim;
+  double cc, cm, cp;
+  double* part;  // [gridDim.x][SKS_NP]
+};
+__global__ void __launch_bounds__(256) whiten_partials_kernel(WpArgs a) {
+  double acc[3 + SKS_KMAX];
+#pragma unroll
+  for (int i = 0; i < 3 + SKS_KMAX; ++i) acc[i] = 0.0;
+  const int64_t m = a.m;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < a.n; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t z = idx / a.plane, ip = idx - z * a.plane;
+    const int64_t x = (a.dim == 3) ? ip % m : ip, y = (a.dim == 3) ? ip / m : 0;
+    const double* u = a.u + idx;
+    double sm = u[-a.plane] + (x > 0 ? u[-1] : 0.0);
+    double sp = u[a.plane] + (x < m - 1 ? u[1] : 0.0);
+    if (a.dim == 3) {
+      sm += (y > 0) ? u[-m] : 0.0;
+      sp += (y < m - 1) ? u[m] : 0.0;
+    }
+    const double uc = u[0];
+    const double Au = a.cc * uc + a.cm * sm + a.cp * sp;
+    acc[0] = fma(uc, uc, acc[0]);
+    acc[1] = fma(uc, Au, acc[1]);
+    acc[2] = fma(Au, Au, acc[2]);
+    for (int l = 0; l < a.nv; ++l) acc[3 + l] = fma(a.v[l][idx], Au, acc[3 + l]);
+  }
+  __shared__ double red[(3 + SKS_KMAX) * 32];
+  __shared__ double R[3 + SKS_KMAX];
+  block_sum_n<3 + SKS_KMAX>(acc, red, R);
+  if (threadIdx.x == 0) {
+    double out[SKS_NP];
+    for (int i = 0; i < SKS_NP; ++i) out[i] = 0.0;
+    out[0] = R[0];
+    out[1] = R[1];
+    out[2] = R[2];
+    for (int l = 0; l < a.nv; ++l)
+      if (a.slot[l] >= 3 && a.slot[l] < SKS_NP) out[a.slot[l]] = R[3 + l];
+    for (int i = 0; i < SKS_NP; ++i) a.part[(int64_t)blockIdx.x * SKS_NP + i] = out[i];
+  }
+}
+
+// r = g - U[:, :J] rho[:J]  (the explicit sketched residual vector of the QR, reading O12)
+__global__ void resid_restore_kernel(double* __restrict__ r, const double* __restrict__ g, const double* __restrict__ U,
+                                     int ldu, const double* __restrict__ rho, int J, int s) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= s) return;
+  double t = g[q];
+  for (int i = 0; i < J; ++i) t -= U[q + (int64_t)i * ldu] * rho[i];
+  r[q] = t;
+}
+
+cudaError_t launch_resid_restore(double* r, const double* g, const double* U, int ldu, const double* rho, int J, int s,
+                                 cudaStream_t st) {
+  resid_restore_kernel<<<(s + 127) / 128, 128, 0, st>>>(r, g, U, ldu, rho, J, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_whiten_gemm(const double* W, int64_t ld, int64_t off, int64_t n, int J, const double* Z, int ldz,
+                               double* Wn, double* part, int ngroups, cudaStream_t st) {
+  if (J <= 0) return cudaSuccess;
+  whiten_gemm_kernel<<<dim3((unsigned)((J + WG_C - 1) / WG_C), (unsigned)ngroups), 256, 0, st>>>(W, ld, off, n, J, Z,
+                                                                                                ldz, Wn, part);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_colsum(const double* part, int ng, int J, double* sums, cudaStream_t st) {
+  colsum_kernel<<<(J + 127) / 128, 128, 0, st>>>(part, ng, J, sums);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_whiten_finish(const double* sums, int J, double* sigma, double* T, int ldT, CtrlBlock* ctrl,
+                                 cudaStream_t st) {
+  const int64_t tot = std::max<int64_t>((int64_t)J * J, 1);
+  whiten_finish_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(sums, J, sigma, T, ldT, ctrl);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scale_rows(double* Z, int J, int ldz, const double* sigma, cudaStream_t st) {
+  const int64_t tot = (int64_t)J * J;
+  if (tot <= 0) return cudaSuccess;
+  scale_rows_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(Z, J, ldz, sigma);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_whiten_partials(const double* u, const double* const* v, const int* slot, int nv, int64_t n,
+                                   int64_t plane, int64_t m, int dim, double cc, double cm, double cp, double* part,
+                                   int grid, cudaStream_t st) {
+  WpArgs a;
+  memset(&a, 0, sizeof(a));
+  a.u = u;
+  a.nv = nv;
+  for (int l = 0; l < nv && l < SKS_KMAX; ++l) {
+    a.v[l] = v[l];
+    a.slot[l] = slot[l];
+  }
+  a.n = n;
+  a.plane = plane;
+  a.m = m;
+  a.dim = dim;
+  a.cc = cc;
+  a.cm = cm;
+  a.cp = cp;
+  a.part = part;
+  whiten_partials_kernel<<<grid, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -130,6 +130,17 @@ cudaError_t launch_block_sab(const double* SW, int s, int b, int p, double rho, 
                              cudaStream_t st);
 cudaError_t launch_trsm_upper(const double* T, int ldT, int n, double* X, int ldx, int nrhs, cudaStream_t st);
 cudaError_t launch_eye_ones(double* V, int n, int ldv, double* sigma, int nc, cudaStream_t st);
+cudaError_t launch_whiten_gemm(const double* W, int64_t ld, int64_t off, int64_t n, int J, const double* Z, int ldz,
+                               double* Wn, double* part, int ngroups, cudaStream_t st);
+cudaError_t launch_resid_restore(double* r, const double* g, const double* U, int ldu, const double* rho, int J, int s,
+                                 cudaStream_t st);
+cudaError_t launch_colsum(const double* part, int ng, int J, double* sums, cudaStream_t st);
+cudaError_t launch_whiten_finish(const double* sums, int J, double* sigma, double* T, int ldT, CtrlBlock* ctrl,
+                                 cudaStream_t st);
+cudaError_t launch_scale_rows(double* Z, int J, int ldz, const double* sigma, cudaStream_t st);
+cudaError_t launch_whiten_partials(const double* u, const double* const* v, const int* slot, int nv, int64_t n,
+                                   int64_t plane, int64_t m, int dim, double cc, double cm, double cp, double* part,
+                                   int grid, cudaStream_t st);
 cudaError_t launch_cheb_colsum(const double* part, int grid, int pstride, int j0, int j1, double* sums,
                                cudaStream_t st);
 cudaError_t launch_cheb_finalize(const double* sums, int j0, int j1, double rho, double c0, double e, double* sigma,
