@@ -1114,8 +1114,13 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
     int white_at = -1;   // J of the last whitening event of this cycle
     bool near = false;   // r_est within a factor of the exit threshold: small batches, lag 1
     int jstar = 0;
+    // CSR: a column costs a full matrix sweep, so small fixed batches let the sketched QR's early-exit flag
+    // (checked by the SpMV kernel on the device) stop the basis a few columns after the exit point
+    int csr_batch = 4;
+    if (const char* e = getenv("SKS_CSR_BATCH")) csr_batch = std::max(1, atoi(e));
+    const bool csr = g.kind == SKS_OP_CSR;
     for (;;) {  // basis segments: one, or one more after every whitening event (reading O36)
-    int batch_size = std::min(8, JB);
+    int batch_size = csr ? std::min(csr_batch, JB) : std::min(8, JB);
     int pending_upto = j_begin;
     int lag = near ? 1 : poll_lag;
     last_col = d;
@@ -1126,7 +1131,7 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
       if (batch_done) {
         SKS_TRY(enqueue_side(j + 1, j == d));
         pending_upto = j + 1;
-        batch_size = near ? std::min(8, JB) : std::min(JB, batch_size * 2);
+        batch_size = csr ? std::min(csr_batch, JB) : (near ? std::min(8, JB) : std::min(JB, batch_size * 2));
         // poll the early-exit / breakdown flags of batch nbatch-lag (bounded lag): 2 for stencils
         // (cheap columns: keep the GPU fed), 1 for CSR (a column costs a full matrix sweep, more
         // than the batch's sketched QR, so over-generated columns cost more than the wait); once

@@ -8,6 +8,8 @@
 //                  w_j = sigma_{j-1} mr - sum_i h_i sigma_i w_i;  partial ||w_j||^2.
 // (Eq. partorth; Alg. 1.)  Per-CTA partials are re-reduced in a
 // fixed order by every CTA of the next launch (deterministic, no atomics).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -68,6 +70,78 @@ __global__ void __launch_bounds__(256) csr_spmv_kernel(CsrArgs a) {
           if (l < a.nw) acc[1 + l] += a.W[(int64_t)(a.lo + l) * a.ld + r] * t;
       }
     }
+  }
+  __shared__ double R[KM + 1];
+  block_sum_n<KM + 1>(acc, red, R);
+  if (tid == 0) {
+    for (int i = 0; i < SKS_NP; ++i)
+      a.partials[(int64_t)blockIdx.x * SKS_NP + i] = (i < KM + 1) ? R[i] : 0.0;
+  }
+}
+
+// Row-block SpMV (SKS_CSR_V2=1; measured SLOWER than csr_spmv_kernel at C4 -- 433-500 vs 254 us per launch,
+// ncu: mio_throttle 57 / lg_throttle 16 warps per issue, issue active 5%: the burst of independent 32-address
+// x gathers per thread saturates the memory-instruction queues; profiles/r02/csr_ab_r02.txt): a CTA takes 256
+// consecutive rows; its
+// threads walk the rows' contiguous nonzero range [rp[r0], rp[r0+256]) with a 256-entry stride (coalesced val /
+// col_idx loads, several independent x gathers in flight per thread), stage the products in shared memory, then
+// thread t sums row r0 + t (stride-17-style reads, conflict-free for odd row lengths).  Rows of a block whose nnz
+// exceed the staging buffer are summed directly by their thread.  Same outputs and partial slots as
+// csr_spmv_kernel (mode 0: mr and ||mr||^2, <w_i, mr>; mode 1: r = f - A x and ||r||^2).
+constexpr int CSR2_R = 256;
+constexpr int CSR2_CAP = 256 * 20;  // staged products per block (C4: 17 nnz per row -> 4352)
+template <int KM>
+__global__ void __launch_bounds__(CSR2_R) csr_spmv2_kernel(CsrArgs a) {
+  __shared__ double red[SKS_NP * 32];
+  __shared__ double prod[CSR2_CAP];
+  const int tid = threadIdx.x;
+  if (a.ctrl && (a.ctrl->exit_cols != 0 || a.ctrl->stop_col < 0x7fffffff)) return;
+  double acc[KM + 1];
+#pragma unroll
+  for (int i = 0; i < KM + 1; ++i) acc[i] = 0.0;
+  for (int64_t r0 = (int64_t)blockIdx.x * CSR2_R; r0 < a.n; r0 += (int64_t)gridDim.x * CSR2_R) {
+    const int nr = (int)((a.n - r0) < CSR2_R ? (a.n - r0) : CSR2_R);
+    const int b = a.rp[r0], e = a.rp[r0 + nr];
+    const bool staged = (e - b) <= CSR2_CAP;
+    if (staged) {  // all of this thread's column indices and values in flight, then all of its x gathers
+      constexpr int NPT = CSR2_CAP / CSR2_R;
+      int cix[NPT];
+      double vv[NPT];
+#pragma unroll
+      for (int i = 0; i < NPT; ++i) {
+        const int p = b + tid + i * CSR2_R;
+        cix[i] = (p < e) ? __ldg(a.ci + p) : 0;
+        vv[i] = (p < e) ? __ldg(a.va + p) : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < NPT; ++i) {
+        const int p = b + tid + i * CSR2_R;
+        if (p < e) prod[p - b] = vv[i] * __ldg(a.xg + cix[i]);
+      }
+    }
+    __syncthreads();
+    const int64_t r = r0 + tid;
+    if (tid < nr) {
+      const int rb = a.rp[r], re = a.rp[r + 1];
+      double t = 0.0;
+      if (staged) {
+        for (int p = rb - b; p < re - b; ++p) t += prod[p];
+      } else {
+        for (int p = rb; p < re; ++p) t += a.va[p] * __ldg(a.xg + a.ci[p]);
+      }
+      if (a.mode == 1) {
+        const double rr = a.f[r] - t;
+        a.out[r] = rr;
+        acc[0] += rr * rr;
+      } else {
+        a.out[r] = t;
+        acc[0] += t * t;
+#pragma unroll
+        for (int l = 0; l < KM; ++l)
+          if (l < a.nw) acc[1 + l] += a.W[(int64_t)(a.lo + l) * a.ld + r] * t;
+      }
+    }
+    __syncthreads();  // prod is reused by the next block of rows
   }
   __shared__ double R[KM + 1];
   block_sum_n<KM + 1>(acc, red, R);
@@ -199,10 +273,23 @@ cudaError_t launch_csr_spmv(int64_t n, const int32_t* rp, const int32_t* ci, con
                             double* out, const double* f, int mode, const double* W, int64_t ld, int lo, int nw,
                             int k, double* partials, int grid, cudaStream_t st, const CtrlBlock* ctrl) {
   CsrArgs a{n, rp, ci, va, xg, out, f, mode, W, ld, lo, nw, partials, ctrl};
+  static int v1 = -1;
+  if (v1 < 0) {
+    const char* e = getenv("SKS_CSR_V2");
+    v1 = (e && e[0] == '1') ? 0 : 1;
+  }
+  if (v1) {
+    switch (csr_km(k)) {
+      case 2: csr_spmv_kernel<2><<<grid, 256, 0, st>>>(a); break;
+      case 4: csr_spmv_kernel<4><<<grid, 256, 0, st>>>(a); break;
+      default: csr_spmv_kernel<8><<<grid, 256, 0, st>>>(a); break;
+    }
+    return cudaGetLastError();
+  }
   switch (csr_km(k)) {
-    case 2: csr_spmv_kernel<2><<<grid, 256, 0, st>>>(a); break;
-    case 4: csr_spmv_kernel<4><<<grid, 256, 0, st>>>(a); break;
-    default: csr_spmv_kernel<8><<<grid, 256, 0, st>>>(a); break;
+    case 2: csr_spmv2_kernel<2><<<grid, CSR2_R, 0, st>>>(a); break;
+    case 4: csr_spmv2_kernel<4><<<grid, CSR2_R, 0, st>>>(a); break;
+    default: csr_spmv2_kernel<8><<<grid, CSR2_R, 0, st>>>(a); break;
   }
   return cudaGetLastError();
 }
