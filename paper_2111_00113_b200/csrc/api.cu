@@ -79,7 +79,7 @@ struct sks_ctx {
   // workspaces
   DevBuf W, xb, fb, vb, mr, xg, part, part2, partsk, sigma, H, mnorm, SW, Xp, Zb, U, T, rvec, rho, rest, coef,
       ctrl, small, Mh, Mh2, wr, wi, sel, th, yr, yi, ework, SAB, SB, svw, svs, svU, svV, svH, y2r, y2i, Xr, Xi, AXr, AXi, rpb, cib, vab, cig, rbd,
-      tmp, bgsw, bgsc, plan, gam, rcoef, srft_q, srft_w, partc, partcs, wz, wn, wpart, gsave;
+      tmp, bgsw, bgsc, plan, gam, rcoef, srft_q, srft_w, partc, partcs, wz, wn, wpart, gsave, csync, cctrl;
   CtrlBlock* h_ctrl = nullptr;   // pinned mirror
   double* h_small = nullptr;     // pinned scratch (4096 doubles)
   int64_t w_zeroed_bytes = 0;
@@ -422,7 +422,7 @@ sks_status sks_destroy(sks_ctx* c) {
                     &c->rho,  &c->rest, &c->coef,  &c->ctrl, &c->small, &c->Mh,  &c->Mh2,   &c->wr,    &c->wi,
                     &c->sel,  &c->th,   &c->yr,    &c->yi,   &c->ework, &c->SAB, &c->SB,    &c->Xr,    &c->Xi,
                     &c->AXr,  &c->AXi,  &c->rpb,   &c->cib,  &c->vab,  &c->cig,  &c->rbd,   &c->tmp,
-                    &c->bgsw, &c->bgsc, &c->plan, &c->gam, &c->rcoef, &c->srft_q, &c->srft_w, &c->partc, &c->partcs, &c->wz, &c->wn, &c->wpart, &c->gsave,
+                    &c->bgsw, &c->bgsc, &c->plan, &c->gam, &c->rcoef, &c->srft_q, &c->srft_w, &c->partc, &c->partcs, &c->wz, &c->wn, &c->wpart, &c->gsave, &c->csync, &c->cctrl,
                     &c->svw,  &c->svs,  &c->svU,   &c->svV,  &c->svH,  &c->y2r,   &c->y2i};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
@@ -473,6 +473,8 @@ struct Basis {
   int tma_grid = 0;
   int pslots = 0;      // partial slots (fixed across ranks)
   bool defer = false;  // deferred Chebyshev bookkeeping (StepArgs::defer)
+  bool coop = false;   // small single-rank stencil problem: batches of columns in one cooperative launch
+  int coop_grid = 0;
   int fin_next = 2;    // first column whose deferred bookkeeping is pending
   int defer_grid = 0;  // step grid of the deferred launches (per-column partial rows)
   StepArgs sa;
@@ -572,6 +574,20 @@ static sks_status setup_basis(sks_ctx* c, const sks_operator* A, int k, int ncol
       stencil_tma_tiling(g.dim, g.m, g.nz, c->main_sms, &b->sat, &b->tma_grid);
       if (b->tma_grid > b->pslots) b->tma_grid = b->pslots;
     }
+    {  // SKS_COOP_MAXN=n: problems up to n rows run batches of columns as one cooperative launch (P = 1).
+       // Measured slower at C2 (19.6 vs 14.5 us per column: two grid barriers per column), so off by default
+       // (profiles/r02/coop_ab_r02.txt)
+      int64_t lim = 0;
+      if (const char* e = getenv("SKS_COOP_MAXN")) lim = atoll(e);
+      if (c->nranks == 1 && g.n <= lim) {
+        b->coop_grid = std::min(coop_grid(c->main_sms), b->pslots);
+        b->coop = b->coop_grid > 0;
+      }
+      if (b->coop) {
+        SKS_TRY(ensure(c, c->csync, 64, true));
+        SKS_TRY(ensure(c, c->cctrl, sizeof(CtrlBlock), true));
+      }
+    }
   } else {
     b->step_grid = c->num_sms * 4;
     b->nnz = A->nnz_local;
@@ -640,7 +656,7 @@ static sks_status set_basis(sks_ctx* c, const sks_operator* A, Basis& b, int bas
   const double rho = std::max(bdx, bdy);
   if (!(rho > 0.0) || !std::isfinite(rho) || !std::isfinite(bc_)) return fail(c, SKS_EINVAL, "bad Chebyshev box");
   const char* sync = getenv("SKS_CHEB_SYNC");  // 1: per-column reduction as for Arnoldi (A/B)
-  b.defer = !(sync && sync[0] == '1') && b.g.kind != SKS_OP_CSR;
+  b.defer = !(sync && sync[0] == '1') && b.g.kind != SKS_OP_CSR && !b.coop;  // coop reduces in-kernel
   if (b.defer) {
     SKS_TRY(ensure(c, c->partc, sizeof(double) * (size_t)(b.ncol + 2) * b.pslots * SKS_NP));
     SKS_TRY(ensure(c, c->partcs, sizeof(double) * (size_t)(b.ncol + 2) * SKS_NP));
@@ -773,6 +789,26 @@ static sks_status step_column(sks_ctx* c, Basis& b, int j) {
     b.bytes += 12.0 * b.nnz + 4.0 * (g.n + 1) + 8.0 * g.n * (nwin + 1);
   }
   ++b.steps;
+  return SKS_OK;
+}
+
+// columns j0..j1 in one cooperative launch (Basis::coop)
+static sks_status coop_columns(sks_ctx* c, Basis& b, int j0, int j1) {
+  cudaStream_t st = c->main();
+  const Geo& g = b.g;
+  StepArgs a = b.sa;
+  a.defer = 0;
+  a.ctrl = c->cctrl.as<CtrlBlock>();
+  SKS_CK(c, launch_ctrl_copy(c->cctrl.as<CtrlBlock>(), c->ctrl.as<CtrlBlock>(), st));
+  SKS_CK(c, launch_step_coop(a, j0, j1, b.last_grid, c->part.as<double>(), b.pslots, c->csync.as<unsigned>(),
+                             b.coop_grid, st));
+  SKS_CK(c, launch_ctrl_merge(c->ctrl.as<CtrlBlock>(), c->cctrl.as<CtrlBlock>(), j0 == 1 ? 1 : 0, st));
+  c->launches += 4;
+  b.last_grid = b.coop_grid;
+  for (int j = j0; j <= j1; ++j) {
+    b.bytes += 8.0 * g.n * (std::min(b.k, j) + 1);
+    ++b.steps;
+  }
   return SKS_OK;
 }
 
@@ -1126,7 +1162,13 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
     last_col = d;
     if (j_begin > 1) SKS_CK(c, cudaEventRecord(c->ev_b0, st));
     for (int j = j_begin; j <= d; ++j) {
-      SKS_TRY(step_column(c, b, j));
+      if (b.coop) {  // the rest of this batch in one cooperative launch
+        const int je = std::max(j, std::min(pending_upto + batch_size - 1, d));
+        SKS_TRY(coop_columns(c, b, j, je));
+        j = je;
+      } else {
+        SKS_TRY(step_column(c, b, j));
+      }
       const bool batch_done = (j + 1 - pending_upto >= batch_size) || j == d;
       if (batch_done) {
         SKS_TRY(enqueue_side(j + 1, j == d));
@@ -1332,7 +1374,13 @@ static sks_status basis_and_sketch(sks_ctx* c, Basis& b, int d, int s, int zeta,
   };
   int pending = 0;
   for (int j = 1; j <= d; ++j) {
-    SKS_TRY(step_column(c, b, j));
+    if (b.coop) {
+      const int je = std::max(j, std::min(pending + JB - 1, d));
+      SKS_TRY(coop_columns(c, b, j, je));
+      j = je;
+    } else {
+      SKS_TRY(step_column(c, b, j));
+    }
     if (j + 1 - pending >= JB || j == d) {
       SKS_TRY(side(j + 1));
       pending = j + 1;

@@ -34,6 +34,13 @@ cudaError_t launch_step_stencil_zm(const StepArgs& a, const double* W, int64_t n
                                    const double* fb, const double* vb, int grid, cudaStream_t st, void** cache);
 void stencil_zm_free(void* cache);
 
+// stencil_coop.cu (small problems: a batch of columns in one cooperative launch, single rank)
+int coop_grid(int main_sms);
+cudaError_t launch_step_coop(const StepArgs& a, int j0, int j1, int grid_prev0, double* part, int pstride,
+                             unsigned* sync, int grid, cudaStream_t st);
+cudaError_t launch_ctrl_copy(CtrlBlock* dst, const CtrlBlock* src, cudaStream_t st);
+cudaError_t launch_ctrl_merge(CtrlBlock* real, const CtrlBlock* priv, int first, cudaStream_t st);
+
 // stencil_ym.cu (2D, even m: TMA-fed y-march kernel)
 bool stencil_ym_supported(int dim, int64_t m, int k);
 void stencil_ym_tiling(int64_t m, int64_t nz, int num_sms, StepArgs* a, int* grid);
