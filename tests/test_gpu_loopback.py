@@ -141,3 +141,51 @@ def test_loopback_chebyshev_deferred_matches_single_rank(P):
     x = np.concatenate([o.x for o in outs])
     assert all(o.info["columns"] == ref.info["columns"] for o in outs)
     assert np.abs(x - ref.x).max() <= 1e-10 * np.abs(ref.x).max()
+
+
+def test_loopback_block_srr_and_stabilized_match_single_rank():
+    """Block Chebyshev sRR (per-column halo exchange of every block column) and the stabilised sRR (replicated
+    Jacobi SVD of the all-reduced SB) at P = 2 equal P = 1."""
+    import paper_2111_00113_b200 as PK
+    from inputs import start_block
+    m, P = 96, 2
+    n = m * m
+    Om = start_block(n, 6, 3)
+    v0 = np.random.default_rng(5).standard_normal(n)
+
+    def fn_for(P_, kind):
+        def fn(ctx, r):
+            lo, hi = partition_rows("stencil2d", n, m, P_, r)
+            A = PK.StencilOperator(2, m, 12.0, lo, hi)
+            if kind == "block":
+                return ctx.srr_eigs(A, np.ascontiguousarray(Om[lo:hi]), d=30, k=2, s=60, nev=5, zeta=8, seed=2,
+                                    basis="block_chebyshev")
+            return ctx.srr_eigs(A, v0[lo:hi].copy(), d=30, k=2, s=60, nev=5, zeta=8, seed=2, stabilize="always")
+        return fn
+    for kind in ("block", "stab"):
+        ref = _run_ranks(1, fn_for(1, kind))[0]
+        outs = _run_ranks(P, fn_for(P, kind))
+        for o in outs:
+            rel = np.abs(o["theta"] - ref["theta"]) / np.abs(ref["theta"])
+            assert rel.max() <= 1e-10, (kind, rel)
+            np.testing.assert_allclose(o["res_true"], ref["res_true"], rtol=1e-8)
+
+
+def test_loopback_whitened_sgmres_matches_single_rank():
+    """Whitening (O36) at P = 2: the whitening GEMM runs on each rank's rows, the column norms are all-reduced, the
+    sketch update is replicated; same x as P = 1."""
+    m, P = 32, 2
+    n = m * m
+    f = rhs_normal_local(n)
+    kw = dict(d=45, k=2, s=120, zeta=8, seed=0, tol=1e-12, max_cycles=1, early_exit_factor=0.0, cond_tol=100.0,
+              whiten=True)
+    ref = _solve("stencil2d", m, n, 20.0, f, 1, kw)[0]
+    outs = _solve("stencil2d", m, n, 20.0, f, P, kw)
+    x = np.concatenate([o.x for o in outs])
+    assert ref.info["flags"] & 32 and all(o.info["flags"] & 32 for o in outs)
+    assert np.abs(x - ref.x).max() <= 1e-8 * np.abs(ref.x).max()
+
+
+def rhs_normal_local(n):
+    from inputs import rhs_normal
+    return rhs_normal(n, 0)

@@ -11,7 +11,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2111_00113_b200 as P  # noqa: E402
-from inputs import get_config, rhs_normal, start_vector, random_csr_c4  # noqa: E402
+from inputs import get_config, rhs_normal, start_vector, start_block, random_csr_c4  # noqa: E402
 
 
 def main(names):
@@ -37,8 +37,11 @@ def main(names):
                        rel_res_true=i["rel_res_true"], us_per_column=i["t_basis_s"] / max(i["columns_generated"], 1) * 1e6,
                        launches=i["kernel_launches"])
         else:
-            v0 = torch.from_numpy(start_vector(cfg.n, cfg.seed)).cuda()
-            kw = dict(d=cfg.d, k=cfg.k, s=cfg.s, nev=cfg.nev, zeta=cfg.zeta, seed=cfg.seed)
+            blk = cfg.method == "srr_block"
+            v0 = torch.from_numpy(start_block(cfg.n, cfg.block, cfg.seed) if blk else start_vector(cfg.n, cfg.seed)).cuda()
+            kw = dict(d=cfg.d, k=max(cfg.k, 1), s=cfg.s, nev=cfg.nev, zeta=cfg.zeta, seed=cfg.seed)
+            if blk:
+                kw["basis"] = "block_chebyshev"
             ctx.srr_eigs(A, v0, **kw)
             out_ = ctx.srr_eigs(A, v0, **kw)
             i = out_["info"]
@@ -53,4 +56,4 @@ def main(names):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["C1", "C2", "C3", "C4", "C5"])
+    main(sys.argv[1:] or ["C1", "C2", "C3", "C4", "C5", "C5B"])
