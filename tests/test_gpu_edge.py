@@ -204,3 +204,71 @@ def test_srr_stabilized_rank_below_nev(ctx):
     assert out["info"]["rank"] == 3 and 1 <= out["info"]["nev_out"] <= 4
     err = max(np.abs(orc["theta_all"] - t).min() / np.abs(t) for t in out["theta"])
     assert err <= 1e-8
+
+
+# ---------------------------------------------------------------- round-2 features: edge cases
+def test_block_srr_depth_one_and_block_one(ctx):
+    """p = 1 (d = b: the basis is Omega itself, S A B from the extra block B_2) and b = 1 (the single-vector
+    Chebyshev recurrence without normalisation) both equal the oracle's block sRR."""
+    import paper_2111_00113_b200 as P
+    from inputs import start_block
+    m, beta = 48, 10.0
+    A = O.stencil_matrix(2, m, beta)
+    box = O.spectral_box(2, m, beta)
+    for b, p in ((12, 1), (1, 14)):
+        Om = start_block(m * m, b, 8)
+        out = ctx.srr_eigs(P.StencilOperator(2, m, beta), Om, d=b * p, k=2, s=2 * b * p, nev=4, zeta=8, seed=1,
+                           basis="block_chebyshev")
+        ref = O.srr_eigs_block(lambda v: A @ v, Om, p, *box, 2 * b * p, 8, 1, 4)
+        assert len(out["theta"]) == len(ref["theta"])
+        assert (np.abs(out["theta"] - ref["theta"]) / np.abs(ref["theta"])).max() <= 1e-8, (b, p)
+
+
+def test_whiten_never_triggered_equals_plain(ctx):
+    """cond_tol far above every kappa_2(T_j): whitening never fires and the run is the plain one, bit for bit."""
+    import paper_2111_00113_b200 as P
+    f = rhs_normal(1024, 0)
+    A = P.StencilOperator(2, 32, 20.0)
+    kw = dict(d=40, k=2, s=80, zeta=8, seed=0, tol=1e-12, max_cycles=1, early_exit_factor=0.0, cond_tol=1e12)
+    w = ctx.sgmres_solve(A, f, whiten=True, **kw)
+    p = ctx.sgmres_solve(A, f, **kw)
+    assert not (w.info["flags"] & P._lib.SKS_INFO_WHITEN)
+    assert np.array_equal(np.asarray(w.x), np.asarray(p.x))
+
+
+def test_whiten_threshold_below_first_columns_stops_cleanly(ctx):
+    """A threshold crossed at once (kappa_2(T_2) > tol): whitening keeps J = 1 column, regenerates, crosses again
+    at the same J and ends the cycle (reading O36) -- a valid, finite solution from one column."""
+    import paper_2111_00113_b200 as P
+    f = rhs_normal(1024, 0)
+    Ao = O.stencil_matrix(2, 32, 20.0)
+    res = ctx.sgmres_solve(P.StencilOperator(2, 32, 20.0), f, d=40, k=2, s=80, zeta=8, seed=0, tol=1e-12,
+                           max_cycles=1, early_exit_factor=0.0, cond_tol=1.0 + 1e-9, whiten=True)
+    assert 1 <= res.info["columns"] <= 40
+    rel = np.linalg.norm(f - Ao @ np.asarray(res.x)) / np.linalg.norm(f)
+    assert np.isfinite(rel) and rel <= 1.0
+
+
+@pytest.mark.parametrize("n,c,s", [(1009, 3, 50), (4096, 32, 64), (97, 1, 97)])
+def test_srft_apply_prime_and_full_batches(ctx, n, c, s):
+    """The pruned DFT's degenerate factorisations: prime n (n1 = 1: stage 2 is the direct DFT), a full 32-column
+    batch, and s = n (every DCT coordinate sampled: an orthogonal transform, ||S x|| = ||x||)."""
+    M = np.random.default_rng(n).standard_normal((n, c))
+    SM = ctx.srft_apply(M, s=s, seed=2, cycle=0)
+    ref = O.srft_apply(M, s, 2, 0)
+    assert np.linalg.norm(SM - ref) / np.linalg.norm(ref) <= 1e-12
+    if s == n:
+        np.testing.assert_allclose(np.linalg.norm(SM, axis=0), np.linalg.norm(M, axis=0), rtol=1e-12)
+
+
+def test_loopback_group_limits():
+    import paper_2111_00113_b200 as P
+    with pytest.raises(P.SksError):
+        P.LoopbackGroup(17)
+    g = P.LoopbackGroup(1)             # a one-rank group behaves like a plain context
+    c = P.Context(0, 0, loopback=g)
+    f = rhs_normal(1024, 0)
+    r = c.sgmres_solve(P.StencilOperator(2, 32, 20.0), f, d=20, k=2, s=40, zeta=8, seed=0, max_cycles=1)
+    assert np.isfinite(r.info["rel_res_true"])
+    c.close()
+    g.close()
