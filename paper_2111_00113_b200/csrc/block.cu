@@ -48,24 +48,39 @@ __global__ void __launch_bounds__(BK_TX * BK_TY) block_cheb_kernel(BlockArgs a) 
   const int64_t pl = a.plane;
   const int64_t c0 = (a.dim == 3) ? (int64_t)y * m + x : x;  // in-plane offset
   const bool xl = x > 0, xr = x < m - 1, yl = a.dim == 3 && y > 0, yr = a.dim == 3 && y < m - 1;
-  // march along the slowest axis: the ghost planes (-1 and nz) hold zeros or the neighbour rank's planes
+  // march along the slowest axis: the ghost planes (-1 and nz) hold zeros or the neighbour rank's planes;
+  // BK_U planes per iteration with all their loads issued before any use (memory-level parallelism)
+  constexpr int BK_U = 4;
   double um = __ldg(u + c0 + (int64_t)(z0 - 1) * pl);
   double uc = __ldg(u + c0 + (int64_t)z0 * pl);
-  for (int z = z0; z < z1; ++z) {
-    const double* uz = u + c0 + (int64_t)z * pl;
-    const double up = __ldg(uz + pl);
-    double sm = um + (xl ? __ldg(uz - 1) : 0.0);
-    double sp = up + (xr ? __ldg(uz + 1) : 0.0);
-    if (a.dim == 3) {
-      sm += yl ? __ldg(uz - m) : 0.0;
-      sp += yr ? __ldg(uz + m) : 0.0;
+  for (int zb = z0; zb < z1; zb += BK_U) {
+    double up[BK_U], xm[BK_U], xp[BK_U], ym[BK_U], yp[BK_U], vv[BK_U];
+#pragma unroll
+    for (int i = 0; i < BK_U; ++i) {
+      const int z = zb + i;
+      const bool ok = z < z1;
+      const double* uz = u + c0 + (int64_t)z * pl;
+      up[i] = ok ? __ldg(uz + pl) : 0.0;
+      xm[i] = (ok && xl) ? __ldg(uz - 1) : 0.0;
+      xp[i] = (ok && xr) ? __ldg(uz + 1) : 0.0;
+      ym[i] = (ok && yl) ? __ldg(uz - m) : 0.0;
+      yp[i] = (ok && yr) ? __ldg(uz + m) : 0.0;
+      vv[i] = (ok && v) ? __ldg(v + c0 + (int64_t)z * pl) : 0.0;
     }
-    const double Au = a.cc * uc + a.cm * sm + a.cp * sp;
-    double r = a.alpha * (Au - a.shift * uc);
-    if (v) r += a.gamma * __ldg(v + c0 + (int64_t)z * pl);
-    o[c0 + (int64_t)z * pl] = r;
-    um = uc;
-    uc = up;
+#pragma unroll
+    for (int i = 0; i < BK_U; ++i) {
+      const int z = zb + i;
+      if (z < z1) {
+        const double sm = um + xm[i] + ym[i];
+        const double sp = up[i] + xp[i] + yp[i];
+        const double Au = a.cc * uc + a.cm * sm + a.cp * sp;
+        double r = a.alpha * (Au - a.shift * uc);
+        if (v) r += a.gamma * vv[i];
+        o[c0 + (int64_t)z * pl] = r;
+        um = uc;
+        uc = up[i];
+      }
+    }
   }
 }
 
