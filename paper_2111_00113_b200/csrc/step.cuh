@@ -98,16 +98,21 @@ __device__ __forceinline__ bool step_prologue(const StepArgs& a, StepCoef* cf, d
     __syncthreads();
     return cf->ok != 0;
   }
-  // fixed-order reduction of the previous launch's partials
-  double p[SKS_NP];
-#pragma unroll
-  for (int i = 0; i < SKS_NP; ++i) p[i] = 0.0;
-  for (int b = tid; b < a.grid_prev; b += blockDim.x) {
-#pragma unroll
-    for (int i = 0; i < SKS_NP; ++i) p[i] += a.partials_in[(int64_t)b * SKS_NP + i];
-  }
+  // fixed-order reduction of the previous launch's partials: warp w sums component w (w + nwarps, ...) over the
+  // grid_prev rows (lane-strided, then a butterfly) -- one barrier, ~5 shuffles per component, instead of a
+  // block-wide reduction of all SKS_NP components by every thread
   __shared__ double P[SKS_NP];
-  block_sum_n<SKS_NP>(p, red, P);
+  {
+    const int lane = tid & 31, wid = tid >> 5, nw = (int)(blockDim.x >> 5);
+    for (int cmp = wid; cmp < SKS_NP; cmp += nw) {
+      double t = 0.0;
+      for (int b = lane; b < a.grid_prev; b += 32) t += a.partials_in[(int64_t)b * SKS_NP + cmp];
+      t = warp_sum(t);
+      if (lane == 0) P[cmp] = t;
+    }
+    __syncthreads();
+  }
+  (void)red;
   if (tid == 0) {
     const int j = a.j, k = a.k;
     const int jm = j - 1;
@@ -191,17 +196,29 @@ __device__ __forceinline__ bool step_prologue(const StepArgs& a, StepCoef* cf, d
 template <int KM>
 __device__ __forceinline__ void step_epilogue(const StepArgs& a, const StepCoef* cf,
                                               double (&acc)[KM + 3], double* red) {
-  __shared__ double R[KM + 3];
-  block_sum_n<KM + 3>(acc, red, R);
-  if (threadIdx.x == 0) {
-    double out[SKS_NP];
-    for (int i = 0; i < SKS_NP; ++i) out[i] = 0.0;
-    out[0] = R[0];
-    out[1] = R[1];
-    out[2] = R[2];
-    for (int l = 0; l < KM - 1; ++l)
-      if (l < cf->nv && cf->vslot[l] >= 0) out[cf->vslot[l]] = R[3 + l];
-    if (cf->uslot >= 0) out[cf->uslot] = R[3 + KM - 1];
-    for (int i = 0; i < SKS_NP; ++i) a.partials_out[(int64_t)blockIdx.x * SKS_NP + i] = out[i];
+  // per-warp butterflies, then warp v finishes value v over the warps (fixed order) and the block's
+  // SKS_NP partial slots are written from shared memory (two barriers; no serial pass over all values)
+  __shared__ double R[SKS_NP];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
+#pragma unroll
+  for (int i = 0; i < KM + 3; ++i) acc[i] = warp_sum(acc[i]);
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < KM + 3; ++i) red[i * 32 + wid] = acc[i];
   }
+  if (threadIdx.x < SKS_NP) R[threadIdx.x] = 0.0;
+  __syncthreads();
+  for (int v = wid; v < KM + 3; v += nw) {
+    double t = lane < nw ? red[v * 32 + lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) {
+      int slot = -1;
+      if (v < 3) slot = v;
+      else if (v < KM + 2) slot = (v - 3 < cf->nv) ? cf->vslot[v - 3] : -1;
+      else slot = cf->uslot;
+      if (slot >= 0) R[slot] = t;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < SKS_NP) a.partials_out[(int64_t)blockIdx.x * SKS_NP + threadIdx.x] = R[threadIdx.x];
 }
