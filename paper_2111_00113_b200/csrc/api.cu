@@ -1155,8 +1155,12 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
     int csr_batch = 4;
     if (const char* e = getenv("SKS_CSR_BATCH")) csr_batch = std::max(1, atoi(e));
     const bool csr = g.kind == SKS_OP_CSR;
+    // first sketch batch of a cycle (SKS_FIRST_BATCH; 8: starting C3's cycles with full 32-column batches measured
+    // 50.9 vs 50.6-51.0 ms -- no gain, profiles/r02/coop_ab_r02.txt)
+    int first_batch = 8;
+    if (const char* e = getenv("SKS_FIRST_BATCH")) first_batch = std::max(1, atoi(e));
     for (;;) {  // basis segments: one, or one more after every whitening event (reading O36)
-    int batch_size = csr ? std::min(csr_batch, JB) : std::min(8, JB);
+    int batch_size = csr ? std::min(csr_batch, JB) : std::min(first_batch, JB);
     int pending_upto = j_begin;
     int lag = near ? 1 : poll_lag;
     last_col = d;
