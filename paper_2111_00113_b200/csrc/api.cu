@@ -1158,6 +1158,8 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
     // first sketch batch of a cycle (SKS_FIRST_BATCH; 8: starting C3's cycles with full 32-column batches measured
     // 50.9 vs 50.6-51.0 ms -- no gain, profiles/r02/coop_ab_r02.txt)
     int first_batch = 8;
+    int near_batch = 8;  // batch width once r_est is near the exit threshold (SKS_NEAR_BATCH)
+    if (const char* e = getenv("SKS_NEAR_BATCH")) near_batch = std::max(1, atoi(e));
     if (const char* e = getenv("SKS_FIRST_BATCH")) first_batch = std::max(1, atoi(e));
     for (;;) {  // basis segments: one, or one more after every whitening event (reading O36)
     int batch_size = csr ? std::min(csr_batch, JB) : std::min(first_batch, JB);
@@ -1177,7 +1179,7 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
       if (batch_done) {
         SKS_TRY(enqueue_side(j + 1, j == d));
         pending_upto = j + 1;
-        batch_size = csr ? std::min(csr_batch, JB) : (near ? std::min(8, JB) : std::min(JB, batch_size * 2));
+        batch_size = csr ? std::min(csr_batch, JB) : (near ? std::min(near_batch, JB) : std::min(JB, batch_size * 2));
         // poll the early-exit / breakdown flags of batch nbatch-lag (bounded lag): 2 for stencils
         // (cheap columns: keep the GPU fed), 1 for CSR (a column costs a full matrix sweep, more
         // than the batch's sketched QR, so over-generated columns cost more than the wait); once
@@ -1188,7 +1190,7 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
           if (!near && thr > 0 && hc->r_est_last > 0 && hc->r_est_last <= near_factor * thr) {
             near = true;
             lag = 1;
-            batch_size = std::min(8, JB);
+            batch_size = std::min(near_batch, JB);
           }
           if (hc->exit_cols > 0 || hc->stop_col < INT_MAX || hc->rank_def ||
               (watch && hc->cond > o->cond_tol)) {
