@@ -74,6 +74,7 @@ struct sks_ctx {
   std::vector<cudaEvent_t> ev_step;  // SKS_OPT_TIME_STEPS: [2 i] before / [2 i + 1] after step launch i
   ncclComm_t comm = nullptr;
   LoopGroup* loop = nullptr;   // single-process loopback transport (comm.cu) instead of NCCL
+  int ghost_min = 2;           // ghost planes per side of the next basis (matrix-powers Chebyshev: S + 1)
   std::string err = "";
   int64_t launches = 0;
   // workspaces
@@ -172,8 +173,8 @@ static sks_status make_geo(sks_ctx* c, const sks_operator* A, Geo* g) {
       return fail(c, SKS_EINVAL, "stencil row block must consist of whole lines (2D) / planes (3D)");
     g->nz = g->n / g->plane;
     g->z0 = A->row_begin / g->plane;
-    g->G = 2;
-    if (c->nranks > 1 && g->nz < g->G) return fail(c, SKS_EINVAL, "each rank needs >= 2 planes/lines");
+    g->G = (std::max(2, c->ghost_min) + 1) & ~1;  // even: the interior offset G*plane stays 16-byte aligned
+    if (c->nranks > 1 && g->nz < g->G) return fail(c, SKS_EINVAL, "each rank needs >= G planes/lines");
     if (!std::isfinite(A->beta)) return fail(c, SKS_EINVAL, "beta not finite");
     const double ih2 = (double)(g->m + 1) * (double)(g->m + 1);
     const double ih = (double)(g->m + 1) / 2.0;
@@ -473,6 +474,8 @@ struct Basis {
   int tma_grid = 0;
   int pslots = 0;      // partial slots (fixed across ranks)
   bool defer = false;  // deferred Chebyshev bookkeeping (StepArgs::defer)
+  int mpk_s = 0;       // 2D Chebyshev matrix-powers steps: columns per launch (0 = off)
+  int mpk_grid = 0;
   bool coop = false;   // small single-rank stencil problem: batches of columns in one cooperative launch
   int coop_grid = 0;
   int fin_next = 2;    // first column whose deferred bookkeeping is pending
@@ -812,6 +815,46 @@ static sks_status coop_columns(sks_ctx* c, Basis& b, int j0, int j1) {
   return SKS_OK;
 }
 
+// SKS_MPK_S (default 4; 0 = off): columns per matrix-powers launch of the deferred 2D Chebyshev basis
+// Off by default: at C2 (m = 512, 4 own lines per CTA) the 2 (S + 1) halo lines per launch triple the work and it
+// measured 40.2 vs 33.3 ms (profiles/r02/mpk_ab_r02.txt); its purpose is one depth-(S+1) halo exchange per S
+// columns across ranks (tests/test_gpu_loopback.py)
+static int mpk_request() {
+  const char* e = getenv("SKS_MPK_S");
+  const int v = e ? atoi(e) : 0;
+  return std::max(0, std::min(v, 8));
+}
+
+// decide the matrix-powers mode once the basis is set up (deferred Chebyshev, 2D stencil, ghost depth >= S + 1,
+// the staged lines fit in shared memory with the step kernels' grid)
+static void mpk_setup(sks_ctx* c, Basis& b) {
+  const int S = mpk_request();
+  b.mpk_s = 0;
+  if (!b.defer || b.g.dim != 2 || S < 1 || b.g.G < S + 1) return;
+  const int grid = b.tma ? b.tma_grid : b.step_grid;
+  if (grid < 1 || grid > b.pslots || mpk2d_smem(b.g.m, b.g.nz, grid, S) > 200 * 1024) return;
+  b.mpk_s = S;
+  b.mpk_grid = grid;
+}
+
+// columns j0..j1 (j0 >= 3) of the deferred 2D Chebyshev basis in one matrix-powers launch; at nranks > 1 the
+// two newest columns' ghost lines (depth G >= S + 1) are exchanged once for the next launch
+static sks_status mpk_columns(sks_ctx* c, Basis& b, int j0, int j1) {
+  cudaStream_t st = c->main();
+  const Geo& g = b.g;
+  const int S = j1 - j0 + 1;
+  SKS_CK(c, launch_cheb_mpk2d(c->W.as<double>(), g.ld, g.off, g.m, g.nz, g.z0, g.m, g.cc, g.cm, g.cp, b.sa.cheb_rho,
+                              b.sa.cheb_c, b.sa.cheb_e, j0, S, c->partc.as<double>(), b.pslots, b.mpk_grid,
+                              c->ctrl.as<CtrlBlock>(), b.mpk_grid, st));
+  ++c->launches;
+  b.defer_grid = b.mpk_grid;
+  if (S >= 2) SKS_TRY(halo_exchange(c, g, colp(c, b, j1 - 1)));
+  SKS_TRY(halo_exchange(c, g, colp(c, b, j1)));
+  b.bytes += 8.0 * g.n * (2 + S);
+  b.steps += S;
+  return SKS_OK;
+}
+
 // deferred Chebyshev bookkeeping of the complete columns [fin_next, upto): per-column fixed-order sums, ONE
 // all-reduce of (upto - fin_next) x SKS_NP scalars for the batch at nranks > 1, then sigma / H / gam / breakdown
 static sks_status cheb_finalize(sks_ctx* c, Basis& b, int upto, cudaStream_t st) {
@@ -1012,8 +1055,13 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
   const int64_t launches0 = c->launches;
   cudaStream_t st = c->main();
   Basis b;
-  SKS_TRY(setup_basis(c, A, k, d + 2, &b));
+  c->ghost_min = (o->basis == SKS_BASIS_CHEBYSHEV && A->kind == SKS_OP_STENCIL2D && mpk_request() > 0)
+                     ? mpk_request() + 1 : 2;
+  const sks_status sb = setup_basis(c, A, k, d + 2, &b);
+  c->ghost_min = 2;
+  SKS_TRY(sb);
   SKS_TRY(set_basis(c, A, b, o->basis, o->cheb_c, o->cheb_dx, o->cheb_dy));
+  mpk_setup(c, b);
   const Geo& g = b.g;
   const int JB = panel_jb(s, o->sketch_batch > 0 ? o->sketch_batch : SKS_JB);
   b.time_steps = (o->flags & SKS_OPT_TIME_STEPS) != 0;
@@ -1171,6 +1219,10 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
       if (b.coop) {  // the rest of this batch in one cooperative launch
         const int je = std::max(j, std::min(pending_upto + batch_size - 1, d));
         SKS_TRY(coop_columns(c, b, j, je));
+        j = je;
+      } else if (b.mpk_s > 0 && j >= 3) {  // matrix-powers launch (deferred 2D Chebyshev)
+        const int je = std::max(j, std::min(std::min(j + b.mpk_s - 1, pending_upto + batch_size - 1), d));
+        SKS_TRY(mpk_columns(c, b, j, je));
         j = je;
       } else {
         SKS_TRY(step_column(c, b, j));
@@ -1384,6 +1436,10 @@ static sks_status basis_and_sketch(sks_ctx* c, Basis& b, int d, int s, int zeta,
       const int je = std::max(j, std::min(pending + JB - 1, d));
       SKS_TRY(coop_columns(c, b, j, je));
       j = je;
+    } else if (b.mpk_s > 0 && j >= 3) {
+      const int je = std::max(j, std::min(std::min(j + b.mpk_s - 1, pending + JB - 1), d));
+      SKS_TRY(mpk_columns(c, b, j, je));
+      j = je;
     } else {
       SKS_TRY(step_column(c, b, j));
     }
@@ -1466,8 +1522,13 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
   const int64_t launches0 = c->launches;
   cudaStream_t st = c->main();
   Basis b;
-  SKS_TRY(setup_basis(c, A, k, blk ? d + bs + 2 : d + 2, &b));
+  c->ghost_min = (!blk && o->basis == SKS_BASIS_CHEBYSHEV && A->kind == SKS_OP_STENCIL2D && mpk_request() > 0)
+                     ? mpk_request() + 1 : 2;
+  const sks_status sb = setup_basis(c, A, k, blk ? d + bs + 2 : d + 2, &b);
+  c->ghost_min = 2;
+  SKS_TRY(sb);
   SKS_TRY(set_basis(c, A, b, blk ? (int)SKS_BASIS_CHEBYSHEV : o->basis, o->cheb_c, o->cheb_dx, o->cheb_dy));
+  if (!blk) mpk_setup(c, b);
   const Geo& g = b.g;
   const int JB = panel_jb(s, SKS_JB);
   SKS_TRY(setup_small(c, b, s, JB));

@@ -459,3 +459,144 @@ cudaError_t launch_whiten_partials(const double* u, const double* const* v, cons
 }
 
 }  // namespace sks
+
+namespace sks {
+// ---- 2D Chebyshev matrix-powers step (SURVEY NEXT(1) "depth-s halos"; Eq. Chebrecurse P:1192-1199 with the
+// deferred bookkeeping of O37): S consecutive columns w_j .. w_{j+S-1} of the raw recurrence
+//     w_i = rho^-1 [ (A - cI) w_{i-1} - e w_{i-2} ]
+// in ONE launch.  CTA b owns the lines [y0, y1) of the slab; it stages w_{j-1}, w_{j-2} on the lines
+// [y0 - S - 1, y1 + S + 1) in shared memory (ghost lines: Dirichlet zeros at the domain boundary, the neighbour
+// rank's lines -- exchanged once per launch with depth G >= S + 1 -- inside), then computes step t on the lines
+// [y0 - S + t, y1 + S - t) (the valid region shrinks by one line per step), writes its own lines of every column
+// and their ||w||^2 partial into the per-column partial slots the deferred finalisation reduces.  Per S columns the
+// two input columns are read once (plus 2 (S + 1) halo lines per CTA) and S columns written: about
+// 8 (2 + 2 (2S+2) / lines_per_cta) / S + 8 bytes per row and column instead of 24.
+struct MpkArgs {
+  double* W;
+  int64_t ld, off, m, nz, z0, mglob;
+  double cc, cm, cp, rho, c0, e;
+  int j, S, L;          // first column, columns, staged lines per buffer
+  double* partc;        // partc + col * pstride * SKS_NP + cta * SKS_NP
+  int pstride, zero_to; // rows [gridDim.x, zero_to) of each column's slot are zero-filled
+  const CtrlBlock* ctrl;
+};
+
+__global__ void __launch_bounds__(256) cheb_mpk2d_kernel(MpkArgs a) {
+  extern __shared__ double mk[];
+  if (a.ctrl->stop_col < a.j || a.ctrl->exit_cols != 0) return;
+  const int64_t m = a.m;
+  const int b = blockIdx.x;
+  const int y0 = (int)((a.nz * b) / gridDim.x), y1 = (int)((a.nz * (b + 1)) / gridDim.x);
+  const int lb = y0 - a.S - 1;  // first staged line
+  double* buf[3] = {mk, mk + (size_t)a.L * m, mk + (size_t)2 * a.L * m};
+  double* U = buf[0];
+  double* V = buf[1];
+  double* Wn = buf[2];
+  const double* gU = a.W + (int64_t)(a.j - 1) * a.ld + a.off;
+  const double* gV = a.W + (int64_t)(a.j - 2) * a.ld + a.off;
+  const int nl = y1 - y0 + 2 * a.S + 2;
+  for (int64_t i = threadIdx.x; i < (int64_t)nl * m; i += blockDim.x) {
+    const int l = (int)(i / m);
+    const int64_t x = i - (int64_t)l * m;
+    const int64_t row = (int64_t)(lb + l) * m + x;  // ghost lines are within [-G, nz + G)
+    U[i] = gU[row];
+    V[i] = gV[row];
+  }
+  __syncthreads();
+  const double irho = 1.0 / a.rho;
+  double nrm[8];
+  for (int t = 0; t < 8; ++t) nrm[t] = 0.0;
+  for (int t = 0; t < a.S; ++t) {
+    const int la = y0 - a.S + t, lz = y1 + a.S - t;  // computed lines [la, lz)
+    double* wcol = a.W + (int64_t)(a.j + t) * a.ld + a.off;
+    double nt = 0.0;
+    for (int64_t i = threadIdx.x; i < (int64_t)(lz - la) * m; i += blockDim.x) {
+      const int l = la + (int)(i / m);
+      const int64_t x = i - (int64_t)(l - la) * m;
+      const int64_t k = (int64_t)(l - lb) * m + x;  // index in the staged buffers
+      const int64_t gl = a.z0 + l;                   // global line
+      double w = 0.0;
+      if (gl >= 0 && gl < a.mglob) {
+        const double u = U[k];
+        const double sm = (x > 0 ? U[k - 1] : 0.0) + U[k - m];
+        const double sp = (x < m - 1 ? U[k + 1] : 0.0) + U[k + m];
+        const double Au = a.cc * u + a.cm * sm + a.cp * sp;
+        w = (Au - a.c0 * u - a.e * V[k]) * irho;
+      }
+      Wn[k] = w;
+      if (l >= y0 && l < y1) {
+        wcol[(int64_t)l * m + x] = w;
+        nt = fma(w, w, nt);
+      }
+    }
+    nrm[t] = nt;
+    __syncthreads();
+    double* tmp = V;  // rotate: V <- U, U <- Wn, Wn <- old V
+    V = U;
+    U = Wn;
+    Wn = tmp;
+  }
+  // per-column partial ||w||^2 of this CTA's lines (fixed-order block reduction)
+  __shared__ double red[32 * 8];
+  __shared__ double R[8];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
+  for (int t = 0; t < a.S; ++t) {
+    const double v = warp_sum(nrm[t]);
+    if (lane == 0) red[t * 32 + wid] = v;
+  }
+  __syncthreads();
+  if (wid < a.S) {
+    double v = lane < nw ? red[wid * 32 + lane] : 0.0;
+    v = warp_sum(v);
+    if (lane == 0) R[wid] = v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < a.S * SKS_NP; i += blockDim.x) {
+    const int t = i / SKS_NP, q = i - t * SKS_NP;
+    a.partc[((size_t)(a.j + t) * a.pstride + b) * SKS_NP + q] = (q == 0) ? R[t] : 0.0;
+  }
+  if (b == 0)  // rows past this grid (the step kernels' grid is larger): zero, so the finaliser may sum them
+    for (int i = threadIdx.x; i < a.S * (a.zero_to - (int)gridDim.x) * SKS_NP; i += blockDim.x) {
+      const int per = (a.zero_to - (int)gridDim.x) * SKS_NP;
+      const int t = i / per, r = i - t * per;
+      a.partc[((size_t)(a.j + t) * a.pstride + gridDim.x) * SKS_NP + r] = 0.0;
+    }
+}
+
+size_t mpk2d_smem(int64_t m, int64_t nz, int grid, int S) {
+  const int64_t own = (nz + grid - 1) / grid;
+  return sizeof(double) * 3 * (size_t)(own + 2 * S + 2) * m;
+}
+
+cudaError_t launch_cheb_mpk2d(double* W, int64_t ld, int64_t off, int64_t m, int64_t nz, int64_t z0, int64_t mglob,
+                              double cc, double cm, double cp, double rho, double c0, double e, int j, int S,
+                              double* partc, int pstride, int zero_to, const CtrlBlock* ctrl, int grid,
+                              cudaStream_t st) {
+  if (S < 1 || S > 8) return cudaErrorInvalidValue;
+  MpkArgs a;
+  a.W = W;
+  a.ld = ld;
+  a.off = off;
+  a.m = m;
+  a.nz = nz;
+  a.z0 = z0;
+  a.mglob = mglob;
+  a.cc = cc;
+  a.cm = cm;
+  a.cp = cp;
+  a.rho = rho;
+  a.c0 = c0;
+  a.e = e;
+  a.j = j;
+  a.S = S;
+  a.L = (int)((nz + grid - 1) / grid + 2 * S + 2);
+  a.partc = partc;
+  a.pstride = pstride;
+  a.zero_to = zero_to;
+  a.ctrl = ctrl;
+  const size_t smem = mpk2d_smem(m, nz, grid, S);
+  if (cudaError_t err = set_smem_attr(cheb_mpk2d_kernel, smem)) return err;
+  cheb_mpk2d_kernel<<<grid, 256, smem, st>>>(a);
+  return cudaGetLastError();
+}
+}  // namespace sks

@@ -148,6 +148,11 @@ cudaError_t launch_scale_rows(double* Z, int J, int ldz, const double* sigma, cu
 cudaError_t launch_whiten_partials(const double* u, const double* const* v, const int* slot, int nv, int64_t n,
                                    int64_t plane, int64_t m, int dim, double cc, double cm, double cp, double* part,
                                    int grid, cudaStream_t st);
+size_t mpk2d_smem(int64_t m, int64_t nz, int grid, int S);
+cudaError_t launch_cheb_mpk2d(double* W, int64_t ld, int64_t off, int64_t m, int64_t nz, int64_t z0, int64_t mglob,
+                              double cc, double cm, double cp, double rho, double c0, double e, int j, int S,
+                              double* partc, int pstride, int zero_to, const CtrlBlock* ctrl, int grid,
+                              cudaStream_t st);
 cudaError_t launch_cheb_colsum(const double* part, int grid, int pstride, int j0, int j1, double* sums,
                                cudaStream_t st);
 cudaError_t launch_cheb_finalize(const double* sums, int j0, int j1, double rho, double c0, double e, double* sigma,

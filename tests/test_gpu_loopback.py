@@ -189,3 +189,30 @@ def test_loopback_whitened_sgmres_matches_single_rank():
 def rhs_normal_local(n):
     from inputs import rhs_normal
     return rhs_normal(n, 0)
+
+
+@pytest.mark.parametrize("m,P", [(64, 2), (96, 4), (60, 3)])
+def test_loopback_chebyshev_matrix_powers_2d(m, P):
+    """2D Chebyshev basis with the matrix-powers launches (SKS_MPK_S columns per launch, ghost depth S + 1
+    exchanged once per launch: SURVEY NEXT(1) 'depth-s halos') at P = 2, 3, 4 equals P = 1."""
+    import os
+    n = m * m
+    f = np.random.default_rng(m + P).standard_normal(n)
+    kw = dict(d=40, k=2, s=80, zeta=8, seed=4, tol=1e-10, max_cycles=2, basis="chebyshev")
+    old = os.environ.get("SKS_MPK_S")
+    os.environ["SKS_MPK_S"] = "4"
+    try:
+        ref = _solve("stencil2d", m, n, 15.0, f, 1, kw)[0]
+        outs = _solve("stencil2d", m, n, 15.0, f, P, kw)
+        plain = None
+        os.environ["SKS_MPK_S"] = "0"
+        plain = _solve("stencil2d", m, n, 15.0, f, 1, kw)[0]
+    finally:
+        if old is None:
+            os.environ.pop("SKS_MPK_S", None)
+        else:
+            os.environ["SKS_MPK_S"] = old
+    assert np.abs(ref.x - plain.x).max() <= 1e-10 * np.abs(plain.x).max()   # matrix powers = one step per launch
+    x = np.concatenate([o.x for o in outs])
+    assert all(o.info["columns"] == ref.info["columns"] for o in outs)
+    assert np.abs(x - ref.x).max() <= 1e-10 * np.abs(ref.x).max()
