@@ -1412,10 +1412,12 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
 namespace {
 
 // run the basis loop for columns 1..d with the sketch batches interleaved (no QR)
+// qr_done (optional): the thin QR of SB (mode 1) is appended on the side stream batch by batch while the basis is
+// generated (SB column jj needs sigma_jj, known once column jj + 1 exists); *qr_done = columns factored
 static sks_status basis_and_sketch(sks_ctx* c, Basis& b, int d, int s, int zeta, uint64_t key, int JB,
-                                   bool do_sketch, float* t_basis_ms) {
+                                   bool do_sketch, float* t_basis_ms, int* qr_done = nullptr) {
   cudaStream_t st = c->main();
-  int next_sk = 0;
+  int next_sk = 0, next_qr = 0;
   const void* plan = nullptr;
   SKS_CK(c, cudaEventRecord(c->ev_b0, st));
   b.fin_next = 2;
@@ -1427,6 +1429,18 @@ static sks_status basis_and_sketch(sks_ctx* c, Basis& b, int d, int s, int zeta,
       if (next_sk == 0) SKS_TRY(sketch_plan(c, b.g, s, zeta, key, st, &plan));
       SKS_TRY(sketch_cols(c, b, next_sk, J, s, zeta, key, st, plan));
       next_sk += J;
+    }
+    if (qr_done) {
+      const int qr_upto = std::min(upto - 1, d);
+      if (next_qr < qr_upto) {
+        SKS_CK(c, cudaEventRecord(c->ev_fork, st));
+        SKS_CK(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+        while (next_qr < qr_upto) {
+          const int J = std::min(JB, qr_upto - next_qr);
+          SKS_TRY(qr_append(c, b, 1, next_qr, J, s, 0, d, c->side));
+          next_qr += J;
+        }
+      }
     }
     return SKS_OK;
   };
@@ -1449,6 +1463,11 @@ static sks_status basis_and_sketch(sks_ctx* c, Basis& b, int d, int s, int zeta,
     }
   }
   SKS_CK(c, cudaEventRecord(c->ev_b1, st));
+  if (qr_done) {  // join the side stream's QR
+    SKS_CK(c, cudaEventRecord(c->ev_join, c->side));
+    SKS_CK(c, cudaStreamWaitEvent(st, c->ev_join, 0));
+    *qr_done = next_qr;
+  }
   SKS_CK(c, cudaMemcpyAsync(c->h_ctrl, c->ctrl.p, sizeof(CtrlBlock), cudaMemcpyDeviceToHost, st));
   SKS_CK(c, cudaStreamSynchronize(st));
   float ms = 0.f;
@@ -1554,11 +1573,12 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
   c->sk_seed = o->seed;
   c->sk_cycle = 0;
   float t_basis_ms = 0.f;
+  int qr_done = 0;  // columns of SB already factored during the basis loop (single-vector bases)
   const double bytes0 = b.bytes;
   if (blk)
     SKS_TRY(block_basis_and_sketch(c, b, v0, bs, d / bs, s, zeta, key, JB, &t_basis_ms));
   else
-    SKS_TRY(basis_and_sketch(c, b, d, s, zeta, key, JB, true, &t_basis_ms));
+    SKS_TRY(basis_and_sketch(c, b, d, s, zeta, key, JB, true, &t_basis_ms, &qr_done));
   const double bytes_basis = b.bytes - bytes0;
   CtrlBlock* hc = c->h_ctrl;
   int de = d;
@@ -1570,10 +1590,12 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
   if (de < 2) return fail(c, SKS_EINVAL, "basis broke down before 2 columns");
   cudaEvent_t ev_s0 = c->ev_b0, ev_s1 = c->ev_b1;
   SKS_CK(c, cudaEventRecord(ev_s0, st));
-  // ---- QR of SB[:, :de]
-  for (int j0 = 0; j0 < de; j0 += JB) {
-    const int J = std::min(JB, de - j0);
-    SKS_TRY(qr_append(c, b, 1, j0, J, s, 0, de, st));
+  // ---- QR of SB[:, :de] (already done during the basis loop unless the basis broke down early)
+  if (qr_done != de) {
+    for (int j0 = 0; j0 < de; j0 += JB) {
+      const int J = std::min(JB, de - j0);
+      SKS_TRY(qr_append(c, b, 1, j0, J, s, 0, de, st));
+    }
   }
   SKS_TRY(ensure(c, c->Mh, sizeof(double) * (size_t)de * de));
   SKS_TRY(ensure(c, c->Mh2, sizeof(double) * (size_t)de * de));
