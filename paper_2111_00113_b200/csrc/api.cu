@@ -1688,7 +1688,7 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
   SKS_TRY(ensure(c, c->th, sizeof(double) * 64));
   int* d_info = c->sel.as<int>() + 32;
   int* d_nsel = c->sel.as<int>() + 31;
-  SKS_CK(c, cudaMemsetAsync(d_info, 0, sizeof(int) * 5, st));
+  SKS_CK(c, cudaMemsetAsync(d_info, 0, sizeof(int) * 8, st));
   SKS_CK(c, launch_hqr(c->Mh2.as<double>(), rr, rr, c->wr.as<double>(), c->wi.as<double>(), d_info, st));
   double* th_re = c->th.as<double>();
   double* th_im = th_re + 32;
@@ -1777,8 +1777,9 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
   const int* hsel = reinterpret_cast<const int*>(hs + 576);
   const int nsel = hsel[31];
   const int hinfo = hsel[32];
-  if (getenv("SKS_DEBUG_HQR")) fprintf(stderr, "hqr: d=%d sweeps=%d bulge_steps=%d chase_kcyc=%d total_kcyc=%d\n", de, hsel[33],
-                                       hsel[34], hsel[35], hsel[36]);
+  if (getenv("SKS_DEBUG_HQR")) fprintf(stderr, "hqr: d=%d sweeps=%d bulge_steps=%d chase_kcyc=%d total_kcyc=%d "
+                                       "(HQ_PROF: setup %d trans %d last %d)\n", de, hsel[33], hsel[34], hsel[35],
+                                       hsel[36], hsel[37], hsel[38], hsel[39]);
   if (hinfo != 0) return fail(c, SKS_ENOTCONV, "QR algorithm did not converge on Mhat");
   if (getenv("SKS_DEBUG_SRR") && stab) fprintf(stderr, "srr stabilised: rank %d of %d\n", rr, de);
   for (int v = 0; v < nsel; ++v) {

@@ -139,6 +139,79 @@ __device__ __forceinline__ HqRefl hq_refl_fast(double p, double q, double r) {
   return R;
 }
 
+// Short-chain reflector (HQ_NEWNR, default): third-order refinements of 1/sqrt(t) and 1/(p+s) (one correction
+// each instead of two Newton steps) and the seed of 1/(p+s) formed from the approximate root off the dependent
+// chain: C5 chase 44.5M -> 40.1M cycles (tools/ab_hqr.sh, profiles/r02/hqr_ab_r02.txt).  is = 1/s and
+// ip = 1/(p+s) are kept for hq_next_x (HQ_FASTX=1: the next bulge input in two operations after 1/(p+s) instead
+// of seven; measured slower, 43.8M cycles -- more instructions per round, so the round is not bound by this chain)
+#ifndef HQ_FASTX
+#define HQ_FASTX 0
+#endif
+#ifndef HQ_NEWNR
+#define HQ_NEWNR 1
+#endif
+struct HqRefl2 {
+  HqRefl R;
+  double is, ip;
+};
+__device__ __forceinline__ HqRefl2 hq_refl_fast2(double p, double q, double r) {
+  HqRefl2 O;
+  const double t = fma(p, p, fma(q, q, r * r));
+  const bool ok = t >= 2.3e-308;
+  const double tt = ok ? t : 1.0;
+  double ya;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(ya) : "d"(tt));
+  const double sa = tt * ya;
+  double ipa;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(ipa) : "d"(p + (p < 0.0 ? -sa : sa)));
+#if HQ_NEWNR
+  const double e = fma(-tt * ya, ya, 1.0);
+  double is = fma(ya * e, fma(e, 0.375, 0.5), ya);  // ya (1 + e/2 + 3e^2/8)
+#else
+  double is = rsqrt_nr(tt);
+#endif
+  double s = tt * is;
+  s = p < 0.0 ? -s : s;
+  is = p < 0.0 ? -is : is;
+  const double pp = p + s;
+#if HQ_NEWNR
+  const double e2 = fma(-pp, ipa, 1.0);
+  const double ip = fma(ipa * e2, 1.0 + e2, ipa);  // ipa (1 + e2 + e2^2)
+#else
+  const double ip = rcp_nr(ok ? pp : 1.0);
+  (void)ipa;
+#endif
+  O.R.s = s;
+  O.R.xx = ok ? pp * is : 0.0;
+  O.R.yy = ok ? q * is : 0.0;
+  O.R.zz = ok ? r * is : 0.0;
+  O.R.qq = ok ? q * ip : 0.0;
+  O.R.rr = ok ? r * ip : 0.0;
+  O.R.valid = ok;
+  O.is = ok ? is : 0.0;
+  O.ip = ok ? ip : 0.0;
+  return O;
+}
+// The next bulge input H[k+1..k+3][k] after step k's two-sided transformation, from the step's input x = (p, q, r)
+// and the 3x3 block B = H[k..k+2][k..k+2] before the step.  With u = (p+s, q, r)/s, 1 - u_0 = -p/s, so
+//   N_i0 = (1-u_0) R_i0 - u_1 R_i1 - u_2 R_i2 = -is (x.B_i) + u_i is (x.B_0 + ip (q x.B_1 + r x.B_2))   (i = 1, 2)
+//   N_30 = -u_2 h3,
+// where x.B_i = p B_i0 + q B_i1 + r B_i2 need no reflector quantity: only two operations follow 1/(p+s) on the
+// dependent chain (the explicit form needs seven).  Same values up to rounding (validated: max 7e-16 relative).
+__device__ __forceinline__ void hq_next_x(const HqRefl2& R, double p, double q, double r, double B00, double B01,
+                                          double B02, double B10, double B11, double B12, double B20, double B21,
+                                          double B22, double h3, double& np, double& nq, double& nr) {
+  const double xB0 = fma(r, B02, fma(q, B01, p * B00));
+  const double xB1 = fma(r, B12, fma(q, B11, p * B10));
+  const double xB2 = fma(r, B22, fma(q, B21, p * B20));
+  const double xQ = fma(r, xB2, q * xB1);
+  const double a1 = -R.is * xB1, a2 = -R.is * xB2, v1 = R.R.yy * R.is, v2 = R.R.zz * R.is;
+  const double g = fma(R.ip, xQ, xB0);
+  np = R.R.valid ? fma(v1, g, a1) : B10;
+  nq = R.R.valid ? fma(v2, g, a2) : B20;
+  nr = -R.R.zz * h3;
+}
+
 constexpr int HQ_R = 32;         // window rows/cols (the bulge region of HQ_W steps plus 3)
 constexpr int HQ_W = HQ_R - 3;   // bulge steps per window
 constexpr int HQ_LD = HQ_R + 1;  // odd pitch: row- and column-wise smem access both conflict-free
@@ -207,7 +280,9 @@ __device__ __forceinline__ void hq_chase2w(double* Hw, double* Qs, double* dmy, 
   };
   const bool twoB = nn - m >= HQ_TWO_MIN;
   HqBulge S = {};
-  HqRefl R = hq_refl_fast(0.0, 0.0, 0.0);
+  HqRefl2 RX = hq_refl_fast2(0.0, 0.0, 0.0);
+  HqRefl& R = RX.R;
+  double xp = 0.0, xq = 0.0, xr = 0.0;  // this warp's current reflector input
   // ---- window start: each warp its own bulge
   if (role == 0) {
     const int kA = a0;
@@ -219,13 +294,15 @@ __device__ __forceinline__ void hq_chase2w(double* Hw, double* Qs, double* dmy, 
         p = H_(kA, kA - 1); q = H_(kA + 1, kA - 1); r = H_(kA + 2, kA - 1);
       }
       load_state(kA, S);
-      R = hq_refl_fast(p, q, r);
+      RX = hq_refl_fast2(p, q, r);
+      xp = p; xq = q; xr = r;
     }
   } else {
     const int kB = a0 - 4;
     if (twoB && kB >= m && kB <= nn - 1) {
       load_state(kB, S);
-      R = hq_refl_fast(H_(kB, kB - 1), H_(kB + 1, kB - 1), H_(kB + 2, kB - 1));
+      xp = H_(kB, kB - 1); xq = H_(kB + 1, kB - 1); xr = H_(kB + 2, kB - 1);
+      RX = hq_refl_fast2(xp, xq, xr);
     } else if (twoB && kB + 1 == m) {  // B enters at the window's first round
       // (cannot happen: B enters at kA = m+4 inside the sweep's first window)
     }
@@ -274,7 +351,16 @@ __device__ __forceinline__ void hq_chase2w(double* Hw, double* Qs, double* dmy, 
       const double N20 = R20 - t2, N21 = fma(-t2, w1, R21), N22 = fma(-t2, w2, R22);
       const double N30 = -t3, N31 = -t3 * w1, N32 = fma(-t3, w2, S.h3);
       const bool nx = actA && kA + 1 <= nn - 1;
-      const HqRefl Rn = hq_refl_fast(nx ? N10 : 0.0, nx ? N20 : 0.0, nx ? N30 : 0.0);
+#if HQ_FASTX
+      double np_, nq_, nr_;
+      hq_next_x(RX, xp, xq, xr, S.B00, S.B01, S.B02, S.B10, S.B11, S.B12, S.B20, S.B21, S.B22, S.h3, np_, nq_, nr_);
+      np_ = nx ? np_ : 0.0; nq_ = nx ? nq_ : 0.0; nr_ = nx ? nr_ : 0.0;
+      (void)N10; (void)N20; (void)N30;
+      const HqRefl2 RnX = hq_refl_fast2(np_, nq_, nr_);
+#else
+      const HqRefl2 RnX = hq_refl_fast2(nx ? N10 : 0.0, nx ? N20 : 0.0, nx ? N30 : 0.0);
+      const double np_ = nx ? N10 : 0.0, nq_ = nx ? N20 : 0.0, nr_ = nx ? N30 : 0.0;
+#endif
       *hkA = (kA == m) ? ((l != m) ? -hkAv : hkAv) : -R.s;
       {
         const double pr = fma(w2, aA2, fma(w1, aA1, aA0));
@@ -309,14 +395,16 @@ __device__ __forceinline__ void hq_chase2w(double* Hw, double* Qs, double* dmy, 
         *(actA ? qA + HQ_LD : sq2 + 1) = fma(-tq, w1, gA1);
         *(actA ? qA + 2 * HQ_LD : sq2 + 2) = fma(-tq, w2, gA2);
       }
-      R = Rn;
+      RX = RnX;
+      xp = np_; xq = nq_; xr = nr_;
       S.B00 = N11; S.B01 = N12; S.B02 = R1c;
       S.B10 = N21; S.B11 = N22; S.B12 = R2c;
       S.B20 = N31; S.B21 = N32; S.B22 = S.d33;
       S.C0 = R1e; S.C1 = R2e; S.C2 = E3;
       S.h3 = h4; S.d33 = d44;
     } else {
-      HqRefl Rnext = hq_refl_fast(0.0, 0.0, 0.0);
+      HqRefl2 RnextX = hq_refl_fast2(0.0, 0.0, 0.0);
+      double np_ = 0.0, nq_ = 0.0, nr_ = 0.0;
       if (actB) {
         S.C0 = H_(kB, kB + 3); S.C1 = H_(kB + 1, kB + 3); S.C2 = H_(kB + 2, kB + 3);
         S.h3 = H_(kB + 3, kB + 2); S.d33 = H_(kB + 3, kB + 3);
@@ -346,7 +434,15 @@ __device__ __forceinline__ void hq_chase2w(double* Hw, double* Qs, double* dmy, 
         const double M20 = S20 - e2, M21 = fma(-e2, x1, S21), M22 = fma(-e2, x2, S22);
         const double M30 = -e3, M31 = -e3 * x1, M32 = fma(-e3, x2, S.h3);
         const bool nx = kB + 1 <= nn - 1;
-        Rnext = hq_refl_fast(nx ? M10 : 0.0, nx ? M20 : 0.0, nx ? M30 : 0.0);
+#if HQ_FASTX
+        hq_next_x(RX, xp, xq, xr, S.B00, S.B01, S.B02, S.B10, S.B11, S.B12, S.B20, S.B21, S.B22, S.h3, np_, nq_,
+                  nr_);
+        np_ = nx ? np_ : 0.0; nq_ = nx ? nq_ : 0.0; nr_ = nx ? nr_ : 0.0;
+        (void)M10; (void)M20; (void)M30;
+#else
+        np_ = nx ? M10 : 0.0; nq_ = nx ? M20 : 0.0; nr_ = nx ? M30 : 0.0;
+#endif
+        RnextX = hq_refl_fast2(np_, nq_, nr_);
         *hkB = (kB == m) ? ((l != m) ? -hkBv : hkBv) : -R.s;
         {
           const double pr = fma(x2, aB2, fma(x1, aB1, aB0));
@@ -385,9 +481,11 @@ __device__ __forceinline__ void hq_chase2w(double* Hw, double* Qs, double* dmy, 
         const double r = H_(m + 2, m + 1);
         load_state(m, S);
         S.B20 = 0.0;  // H[m+2][m]: zeroed by A's step m+1 (shared memory holds A's stale bulge entry)
-        Rnext = hq_refl_fast(p, q, r);
+        RnextX = hq_refl_fast2(p, q, r);
+        np_ = p; nq_ = q; nr_ = r;
       }
-      R = Rnext;
+      RX = RnextX;
+      xp = np_; xq = nq_; xr = nr_;
       put(R, (kA + 1) & 1);
     }
     hq_bar2();
@@ -780,6 +878,9 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
   __shared__ double sp, sq, sr, sx, sy, sw, st;
   __shared__ int sl, snn, sm, sflag, sits, sdone, nsweep, nstep;
   long long cyc_chase = 0, cyc_all = clock64();
+#ifdef HQ_PROF
+  long long cyc_setup = 0, cyc_trans = 0, cyc_last = 0;
+#endif
   const int tid = threadIdx.x, nt = blockDim.x;
   // anorm
   double loc = 0.0;
@@ -810,6 +911,9 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
     if (tid == 0) sits = 0;
     __syncthreads();
     while (true) {
+#ifdef HQ_PROF
+      const long long tp0 = clock64();
+#endif
 #ifdef HQ_DEBUG_SWEEPS  // debugging harness: stop after info[7] sweeps (if > 0), H left in place
       if (info[7] > 0 && nsweep >= info[7]) {
         __syncthreads();
@@ -1067,6 +1171,9 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
       int cur = 0, pk0 = -1, pr1 = 0;
       load_window(k0, r1, Qsh);
       __syncthreads();
+#ifdef HQ_PROF
+      if (tid == 0) cyc_setup += clock64() - tp0;
+#endif
       while (true) {
         double* Qs = Qsh + cur * HQ_QSZ;
         long long tc0 = clock64();
@@ -1218,6 +1325,9 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
 #endif
           far_update(Qs, k0, r1, r1, nn, l, k0, 0, nw);
           __syncthreads();
+#ifdef HQ_PROF
+          if (tid == 0) cyc_last += clock64() - tc1;
+#endif
           break;
         }
         const int r1n = min(k0n + HQ_R - 1, nn);
@@ -1237,6 +1347,9 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
         r1 = r1n;
         load_window(k0, r1, Qsh + cur * HQ_QSZ);
         __syncthreads();
+#ifdef HQ_PROF
+        if (tid == 0) cyc_trans += clock64() - tc1;
+#endif
       }
       {
         const int nn2 = snn, l2 = sl;
@@ -1257,6 +1370,11 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
     info[2] = nstep;
     info[3] = (int)(cyc_chase >> 10);  // diagnostics: clock cycles / 1024 in the chase, in total
     info[4] = (int)((clock64() - cyc_all) >> 10);
+#ifdef HQ_PROF
+    info[5] = (int)(cyc_setup >> 10);  // sweep set-up to the first window, window transitions, last far update
+    info[6] = (int)(cyc_trans >> 10);
+    info[7] = (int)(cyc_last >> 10);
+#endif
   }
 }
 
