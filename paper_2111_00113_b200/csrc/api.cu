@@ -478,6 +478,7 @@ struct Basis {
   int mpk_grid = 0;
   bool coop = false;   // small single-rank stencil problem: batches of columns in one cooperative launch
   int coop_grid = 0;
+  int coop1_lines = 0; // > 0: the one-barrier-per-column 2D kernel (step_coop1_kernel), lines per CTA
   int fin_next = 2;    // first column whose deferred bookkeeping is pending
   int defer_grid = 0;  // step grid of the deferred launches (per-column partial rows)
   StepArgs sa;
@@ -586,8 +587,19 @@ static sks_status setup_basis(sks_ctx* c, const sks_operator* A, int k, int ncol
         b->coop_grid = std::min(coop_grid(c->main_sms), b->pslots);
         b->coop = b->coop_grid > 0;
       }
+      // SKS_COOP1_MAXN (2D, P = 1): one cooperative launch per batch with one grid barrier per column and a
+      // recomputed halo line (step_coop1_kernel)
+      int64_t lim1 = 0;
+      if (const char* e = getenv("SKS_COOP1_MAXN")) lim1 = atoll(e);
+      if (c->nranks == 1 && g.n <= lim1 && !b->coop) {
+        b->coop1_lines = coop1_lines(g.dim, g.m, g.nz, b->k, std::min(c->main_sms, b->pslots));
+        if (b->coop1_lines > 0) {
+          b->coop = true;
+          b->coop_grid = (int)((g.nz + b->coop1_lines - 1) / b->coop1_lines);
+        }
+      }
       if (b->coop) {
-        SKS_TRY(ensure(c, c->csync, 64, true));
+        SKS_TRY(ensure(c, c->csync, 512, true));  // counter, flag, reduced partials (stencil_coop.cu)
         SKS_TRY(ensure(c, c->cctrl, sizeof(CtrlBlock), true));
       }
     }
@@ -803,8 +815,12 @@ static sks_status coop_columns(sks_ctx* c, Basis& b, int j0, int j1) {
   a.defer = 0;
   a.ctrl = c->cctrl.as<CtrlBlock>();
   SKS_CK(c, launch_ctrl_copy(c->cctrl.as<CtrlBlock>(), c->ctrl.as<CtrlBlock>(), st));
-  SKS_CK(c, launch_step_coop(a, j0, j1, b.last_grid, c->part.as<double>(), b.pslots, c->csync.as<unsigned>(),
-                             b.coop_grid, st));
+  if (b.coop1_lines > 0)
+    SKS_CK(c, launch_step_coop1(a, j0, j1, b.last_grid, c->part.as<double>(), b.pslots, c->csync.as<unsigned>(),
+                                b.coop1_lines, st));
+  else
+    SKS_CK(c, launch_step_coop(a, j0, j1, b.last_grid, c->part.as<double>(), b.pslots, c->csync.as<unsigned>(),
+                               b.coop_grid, st));
   SKS_CK(c, launch_ctrl_merge(c->ctrl.as<CtrlBlock>(), c->cctrl.as<CtrlBlock>(), j0 == 1 ? 1 : 0, st));
   c->launches += 4;
   b.last_grid = b.coop_grid;

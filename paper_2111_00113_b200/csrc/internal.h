@@ -36,6 +36,9 @@ void stencil_zm_free(void* cache);
 
 // stencil_coop.cu (small problems: a batch of columns in one cooperative launch, single rank)
 int coop_grid(int main_sms);
+int coop1_lines(int dim, int64_t m, int64_t nz, int k, int max_grid);
+cudaError_t launch_step_coop1(const StepArgs& a, int j0, int j1, int grid_prev0, double* part, int pstride,
+                              unsigned* sync, int lines, cudaStream_t st);
 cudaError_t launch_step_coop(const StepArgs& a, int j0, int j1, int grid_prev0, double* part, int pstride,
                              unsigned* sync, int grid, cudaStream_t st);
 cudaError_t launch_ctrl_copy(CtrlBlock* dst, const CtrlBlock* src, cudaStream_t st);
