@@ -1,4 +1,4 @@
-python -m paper_2111_00113_b200.build > /dev/null 2>&1
+[ -z "$NOBUILD" ] && python -m paper_2111_00113_b200.build > /dev/null 2>&1
 timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_golden.py tests/test_gpu_loopback.py tests/test_gpu_determinism.py -q -m gpu -k "csr or C4" 2>&1 | tail -2
 for v in ${VARIANTS:-"SKS_CSR_BATCH=8" "-" "SKS_CSR_BATCH=2" "SKS_CSR_V2=1"}; do
   EE=$v; [ "$v" = "-" ] && EE=""
