@@ -150,6 +150,14 @@ __device__ __forceinline__ HqRefl hq_refl_fast(double p, double q, double r) {
 #ifndef HQ_NEWNR
 #define HQ_NEWNR 1
 #endif
+// HQ_XPF (default, HQ_NB == 3): window transitions without L2 round trips on the critical path -- while the
+// chase runs, the spare warps write the previous window back, apply its deferred off-window update and then
+// prefetch what the next window needs from global memory (the rows below this window into the second window
+// buffer, this window's rows x the next window's new columns into Xb); after the chase the next window is
+// assembled in shared memory (overlap copy + Q^T Xb) and the chase resumes
+#ifndef HQ_XPF
+#define HQ_XPF 1
+#endif
 struct HqRefl2 {
   HqRefl R;
   double is, ip;
@@ -871,6 +879,10 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
                                                          double* __restrict__ wr, double* __restrict__ wi,
                                                          int* __restrict__ info) {
   __shared__ double Hw[HQ_LD * (HQ_R + 1) + 16 * 32];  // window + per-lane scratch
+#if HQ_XPF && HQ_NB == 3
+  __shared__ double Hw2[HQ_LD * (HQ_R + 1)];  // the other window buffer
+  __shared__ double Xb[HQ_R * (HQ_R - 3)];    // prefetched H[window rows][next window's new columns]
+#endif
   __shared__ double Qsh[2 * HQ_QSZ];  // accumulated Q of the current / previous window
   __shared__ double hq_x[16 * 8];     // HQ_NB=3: each chase warp's next reflector, by round parity
   __shared__ double red[32];
@@ -1169,6 +1181,12 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
 #endif
       int r1 = min(k0 + HQ_R - 1, nn);
       int cur = 0, pk0 = -1, pr1 = 0;
+      double* Hc = Hw;  // the current window's buffer
+#if HQ_XPF && HQ_NB == 3
+      const bool sp_ok = (HQ_NW <= 2) ? ((warp & 3) >= 2) : (warp >= HQ_NW);  // warps off the chase schedulers
+      const int sp_t = (HQ_NW <= 2) ? (((warp >> 2) * 2 + (warp & 3) - 2) * 32 + lane) : ((warp - HQ_NW) * 32 + lane);
+      const int sp_n = (HQ_NW <= 2) ? (nw / 2) * 32 : (nw - HQ_NW) * 32;
+#endif
       load_window(k0, r1, Qsh);
       __syncthreads();
 #ifdef HQ_PROF
@@ -1182,12 +1200,43 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
           // two bulges: the role-specialised chase; more: the general one (correct, but every warp then
           // issues the union of both roles' work: C5 hqr 33 ms at 4 bulges vs 27.6 ms here)
           if (HQ_NW == 2)
-            hq_chase2w(Hw, Qs, Hw + HQ_LD * (HQ_R + 1), hq_x, k0, r1, a0, a1, m, nn, l, sp, sq, sr, sx, sy, sw, lane,
+            hq_chase2w(Hc, Qs, Hw + HQ_LD * (HQ_R + 1), hq_x, k0, r1, a0, a1, m, nn, l, sp, sq, sr, sx, sy, sw, lane,
                        warp);
           else
-            hq_chasew(Hw, Qs, Hw + HQ_LD * (HQ_R + 1), hq_x, k0, r1, a0, a1, m, nn, l, sp, sq, sr, sx, sy, sw, lane,
+            hq_chasew(Hc, Qs, Hw + HQ_LD * (HQ_R + 1), hq_x, k0, r1, a0, a1, m, nn, l, sp, sq, sr, sx, sy, sw, lane,
                       warp);
         }
+#if HQ_XPF
+        else if (sp_ok) {  // spare warps: pending write-back, deferred off-window update, next-window prefetch
+          double* Hn = (Hc == Hw) ? Hw2 : Hw;  // the previous window's buffer = the next window's
+          if (pk0 >= 0) {
+            for (int idx = sp_t; idx < HQ_R * (HQ_R + 1); idx += sp_n) {  // write the previous window back
+              const int i = idx % HQ_R, c = idx / HQ_R;
+              const int gj = pk0 - 1 + c;
+              if (i <= pr1 - pk0 && gj >= 0 && gj <= pr1) HA(pk0 + i, gj) = Hn[i + c * HQ_LD];
+            }
+            far_update(Qsh + (cur ^ 1) * HQ_QSZ, pk0, pr1, r1, nn, l, pk0, -1, HQ_NW <= 2 ? nw / 2 : nw - HQ_NW);
+            __threadfence_block();
+            asm volatile("bar.sync 2, %0;" ::"r"(sp_n) : "memory");
+          }
+          const int k0n = a1 - hspan;
+          if (a1 < nn + hspan) {  // not the last window: prefetch for window [k0n, r1n]
+            const int r1n = min(k0n + HQ_R - 1, nn), ncx = r1n - r1, wnr = r1 - k0 + 1;
+            for (int idx = sp_t; idx < wnr * ncx; idx += sp_n) {
+              const int i = idx % wnr, c = idx / wnr;
+              Xb[i + c * HQ_R] = HA(k0 + i, r1 + 1 + c);
+            }
+            // rows below this window (local rows > r1 - k0n of the next window), every local column; zeros
+            // beyond the active block; also zero the next window's columns beyond r1n on the overlap rows
+            for (int idx = sp_t; idx < HQ_R * (HQ_R + 1); idx += sp_n) {
+              const int i = idx % HQ_R, c = idx / HQ_R;
+              const int gi = k0n + i, gj = k0n - 1 + c;
+              if (gi > r1) Hn[i + c * HQ_LD] = (gi <= r1n && gj >= 0 && gj <= r1n) ? HA(gi, gj) : 0.0;
+              else if (gj > r1n) Hn[i + c * HQ_LD] = 0.0;
+            }
+          }
+        }
+#endif
 #elif HQ_NB == 2
         if (warp == 0) {
           hq_chase2(Hw, Qs, Hw + HQ_LD * (HQ_R + 1), k0, r1, a0, a1, m, nn, l, sp, sq, sr, sx, sy, sw, lane);
@@ -1304,13 +1353,79 @@ __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a,
           }
         }
 #endif
+#if !(HQ_XPF && HQ_NB == 3)
         else if (pk0 >= 0) {
           far_update(Qsh + (cur ^ 1) * HQ_QSZ, pk0, pr1, r1, nn, l, pk0, -1,
                      HQ_NB == 3 ? (HQ_NW <= 2 ? nw / 2 : nw - HQ_NW) : nw - (nw >> 2));
         }
+#endif
         __syncthreads();
         long long tc1 = clock64();
         if (tid == 0) cyc_chase += tc1 - tc0;
+#if HQ_XPF && HQ_NB == 3
+        {
+          const int k0n = a1 - hspan;  // the next window starts at the last bulge's row
+          if (a1 >= nn + hspan) {      // last window: write back, its whole off-window update now
+            for (int idx = tid; idx < HQ_R * (HQ_R + 1); idx += nt) {
+              const int i = idx % HQ_R, c = idx / HQ_R;
+              const int gj = k0 - 1 + c;
+              if (i <= r1 - k0 && gj >= 0 && gj <= r1) HA(k0 + i, gj) = Hc[i + c * HQ_LD];
+            }
+            far_update(Qs, k0, r1, r1, nn, l, k0, 0, nw);
+            __syncthreads();
+#ifdef HQ_PROF
+            if (tid == 0) cyc_last += clock64() - tc1;
+#endif
+            break;
+          }
+          const int r1n = min(k0n + HQ_R - 1, nn), ncx = r1n - r1, wnr = r1 - k0 + 1;
+          double* Hn = (Hc == Hw) ? Hw2 : Hw;
+          // next window's new columns (r1, r1n] on this window's rows: Q^T Xb (global: rows above the next window)
+          for (int idx = tid; idx < wnr * ncx; idx += nt) {
+            const int i = idx % wnr, c = idx / wnr;
+            const double* qi = Qs + i * HQ_LD;
+            const double* xc = Xb + c * HQ_R;
+            double z0 = 0.0, z1 = 0.0, z2 = 0.0, z3 = 0.0;
+            int kq = 0;
+            for (; kq + 3 < wnr; kq += 4) {
+              z0 = fma(qi[kq], xc[kq], z0);
+              z1 = fma(qi[kq + 1], xc[kq + 1], z1);
+              z2 = fma(qi[kq + 2], xc[kq + 2], z2);
+              z3 = fma(qi[kq + 3], xc[kq + 3], z3);
+            }
+            for (; kq < wnr; ++kq) z0 = fma(qi[kq], xc[kq], z0);
+            const double z = (z0 + z1) + (z2 + z3);
+            const int gi = k0 + i, gj = r1 + 1 + c;
+            HA(gi, gj) = z;
+            if (gi >= k0n) Hn[(gi - k0n) + (gj - k0n + 1) * HQ_LD] = z;
+          }
+          // the overlap block rows/cols [k0n, r1] (and column k0n - 1) from this window
+          for (int idx = tid; idx < HQ_R * (HQ_R + 1); idx += nt) {
+            const int i = idx % HQ_R, c = idx / HQ_R;
+            const int gi = k0n + i, gj = k0n - 1 + c;
+            if (gi <= r1 && gj <= r1) Hn[i + c * HQ_LD] = Hc[(gi - k0) + (gj - k0 + 1) * HQ_LD];
+          }
+          double* qn = Qsh + (cur ^ 1) * HQ_QSZ;  // the previous window's Q (its deferred update is done)
+          for (int idx = tid; idx < HQ_R * HQ_R; idx += nt) {
+            const int i = idx % HQ_R, c = idx / HQ_R;
+            qn[i + c * HQ_LD] = (i == c) ? 1.0 : 0.0;
+          }
+          __syncthreads();
+          pk0 = k0;
+          pr1 = r1;
+          cur ^= 1;
+          k0 = k0n;
+          a0 = a1;
+          a1 = min(k0 + HQ_R - 3, nn + hspan);
+          k1 = a1;
+          r1 = r1n;
+          Hc = Hn;
+#ifdef HQ_PROF
+          if (tid == 0) cyc_trans += clock64() - tc1;
+#endif
+          continue;
+        }
+#endif
         for (int idx = tid; idx < HQ_R * (HQ_R + 1); idx += nt) {  // write the window back
           const int i = idx % HQ_R, c = idx / HQ_R;
           const int gj = k0 - 1 + c;
