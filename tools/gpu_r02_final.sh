@@ -25,6 +25,9 @@ timeout 900 $NCU -k regex:block_cheb --launch-skip 3 --launch-count 1 -o "$OUT/b
   python tools/run_srr_once.py C5B 1 > "$OUT/ncu_block.log" 2>&1; echo "ncu-block rc=$?" >> "$OUT/rc.txt"
 timeout 900 $NCU -k regex:srft_stage --launch-skip 6 --launch-count 2 -o "$OUT/srft_c3" -f \
   python tools/run_srft_once.py > "$OUT/ncu_srft.log" 2>&1; echo "ncu-srft rc=$?" >> "$OUT/rc.txt"
+timeout 900 $NCU -k regex:hqr_kernel --launch-count 1 -o "$OUT/hqr_c5" -f \
+  python tools/run_srr_once.py C5 1 > "$OUT/ncu_hqr.log" 2>&1; echo "ncu-hqr rc=$?" >> "$OUT/rc.txt"
+SKS_DEBUG_HQR=1 python tools/run_srr_once.py C5 2 > "$OUT/hqr_counters.txt" 2>&1
 for r in "$OUT"/*.ncu-rep; do python tools/ncu_summary.py "$r"; done > "$OUT/ncu_summaries.txt" 2>&1
 python - "$OUT" <<'PY'
 import csv, io, subprocess, sys, json
