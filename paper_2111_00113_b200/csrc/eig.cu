@@ -220,6 +220,11 @@ __device__ __forceinline__ void hq_next_x(const HqRefl2& R, double p, double q, 
   nr = -R.R.zz * h3;
 }
 
+// per-lane scratch of the masked stores: HQ_SS doubles per lane (odd: the lanes of a half-warp hit distinct banks;
+// 16 made every masked access a 16-way bank conflict -- ncu: 16.4M conflicts per C5 launch)
+#ifndef HQ_SS
+#define HQ_SS 17
+#endif
 constexpr int HQ_R = 32;         // window rows/cols (the bulge region of HQ_W steps plus 3)
 constexpr int HQ_W = HQ_R - 3;   // bulge steps per window
 constexpr int HQ_LD = HQ_R + 1;  // odd pitch: row- and column-wise smem access both conflict-free
@@ -324,16 +329,19 @@ __device__ __forceinline__ void hq_chase2w(double* Hw, double* Qs, double* dmy, 
     if (role == 0) {
       const HqRefl RB = get(kA & 1);  // B's reflector of this round (identity if B is not running)
       const double v0 = RB.xx, v1 = RB.yy, v2 = RB.zz, x1 = RB.qq, x2 = RB.rr;
-      const double E0 = H_(kA, kA + 4), E1 = H_(kA + 1, kA + 4), E2 = H_(kA + 2, kA + 4), E3 = H_(kA + 3, kA + 4);
-      const double h4 = H_(kA + 4, kA + 3), d44 = H_(kA + 4, kA + 4);
+      double E0, E1, E2, E3, h4, d44;
       double Z[3][3];
+      {
+        E0 = H_(kA, kA + 4); E1 = H_(kA + 1, kA + 4); E2 = H_(kA + 2, kA + 4); E3 = H_(kA + 3, kA + 4);
+        h4 = H_(kA + 4, kA + 3); d44 = H_(kA + 4, kA + 4);
 #pragma unroll
-      for (int i = 0; i < 3; ++i)
+        for (int i = 0; i < 3; ++i)
 #pragma unroll
-        for (int j = 0; j < 3; ++j) Z[i][j] = H_(kB + i, kA + j);
+          for (int j = 0; j < 3; ++j) Z[i][j] = H_(kB + i, kA + j);
+      }
       const int jA = kA + 3 + lane;
       const bool rokA = actA && jA <= r1;
-      double* colA = rokA ? Hw + (jA - lo + 1) * HQ_LD + (kA - lo) : dmy + 16 * lane;
+      double* colA = rokA ? Hw + (jA - lo + 1) * HQ_LD + (kA - lo) : dmy + HQ_SS * lane;
       const double aA0 = colA[0], aA1 = colA[1], aA2 = colA[2];
       const bool cokA = actA && ir <= min(nn, kA + 3);
       const bool specA = ir >= kB && ir <= kB + 2;
@@ -342,7 +350,7 @@ __device__ __forceinline__ void hq_chase2w(double* Hw, double* Qs, double* dmy, 
       const double bA0 = ldA ? rowA[0] : 0.0, bA1 = ldA ? rowA[HQ_LD] : 0.0, bA2 = ldA ? rowA[2 * HQ_LD] : 0.0;
       double* qA = Qs + lane + (actA ? kA - lo : 0) * HQ_LD;
       const double gA0 = qA[0], gA1 = qA[HQ_LD], gA2 = qA[2 * HQ_LD];
-      double* hkA = (lane == 0 && actA && R.valid) ? Hw + (kA - lo) + (kA - lo) * HQ_LD : dmy + 16 * lane + 6;
+      double* hkA = (lane == 0 && actA && R.valid) ? Hw + (kA - lo) + (kA - lo) * HQ_LD : dmy + HQ_SS * lane + 6;
       const double hkAv = *hkA;
       const double u0 = R.xx, u1 = R.yy, u2 = R.zz, w1 = R.qq, w2 = R.rr;
       const double pp0 = fma(w2, S.B20, fma(w1, S.B10, S.B00)), pp1 = fma(w2, S.B21, fma(w1, S.B11, S.B01)),
@@ -374,7 +382,7 @@ __device__ __forceinline__ void hq_chase2w(double* Hw, double* Qs, double* dmy, 
         const double pr = fma(w2, aA2, fma(w1, aA1, aA0));
         colA[0] = fma(-u0, pr, aA0);
         colA[1] = fma(-u1, pr, aA1);
-        *((rokA && kA + 2 <= nn) ? colA + 2 : dmy + 16 * lane + 2) = fma(-u2, pr, aA2);
+        *((rokA && kA + 2 <= nn) ? colA + 2 : dmy + HQ_SS * lane + 2) = fma(-u2, pr, aA2);
       }
       {
         const int d = ir - kA, dB = ir - kB;
@@ -391,13 +399,13 @@ __device__ __forceinline__ void hq_chase2w(double* Hw, double* Qs, double* dmy, 
         const double c1 = specA ? zr1 : (own ? (d == 0 ? X1 : (d == 1 ? R11 : (d == 2 ? R21 : 0.0))) : bA1);
         const double c2 = specA ? zr2 : (own ? (d == 0 ? X2 : (d == 1 ? R12 : (d == 2 ? R22 : S.h3))) : bA2);
         const double tt = fma(u2, c2, fma(u1, c1, u0 * c0));
-        double* sc = dmy + 16 * lane;
+        double* sc = dmy + HQ_SS * lane;
         *(cokA ? rowA : sc) = c0 - tt;
         *(cokA && kA + 1 <= nn ? rowA + HQ_LD : sc + 1) = fma(-tt, w1, c1);
         *(cokA && kA + 2 <= nn ? rowA + 2 * HQ_LD : sc + 2) = fma(-tt, w2, c2);
       }
       {
-        double* sq2 = dmy + 16 * lane + 8;
+        double* sq2 = dmy + HQ_SS * lane + 8;
         const double tq = fma(u2, gA2, fma(u1, gA1, u0 * gA0));
         *(actA ? qA : sq2) = gA0 - tq;
         *(actA ? qA + HQ_LD : sq2 + 1) = fma(-tq, w1, gA1);
@@ -414,11 +422,13 @@ __device__ __forceinline__ void hq_chase2w(double* Hw, double* Qs, double* dmy, 
       HqRefl2 RnextX = hq_refl_fast2(0.0, 0.0, 0.0);
       double np_ = 0.0, nq_ = 0.0, nr_ = 0.0;
       if (actB) {
-        S.C0 = H_(kB, kB + 3); S.C1 = H_(kB + 1, kB + 3); S.C2 = H_(kB + 2, kB + 3);
-        S.h3 = H_(kB + 3, kB + 2); S.d33 = H_(kB + 3, kB + 3);
+        {
+          S.C0 = H_(kB, kB + 3); S.C1 = H_(kB + 1, kB + 3); S.C2 = H_(kB + 2, kB + 3);
+          S.h3 = H_(kB + 3, kB + 2); S.d33 = H_(kB + 3, kB + 3);
+        }
         const int jB = kB + 3 + lane;
         const bool rokB = jB <= r1 && (!actA || lane < 1 || lane > 3);
-        double* colB = rokB ? Hw + (jB - lo + 1) * HQ_LD + (kB - lo) : dmy + 16 * lane + 3;
+        double* colB = rokB ? Hw + (jB - lo + 1) * HQ_LD + (kB - lo) : dmy + HQ_SS * lane + 3;
         const double aB0 = colB[0], aB1 = colB[1], aB2 = colB[2];
         const bool cokB = ir <= min(nn, kB + 3);
         const bool ldB = cokB && ir < kB;
@@ -426,7 +436,7 @@ __device__ __forceinline__ void hq_chase2w(double* Hw, double* Qs, double* dmy, 
         const double bB0 = ldB ? rowB[0] : 0.0, bB1 = ldB ? rowB[HQ_LD] : 0.0, bB2 = ldB ? rowB[2 * HQ_LD] : 0.0;
         double* qB = Qs + lane + (kB - lo) * HQ_LD;
         const double gB0 = qB[0], gB1 = qB[HQ_LD], gB2 = qB[2 * HQ_LD];
-        double* hkB = (lane == 0 && R.valid) ? Hw + (kB - lo) + (kB - lo) * HQ_LD : dmy + 16 * lane + 7;
+        double* hkB = (lane == 0 && R.valid) ? Hw + (kB - lo) + (kB - lo) * HQ_LD : dmy + HQ_SS * lane + 7;
         const double hkBv = *hkB;
         const double v0 = R.xx, v1 = R.yy, v2 = R.zz, x1 = R.qq, x2 = R.rr;
         const double qq0 = fma(x2, S.B20, fma(x1, S.B10, S.B00)), qq1 = fma(x2, S.B21, fma(x1, S.B11, S.B01)),
@@ -456,7 +466,7 @@ __device__ __forceinline__ void hq_chase2w(double* Hw, double* Qs, double* dmy, 
           const double pr = fma(x2, aB2, fma(x1, aB1, aB0));
           colB[0] = fma(-v0, pr, aB0);
           colB[1] = fma(-v1, pr, aB1);
-          *((rokB && kB + 2 <= nn) ? colB + 2 : dmy + 16 * lane + 5) = fma(-v2, pr, aB2);
+          *((rokB && kB + 2 <= nn) ? colB + 2 : dmy + HQ_SS * lane + 5) = fma(-v2, pr, aB2);
         }
         {
           const int d = ir - kB;
@@ -466,7 +476,7 @@ __device__ __forceinline__ void hq_chase2w(double* Hw, double* Qs, double* dmy, 
           const double c1 = own ? (d == 0 ? Y1 : (d == 1 ? S11 : (d == 2 ? S21 : 0.0))) : bB1;
           const double c2 = own ? (d == 0 ? Y2 : (d == 1 ? S12 : (d == 2 ? S22 : S.h3))) : bB2;
           const double tt = fma(v2, c2, fma(v1, c1, v0 * c0));
-          double* sc = dmy + 16 * lane + 3;
+          double* sc = dmy + HQ_SS * lane + 3;
           *(cokB ? rowB : sc) = c0 - tt;
           *(cokB ? rowB + HQ_LD : sc + 1) = fma(-tt, x1, c1);
           *((cokB && kB + 2 <= nn) ? rowB + 2 * HQ_LD : sc + 2) = fma(-tt, x2, c2);
@@ -590,7 +600,7 @@ __device__ __forceinline__ void hq_chasew(double* Hw, double* Qs, double* dmy, d
       const int jc = k + 3 + lane, dc = jc - k, ja = dc >> 2, ta = dc & 3;
       const bool skip = ja >= 1 && ta <= 2 && w - ja >= 0 && k + 4 * ja <= nn - 1;
       const bool rok = jc <= r1 && !skip;
-      double* colp = rok ? Hw + (jc - lo + 1) * HQ_LD + (k - lo) : dmy + 16 * lane;
+      double* colp = rok ? Hw + (jc - lo + 1) * HQ_LD + (k - lo) : dmy + HQ_SS * lane;
       const double aa0 = colp[0], aa1 = colp[1], aa2 = colp[2];
       const bool cok = cok_pre(ir);
       const bool ld = cok && ir < k && !spec;
@@ -598,7 +608,7 @@ __device__ __forceinline__ void hq_chasew(double* Hw, double* Qs, double* dmy, d
       const double b0 = ld ? rowp[0] : 0.0, b1 = ld ? rowp[HQ_LD] : 0.0, b2 = ld ? rowp[2 * HQ_LD] : 0.0;
       double* qp = Qs + lane + (k - lo) * HQ_LD;
       const double g0 = qp[0], g1 = qp[HQ_LD], g2 = qp[2 * HQ_LD];
-      double* hk = (lane == 0 && R.valid) ? Hw + (k - lo) + (k - lo) * HQ_LD : dmy + 16 * lane + 6;
+      double* hk = (lane == 0 && R.valid) ? Hw + (k - lo) + (k - lo) * HQ_LD : dmy + HQ_SS * lane + 6;
       const double hkv = *hk;
       const double u0 = R.xx, u1 = R.yy, u2 = R.zz, w1 = R.qq, w2 = R.rr;
       const double pp0 = fma(w2, S.B20, fma(w1, S.B10, S.B00)), pp1 = fma(w2, S.B21, fma(w1, S.B11, S.B01)),
@@ -621,7 +631,7 @@ __device__ __forceinline__ void hq_chasew(double* Hw, double* Qs, double* dmy, d
         const double pr = fma(w2, aa2, fma(w1, aa1, aa0));
         colp[0] = fma(-u0, pr, aa0);
         colp[1] = fma(-u1, pr, aa1);
-        *((rok && k + 2 <= nn) ? colp + 2 : dmy + 16 * lane + 2) = fma(-u2, pr, aa2);
+        *((rok && k + 2 <= nn) ? colp + 2 : dmy + HQ_SS * lane + 2) = fma(-u2, pr, aa2);
       }
       {
         const int d = ir - k, dB = tb;
@@ -638,7 +648,7 @@ __device__ __forceinline__ void hq_chasew(double* Hw, double* Qs, double* dmy, d
         const double c1 = spec ? zr1 : (own ? (d == 0 ? X1 : (d == 1 ? R11 : (d == 2 ? R21 : 0.0))) : b1);
         const double c2 = spec ? zr2 : (own ? (d == 0 ? X2 : (d == 1 ? R12 : (d == 2 ? R22 : S.h3))) : b2);
         const double tt = fma(u2, c2, fma(u1, c1, u0 * c0));
-        double* sc = dmy + 16 * lane;
+        double* sc = dmy + HQ_SS * lane;
         *(cok ? rowp : sc) = c0 - tt;
         *(cok && k + 1 <= nn ? rowp + HQ_LD : sc + 1) = fma(-tt, w1, c1);
         *(cok && k + 2 <= nn ? rowp + 2 * HQ_LD : sc + 2) = fma(-tt, w2, c2);
@@ -744,12 +754,12 @@ __device__ __forceinline__ void hq_chase2(double* Hw, double* Qs, double* dmy, i
     // A row transformation: column kA+3+lane
     const int jA = kA + 3 + lane;
     const bool rokA = actA && jA <= r1;
-    double* colA = rokA ? Hw + (jA - lo + 1) * HQ_LD + (kA - lo) : dmy + 16 * lane;
+    double* colA = rokA ? Hw + (jA - lo + 1) * HQ_LD + (kA - lo) : dmy + HQ_SS * lane;
     const double aA0 = colA[0], aA1 = colA[1], aA2 = colA[2];
     // B row transformation: column kB+3+lane, except A's columns kA..kA+2 (lanes 1..3)
     const int jB = kB + 3 + lane;
     const bool rokB = actB && jB <= r1 && (!actA || lane < 1 || lane > 3);
-    double* colB = rokB ? Hw + (jB - lo + 1) * HQ_LD + (kB - lo) : dmy + 16 * lane + 3;
+    double* colB = rokB ? Hw + (jB - lo + 1) * HQ_LD + (kB - lo) : dmy + HQ_SS * lane + 3;
     const double aB0 = colB[0], aB1 = colB[1], aB2 = colB[2];
     // A column transformation of row ir: loaded rows are those above kA outside B's rows
     const bool cokA = actA && ir <= min(nn, kA + 3);
@@ -765,8 +775,8 @@ __device__ __forceinline__ void hq_chase2(double* Hw, double* Qs, double* dmy, i
     double* qB = Qs + lane + (actB ? kB - lo : 0) * HQ_LD;
     const double gA0 = qA[0], gA1 = qA[HQ_LD], gA2 = qA[2 * HQ_LD];
     const double gB0 = qB[0], gB1 = qB[HQ_LD], gB2 = qB[2 * HQ_LD];
-    double* hkA = (lane == 0 && actA && RA.valid) ? Hw + (kA - lo) + (kA - lo) * HQ_LD : dmy + 16 * lane + 6;
-    double* hkB = (lane == 0 && actB && RB.valid) ? Hw + (kB - lo) + (kB - lo) * HQ_LD : dmy + 16 * lane + 7;
+    double* hkA = (lane == 0 && actA && RA.valid) ? Hw + (kA - lo) + (kA - lo) * HQ_LD : dmy + HQ_SS * lane + 6;
+    double* hkB = (lane == 0 && actB && RB.valid) ? Hw + (kB - lo) + (kB - lo) * HQ_LD : dmy + HQ_SS * lane + 7;
     const double hkAv = *hkA, hkBv = *hkB;
     // ---- forward of A (as in the one-bulge chase)
     const double u0 = RA.xx, u1 = RA.yy, u2 = RA.zz, w1 = RA.qq, w2 = RA.rr;
@@ -808,11 +818,11 @@ __device__ __forceinline__ void hq_chase2(double* Hw, double* Qs, double* dmy, i
       const double prA = fma(w2, aA2, fma(w1, aA1, aA0));
       colA[0] = fma(-u0, prA, aA0);
       colA[1] = fma(-u1, prA, aA1);
-      *((rokA && kA + 2 <= nn) ? colA + 2 : dmy + 16 * lane + 2) = fma(-u2, prA, aA2);
+      *((rokA && kA + 2 <= nn) ? colA + 2 : dmy + HQ_SS * lane + 2) = fma(-u2, prA, aA2);
       const double prB = fma(x2, aB2, fma(x1, aB1, aB0));
       colB[0] = fma(-v0, prB, aB0);
       colB[1] = fma(-v1, prB, aB1);
-      *((rokB && kB + 2 <= nn) ? colB + 2 : dmy + 16 * lane + 5) = fma(-v2, prB, aB2);
+      *((rokB && kB + 2 <= nn) ? colB + 2 : dmy + HQ_SS * lane + 5) = fma(-v2, prB, aB2);
     }
     {  // A's column transformation (cols kA..kA+2)
       const int d = ir - kA, dB = ir - kB;
@@ -832,7 +842,7 @@ __device__ __forceinline__ void hq_chase2(double* Hw, double* Qs, double* dmy, i
       const double tt = fma(u2, c2, fma(u1, c1, u0 * c0));
       // the special block exists only where both columns and rows are real (<= nn, in the window)
       const bool stA = cokA;
-      double* sc = dmy + 16 * lane;
+      double* sc = dmy + HQ_SS * lane;
       *(stA ? rowA : sc) = c0 - tt;
       *(stA && kA + 1 <= nn ? rowA + HQ_LD : sc + 1) = fma(-tt, w1, c1);
       *(stA && kA + 2 <= nn ? rowA + 2 * HQ_LD : sc + 2) = fma(-tt, w2, c2);
@@ -845,13 +855,13 @@ __device__ __forceinline__ void hq_chase2(double* Hw, double* Qs, double* dmy, i
       const double c1 = own ? (d == 0 ? Y1 : (d == 1 ? S11 : (d == 2 ? S21 : 0.0))) : bB1;
       const double c2 = own ? (d == 0 ? Y2 : (d == 1 ? S12 : (d == 2 ? S22 : Bb.h3))) : bB2;
       const double tt = fma(v2, c2, fma(v1, c1, v0 * c0));
-      double* sc = dmy + 16 * lane + 3;
+      double* sc = dmy + HQ_SS * lane + 3;
       *(cokB ? rowB : sc) = c0 - tt;
       *(cokB ? rowB + HQ_LD : sc + 1) = fma(-tt, x1, c1);
       *((cokB && kB + 2 <= nn) ? rowB + 2 * HQ_LD : sc + 2) = fma(-tt, x2, c2);
     }
     {  // Q <- Q P_A P_B (disjoint columns; an inactive bulge's stores go to scratch, not over the other's)
-      double* sq = dmy + 16 * lane + 8;
+      double* sq = dmy + HQ_SS * lane + 8;
       const double tqA = fma(u2, gA2, fma(u1, gA1, u0 * gA0));
       *(actA ? qA : sq) = gA0 - tqA;
       *(actA ? qA + HQ_LD : sq + 1) = fma(-tqA, w1, gA1);
@@ -878,7 +888,7 @@ __device__ __forceinline__ void hq_chase2(double* Hw, double* Qs, double* dmy, i
 __global__ void __launch_bounds__(HQ_THREADS) hqr_kernel(double* __restrict__ a, int n, int lda,
                                                          double* __restrict__ wr, double* __restrict__ wi,
                                                          int* __restrict__ info) {
-  __shared__ double Hw[HQ_LD * (HQ_R + 1) + 16 * 32];  // window + per-lane scratch
+  __shared__ double Hw[HQ_LD * (HQ_R + 1) + HQ_SS * 32];  // window + per-lane scratch
 #if HQ_XPF && HQ_NB == 3
   __shared__ double Hw2[HQ_LD * (HQ_R + 1)];  // the other window buffer
   __shared__ double Xb[HQ_R * (HQ_R - 3)];    // prefetched H[window rows][next window's new columns]
