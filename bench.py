@@ -316,7 +316,7 @@ def main():
     ok = info["rel_res_true"] <= cfg.tol
     if rank == 0:
         cpu = None
-        if not args.no_oracle:
+        if not args.no_oracle and ws == 1:  # the CPU baseline is taken at N = 1 only
             try:
                 smp = OracleSampler(cfg)
                 for comp in OracleSampler.COMPONENTS:
