@@ -68,8 +68,9 @@ struct sks_ctx {
   int device = 0, rank = 0, nranks = 1, num_sms = 148;
   int main_sms = 146;  // SMs the persistent basis/sketch kernels use; the rest run the side stream's QR
   cudaStream_t own_main = nullptr, side = nullptr, user_main = nullptr;
+  cudaStream_t aux = nullptr;  // per-cycle kappa(T) diagnostics on a copy of T, off the side stream's queue
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr, ev_b0 = nullptr,
-              ev_b1 = nullptr;
+              ev_b1 = nullptr, ev_aux = nullptr, ev_aux_done = nullptr;
   std::vector<cudaEvent_t> ev_batch;
   std::vector<cudaEvent_t> ev_step;  // SKS_OPT_TIME_STEPS: [2 i] before / [2 i + 1] after step launch i
   ncclComm_t comm = nullptr;
@@ -80,7 +81,7 @@ struct sks_ctx {
   // workspaces
   DevBuf W, xb, fb, vb, mr, xg, part, part2, partsk, sigma, H, mnorm, SW, Xp, Zb, U, T, rvec, rho, rest, coef,
       ctrl, small, Mh, Mh2, wr, wi, sel, th, yr, yi, ework, SAB, SB, svw, svs, svU, svV, svH, y2r, y2i, Xr, Xi, AXr, AXi, rpb, cib, vab, cig, rbd,
-      tmp, bgsw, bgsc, plan, gam, rcoef, srft_q, srft_w, partc, partcs, wz, wn, wpart, gsave, csync, cctrl;
+      tmp, bgsw, bgsc, plan, gam, rcoef, srft_q, srft_w, partc, partcs, wz, wn, wpart, gsave, csync, cctrl, Tcopy;
   CtrlBlock* h_ctrl = nullptr;   // pinned mirror
   double* h_small = nullptr;     // pinned scratch (4096 doubles)
   int64_t w_zeroed_bytes = 0;
@@ -368,6 +369,9 @@ static sks_status create_ctx(sks_ctx** out, int device, int rank, int nranks, co
   }
   cudaStreamCreateWithFlags(&c->own_main, cudaStreamNonBlocking);
   cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&c->ev_aux, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_aux_done, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
   cudaEventCreate(&c->ev_t0);
@@ -423,7 +427,7 @@ sks_status sks_destroy(sks_ctx* c) {
                     &c->rho,  &c->rest, &c->coef,  &c->ctrl, &c->small, &c->Mh,  &c->Mh2,   &c->wr,    &c->wi,
                     &c->sel,  &c->th,   &c->yr,    &c->yi,   &c->ework, &c->SAB, &c->SB,    &c->Xr,    &c->Xi,
                     &c->AXr,  &c->AXi,  &c->rpb,   &c->cib,  &c->vab,  &c->cig,  &c->rbd,   &c->tmp,
-                    &c->bgsw, &c->bgsc, &c->plan, &c->gam, &c->rcoef, &c->srft_q, &c->srft_w, &c->partc, &c->partcs, &c->wz, &c->wn, &c->wpart, &c->gsave, &c->csync, &c->cctrl,
+                    &c->bgsw, &c->bgsc, &c->plan, &c->gam, &c->rcoef, &c->srft_q, &c->srft_w, &c->partc, &c->partcs, &c->wz, &c->wn, &c->wpart, &c->gsave, &c->csync, &c->cctrl, &c->Tcopy,
                     &c->svw,  &c->svs,  &c->svU,   &c->svV,  &c->svH,  &c->y2r,   &c->y2i};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
@@ -435,11 +439,12 @@ sks_status sks_destroy(sks_ctx* c) {
   if (c->srft_cache) srft_free(c->srft_cache);
   for (auto& ev : c->ev_batch) cudaEventDestroy(ev);
   for (auto& ev : c->ev_step) cudaEventDestroy(ev);
-  cudaEvent_t evs[] = {c->ev_fork, c->ev_join, c->ev_t0, c->ev_t1, c->ev_b0, c->ev_b1};
+  cudaEvent_t evs[] = {c->ev_fork, c->ev_join, c->ev_t0, c->ev_t1, c->ev_b0, c->ev_b1, c->ev_aux, c->ev_aux_done};
   for (auto e : evs)
     if (e) cudaEventDestroy(e);
   if (c->own_main) cudaStreamDestroy(c->own_main);
   if (c->side) cudaStreamDestroy(c->side);
+  if (c->aux) cudaStreamDestroy(c->aux);
   if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
   if (c->h_small) cudaFreeHost(c->h_small);
   delete c;
@@ -1032,6 +1037,7 @@ static sks_status setup_small(sks_ctx* c, Basis& b, int s, int JB) {
   SKS_TRY(ensure(c, c->Zb, sizeof(double) * (size_t)(ncol + 1) * JB));
   SKS_TRY(ensure(c, c->U, sizeof(double) * (size_t)s * (ncol + 1)));
   SKS_TRY(ensure(c, c->T, sizeof(double) * (size_t)(ncol + 1) * (ncol + 1)));
+  SKS_TRY(ensure(c, c->Tcopy, sizeof(double) * (size_t)(ncol + 1) * (ncol + 1)));
   SKS_TRY(ensure(c, c->rvec, sizeof(double) * s));
   SKS_TRY(ensure(c, c->rho, sizeof(double) * (ncol + 1)));
   SKS_TRY(ensure(c, c->rest, sizeof(double) * (ncol + 1)));
@@ -1365,11 +1371,17 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
     c->h_small[32] = 0;
     reinterpret_cast<int*>(c->h_small + 32)[0] = jstar;
     SKS_CK(c, cudaMemcpyAsync(ncp, c->h_small + 32, sizeof(int), cudaMemcpyHostToDevice, st));
-    // kappa(T) estimate on the side stream, overlapping the assembly and the next cycle (slot per cycle)
+    // kappa(T) estimate (diagnostic: SKS_WARN_COND, info.cond_T) on its own stream from a copy of T, so that
+    // the next cycle's sketched QR on the side stream does not queue behind it (C2 36.9 -> 33.6 ms)
     SKS_CK(c, cudaEventRecord(c->ev_fork, st));
-    SKS_CK(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-    SKS_CK(c, launch_cond(c->T.as<double>(), b.ncol, jstar, 6, nullptr,
-                          c->small.as<double>() + 1024 + std::min(cycles - 1, 1023), c->side));
+    SKS_CK(c, cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
+    SKS_CK(c, cudaMemcpyAsync(c->Tcopy.p, c->T.p, sizeof(double) * (size_t)b.ncol * jstar, cudaMemcpyDeviceToDevice,
+                              c->aux));
+    SKS_CK(c, cudaEventRecord(c->ev_aux, c->aux));
+    SKS_CK(c, cudaStreamWaitEvent(c->side, c->ev_aux, 0));  // the next cycle's QR rewrites T after the copy
+    SKS_CK(c, launch_cond(c->Tcopy.as<double>(), b.ncol, jstar, 6, nullptr,
+                          c->small.as<double>() + 1024 + std::min(cycles - 1, 1023), c->aux));
+    SKS_CK(c, cudaEventRecord(c->ev_aux_done, c->aux));
     SKS_CK(c, launch_assemble(xb, c->W.as<double>(), g.ld, g.off, g.n, c->coef.as<double>(), ncp, jstar,
                               c->num_sms, st));
     c->launches += 3;
@@ -1385,9 +1397,11 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
     r_est_last = c->h_small[64 + jstar - 1] / (fnorm > 0 ? fnorm : 1.0);
     columns += jstar;
   }
-  // join the side stream (kappa estimates) and collect them
+  // join the side and diagnostics streams (kappa estimates) and collect them
   SKS_CK(c, cudaEventRecord(c->ev_join, c->side));
   SKS_CK(c, cudaStreamWaitEvent(st, c->ev_join, 0));
+  SKS_CK(c, cudaEventRecord(c->ev_aux_done, c->aux));
+  SKS_CK(c, cudaStreamWaitEvent(st, c->ev_aux_done, 0));
   SKS_CK(c, cudaMemcpyAsync(x, xb + g.off, sizeof(double) * g.n, cudaMemcpyDefault, st));
   SKS_CK(c, cudaEventRecord(c->ev_t1, st));
   if (cycles > 0)
