@@ -1140,6 +1140,18 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
   sks_status result = SKS_ENOTCONV;
   CtrlBlock* dctrl = c->ctrl.as<CtrlBlock>();
   CtrlBlock* hc = c->h_ctrl;
+  int pend_hist = -1;  // jstar of a cycle whose r_est history sits in h_small[64..] (stream-ordered copy)
+  auto flush_hist = [&]() {
+    if (pend_hist < 0) return;
+    const int js = pend_hist;
+    pend_hist = -1;
+    for (int j = 0; j < js && j < 2048; ++j) {
+      if (hist && nh < hist_cap) hist[nh] = c->h_small[64 + j] / (fnorm > 0 ? fnorm : 1.0);
+      ++nh;
+    }
+    r_est_last = c->h_small[64 + js - 1] / (fnorm > 0 ? fnorm : 1.0);
+    columns += js;
+  };
 
   for (int cyc = 0; cyc <= o->max_cycles; ++cyc) {
     // ---- residual r = f - A x  (w_0), true residual of the previous cycle
@@ -1152,6 +1164,7 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
     ++c->launches;
     SKS_CK(c, cudaMemcpyAsync(c->h_small, c->small.p, sizeof(double), cudaMemcpyDeviceToHost, st));
     SKS_CK(c, cudaStreamSynchronize(st));
+    flush_hist();  // the previous cycle's r_est history (copied before this point on the same stream)
     const double rnorm = std::sqrt(c->h_small[0]);
     rel = fnorm > 0 ? rnorm / fnorm : 0.0;
     if (cyc > 0) {
@@ -1387,15 +1400,11 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
     c->launches += 3;
     SKS_TRY(halo_exchange(c, g, xb));
     // history: r_est,j / ||f||
+    // (read at the next host synchronisation -- the next cycle's residual check or the end of the solve --
+    // instead of a synchronisation of its own: one GPU bubble less per cycle)
     SKS_CK(c, cudaMemcpyAsync(c->h_small + 64, c->rest.p, sizeof(double) * std::min(jstar, 2048),
                               cudaMemcpyDeviceToHost, st));
-    SKS_CK(c, cudaStreamSynchronize(st));
-    for (int j = 0; j < jstar && j < 2048; ++j) {
-      if (hist && nh < hist_cap) hist[nh] = c->h_small[64 + j] / (fnorm > 0 ? fnorm : 1.0);
-      ++nh;
-    }
-    r_est_last = c->h_small[64 + jstar - 1] / (fnorm > 0 ? fnorm : 1.0);
-    columns += jstar;
+    pend_hist = jstar;
   }
   // join the side and diagnostics streams (kappa estimates) and collect them
   SKS_CK(c, cudaEventRecord(c->ev_join, c->side));
@@ -1408,6 +1417,7 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
     SKS_CK(c, cudaMemcpyAsync(c->h_small + 1024, c->small.as<double>() + 1024,
                               sizeof(double) * std::min(cycles, 1024), cudaMemcpyDeviceToHost, st));
   SKS_CK(c, cudaStreamSynchronize(st));
+  flush_hist();
   for (int i = 0; i < std::min(cycles, 1024); ++i) {
     cond_last = c->h_small[1024 + i];
     if (cond_last > cond_tol) flags |= SKS_WARN_COND;
