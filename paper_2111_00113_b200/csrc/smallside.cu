@@ -561,6 +561,19 @@ __global__ void ritz_coef_kernel(const double* __restrict__ sigma, const double*
 }
 
 // one pass over W for compact columns [c0, c0 + NC); RB rows per thread
+#ifndef RV_RB
+#define RV_RB 2
+#endif
+// launch shape of ritz_vectors_kernel (RV_RB rows per thread, RV_MINB CTAs per SM, columns unrolled RV_UNR):
+// C5 (10 GB read) 2.41 ms at (2, 3, 4) -> 2.12 ms at (2, 2, 8), 0.74 of the measured HBM bandwidth
+// (tools/ab_ritz.sh; RB 1/4, MINB 1/4-8 and UNR 12/16 slower)
+#ifndef RV_MINB
+#define RV_MINB 2
+#endif
+#ifndef RV_UNR
+#define RV_UNR 8
+#endif
+constexpr int kRvUnr = RV_UNR;
 template <int NC, int RB>
 __device__ __forceinline__ void ritz_body(const double* __restrict__ W, int64_t ld, int64_t off, int64_t n, int nc,
                                           const double* __restrict__ cs, const int* __restrict__ dst, int c0,
@@ -579,7 +592,7 @@ __device__ __forceinline__ void ritz_body(const double* __restrict__ W, int64_t 
       for (int c = 0; c < NC; ++c) acc[r][c] = 0.0;
     }
     const double* wp = W + off;
-#pragma unroll 4
+#pragma unroll (kRvUnr)
     for (int i = 0; i < nc; ++i) {
       double w[RB];
 #pragma unroll
@@ -613,7 +626,7 @@ __device__ __forceinline__ void ritz_body(const double* __restrict__ W, int64_t 
   }
 }
 
-__global__ void __launch_bounds__(256, 3) ritz_vectors_kernel(const double* __restrict__ W, int64_t ld, int64_t off,
+__global__ void __launch_bounds__(256, RV_MINB) ritz_vectors_kernel(const double* __restrict__ W, int64_t ld, int64_t off,
                                                               int64_t n, int nc, const double* __restrict__ coef,
                                                               const int* __restrict__ meta, double* __restrict__ Xr,
                                                               double* __restrict__ Xi, int64_t ldx, int64_t xoff) {
@@ -626,9 +639,9 @@ __global__ void __launch_bounds__(256, 3) ritz_vectors_kernel(const double* __re
   // C5's ten Ritz vectors need 10-12 compact columns: one pass; more columns take more passes
   for (int c0 = 0; c0 < nco; c0 += 12) {
     if (nco - c0 <= 4)
-      ritz_body<4, 2>(W, ld, off, n, nc, cs, dst, c0, nco, Xr, Xi, ldx, xoff);
+      ritz_body<4, RV_RB>(W, ld, off, n, nc, cs, dst, c0, nco, Xr, Xi, ldx, xoff);
     else
-      ritz_body<12, 2>(W, ld, off, n, nc, cs, dst, c0, nco, Xr, Xi, ldx, xoff);
+      ritz_body<12, RV_RB>(W, ld, off, n, nc, cs, dst, c0, nco, Xr, Xi, ldx, xoff);
   }
 }
 
@@ -795,7 +808,7 @@ cudaError_t launch_ritz_vectors(const double* W, int64_t ld, int64_t off, int64_
   if (smem > 48 * 1024 &&
       cudaFuncSetAttribute(ritz_vectors_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return cudaGetLastError();
-  int grid = (int)std::min<int64_t>((n + 511) / 512, (int64_t)num_sms * 3);
+  int grid = (int)std::min<int64_t>((n + 256 * RV_RB - 1) / (256 * RV_RB), (int64_t)num_sms * RV_MINB);
   if (grid < 1) grid = 1;
   ritz_vectors_kernel<<<grid, 256, smem, st>>>(W, ld, off, n, nc, coef, meta, Xr, Xi, ldx, xoff);
   return cudaGetLastError();
