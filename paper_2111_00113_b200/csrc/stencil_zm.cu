@@ -295,7 +295,14 @@ __global__ void __launch_bounds__(ZT, ZM_CPS)
 static_assert(ZWY % 2 == 0, "the pair kernel needs an even tile height");
 constexpr int ZPT = (ZWX * (ZWY / 2) + 31) / 32 * 32;  // 34 x 9 pairs -> 320 threads
 
-template <int KM, int ZS, bool FULL, bool USL>
+// FE (forward-edge, k <= 2 only, default; SKS_ZM_FE=0 turns it off): the second stencil A w_j of phase B is
+// replaced by the forward-edge form of the one quadratic form the next step needs,
+//     <w, A w> = cc ||w||^2 + (cm + cp) sum_p w_p (w_{p+x} + w_{p+y} + w_{p+z})
+// (each edge (p, p+e) contributes w_p cp w_{p+e} from row p and w_{p+e} cm w_p from row p+e; zero Dirichlet values
+// outside), and <U, A w_j> is accumulated in phase A as <A^T U, w_j> from the same neighbour sums as A U (reading
+// O35); ||A w_j||^2 is not formed (the breakdown reference is derived, reading O39).  Phase B then reads only the
+// +x and +y neighbours of w_j from the ring (the +z one is in registers).
+template <int KM, int ZS, bool FULL, bool USL, bool FE = false>
 __global__ void __launch_bounds__(ZPT, ZM_CPS)
     step3d_zmp_kernel(StepArgs a, ZmArgs z, const __grid_constant__ CUtensorMap tmU,
                       const __grid_constant__ CUtensorMap tmV) {
@@ -456,8 +463,10 @@ __global__ void __launch_bounds__(ZPT, ZM_CPS)
         const double* q0 = sU + (i + 1) * ZUP + cu0;
         const double* q1 = q0 + ZUX;
         // column a (y = by0): y+1 neighbour is column b's centre; column b: y-1 is column a's centre
-        const double Aua = cc * ca[i + 1] + cm * (q0[-1] + q0[-ZUX] + ca[i]) + cp * (q0[1] + cb[i + 1] + ca[i + 2]);
-        const double Aub = cc * cb[i + 1] + cm * (q1[-1] + ca[i + 1] + cb[i]) + cp * (q1[1] + q1[ZUX] + cb[i + 2]);
+        const double sma = q0[-1] + q0[-ZUX] + ca[i], spa = q0[1] + cb[i + 1] + ca[i + 2];
+        const double smb = q1[-1] + ca[i + 1] + cb[i], spb = q1[1] + q1[ZUX] + cb[i + 2];
+        const double Aua = cc * ca[i + 1] + cm * sma + cp * spa;
+        const double Aub = cc * cb[i + 1] + cm * smb + cp * spb;
         double w0v, w1v;
         if (fast) {
           w0v = am0 * Aua + bm0 * ca[i + 1];
@@ -487,6 +496,13 @@ __global__ void __launch_bounds__(ZPT, ZM_CPS)
           rw0[i * ZW] = w0v;
           rw1[i * ZW] = w1v;
         }
+        if constexpr (FE && USL) {  // <U, A w_j> = <A^T U, w_j> on the owned points (plane p in [za, zb))
+          const bool zin = p >= za && p < zb;
+          const double ta = (aw0 && zin) ? cc * ca[i + 1] + cp * sma + cm * spa : 0.0;
+          const double tb = (aw1 && zin) ? cc * cb[i + 1] + cp * smb + cm * spb : 0.0;
+          acc[KM + 2] += ta * w0v;
+          acc[KM + 2] += tb * w1v;
+        }
       }
       __syncthreads();
       if (tid == 0) {
@@ -513,6 +529,25 @@ __global__ void __launch_bounds__(ZPT, ZM_CPS)
             const double wmb = (i == 0) ? wp2b : (i == 1 ? wp1b : wb_[i - 2]);
             const double* r0 = (i == 0) ? rp0 : rw0 + (i - 1) * ZW;
             const double* r1 = (i == 0) ? rp1 : rw1 + (i - 1) * ZW;
+            if constexpr (FE) {
+              // forward edges: +x from the ring, +y of a is b's centre, +y of b from the ring, +z in registers
+              const double yb = aw1 ? r1[ZWX] : 0.0;
+              if (aw0) {
+                *wo0 = wqa;
+                acc[0] += wqa * wqa;
+                acc[2] += wqa * (r0[1] + wqb + wa_[i]);
+              }
+              if (aw1) {
+                *wo1 = wqb;
+                acc[0] += wqb * wqb;
+                acc[2] += wqb * (r1[1] + yb + wb_[i]);
+              }
+              (void)wma;
+              (void)wmb;
+              wo0 += pl;
+              wo1 += pl;
+              continue;
+            }
             // the pair's outer y neighbours are read only for an output column (the row past the
             // last W row lies outside the ring)
             const double ya = aw0 ? r0[-ZWX] : 0.0, yb = aw1 ? r1[ZWX] : 0.0;
@@ -562,6 +597,10 @@ __global__ void __launch_bounds__(ZPT, ZM_CPS)
     }
     sidx = s0 + (uint32_t)nsteps;
     __syncthreads();
+  }
+  if constexpr (FE) {  // slot 1: <w, A w> from ||w||^2 and the forward-edge sum; slot 2 (||A w||^2) is not formed
+    acc[1] = cc * acc[0] + (cm + cp) * acc[2];
+    acc[2] = 0.0;
   }
   step_epilogue<KM>(a, &cf, acc, red);
 }
@@ -981,9 +1020,29 @@ static bool zm_ws() {
   return ws == 1;
 }
 
+// forward-edge pair kernel (default for k <= 2 and the Chebyshev basis; SKS_ZM_FE=0 restores the two-stencil
+// kernel for A/B)
+static bool zm_fe() {
+  static int fe = -1;
+  if (fe < 0) {
+    const char* e = getenv("SKS_ZM_FE");
+    fe = e ? (e[0] == '1') : 1;
+  }
+  return fe == 1;
+}
+
 template <int KM, int ZS, bool FULL, bool USL>
 static cudaError_t zmp_launch(const StepArgs& a, const ZmArgs& z, const CUtensorMap& mu, const CUtensorMap& mv,
                               int grid, size_t smem, cudaStream_t st) {
+  if constexpr (KM == 2) {
+    // k <= 2: the next step needs <w_j, A w_j> and <w_{j-1}, A w_j> only (no window column V_l with vdot)
+    if (zm_fe() && z.vdot == 0) {
+      StepArgs af = a;
+      af.fe = 1;
+      if (cudaError_t e = set_smem_attr(step3d_zmp_kernel<KM, ZS, FULL, USL, true>, smem)) return e;
+      return launch_pdl(step3d_zmp_kernel<KM, ZS, FULL, USL, true>, grid, ZPT, smem, st, af, z, mu, mv);
+    }
+  }
   if (cudaError_t e = set_smem_attr(step3d_zmp_kernel<KM, ZS, FULL, USL>, smem)) return e;
   return launch_pdl(step3d_zmp_kernel<KM, ZS, FULL, USL>, grid, ZPT, smem, st, a, z, mu, mv);
 }

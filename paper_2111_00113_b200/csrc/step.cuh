@@ -43,6 +43,9 @@ struct StepArgs {
   int defer;        // Chebyshev: from column 2 on the recurrence coefficients are constants, so
                     // launches j >= 3 skip the previous launch's partials; the norms, sigma and the recurrence
                     // bookkeeping of a whole batch are finalised at once (cheb_finalize_kernel)
+  int fe;           // forward-edge step (3D z-march, k <= 2; set by the launcher): the kernel produces
+                    // ||w||^2, <w,Aw> = cc ||w||^2 + (cm+cp) sum_{forward edges} w_p w_q and <U,Aw> = <A^T U,w>
+                    // but not ||A w||^2, so the breakdown reference ||m_{j-1}|| is derived (reading O39)
   CtrlBlock* ctrl;
   int64_t ntiles;   // work items
   int tiles_x, tiles_y, zchunk;  // tiling
@@ -123,7 +126,18 @@ __device__ __forceinline__ bool step_prologue(const StepArgs& a, StepCoef* cf, d
     bool bd = !(N > 0.0) || !isfinite(N);
     // breakdown (reading O10): ||w_j|| negligible against the scale of the vector it came from
     // (Arnoldi: ||A b_{j-1}||; Chebyshev: the previous raw vector, raw_0 = b_0 has norm 1)
-    const double ref = (a.basis == 1) ? (jm >= 2 ? 1.0 / a.sigma[jm - 1] : 1.0) : (jm >= 1 ? a.mnorm[jm - 1] : 0.0);
+    double ref = (a.basis == 1) ? (jm >= 2 ? 1.0 / a.sigma[jm - 1] : 1.0) : (jm >= 1 ? a.mnorm[jm - 1] : 0.0);
+    if (a.basis == 0 && jm >= 1 && ref < 0.0) {
+      // forward-edge launches leave ||m_{jm-1}|| as the marker -1: m_{jm-1} = A b_{jm-1} = w_jm + sum_l H[l, jm-1] b_l
+      // over a window of k+1 consecutive columns, which k-truncated Arnoldi makes orthonormal (Eq. partorth
+      // P:208-218), so ||m_{jm-1}||^2 = ||w_jm||^2 + sum_l H[l, jm-1]^2 (reading O39)
+      double s2 = N;
+      for (int l = max(0, jm - k); l <= jm - 1; ++l) {
+        const double h = a.H[l + (int64_t)(jm - 1) * a.ldH];
+        s2 += h * h;
+      }
+      ref = sqrt(s2);
+    }
     if (jm >= 1 && nu <= 1e-14 * ref) bd = true;
     if (cf->ok && bd) {
       cf->ok = 0;
@@ -182,7 +196,7 @@ __device__ __forceinline__ bool step_prologue(const StepArgs& a, StepCoef* cf, d
           a.H[i + (int64_t)jm * a.ldH] = -sg * cf->c[l] / (al * si);
         }
         a.sigma[jm] = sg;
-        a.mnorm[jm] = sg * sqrt(P[2]);
+        a.mnorm[jm] = a.fe ? -1.0 : sg * sqrt(P[2]);
         if (jm >= 1) a.H[jm + (int64_t)(jm - 1) * a.ldH] = a.gam[jm - 1] * nu;
         if (jm == 0) a.ctrl->rnorm = nu;
       }
