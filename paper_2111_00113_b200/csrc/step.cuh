@@ -104,38 +104,71 @@ __device__ __forceinline__ bool step_prologue(const StepArgs& a, StepCoef* cf, d
   // fixed-order reduction of the previous launch's partials: warp w sums component w (w + nwarps, ...) over the
   // grid_prev rows (lane-strided, then a butterfly) -- one barrier, ~5 shuffles per component, instead of a
   // block-wide reduction of all SKS_NP components by every thread
+  // Only components 0 .. k+1 are read below (the window dots end at slot k+1).  Each lane issues all of its loads
+  // before the first add (the partials were written by the previous launch and sit in L2: a load-add loop would be a
+  // chain of L2 round trips); the sums keep the lane-strided sequential order.
   __shared__ double P[SKS_NP];
+  // thread 0's scalar state (stop/exit flags, sigma, ||m||, gamma, the H column of the FE breakdown reference) is
+  // loaded before the reduction, so its latency overlaps the partials' instead of following the barrier
+  const int j = a.j, k = a.k;
+  const int jm = j - 1;
+  const int lo = max(0, j - k);
+  int stop_col = 0, exit_cols = 0;
+  double sgw[SKS_KMAX], hcw[SKS_KMAX], s_jm1 = 1.0, s_0 = 1.0, mn_jm1 = 0.0, gm_jm1 = 0.0;
+  if (tid == 0) {
+    stop_col = a.ctrl->stop_col;
+    exit_cols = a.ctrl->exit_cols;
+#pragma unroll
+    for (int l = 0; l < SKS_KMAX; ++l) sgw[l] = (lo + l <= jm - 1) ? a.sigma[lo + l] : 0.0;
+    const int lo2 = max(0, jm - k);
+#pragma unroll
+    for (int l = 0; l < SKS_KMAX; ++l)
+      hcw[l] = (a.fe && jm >= 1 && lo2 + l <= jm - 1) ? a.H[(lo2 + l) + (int64_t)(jm - 1) * a.ldH] : 0.0;
+    if (jm >= 1) {
+      s_jm1 = a.sigma[jm - 1];
+      mn_jm1 = a.mnorm[jm - 1];
+      gm_jm1 = a.gam[jm - 1];
+    }
+    s_0 = a.sigma[0];
+  }
   {
     const int lane = tid & 31, wid = tid >> 5, nw = (int)(blockDim.x >> 5);
-    for (int cmp = wid; cmp < SKS_NP; cmp += nw) {
+    const int ncmp = min(SKS_NP, k + 2);
+    for (int cmp = wid; cmp < ncmp; cmp += nw) {
       double t = 0.0;
-      for (int b = lane; b < a.grid_prev; b += 32) t += a.partials_in[(int64_t)b * SKS_NP + cmp];
+      for (int b0 = lane; b0 < a.grid_prev; b0 += 256) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int b = b0 + 32 * u;
+          v[u] = (b < a.grid_prev) ? a.partials_in[(int64_t)b * SKS_NP + cmp] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t += v[u];
+      }
       t = warp_sum(t);
       if (lane == 0) P[cmp] = t;
     }
+    if (tid >= ncmp && tid < SKS_NP) P[tid] = 0.0;
     __syncthreads();
   }
   (void)red;
   if (tid == 0) {
-    const int j = a.j, k = a.k;
-    const int jm = j - 1;
     cf->ok = 1;
-    if (a.ctrl->stop_col <= jm || a.ctrl->exit_cols != 0) cf->ok = 0;
+    if (stop_col <= jm || exit_cols != 0) cf->ok = 0;
     const double N = P[0];
     const double nu = sqrt(N);
     bool bd = !(N > 0.0) || !isfinite(N);
     // breakdown (reading O10): ||w_j|| negligible against the scale of the vector it came from
     // (Arnoldi: ||A b_{j-1}||; Chebyshev: the previous raw vector, raw_0 = b_0 has norm 1)
-    double ref = (a.basis == 1) ? (jm >= 2 ? 1.0 / a.sigma[jm - 1] : 1.0) : (jm >= 1 ? a.mnorm[jm - 1] : 0.0);
+    double ref = (a.basis == 1) ? (jm >= 2 ? 1.0 / s_jm1 : 1.0) : (jm >= 1 ? mn_jm1 : 0.0);
     if (a.basis == 0 && jm >= 1 && ref < 0.0) {
       // forward-edge launches leave ||m_{jm-1}|| as the marker -1: m_{jm-1} = A b_{jm-1} = w_jm + sum_l H[l, jm-1] b_l
       // over a window of k+1 consecutive columns, which k-truncated Arnoldi makes orthonormal (Eq. partorth
       // P:208-218), so ||m_{jm-1}||^2 = ||w_jm||^2 + sum_l H[l, jm-1]^2 (reading O39)
       double s2 = N;
-      for (int l = max(0, jm - k); l <= jm - 1; ++l) {
-        const double h = a.H[l + (int64_t)(jm - 1) * a.ldH];
-        s2 += h * h;
-      }
+#pragma unroll
+      for (int l = 0; l < SKS_KMAX; ++l) s2 += hcw[l] * hcw[l];  // zero beyond the window
       ref = sqrt(s2);
     }
     if (jm >= 1 && nu <= 1e-14 * ref) bd = true;
@@ -144,13 +177,12 @@ __device__ __forceinline__ bool step_prologue(const StepArgs& a, StepCoef* cf, d
       if (blockIdx.x == 0) {
         a.ctrl->stop_col = jm;
         a.ctrl->breakdown = 1;
-        if (jm >= 1) a.H[jm + (int64_t)(jm - 1) * a.ldH] = a.gam[jm - 1] * nu;
+        if (jm >= 1) a.H[jm + (int64_t)(jm - 1) * a.ldH] = gm_jm1 * nu;
         if (jm == 0) a.ctrl->rnorm = nu;
       }
     }
     if (cf->ok) {
       const double sg = 1.0 / nu;
-      const int lo = max(0, j - k);
       cf->U = a.W + (int64_t)jm * a.ld;
       if (a.basis == 1) {
         // Chebyshev on the raw vectors w: w_1 = (A - cI) b_0 / (2 rho) with
@@ -163,7 +195,7 @@ __device__ __forceinline__ bool step_prologue(const StepArgs& a, StepCoef* cf, d
         cf->nv = (jm >= 1) ? 1 : 0;
         if (jm >= 1) {
           cf->V[0] = a.W + (int64_t)(jm - 1) * a.ld;
-          cf->c[0] = -(e / rho) * (jm == 1 ? a.sigma[0] : 1.0);
+          cf->c[0] = -(e / rho) * (jm == 1 ? s_0 : 1.0);
           cf->vslot[0] = -1;
         }
       } else {
@@ -172,9 +204,11 @@ __device__ __forceinline__ bool step_prologue(const StepArgs& a, StepCoef* cf, d
         cf->beta_u = -hj * sg;
         const int nv = jm - lo;
         cf->nv = nv;
-        for (int l = 0; l < nv; ++l) {
+#pragma unroll
+        for (int l = 0; l < SKS_KMAX; ++l) {
+          if (l >= nv) break;
           const int i = lo + l;
-          const double si = a.sigma[i];
+          const double si = sgw[l];
           const double hi = sg * si * P[3 + i - (j - k)];
           cf->V[l] = a.W + (int64_t)i * a.ld;
           cf->c[l] = -hi * si;
@@ -190,14 +224,17 @@ __device__ __forceinline__ bool step_prologue(const StepArgs& a, StepCoef* cf, d
         const double gm = sg / al;
         a.gam[jm] = gm;
         a.H[jm + (int64_t)jm * a.ldH] = -cf->beta_u / al;
-        for (int l = 0; l < cf->nv; ++l) {
+        const int nvb = cf->nv;
+#pragma unroll
+        for (int l = 0; l < SKS_KMAX; ++l) {
+          if (l >= nvb) break;
           const int i = (a.basis == 1) ? jm - 1 : lo + l;
-          const double si = (a.basis == 1 && i == 0) ? a.sigma[0] : a.sigma[i];
+          const double si = (a.basis == 1) ? s_jm1 : sgw[l];
           a.H[i + (int64_t)jm * a.ldH] = -sg * cf->c[l] / (al * si);
         }
         a.sigma[jm] = sg;
         a.mnorm[jm] = a.fe ? -1.0 : sg * sqrt(P[2]);
-        if (jm >= 1) a.H[jm + (int64_t)(jm - 1) * a.ldH] = a.gam[jm - 1] * nu;
+        if (jm >= 1) a.H[jm + (int64_t)(jm - 1) * a.ldH] = gm_jm1 * nu;
         if (jm == 0) a.ctrl->rnorm = nu;
       }
     }
