@@ -90,6 +90,10 @@ template <int KM, int ZS>
 __host__ __device__ constexpr int zm_vblk() { return zm_al16(ZVP * ZS); }
 template <int KM, int ZS>
 __host__ __device__ constexpr int zm_stage() { return zm_ublk<KM, ZS>() + (KM - 1) * zm_vblk<KM, ZS>(); }
+template <int KM, int ZS, int NSTG>
+__host__ __device__ constexpr size_t zm_smem_bytes_n() {
+  return 128 + sizeof(double) * ((size_t)NSTG * zm_stage<KM, ZS>() + (size_t)(3 * ZS) * ZR);
+}
 template <int KM, int ZS>
 __host__ __device__ constexpr size_t zm_smem_bytes() {
   return 128 + sizeof(double) * ((size_t)2 * zm_stage<KM, ZS>() + (size_t)(3 * ZS) * ZR);
@@ -302,8 +306,20 @@ constexpr int ZPT = (ZWX * (ZWY / 2) + 31) / 32 * 32;  // 34 x 9 pairs -> 320 th
 // outside), and <U, A w_j> is accumulated in phase A as <A^T U, w_j> from the same neighbour sums as A U (reading
 // O35); ||A w_j||^2 is not formed (the breakdown reference is derived, reading O39).  Phase B then reads only the
 // +x and +y neighbours of w_j from the ring (the +z one is in registers).
+#ifndef ZM_NST
+#define ZM_NST 3  // TMA stages of the FE pair kernel (3 fit at ZS = 4: 219.5 KB); 2 for the others
+#endif
+template <int KM, int ZS, bool FE>
+__host__ __device__ constexpr int zm_nst() {  // the FE kernel takes ZM_NST stages when they fit
+  return (FE && zm_smem_bytes_n<KM, ZS, ZM_NST>() <= 230400) ? ZM_NST : 2;
+}
+#ifndef ZM_PROD
+#define ZM_PROD 1  // 1: an extra (11th) warp issues the TMA stages instead of thread 0 of compute warp 0
+#endif
+constexpr int ZM_PT = ZM_PROD ? ZPT : 0;          // the issuing thread
+constexpr int ZPT_L = ZPT + (ZM_PROD ? 32 : 0);   // threads per CTA of the pair kernel
 template <int KM, int ZS, bool FULL, bool USL, bool FE = false>
-__global__ void __launch_bounds__(ZPT, ZM_CPS)
+__global__ void __launch_bounds__(ZPT_L, ZM_CPS)
     step3d_zmp_kernel(StepArgs a, ZmArgs z, const __grid_constant__ CUtensorMap tmU,
                       const __grid_constant__ CUtensorMap tmV) {
   extern __shared__ __align__(128) unsigned char smraw_p[];
@@ -311,16 +327,16 @@ __global__ void __launch_bounds__(ZPT, ZM_CPS)
   constexpr int STG = zm_stage<KM, ZS>();
   constexpr int UB = zm_ublk<KM, ZS>(), VB = zm_vblk<KM, ZS>();
   constexpr int R = 3 * ZS;
-  double* ring = sm + 2 * STG;
+  constexpr int NST = zm_nst<KM, ZS, FE>();
+  double* ring = sm + NST * STG;
   __shared__ StepCoef cf;
   __shared__ double red[SKS_NP * 32];
-  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ __align__(8) uint64_t bar[NST];
   const int tid = threadIdx.x;
   if (tid == 0) {
     tma_prefetch_desc(&tmU);
     tma_prefetch_desc(&tmV);
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (int t = 0; t < NST; ++t) mbar_init(&bar[t], 1);
     fence_mbar_init();
   }
   pdl_wait_and_release();
@@ -332,13 +348,13 @@ __global__ void __launch_bounds__(ZPT, ZM_CPS)
   // the first piece's first two stages are issued before the partials reduction of the prologue:
   // their inputs (w_{j-1} and the window) were complete at the PDL wait
   int pre = 0;
-  if (ZM_EARLY && tid == 0 && u_lo < u_hi) {
+  if (ZM_EARLY && tid == ZM_PT && u_lo < u_hi) {
     const int col = (int)(u_lo / nz), za = (int)(u_lo % nz);
     const int64_t zr = za + (u_hi - u_lo);
     const int zb = (int)(zr < nz ? zr : nz);
     const int x0 = (col % z.tiles_x) * ZX, y0 = (col / z.tiles_x) * ZY, wa = za - 1;
     const int nsteps = (zb - wa + 1 + ZS - 1) / ZS;
-    for (int t = 0; t < 2 && t < nsteps; ++t) {
+    for (int t = 0; t < NST && t < nsteps; ++t) {
       double* dst = sm + t * STG;
       const int p0 = wa + t * ZS;
       mbar_arrive_expect_tx(&bar[t], sbytes);
@@ -386,7 +402,7 @@ __global__ void __launch_bounds__(ZPT, ZM_CPS)
     const int nsteps = (zb - wa + 1 + ZS - 1) / ZS;
     const uint32_t s0 = sidx;
     auto issue = [&](int t) {
-      const uint32_t slot = (s0 + (uint32_t)t) & 1u;
+      const uint32_t slot = (s0 + (uint32_t)t) % NST;
       double* dst = sm + slot * STG;
       const int p0 = wa + t * ZS;
       mbar_arrive_expect_tx(&bar[slot], sbytes);
@@ -402,15 +418,15 @@ __global__ void __launch_bounds__(ZPT, ZM_CPS)
     const int nx0 = (ncol % z.tiles_x) * ZX, ny0 = (ncol / z.tiles_x) * ZY, nwa = nza - 1;
     const int nnsteps = has_next ? (nzb - nwa + 1 + ZS - 1) / ZS : 0;
     auto issue_next = [&](int tn) {
-      const uint32_t slot = (s0 + (uint32_t)nsteps + (uint32_t)tn) & 1u;
+      const uint32_t slot = (s0 + (uint32_t)nsteps + (uint32_t)tn) % NST;
       double* dst = sm + slot * STG;
       const int p0 = nwa + tn * ZS;
       mbar_arrive_expect_tx(&bar[slot], sbytes);
       tma_load_4d(dst, &tmU, &bar[slot], nx0 - 2, ny0 - 2, p0 - 1 + G, z.ucol);
       for (int l = 0; l < nv; ++l) tma_load_4d(dst + UB + l * VB, &tmV, &bar[slot], nx0 - 2, ny0 - 1, p0 + G, z.vcol[l]);
     };
-    if (tid == 0)
-      for (int t = carried; t < 2 && t < nsteps; ++t) issue(t);
+    if (tid == ZM_PT)
+      for (int t = carried; t < NST && t < nsteps; ++t) issue(t);
     carried = 0;
     double wp1a = 0.0, wp2a = 0.0, wp1b = 0.0, wp2b = 0.0;
     double vla[KM - 1], vlb[KM - 1];
@@ -435,7 +451,7 @@ __global__ void __launch_bounds__(ZPT, ZM_CPS)
       constexpr int PH = decltype(phc)::value;
       constexpr int SBW = ((PH + 1) % 3) * ZS;
       constexpr int SBP = SBW == 0 ? R - 1 : SBW - 1;
-      const uint32_t slot = (s0 + (uint32_t)t) & 1u;
+      const uint32_t slot = (s0 + (uint32_t)t) % NST;
       mbar_wait(&bar[slot], (phase >> slot) & 1u);
       phase ^= 1u << slot;
       const double* sU = sm + slot * STG;
@@ -447,6 +463,8 @@ __global__ void __launch_bounds__(ZPT, ZM_CPS)
       double* rw1 = ring + SBW * ZW + cw1;
       const double* rp0 = ring + SBP * ZW + cw0;
       const double* rp1 = ring + SBP * ZW + cw1;
+      if (ZM_PROD && tid >= ZPT) {  // producer warp: no compute
+      } else {
 #pragma unroll
       for (int k = 0; k < ZS + 2; ++k) {
         ca[k] = sU[k * ZUP + cu0];
@@ -504,12 +522,13 @@ __global__ void __launch_bounds__(ZPT, ZM_CPS)
           acc[KM + 2] += tb * w1v;
         }
       }
+      }
       __syncthreads();
-      if (tid == 0) {
-        if (t + 2 < nsteps) {
-          issue(t + 2);
-        } else if (ZM_NEXT && has_next && nsteps >= 2) {
-          const int tn = t + 2 - nsteps;  // 0 after step nsteps-2, 1 after step nsteps-1
+      if (tid == ZM_PT) {
+        if (t + NST < nsteps) {
+          issue(t + NST);
+        } else if (ZM_NEXT && has_next && nsteps >= NST) {
+          const int tn = t + NST - nsteps;  // 0 after step nsteps-NST, ..., NST-1 after the last step
           if (tn < nnsteps) {
             issue_next(tn);
             carried = tn + 1;
@@ -605,6 +624,254 @@ __global__ void __launch_bounds__(ZPT, ZM_CPS)
   step_epilogue<KM>(a, &cf, acc, red);
 }
 
+
+// ---- plane-split forward-edge kernel (opt-in SKS_ZM_NG=2; measured slower: 38.8 vs 31.6 us at C3, 96 registers with spills).
+// The FE pair kernel runs 10 warps per SM (150 registers) and is latency-bound: each warp walks the ZS planes of a
+// step as one long dependent stream.  Here NG thread groups share a step: group g owns planes [g H, (g+1) H) of the
+// step (H = ZS / NG) for the same 34 x 9 pairs, so the SM holds NG x 10 warps with the same stages and ring.  Phase A
+// of group g reads its U planes p-1 .. p+H from the stage; phase B of group g needs w_j at its planes q = p-1 ..
+// p+H-2 and the +z neighbour q+1 (own registers), except that the first plane q = p-1 of a group was formed by the
+// group (or step) before it and is read from the ring.  Arithmetic per point is that of the FE pair kernel.
+template <int ZS, int NG, bool FULL, bool USL>
+__global__ void __launch_bounds__(ZPT * NG, 1)
+    step3d_zfe_kernel(StepArgs a, ZmArgs z, const __grid_constant__ CUtensorMap tmU,
+                      const __grid_constant__ CUtensorMap tmV) {
+  constexpr int KM = 2;
+  constexpr int H = ZS / NG;
+  static_assert(ZS % NG == 0, "planes per step must split evenly over the groups");
+  extern __shared__ __align__(128) unsigned char smraw_f[];
+  double* sm = reinterpret_cast<double*>(smraw_f + ((128u - (smem_u32(smraw_f) & 127u)) & 127u));
+  constexpr int STG = zm_stage<KM, ZS>();
+  constexpr int UB = zm_ublk<KM, ZS>();
+  constexpr int R = 3 * ZS;
+  double* ring = sm + 2 * STG;
+  __shared__ StepCoef cf;
+  __shared__ double red[SKS_NP * 32];
+  __shared__ __align__(8) uint64_t bar[2];
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    tma_prefetch_desc(&tmU);
+    tma_prefetch_desc(&tmV);
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  pdl_wait_and_release();
+  const int nv = FULL ? KM - 1 : z.nv;
+  const uint32_t sbytes = (uint32_t)(ZUP * (ZS + 2) * 8 + nv * ZVP * ZS * 8);
+  const int m = (int)a.m, nz = (int)a.nz, z0g = (int)a.z0, G = a.G;
+  const int64_t u_lo = z.use_ub ? (int64_t)z.ub[blockIdx.x] : (z.units * blockIdx.x) / gridDim.x;
+  const int64_t u_hi = z.use_ub ? (int64_t)z.ub[blockIdx.x + 1] : (z.units * (blockIdx.x + 1)) / gridDim.x;
+  int pre = 0;
+  if (ZM_EARLY && tid == 0 && u_lo < u_hi) {
+    const int col = (int)(u_lo / nz), za = (int)(u_lo % nz);
+    const int64_t zr = za + (u_hi - u_lo);
+    const int zb = (int)(zr < nz ? zr : nz);
+    const int x0 = (col % z.tiles_x) * ZX, y0 = (col / z.tiles_x) * ZY, wa = za - 1;
+    const int nsteps = (zb - wa + 1 + ZS - 1) / ZS;
+    for (int t = 0; t < 2 && t < nsteps; ++t) {
+      double* dst = sm + t * STG;
+      const int p0 = wa + t * ZS;
+      mbar_arrive_expect_tx(&bar[t], sbytes);
+      tma_load_4d(dst, &tmU, &bar[t], x0 - 2, y0 - 2, p0 - 1 + G, z.ucol);
+      for (int l = 0; l < nv; ++l) tma_load_4d(dst + UB, &tmV, &bar[t], x0 - 2, y0 - 1, p0 + G, z.vcol[l]);
+      pre = t + 1;
+    }
+  }
+  if (!step_prologue(a, &cf, red)) {
+    for (int t = 0; t < pre; ++t) mbar_wait(&bar[t], 0u);
+    return;
+  }
+  const int64_t pl = a.plane;
+  const double cc = a.cc, cm = a.cm, cp = a.cp, alpha = cf.alpha, beta_u = cf.beta_u;
+  const double cl = (nv > 0) ? cf.c[0] : 0.0;
+  double* Wout = a.W + (a.mode == 0 ? (int64_t)a.j * a.ld : 0) + a.off;
+
+  constexpr int NPAIR = ZWX * (ZWY / 2);
+  const int grp = tid / ZPT, tin = tid - grp * ZPT;
+  const int i0 = grp * H;  // first plane (within a step) of this group
+  const bool wt = tin < NPAIR;
+  const int tp = wt ? tin : NPAIR - 1;
+  const int bx = tp % ZWX, by0 = 2 * (tp / ZWX), by1 = by0 + 1;
+  const int cu0 = (by0 + 1) * ZUX + (bx + 1), cu1 = cu0 + ZUX;
+  const int cv0 = by0 * ZVX + (bx + 1), cv1 = cv0 + ZVX;
+  const int cw0 = by0 * ZWX + bx, cw1 = cw0 + ZWX;
+  const bool xin_box = bx >= 1 && bx <= ZX;
+  const bool in0 = wt && xin_box && by0 >= 1 && by0 <= ZY, in1 = wt && xin_box && by1 >= 1 && by1 <= ZY;
+
+  double acc[KM + 3];
+#pragma unroll
+  for (int i = 0; i < KM + 3; ++i) acc[i] = 0.0;
+  uint32_t phase = 0, sidx = 0;
+  int carried = pre;
+  for (int64_t u = u_lo; u < u_hi;) {
+    const int col = (int)(u / nz);
+    const int za = (int)(u % nz);
+    const int64_t zr = za + (u_hi - u);
+    const int zb = (int)(zr < nz ? zr : nz);
+    u += zb - za;
+    const int tx = col % z.tiles_x, ty = col / z.tiles_x;
+    const int x0 = tx * ZX, y0 = ty * ZY;
+    const int wa = za - 1;
+    const int nsteps = (zb - wa + 1 + ZS - 1) / ZS;
+    const uint32_t s0 = sidx;
+    auto issue = [&](int t) {
+      const uint32_t slot = (s0 + (uint32_t)t) & 1u;
+      double* dst = sm + slot * STG;
+      const int p0 = wa + t * ZS;
+      mbar_arrive_expect_tx(&bar[slot], sbytes);
+      tma_load_4d(dst, &tmU, &bar[slot], x0 - 2, y0 - 2, p0 - 1 + G, z.ucol);
+      for (int l = 0; l < nv; ++l) tma_load_4d(dst + UB, &tmV, &bar[slot], x0 - 2, y0 - 1, p0 + G, z.vcol[l]);
+    };
+    const bool has_next = u < u_hi;
+    const int ncol = has_next ? (int)(u / nz) : 0, nza = has_next ? (int)(u % nz) : 0;
+    const int64_t nzr = nza + (u_hi - u);
+    const int nzb = (int)(nzr < nz ? nzr : nz);
+    const int nx0 = (ncol % z.tiles_x) * ZX, ny0 = (ncol / z.tiles_x) * ZY, nwa = nza - 1;
+    const int nnsteps = has_next ? (nzb - nwa + 1 + ZS - 1) / ZS : 0;
+    auto issue_next = [&](int tn) {
+      const uint32_t slot = (s0 + (uint32_t)nsteps + (uint32_t)tn) & 1u;
+      double* dst = sm + slot * STG;
+      const int p0 = nwa + tn * ZS;
+      mbar_arrive_expect_tx(&bar[slot], sbytes);
+      tma_load_4d(dst, &tmU, &bar[slot], nx0 - 2, ny0 - 2, p0 - 1 + G, z.ucol);
+      for (int l = 0; l < nv; ++l) tma_load_4d(dst + UB, &tmV, &bar[slot], nx0 - 2, ny0 - 1, p0 + G, z.vcol[l]);
+    };
+    if (tid == 0)
+      for (int t = carried; t < 2 && t < nsteps; ++t) issue(t);
+    carried = 0;
+    const int gx = x0 - 1 + bx, gy0 = y0 - 1 + by0, gy1 = gy0 + 1;
+    const bool xok = wt && (unsigned)gx < (unsigned)m;
+    const bool xy0 = xok && (unsigned)gy0 < (unsigned)m, xy1 = xok && (unsigned)gy1 < (unsigned)m;
+    const bool aw0 = in0 && gx < m && gy0 < m, aw1 = in1 && gx < m && gy1 < m;
+    // global output of this group's first phase-B plane q = p0 - 1 + i0 (step 0)
+    double* wc0 = Wout + (int64_t)(wa - 1 + i0) * pl + (int64_t)gy0 * m + gx;
+    double* wc1 = wc0 + m;
+    const double am0 = xy0 ? alpha : 0.0, bm0 = xy0 ? beta_u : 0.0, clm0 = xy0 ? cl : 0.0;
+    const double am1 = xy1 ? alpha : 0.0, bm1 = xy1 ? beta_u : 0.0, clm1 = xy1 ? cl : 0.0;
+    constexpr int T0 = ZS == 1 ? 2 : 1;
+    auto step = [&](int t, auto phc) {
+      constexpr int PH = decltype(phc)::value;
+      constexpr int SBW = ((PH + 1) % 3) * ZS;
+      constexpr int SBP = SBW == 0 ? R - 1 : SBW - 1;
+      const uint32_t slot = (s0 + (uint32_t)t) & 1u;
+      mbar_wait(&bar[slot], (phase >> slot) & 1u);
+      phase ^= 1u << slot;
+      const double* sU = sm + slot * STG;
+      const double* sV = sU + UB;
+      const int p0 = wa + t * ZS;
+      const int pg = p0 + i0;  // this group's first plane
+      const bool fast = t >= T0 && p0 + ZS - 1 <= zb && z0g + p0 + ZS - 1 < m;
+      double wa_[H], wb_[H], ca[H + 2], cb[H + 2], va[H], vb[H];
+      double* rw0 = ring + SBW * ZW + i0 * ZW + cw0;
+      double* rw1 = ring + SBW * ZW + i0 * ZW + cw1;
+#pragma unroll
+      for (int k = 0; k < H + 2; ++k) {
+        ca[k] = sU[(i0 + k) * ZUP + cu0];
+        cb[k] = sU[(i0 + k) * ZUP + cu1];
+      }
+#pragma unroll
+      for (int ii = 0; ii < H; ++ii) {
+        const int p = pg + ii;
+        va[ii] = (FULL || nv > 0) ? sV[(i0 + ii) * ZVP + cv0] : 0.0;
+        vb[ii] = (FULL || nv > 0) ? sV[(i0 + ii) * ZVP + cv1] : 0.0;
+        const double* q0 = sU + (i0 + ii + 1) * ZUP + cu0;
+        const double* q1 = q0 + ZUX;
+        const double sma = q0[-1] + q0[-ZUX] + ca[ii], spa = q0[1] + cb[ii + 1] + ca[ii + 2];
+        const double smb = q1[-1] + ca[ii + 1] + cb[ii], spb = q1[1] + q1[ZUX] + cb[ii + 2];
+        const double Aua = cc * ca[ii + 1] + cm * sma + cp * spa;
+        const double Aub = cc * cb[ii + 1] + cm * smb + cp * spb;
+        double w0v, w1v;
+        if (fast) {
+          w0v = am0 * Aua + bm0 * ca[ii + 1];
+          w1v = am1 * Aub + bm1 * cb[ii + 1];
+          if (FULL || nv > 0) {
+            w0v += clm0 * va[ii];
+            w1v += clm1 * vb[ii];
+          }
+        } else {
+          w0v = alpha * Aua + beta_u * ca[ii + 1];
+          w1v = alpha * Aub + beta_u * cb[ii + 1];
+          if (FULL || nv > 0) {
+            w0v += cl * va[ii];
+            w1v += cl * vb[ii];
+          }
+          const bool zok = (unsigned)(z0g + p) < (unsigned)m && p <= zb;
+          w0v = (xy0 && zok) ? w0v : 0.0;
+          w1v = (xy1 && zok) ? w1v : 0.0;
+        }
+        wa_[ii] = w0v;
+        wb_[ii] = w1v;
+        if (wt) {
+          rw0[ii * ZW] = w0v;
+          rw1[ii * ZW] = w1v;
+        }
+        if constexpr (USL) {  // <U, A w_j> = <A^T U, w_j> on the owned points (plane p in [za, zb))
+          const bool zin = p >= za && p < zb;
+          const double ta = (aw0 && zin) ? cc * ca[ii + 1] + cp * sma + cm * spa : 0.0;
+          const double tb = (aw1 && zin) ? cc * cb[ii + 1] + cp * smb + cm * spb : 0.0;
+          acc[KM + 2] += ta * w0v;
+          acc[KM + 2] += tb * w1v;
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        if (t + 2 < nsteps) {
+          issue(t + 2);
+        } else if (ZM_NEXT && has_next && nsteps >= 2) {
+          const int tn = t + 2 - nsteps;
+          if (tn < nnsteps) {
+            issue_next(tn);
+            carried = tn + 1;
+          }
+        }
+      }
+      if (aw0 || aw1) {
+        // the group's first phase-B plane q = pg - 1: formed by the previous group (this step's ring) or, for group 0,
+        // by the last group of the previous step (the previous segment's last plane)
+        const double* rf0 = (i0 == 0) ? ring + SBP * ZW + cw0 : rw0 - ZW;
+        const double* rf1 = (i0 == 0) ? ring + SBP * ZW + cw1 : rw1 - ZW;
+        double* wo0 = wc0;
+        double* wo1 = wc1;
+#pragma unroll
+        for (int ii = 0; ii < H; ++ii) {
+          const int qp = pg - 1 + ii;
+          if (fast || (qp >= za && qp < zb)) {
+            const double* r0 = (ii == 0) ? rf0 : rw0 + (ii - 1) * ZW;
+            const double* r1 = (ii == 0) ? rf1 : rw1 + (ii - 1) * ZW;
+            const double wqa = (ii == 0) ? r0[0] : wa_[ii - 1];
+            const double wqb = (ii == 0) ? r1[0] : wb_[ii - 1];
+            const double yb = aw1 ? r1[ZWX] : 0.0;
+            if (aw0) {
+              *wo0 = wqa;
+              acc[0] += wqa * wqa;
+              acc[2] += wqa * (r0[1] + wqb + wa_[ii]);
+            }
+            if (aw1) {
+              *wo1 = wqb;
+              acc[0] += wqb * wqb;
+              acc[2] += wqb * (r1[1] + yb + wb_[ii]);
+            }
+          }
+          wo0 += pl;
+          wo1 += pl;
+        }
+      }
+      wc0 += (int64_t)ZS * pl;
+      wc1 += (int64_t)ZS * pl;
+    };
+    for (int t = 0; t < nsteps; t += 3) {
+      step(t, std::integral_constant<int, 0>{});
+      if (t + 1 < nsteps) step(t + 1, std::integral_constant<int, 1>{});
+      if (t + 2 < nsteps) step(t + 2, std::integral_constant<int, 2>{});
+    }
+    sidx = s0 + (uint32_t)nsteps;
+    __syncthreads();
+  }
+  acc[1] = cc * acc[0] + (cm + cp) * acc[2];  // <w, A w> from ||w||^2 and the forward-edge sum (reading O39)
+  acc[2] = 0.0;
+  step_epilogue<KM>(a, &cf, acc, red);
+}
 
 // ---- warp-specialised variant (SKS_ZM_WS=1; measured 37.5 us vs 35.1 us for the pair kernel at C3, so the
 // pair kernel stays the default -- DESIGN.md section 11).
@@ -1031,6 +1298,17 @@ static bool zm_fe() {
   return fe == 1;
 }
 
+// plane-split FE kernel: thread groups per step (SKS_ZM_NG=2; default 1 = the FE pair kernel)
+static int zm_ng() {
+  static int ng = -1;
+  if (ng < 0) {
+    const char* e = getenv("SKS_ZM_NG");
+    ng = e ? atoi(e) : 1;
+    if (ng != 1 && ng != 2) ng = 1;
+  }
+  return ng;
+}
+
 template <int KM, int ZS, bool FULL, bool USL>
 static cudaError_t zmp_launch(const StepArgs& a, const ZmArgs& z, const CUtensorMap& mu, const CUtensorMap& mv,
                               int grid, size_t smem, cudaStream_t st) {
@@ -1039,12 +1317,17 @@ static cudaError_t zmp_launch(const StepArgs& a, const ZmArgs& z, const CUtensor
     if (zm_fe() && z.vdot == 0) {
       StepArgs af = a;
       af.fe = 1;
-      if (cudaError_t e = set_smem_attr(step3d_zmp_kernel<KM, ZS, FULL, USL, true>, smem)) return e;
-      return launch_pdl(step3d_zmp_kernel<KM, ZS, FULL, USL, true>, grid, ZPT, smem, st, af, z, mu, mv);
+      if (zm_ng() == 2 && ZS % 2 == 0) {
+        if (cudaError_t e = set_smem_attr(step3d_zfe_kernel<ZS, 2, FULL, USL>, smem)) return e;
+        return launch_pdl(step3d_zfe_kernel<ZS, 2, FULL, USL>, grid, ZPT * 2, smem, st, af, z, mu, mv);
+      }
+      const size_t smf = zm_smem_bytes_n<KM, ZS, zm_nst<KM, ZS, true>()>();
+      if (cudaError_t e = set_smem_attr(step3d_zmp_kernel<KM, ZS, FULL, USL, true>, smf)) return e;
+      return launch_pdl(step3d_zmp_kernel<KM, ZS, FULL, USL, true>, grid, ZPT_L, smf, st, af, z, mu, mv);
     }
   }
   if (cudaError_t e = set_smem_attr(step3d_zmp_kernel<KM, ZS, FULL, USL>, smem)) return e;
-  return launch_pdl(step3d_zmp_kernel<KM, ZS, FULL, USL>, grid, ZPT, smem, st, a, z, mu, mv);
+  return launch_pdl(step3d_zmp_kernel<KM, ZS, FULL, USL>, grid, ZPT_L, smem, st, a, z, mu, mv);
 }
 
 bool stencil_zm_supported(int dim, int64_t m, int k) {
