@@ -385,9 +385,14 @@ __global__ void __launch_bounds__(S4_THREADS, 1) sketch_plan_kernel(int64_t nrow
 }
 
 // ---- gather kernel: stage the batch + load the tile plan (cp.async), gather
-template <int QPW>
+// LPE = lanes per plan entry (32 for J > 16).  A batch of J <= 16 (<= 8) columns is gathered by half- (quarter-)
+// warps: lane = (entry slot, column), so one warp instruction moves 2 (4) entries and a narrow batch costs
+// proportionally fewer shared-memory wavefronts (a half-row of 16 columns of Mt covers the 32 banks once, whatever
+// its swizzle); each lane's sums are partial over its entry slot and are combined by a fixed shuffle at the end.
+template <int QPW, int LPE>
 __global__ void __launch_bounds__(S4_THREADS, 1) sketch_v5_kernel(SketchArgs a, const uint32_t* __restrict__ pent,
                                                                   const uint16_t* __restrict__ pkst, int ES, int KS) {
+  constexpr int EPI = 32 / LPE;  // entries per warp instruction
   extern __shared__ __align__(16) unsigned char smraw[];
   const int s = a.s;
   double* Mt = reinterpret_cast<double*>(smraw);                   // [(R+1)*32]
@@ -395,7 +400,8 @@ __global__ void __launch_bounds__(S4_THREADS, 1) sketch_v5_kernel(SketchArgs a, 
   uint16_t* kst = reinterpret_cast<uint16_t*>(ent + ES);             // [KS]
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   uint32_t lane8, amask;  // opaque to the optimiser (keeps the gather address a single LOP3)
-  asm("mov.b32 %0, %1;" : "=r"(lane8) : "r"((uint32_t)lane * 8u));
+  asm("mov.b32 %0, %1;" : "=r"(lane8) : "r"((uint32_t)(lane % LPE) * 8u));
+  const int slot_e = lane / LPE;  // entry slot of this lane
   asm("mov.b32 %0, %1;" : "=r"(amask) : "r"(0x7fffffffu));
   const uint32_t mt_s = smem_addr(Mt), ent_s = smem_addr(ent), kst_s = smem_addr(kst);
   const int qlo = wid * QPW;
@@ -448,6 +454,25 @@ __global__ void __launch_bounds__(S4_THREADS, 1) sketch_v5_kernel(SketchArgs a, 
       for (int i = 0; i < QPW; ++i) {
         const int e = __shfl_sync(0xffffffffu, kb, i + 1);
         double t0a = 0.0, t1a = 0.0;
+        if constexpr (LPE < 32) {
+          // EPI entries per instruction; entries past the bucket end read the zero row (offset R*256)
+#pragma unroll 1
+          for (; p < e; p += 2 * EPI) {
+            const int i0 = p + slot_e, i1 = p + EPI + slot_e;
+            const uint32_t e0 = (EPI == 2 || i0 < e) ? ent[i0] : (uint32_t)S4_R * 256u;
+            const uint32_t e1 = (i1 < e) ? ent[i1] : (uint32_t)S4_R * 256u;
+            double x0, x1;
+            uint32_t o0, o1;
+            asm("lop3.b32 %0, %1, %2, %3, 0x28;" : "=r"(o0) : "r"(e0), "r"(lane8), "r"(amask));
+            asm("lop3.b32 %0, %1, %2, %3, 0x28;" : "=r"(o1) : "r"(e1), "r"(lane8), "r"(amask));
+            asm volatile("ld.shared.f64 %0, [%2];\n\tld.shared.f64 %1, [%3];"
+                         : "=d"(x0), "=d"(x1)
+                         : "r"(mt_s + o0), "r"(mt_s + o1));
+            t0a += __hiloint2double(__double2hiint(x0) ^ (int)(e0 & 0x80000000u), __double2loint(x0));
+            t1a += __hiloint2double(__double2hiint(x1) ^ (int)(e1 & 0x80000000u), __double2loint(x1));
+          }
+          p = e;
+        } else
 #pragma unroll 1
         for (; p < e; p += 2) {
           const uint2 ee = *reinterpret_cast<const uint2*>(ent + p);
@@ -465,6 +490,13 @@ __global__ void __launch_bounds__(S4_THREADS, 1) sketch_v5_kernel(SketchArgs a, 
       }
     }
     __syncthreads();
+  }
+  if constexpr (LPE < 32) {  // combine the entry slots' partial sums (fixed order)
+#pragma unroll
+    for (int i = 0; i < QPW; ++i) {
+#pragma unroll
+      for (int o = 16; o >= LPE; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+    }
   }
   if (lane < a.J) {
 #pragma unroll
@@ -585,16 +617,32 @@ cudaError_t launch_sketch_plan(int64_t nrows, int64_t row_begin, int s, int zeta
   return cudaGetLastError();
 }
 
-template <int QPW>
-static cudaError_t launch_v5(const SketchArgs& a, const void* plan, int grid, cudaStream_t st) {
+template <int QPW, int LPE>
+static cudaError_t launch_v5l(const SketchArgs& a, const void* plan, int grid, cudaStream_t st) {
   const size_t smem = sketch_v5_smem(a.s, a.zeta);
-  cudaError_t e = set_smem(sketch_v5_kernel<QPW>, smem);
+  cudaError_t e = set_smem(sketch_v5_kernel<QPW, LPE>, smem);
   if (e != cudaSuccess) return e;
   const int ES = s5_ent_stride(a.s, a.zeta), KS = s5_kst_stride(a.s);
   const uint32_t* pent = reinterpret_cast<const uint32_t*>(plan);
   const uint16_t* pkst = reinterpret_cast<const uint16_t*>(pent + a.tiles * (int64_t)ES);
-  sketch_v5_kernel<QPW><<<grid, S4_THREADS, smem, st>>>(a, pent, pkst, ES, KS);
+  sketch_v5_kernel<QPW, LPE><<<grid, S4_THREADS, smem, st>>>(a, pent, pkst, ES, KS);
   return cudaGetLastError();
+}
+
+static int sketch_narrow() {  // SKS_SKETCH_NARROW=0: every batch gathered with 32 lanes per entry (A/B)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SKS_SKETCH_NARROW");
+    v = e ? (e[0] != '0') : 1;
+  }
+  return v;
+}
+
+template <int QPW>
+static cudaError_t launch_v5(const SketchArgs& a, const void* plan, int grid, cudaStream_t st) {
+  if (sketch_narrow() && a.J <= 8) return launch_v5l<QPW, 8>(a, plan, grid, st);
+  if (sketch_narrow() && a.J <= 16) return launch_v5l<QPW, 16>(a, plan, grid, st);
+  return launch_v5l<QPW, 32>(a, plan, grid, st);
 }
 
 static cudaError_t launch_v5_q(const SketchArgs& a, const void* plan, int grid, cudaStream_t st) {

@@ -45,7 +45,9 @@ def test_sketch_table_bit_exact(ctx, s, zeta, seed, cycle, rb):
 
 
 @pytest.mark.parametrize("n,c,s,rb", [(1024, 1, 120, 0), (50_001, 40, 600, 0), (99_999, 32, 400, 4096 * 7),
-                                      (777, 5, 600, 3), (300_000, 7, 2048, 0)])
+                                      (777, 5, 600, 3), (300_000, 7, 2048, 0),
+                                      # narrow batches (half- / quarter-warp gathers): J = 13, 16, 44 = 32 + 12, 3
+                                      (60_001, 13, 600, 0), (40_000, 16, 400, 100), (70_003, 44, 600, 9), (513, 3, 600, 0)])
 def test_sketch_apply_parity(ctx, n, c, s, rb):
     rng = np.random.default_rng(n + c)
     M = rng.standard_normal((n, c))
