@@ -81,7 +81,7 @@ struct sks_ctx {
   // workspaces
   DevBuf W, xb, fb, vb, mr, xg, part, part2, partsk, sigma, H, mnorm, SW, Xp, Zb, U, T, rvec, rho, rest, coef,
       ctrl, small, Mh, Mh2, wr, wi, sel, th, yr, yi, ework, SAB, SB, svw, svs, svU, svV, svH, y2r, y2i, Xr, Xi, AXr, AXi, rpb, cib, vab, cig, rbd,
-      tmp, bgsw, bgsc, plan, gam, rcoef, srft_q, srft_w, partc, partcs, wz, wn, wpart, gsave, csync, cctrl, Tcopy;
+      tmp, bgsw, bgsc, plan, gam, rcoef, srft_q, srft_w, partc, partcs, wz, wn, wpart, gsave, csync, cctrl, Tcopy, ellc, ellv;
   CtrlBlock* h_ctrl = nullptr;   // pinned mirror
   double* h_small = nullptr;     // pinned scratch (4096 doubles)
   int64_t w_zeroed_bytes = 0;
@@ -491,6 +491,9 @@ struct Basis {
   const int32_t* rp = nullptr;
   const int32_t* ci = nullptr;
   const double* va = nullptr;
+  const int32_t* ell_ci = nullptr;  // ELL copy (column-major [ell_w][n]) when the rows are near-uniform
+  const double* ell_va = nullptr;
+  int ell_w = 0;
   int64_t maxn = 0;    // max local rows over ranks (CSR gather)
   int64_t nnz = 0;
   double bytes = 0.0;  // algorithmic bytes of the basis loop
@@ -644,6 +647,29 @@ static sks_status setup_basis(sks_ctx* c, const sks_operator* A, int k, int ncol
       // every column must be readable up to maxn rows for the all-gather
       if (b->maxn > g.ld) return fail(c, SKS_EINVAL, "internal: maxn > ld");
     }
+    // ELL copy for the SpMV when the longest row is short and close to the average (C4: <= 17 per row):
+    // SKS_CSR_ELL=0 keeps the CSR kernel
+    {
+      const char* e = getenv("SKS_CSR_ELL");
+      const bool want = !(e && e[0] == '0');
+      if (want && g.n > 0) {
+        int* dmax = reinterpret_cast<int*>(c->small.p);
+        SKS_CK(c, launch_csr_max_row(g.n, b->rp, dmax, c->main()));
+        int wmax = 0;
+        SKS_CK(c, cudaMemcpyAsync(&wmax, dmax, sizeof(int), cudaMemcpyDeviceToHost, c->main()));
+        SKS_CK(c, cudaStreamSynchronize(c->main()));
+        const double avg = (double)b->nnz / (double)g.n;
+        if (wmax > 0 && wmax <= 32 && wmax <= 1.25 * avg + 1.0) {
+          SKS_TRY(ensure(c, c->ellc, sizeof(int32_t) * (size_t)wmax * g.n));
+          SKS_TRY(ensure(c, c->ellv, sizeof(double) * (size_t)wmax * g.n));
+          SKS_CK(c, launch_csr_to_ell(g.n, b->rp, b->ci, b->va, wmax, c->ellc.as<int32_t>(), c->ellv.as<double>(),
+                                      c->main()));
+          b->ell_ci = c->ellc.as<int32_t>();
+          b->ell_va = c->ellv.as<double>();
+          b->ell_w = wmax;
+        }
+      }
+    }
     SKS_CK(c, cudaStreamSynchronize(c->main()));  // host CSR arrays may be freed after return
   }
   SKS_CK(c, cudaMemsetAsync(c->part.p, 0, c->part.bytes, c->main()));
@@ -733,7 +759,7 @@ static sks_status first_column(sks_ctx* c, Basis& b, int mode, const double* xve
       const double* xg = nullptr;
       SKS_TRY(csr_gather(c, g, xvec, &xg, b.maxn));
       SKS_CK(c, launch_csr_spmv(g.n, b.rp, b.ci, b.va, xg, colp(c, b, 0), fvec, 1, nullptr, 0, 0, 0, b.k, p0,
-                                b.step_grid, st));
+                                b.step_grid, st, nullptr, b.ell_ci, b.ell_va, b.ell_w));
     } else {
       SKS_CK(c, launch_copy_norm(g.n, xvec, colp(c, b, 0), p0, b.step_grid, st));
     }
@@ -793,7 +819,8 @@ static sks_status step_column(sks_ctx* c, Basis& b, int j) {
     SKS_TRY(csr_gather(c, g, colp(c, b, j - 1), &xg, b.maxn));
     double* pd = c->part2.as<double>();  // spmv partials (single slot)
     SKS_CK(c, launch_csr_spmv(g.n, b.rp, b.ci, b.va, xg, c->mr.as<double>(), nullptr, 0, c->W.as<double>(), g.ld,
-                              lo, nw, b.k, pd, b.step_grid, st, c->ctrl.as<CtrlBlock>()));
+                              lo, nw, b.k, pd, b.step_grid, st, c->ctrl.as<CtrlBlock>(), b.ell_ci, b.ell_va,
+                              b.ell_w));
     SKS_TRY(reduce_partials(c, pd, b.step_grid, st));
     SKS_CK(c, launch_csr_orth(g.n, j, b.k, c->W.as<double>(), g.ld, c->mr.as<double>(), pslot(c, b, c->part, j - 1),
                               grid_prev, pd, grid_prev, pslot(c, b, c->part, j), c->sigma.as<double>(),
@@ -1794,7 +1821,7 @@ extern "C" sks_status sks_srr_eigs(sks_ctx* c, const sks_operator* A, const doub
         const double* xg = nullptr;
         SKS_TRY(csr_gather(c, g, src, &xg, b.maxn));
         SKS_CK(c, launch_csr_spmv(g.n, b.rp, b.ci, b.va, xg, dst, nullptr, 0, nullptr, 0, 0, 0, k,
-                                  c->part2.as<double>(), b.step_grid, st));
+                                  c->part2.as<double>(), b.step_grid, st, nullptr, b.ell_ci, b.ell_va, b.ell_w));
         ++c->launches;
       }
     }
@@ -1969,7 +1996,7 @@ extern "C" sks_status sks_apply_operator(sks_ctx* c, const sks_operator* A, cons
     const double* xg = nullptr;
     SKS_TRY(csr_gather(c, g, xb, &xg, b.maxn));
     SKS_CK(c, launch_csr_spmv(g.n, b.rp, b.ci, b.va, xg, yb, nullptr, 0, nullptr, 0, 0, 0, 2, c->part2.as<double>(),
-                              b.step_grid, st));
+                              b.step_grid, st, nullptr, b.ell_ci, b.ell_va, b.ell_w));
   }
   ++c->launches;
   SKS_CK(c, cudaMemcpyAsync(y, yb + g.off, sizeof(double) * g.n, cudaMemcpyDefault, st));

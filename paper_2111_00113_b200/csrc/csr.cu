@@ -269,10 +269,104 @@ __global__ void copy_norm_kernel(int64_t n, const double* __restrict__ src, doub
 // ------------------------------------------------------------------------------
 static int csr_km(int k) { return k <= 2 ? 2 : (k <= 4 ? 4 : 8); }
 
+#ifndef CSR_ELL_CH
+#define CSR_ELL_CH 6  // entries (x gathers) in flight per thread (C4 sweep: 2 181, 3 183, 4 152, 6 147, 8 184, 16 157, 17 154 us)
+#endif
+// ELL SpMV (one thread per row, column-major [w][n] arrays: the k-th entries of 32 consecutive rows are one
+// coalesced load, and each thread has 8 independent x gathers in flight).  Same outputs and partial slots as
+// csr_spmv_kernel; row sums in entry order.
+template <int KM>
+__global__ void __launch_bounds__(256) csr_ell_kernel(CsrArgs a, const int32_t* __restrict__ eci,
+                                                       const double* __restrict__ eva, int w) {
+  __shared__ double red[SKS_NP * 32];
+  const int tid = threadIdx.x;
+  if (a.ctrl && (a.ctrl->exit_cols != 0 || a.ctrl->stop_col < 0x7fffffff)) return;
+  double acc[KM + 1];
+#pragma unroll
+  for (int i = 0; i < KM + 1; ++i) acc[i] = 0.0;
+  const int64_t n = a.n;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + tid; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    double t = 0.0;
+    int k = 0;
+    for (; k + CSR_ELL_CH <= w; k += CSR_ELL_CH) {
+      int c[CSR_ELL_CH];
+      double v[CSR_ELL_CH], x[CSR_ELL_CH];
+#pragma unroll
+      for (int u = 0; u < CSR_ELL_CH; ++u) {
+        c[u] = __ldcs(eci + (int64_t)(k + u) * n + r);
+        v[u] = __ldcs(eva + (int64_t)(k + u) * n + r);
+      }
+#pragma unroll
+      for (int u = 0; u < CSR_ELL_CH; ++u) x[u] = __ldg(a.xg + c[u]);
+#pragma unroll
+      for (int u = 0; u < CSR_ELL_CH; ++u) t += v[u] * x[u];
+    }
+    for (; k < w; ++k) t += __ldcs(eva + (int64_t)k * n + r) * __ldg(a.xg + __ldcs(eci + (int64_t)k * n + r));
+    if (a.mode == 1) {
+      const double rr = a.f[r] - t;
+      a.out[r] = rr;
+      acc[0] += rr * rr;
+    } else {
+      a.out[r] = t;
+      acc[0] += t * t;
+#pragma unroll
+      for (int l = 0; l < KM; ++l)
+        if (l < a.nw) acc[1 + l] += a.W[(int64_t)(a.lo + l) * a.ld + r] * t;
+    }
+  }
+  __shared__ double R[KM + 1];
+  block_sum_n<KM + 1>(acc, red, R);
+  if (tid == 0) {
+    for (int i = 0; i < SKS_NP; ++i)
+      a.partials[(int64_t)blockIdx.x * SKS_NP + i] = (i < KM + 1) ? R[i] : 0.0;
+  }
+}
+
+__global__ void csr_max_row_kernel(int64_t n, const int32_t* __restrict__ rp, int* out) {
+  int m = 0;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, rp[r + 1] - rp[r]);
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+__global__ void csr_to_ell_kernel(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                  const double* __restrict__ va, int w, int32_t* __restrict__ eci,
+                                  double* __restrict__ eva) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    const int b = rp[r], len = rp[r + 1] - b;
+    for (int k = 0; k < w; ++k) {
+      eci[(int64_t)k * n + r] = k < len ? ci[b + k] : 0;
+      eva[(int64_t)k * n + r] = k < len ? va[b + k] : 0.0;
+    }
+  }
+}
+
+cudaError_t launch_csr_max_row(int64_t n, const int32_t* rp, int* out, cudaStream_t st) {
+  cudaMemsetAsync(out, 0, sizeof(int), st);
+  csr_max_row_kernel<<<592, 256, 0, st>>>(n, rp, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_csr_to_ell(int64_t n, const int32_t* rp, const int32_t* ci, const double* va, int w, int32_t* eci,
+                              double* eva, cudaStream_t st) {
+  csr_to_ell_kernel<<<592, 256, 0, st>>>(n, rp, ci, va, w, eci, eva);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_csr_spmv(int64_t n, const int32_t* rp, const int32_t* ci, const double* va, const double* xg,
                             double* out, const double* f, int mode, const double* W, int64_t ld, int lo, int nw,
-                            int k, double* partials, int grid, cudaStream_t st, const CtrlBlock* ctrl) {
+                            int k, double* partials, int grid, cudaStream_t st, const CtrlBlock* ctrl,
+                            const int32_t* ell_ci, const double* ell_va, int ell_w) {
   CsrArgs a{n, rp, ci, va, xg, out, f, mode, W, ld, lo, nw, partials, ctrl};
+  if (ell_w > 0) {
+    switch (csr_km(k)) {
+      case 2: csr_ell_kernel<2><<<grid, 256, 0, st>>>(a, ell_ci, ell_va, ell_w); break;
+      case 4: csr_ell_kernel<4><<<grid, 256, 0, st>>>(a, ell_ci, ell_va, ell_w); break;
+      default: csr_ell_kernel<8><<<grid, 256, 0, st>>>(a, ell_ci, ell_va, ell_w); break;
+    }
+    return cudaGetLastError();
+  }
   static int v1 = -1;
   if (v1 < 0) {
     const char* e = getenv("SKS_CSR_V2");

@@ -164,7 +164,12 @@ cudaError_t launch_cheb_finalize(const double* sums, int j0, int j1, double rho,
 // csr.cu
 cudaError_t launch_csr_spmv(int64_t n, const int32_t* rp, const int32_t* ci, const double* va, const double* xg,
                             double* out, const double* f, int mode, const double* W, int64_t ld, int lo, int nw,
-                            int k, double* partials, int grid, cudaStream_t st, const CtrlBlock* ctrl = nullptr);
+                            int k, double* partials, int grid, cudaStream_t st, const CtrlBlock* ctrl = nullptr,
+                            const int32_t* ell_ci = nullptr, const double* ell_va = nullptr, int ell_w = 0);
+// ELL copy of a CSR matrix (column-major [ell_w][n], rows padded with (0, 0.0)); width = max row length
+cudaError_t launch_csr_max_row(int64_t n, const int32_t* rp, int* out, cudaStream_t st);
+cudaError_t launch_csr_to_ell(int64_t n, const int32_t* rp, const int32_t* ci, const double* va, int w, int32_t* eci,
+                              double* eva, cudaStream_t st);
 cudaError_t launch_csr_orth(int64_t n, int j, int k, double* W, int64_t ld, const double* mr, const double* pnorm,
                             int grid_n, const double* pdot, int grid_s, double* partials, double* sigma, double* H,
                             int ldH, double* mnorm, CtrlBlock* ctrl, int grid, cudaStream_t st);
