@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-2 measurement pass (run under gpurun from the repo root): GPU tests, smoke, bench (both arms, the driver's
 # K/W), all-config sweep, ncu launch list of the bench command, ncu --set full of the bench kernel and the new ones.
-TAG=${1:-r02f}
+TAG=${1:-r02h}
 OUT=gpurun_out/$TAG
 mkdir -p "$OUT"
 : > "$OUT/rc.txt"
@@ -27,6 +27,11 @@ timeout 900 $NCU -k regex:srft_stage --launch-skip 6 --launch-count 2 -o "$OUT/s
   python tools/run_srft_once.py > "$OUT/ncu_srft.log" 2>&1; echo "ncu-srft rc=$?" >> "$OUT/rc.txt"
 timeout 900 $NCU -k regex:hqr_kernel --launch-count 1 -o "$OUT/hqr_c5" -f \
   python tools/run_srr_once.py C5 1 > "$OUT/ncu_hqr.log" 2>&1; echo "ncu-hqr rc=$?" >> "$OUT/rc.txt"
+timeout 900 $NCU -k regex:"csr_ell|csr_orth" --launch-skip 4 --launch-count 2 -o "$OUT/csr_c4" -f \
+  python tools/run_cfg_once.py C4 > "$OUT/ncu_csr.log" 2>&1; echo "ncu-csr rc=$?" >> "$OUT/rc.txt"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$OUT/launches_c4.csv" \
+  python tools/run_cfg_once.py C4 > "$OUT/ncu_launches_c4.log" 2>&1
+python tools/launches.py "$OUT/launches_c4.csv" > "$OUT/launches_summary_c4.txt" 2>&1
 SKS_DEBUG_HQR=1 python tools/run_srr_once.py C5 2 > "$OUT/hqr_counters.txt" 2>&1
 for r in "$OUT"/*.ncu-rep; do python tools/ncu_summary.py "$r"; done > "$OUT/ncu_summaries.txt" 2>&1
 python - "$OUT" <<'PY'
