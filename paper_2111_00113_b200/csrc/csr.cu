@@ -275,8 +275,11 @@ static int csr_km(int k) { return k <= 2 ? 2 : (k <= 4 ? 4 : 8); }
 // ELL SpMV (one thread per row, column-major [w][n] arrays: the k-th entries of 32 consecutive rows are one
 // coalesced load, and each thread has 8 independent x gathers in flight).  Same outputs and partial slots as
 // csr_spmv_kernel; row sums in entry order.
+#ifndef CSR_ELL_T
+#define CSR_ELL_T 256  // threads per CTA (the grid is the partial-slot count, 4 x SMs)
+#endif
 template <int KM>
-__global__ void __launch_bounds__(256) csr_ell_kernel(CsrArgs a, const int32_t* __restrict__ eci,
+__global__ void __launch_bounds__(CSR_ELL_T) csr_ell_kernel(CsrArgs a, const int32_t* __restrict__ eci,
                                                        const double* __restrict__ eva, int w) {
   __shared__ double red[SKS_NP * 32];
   const int tid = threadIdx.x;
@@ -361,9 +364,9 @@ cudaError_t launch_csr_spmv(int64_t n, const int32_t* rp, const int32_t* ci, con
   CsrArgs a{n, rp, ci, va, xg, out, f, mode, W, ld, lo, nw, partials, ctrl};
   if (ell_w > 0) {
     switch (csr_km(k)) {
-      case 2: csr_ell_kernel<2><<<grid, 256, 0, st>>>(a, ell_ci, ell_va, ell_w); break;
-      case 4: csr_ell_kernel<4><<<grid, 256, 0, st>>>(a, ell_ci, ell_va, ell_w); break;
-      default: csr_ell_kernel<8><<<grid, 256, 0, st>>>(a, ell_ci, ell_va, ell_w); break;
+      case 2: csr_ell_kernel<2><<<grid, CSR_ELL_T, 0, st>>>(a, ell_ci, ell_va, ell_w); break;
+      case 4: csr_ell_kernel<4><<<grid, CSR_ELL_T, 0, st>>>(a, ell_ci, ell_va, ell_w); break;
+      default: csr_ell_kernel<8><<<grid, CSR_ELL_T, 0, st>>>(a, ell_ci, ell_va, ell_w); break;
     }
     return cudaGetLastError();
   }

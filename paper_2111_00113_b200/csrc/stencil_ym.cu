@@ -55,7 +55,10 @@ __host__ __device__ constexpr size_t ym_smem_bytes() {
   return 128 + sizeof(double) * ((size_t)2 * ym_stage<KM, ZS>() + (size_t)(3 * ZS) * YWX);
 }
 
-template <int KM, int ZS, bool FULL, bool USL>
+// FE (k <= 2, default; SKS_YM_FE=0 for A/B): forward-edge form of the next step's quadratic form and <A^T U, w_j>
+// in phase A, as in the 3D pair kernel (stencil_zm.cu, reading O39): phase B reads only the +x neighbour from the ring
+// (+y is the next line, in registers) and forms no A w_j.
+template <int KM, int ZS, bool FULL, bool USL, bool FE = false>
 __global__ void __launch_bounds__(YT, YCPS)
     step2d_ym_kernel(StepArgs a, YmArgs z, const __grid_constant__ CUtensorMap tmU,
                      const __grid_constant__ CUtensorMap tmV) {
@@ -181,7 +184,8 @@ __global__ void __launch_bounds__(YT, YCPS)
 #pragma unroll
         for (int l = 0; l < KM - 1; ++l) v[l][i] = (FULL || l < nv) ? sV[l * VB + i * YUX + cu] : 0.0;
         const double* q = sU + (i + 1) * YUX + cu;
-        const double Au = cc * c[i + 1] + cm * (q[-1] + c[i]) + cp * (q[1] + c[i + 2]);
+        const double smn = q[-1] + c[i], spl = q[1] + c[i + 2];
+        const double Au = cc * c[i + 1] + cm * smn + cp * spl;
         double wv;
         if (fast) {
           wv = am * Au + bm * c[i + 1];
@@ -197,6 +201,10 @@ __global__ void __launch_bounds__(YT, YCPS)
         }
         w[i] = wv;
         if (wt) rw[i * YWX] = wv;
+        if constexpr (FE && USL) {  // <U, A w_j> = <A^T U, w_j> on the owned points (line p in [za, zb))
+          const double ta = (aw && p >= za && p < zb) ? cc * c[i + 1] + cp * smn + cm * spl : 0.0;
+          acc[KM + 2] += ta * wv;
+        }
       }
       __syncthreads();
       if (tid == 0 && t + 2 < nsteps) issue(t + 2);
@@ -209,6 +217,14 @@ __global__ void __launch_bounds__(YT, YCPS)
             const double wq = (i == 0) ? wp1 : w[i - 1];
             const double wqm = (i == 0) ? wp2 : (i == 1 ? wp1 : w[i - 2]);
             const double* r = (i == 0) ? rp : rw + (i - 1) * YWX;
+            if constexpr (FE) {  // forward edges: +x from the ring, +y = the next line
+              *wo = wq;
+              acc[0] += wq * wq;
+              acc[2] += wq * (r[1] + w[i]);
+              (void)wqm;
+              wo += pl;
+              continue;
+            }
             const double Aw = cc * wq + cm * (r[-1] + wqm) + cp * (r[1] + w[i]);
             *wo = wq;
             acc[0] += wq * wq;
@@ -240,6 +256,10 @@ __global__ void __launch_bounds__(YT, YCPS)
     }
     sidx = s0 + (uint32_t)nsteps;
     __syncthreads();
+  }
+  if constexpr (FE) {  // slot 1: <w, A w> = cc ||w||^2 + (cm + cp) sum of forward-edge products; no ||A w||^2
+    acc[1] = cc * acc[0] + (cm + cp) * acc[2];
+    acc[2] = 0.0;
   }
   step_epilogue<KM>(a, &cf, acc, red);
 }
@@ -309,6 +329,19 @@ static cudaError_t ym_launch_v(const StepArgs& a, const YmArgs& z, const CUtenso
                                int grid, cudaStream_t st) {
   constexpr int ZS = ym_zs<KM>();
   const size_t smem = ym_smem_bytes<KM, ZS>();
+  if constexpr (KM == 2) {
+    static int fe = -1;
+    if (fe < 0) {
+      const char* e = getenv("SKS_YM_FE");
+      fe = e ? (e[0] == '1') : 1;
+    }
+    if (fe) {
+      StepArgs af = a;
+      af.fe = 1;
+      if (cudaError_t e = set_smem_attr(step2d_ym_kernel<KM, ZS, FULL, USL, true>, smem)) return e;
+      return launch_pdl(step2d_ym_kernel<KM, ZS, FULL, USL, true>, grid, YT, smem, st, af, z, mu, mv);
+    }
+  }
   if (cudaError_t e = set_smem_attr(step2d_ym_kernel<KM, ZS, FULL, USL>, smem)) return e;
   return launch_pdl(step2d_ym_kernel<KM, ZS, FULL, USL>, grid, YT, smem, st, a, z, mu, mv);
 }
