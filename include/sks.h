@@ -110,7 +110,9 @@ typedef enum {
  * "minus" neighbours (i-1, j-1, l-1) -1/h^2 - beta/(2h), "plus" -1/h^2 + beta/(2h).
  * CSR: rows [row_begin,row_end) of A; row_ptr has (row_end-row_begin+1) int32
  * entries starting at 0; col_idx are GLOBAL int32 column indices; val fp64.
- * The library copies the CSR arrays to the device once per call. */
+ * The library copies the CSR arrays to the device once per call.  When the rows are near-uniform (longest row
+ * w <= 32 and <= 1.25 x the average + 1) it also builds a column-major ELL copy (w x rows, 12 bytes per entry,
+ * library-owned device memory reused across calls) that the SpMV reads instead; SKS_CSR_ELL=0 disables it. */
 typedef struct {
   int32_t kind;            /* sks_op_kind */
   int32_t reserved0;
