@@ -1317,9 +1317,11 @@ static cudaError_t zmp_launch(const StepArgs& a, const ZmArgs& z, const CUtensor
     if (zm_fe() && z.vdot == 0) {
       StepArgs af = a;
       af.fe = 1;
-      if (zm_ng() == 2 && ZS % 2 == 0) {
-        if (cudaError_t e = set_smem_attr(step3d_zfe_kernel<ZS, 2, FULL, USL>, smem)) return e;
-        return launch_pdl(step3d_zfe_kernel<ZS, 2, FULL, USL>, grid, ZPT * 2, smem, st, af, z, mu, mv);
+      if constexpr (ZS % 2 == 0) {
+        if (zm_ng() == 2) {
+          if (cudaError_t e = set_smem_attr(step3d_zfe_kernel<ZS, 2, FULL, USL>, smem)) return e;
+          return launch_pdl(step3d_zfe_kernel<ZS, 2, FULL, USL>, grid, ZPT * 2, smem, st, af, z, mu, mv);
+        }
       }
       const size_t smf = zm_smem_bytes_n<KM, ZS, zm_nst<KM, ZS, true>()>();
       if (cudaError_t e = set_smem_attr(step3d_zmp_kernel<KM, ZS, FULL, USL, true>, smf)) return e;
