@@ -174,18 +174,24 @@ __global__ void __launch_bounds__(QT, 1)
 }
 
 // ---------------------------------------------------------------- 2D
-constexpr int Q2X = 64, Q2Y = 32;
+#ifndef Q2Y_M
+#define Q2Y_M 32  // 2D tile height (C2: 64 x 32 -> 128 tiles)
+#endif
+#ifndef Q2_MINB
+#define Q2_MINB 1  // resident CTAs per SM the 2D kernel is compiled for
+#endif
+constexpr int Q2X = 64, Q2Y = Q2Y_M;
 constexpr int QU2X = Q2X + 4, QU2Y = Q2Y + 4;  // 68 x 36
 constexpr int QV2X = Q2X + 2, QV2Y = Q2Y + 2;  // 66 x 34
 constexpr int QU2 = QU2X * QU2Y;               // 2448
 constexpr int QV2 = QV2X * QV2Y;               // 2244 (W box)
-constexpr int QV2P = 2256;                     // W box padded to 128 B
+constexpr int QV2P = (QV2 + 15) / 16 * 16;       // W box padded to 128 B (2256 at 64 x 32)
 constexpr int QB2X = QU2X;                     // V box 68 wide (16-byte aligned origin, see 3D)
 constexpr int QB2 = QB2X * QV2Y;               // 2312
-constexpr int QB2P = 2320;
+constexpr int QB2P = (QB2 + 15) / 16 * 16;       // 2320 at 64 x 32
 
 template <int KM, int NST>
-__global__ void __launch_bounds__(QT, 1)
+__global__ void __launch_bounds__(QT, Q2_MINB)
     step2d_tma_kernel(StepArgs a, TmaCols tc, const __grid_constant__ CUtensorMap tmU,
                       const __grid_constant__ CUtensorMap tmV) {
   extern __shared__ __align__(128) unsigned char smraw_t[];
