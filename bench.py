@@ -291,8 +291,10 @@ def main():
     t_e2e = e0.elapsed_time(e1) * 1e-3 / max(1, args.steps // 2)
 
     # roofline of the dominant kernel (the fused Arnoldi step): algorithmic bytes of its launches
-    # / their summed duration, both from the library (CUDA events bracketing every step launch on
-    # the main stream inside the timed solves, SKS_OPT_TIME_STEPS)
+    # / their summed duration, both from the library: CUDA events on the main stream inside the timed
+    # solves (SKS_OPT_TIME_STEPS) around windows of time_stride = 16 consecutive step launches within a
+    # sketch batch, so consecutive launches keep their programmatic (PDL) overlap as in the untimed
+    # pipeline; SKS_TIME_WINDOW=1 brackets single launches instead (each then loses that overlap)
     t_basis = statistics.mean(i["t_basis_s"] for i in infos)
     bytes_basis = statistics.mean(i["bytes_basis"] for i in infos)
     steps_per_solve = statistics.mean(i["steps"] for i in infos)

@@ -140,7 +140,10 @@ typedef struct {
   double early_exit_factor;  /* in-cycle exit when r_est,j <= factor*tol*||f|| (O16); 0 = never */
   double cond_tol;           /* kappa(T) warning threshold, default 1e14 */
   int32_t flags;             /* SKS_OPT_* bits */
-  int32_t time_stride;       /* SKS_OPT_TIME_STEPS: time every time_stride-th step launch (0/1 = all) */
+  int32_t time_stride;       /* SKS_OPT_TIME_STEPS: time every time_stride-th step launch (0/1 = all); for
+                                stencil operators with time_stride > 1 one event pair brackets a window of
+                                time_stride consecutive launches inside a sketch batch (SKS_TIME_WINDOW=n:
+                                windows of n, 1 = single launches) */
   int32_t basis;             /* SKS_BASIS_ARNOLDI (k-truncated, Eq. partorth) or SKS_BASIS_CHEBYSHEV */
   int32_t sketch;            /* SKS_SKETCH_SPARSE (Eq. sparse-map) or SKS_SKETCH_SRFT (Eq. SRFT, single GPU) */
   double cheb_c, cheb_dx, cheb_dy;  /* Chebyshev: spectrum inside [c +- dx] x [+- i dy];

@@ -500,6 +500,11 @@ struct Basis {
   int64_t steps = 0;
   bool time_steps = false;  // bracket step launches with events (SKS_OPT_TIME_STEPS)
   int time_stride = 1;      // ... every time_stride-th launch
+  int time_window = 1;      // > 1: one event pair around time_window consecutive step launches inside a sketch batch
+                            // (keeps the programmatic overlap between the window's launches; SKS_TIME_WINDOW)
+  int win_end = -1;         // last column of the open window, -1 = none
+  double win_bytes = 0.0;
+  int64_t launches_timed = 0;  // step launches covered by the recorded event pairs
   int ntimed = 0;           // event pairs recorded in this cycle
   double bytes_timed = 0.0; // algorithmic bytes of the timed launches (this cycle)
 };
@@ -783,7 +788,8 @@ static sks_status step_column(sks_ctx* c, Basis& b, int j) {
     StepArgs a = use_t ? b.sat : b.sa;
     a.mode = 0;
     a.j = j;
-    const bool tm = b.time_steps && j % b.time_stride == 0 && 2 * b.ntimed + 1 < (int)c->ev_step.size();
+    const bool tm = b.time_steps && b.time_window <= 1 && j % b.time_stride == 0 &&
+                    2 * b.ntimed + 1 < (int)c->ev_step.size();
     if (tm) SKS_CK(c, cudaEventRecord(c->ev_step[2 * b.ntimed], st));
     a.partials_in = pslot(c, b, c->part, j - 1);
     a.grid_prev = c->nranks > 1 ? 1 : b.last_grid;
@@ -806,8 +812,10 @@ static sks_status step_column(sks_ctx* c, Basis& b, int j) {
     if (tm) {
       SKS_CK(c, cudaEventRecord(c->ev_step[2 * b.ntimed + 1], st));
       ++b.ntimed;
+      ++b.launches_timed;
       b.bytes_timed += 8.0 * g.n * (nwin + 1);
     }
+    if (b.win_end >= 0) b.win_bytes += 8.0 * g.n * (nwin + 1);
     if (!dcol) SKS_TRY(reduce_partials(c, a.partials_out, b.last_grid, st));  // deferred: once per batch
     SKS_TRY(halo_exchange(c, g, colp(c, b, j)));
     b.bytes += 8.0 * g.n * (nwin + 1);
@@ -831,6 +839,7 @@ static sks_status step_column(sks_ctx* c, Basis& b, int j) {
     if (tm) {
       SKS_CK(c, cudaEventRecord(c->ev_step[2 * b.ntimed + 1], st));
       ++b.ntimed;
+      ++b.launches_timed;
       b.bytes_timed += 12.0 * b.nnz + 4.0 * (g.n + 1) + 8.0 * g.n * (nwin + 1);
     }
     b.bytes += 12.0 * b.nnz + 4.0 * (g.n + 1) + 8.0 * g.n * (nwin + 1);
@@ -1115,6 +1124,11 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
   const int JB = panel_jb(s, o->sketch_batch > 0 ? o->sketch_batch : SKS_JB);
   b.time_steps = (o->flags & SKS_OPT_TIME_STEPS) != 0;
   b.time_stride = o->time_stride > 1 ? o->time_stride : 1;
+  {  // windows of consecutive launches when sampling (time_stride > 1); SKS_TIME_WINDOW=1 restores single launches
+    const char* e = getenv("SKS_TIME_WINDOW");
+    b.time_window = e ? std::max(1, atoi(e)) : b.time_stride;
+    if (g.kind == SKS_OP_CSR) b.time_window = 1;
+  }
   if (b.time_steps && (int)c->ev_step.size() < 2 * (d + 2)) {
     const size_t old_n = c->ev_step.size();
     c->ev_step.resize(2 * (d + 2));
@@ -1287,7 +1301,22 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
         SKS_TRY(mpk_columns(c, b, j, je));
         j = je;
       } else {
+        // windowed step timing: events around time_window consecutive step launches of one sketch batch
+        if (b.time_steps && b.time_window > 1 && b.win_end < 0 && j % b.time_stride == 0 &&
+            j + b.time_window - 1 < pending_upto + batch_size && j + b.time_window - 1 <= d &&
+            2 * b.ntimed + 1 < (int)c->ev_step.size()) {
+          SKS_CK(c, cudaEventRecord(c->ev_step[2 * b.ntimed], st));
+          b.win_end = j + b.time_window - 1;
+          b.win_bytes = 0.0;
+        }
         SKS_TRY(step_column(c, b, j));
+        if (b.win_end == j) {
+          SKS_CK(c, cudaEventRecord(c->ev_step[2 * b.ntimed + 1], st));
+          ++b.ntimed;
+          b.launches_timed += b.time_window;
+          b.bytes_timed += b.win_bytes;
+          b.win_end = -1;
+        }
       }
       const bool batch_done = (j + 1 - pending_upto >= batch_size) || j == d;
       if (batch_done) {
@@ -1314,6 +1343,13 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
         }
       }
     }
+    if (b.win_end >= 0) {  // a window cut short by an early stop: close it over the launches it covered
+      SKS_CK(c, cudaEventRecord(c->ev_step[2 * b.ntimed + 1], st));
+      ++b.ntimed;
+      b.launches_timed += std::max(0, last_col - (b.win_end - b.time_window));
+      b.bytes_timed += b.win_bytes;
+      b.win_end = -1;
+    }
     SKS_CK(c, cudaEventRecord(c->ev_b1, st));
     // remaining side work for everything generated, then join
     if (next_sk < last_col + 1) SKS_TRY(enqueue_side(last_col + 1, true));
@@ -1330,9 +1366,10 @@ extern "C" sks_status sks_sgmres_solve(sks_ctx* c, const sks_operator* A, const 
         cudaEventElapsedTime(&t, c->ev_step[2 * i], c->ev_step[2 * i + 1]);
         t_step_total += t * 1e-3;
       }
-      steps_timed += b.ntimed;
+      steps_timed += b.launches_timed;
       bytes_step_total += b.bytes_timed;
       b.ntimed = 0;
+      b.launches_timed = 0;
       b.bytes_timed = 0.0;
     }
     bytes_basis_total += b.bytes - bytes_first;
