@@ -226,6 +226,9 @@ __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
 }
+#ifndef SK_PF
+#define SK_PF 1
+#endif
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
@@ -450,6 +453,9 @@ __global__ void __launch_bounds__(S4_THREADS, 1) sketch_v5_kernel(SketchArgs a, 
     {
       const int kb = (lane <= QPW) ? (int)kst[min(qlo + lane, s)] : 0;
       int p = __shfl_sync(0xffffffffu, kb, 0);
+      // SK_PF: the next entry pair is loaded one iteration ahead (the warp's buckets are contiguous in ent[], and
+      // ent[] extends past the last bucket), so the gather's two dependent shared loads overlap
+      uint2 eenx = (SK_PF && LPE == 32) ? *reinterpret_cast<const uint2*>(ent + p) : make_uint2(0u, 0u);
 #pragma unroll
       for (int i = 0; i < QPW; ++i) {
         const int e = __shfl_sync(0xffffffffu, kb, i + 1);
@@ -475,7 +481,12 @@ __global__ void __launch_bounds__(S4_THREADS, 1) sketch_v5_kernel(SketchArgs a, 
         } else
 #pragma unroll 1
         for (; p < e; p += 2) {
+#if SK_PF
+          const uint2 ee = eenx;
+          eenx = *reinterpret_cast<const uint2*>(ent + p + 2);
+#else
           const uint2 ee = *reinterpret_cast<const uint2*>(ent + p);
+#endif
           double x0, x1;  // both loads in flight before either is used
           uint32_t o0, o1;  // (E ^ 8 lane) & 0x7fffffff as one LOP3 each
           asm("lop3.b32 %0, %1, %2, %3, 0x28;" : "=r"(o0) : "r"(ee.x), "r"(lane8), "r"(amask));
